@@ -1,0 +1,142 @@
+/*
+ * lbfs.h — C ABI of the B200-native top-down BFS (sm_100a).
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `lanebfs` (arXiv 1604.02844): everything below `run_bfs(g, s, policy)`
+ * (reference pkg/src/lanebfs/traversal.py:413-422) and the graph inputs it
+ * consumes (graph.py:68-160). Plain pointers and sizes only; no torch types.
+ *
+ * Conventions
+ *   - Return 0 on success or a negative LBFS_E* code. The message of the last
+ *     failure on the calling thread is in lbfs_last_error().
+ *   - Vertex ids are int32 (the reference caps SCALE at 30 so ids stay below
+ *     the sentinel, graph.py:11-13); CSR offsets are int64 (graph.py:156).
+ *   - Host output buffers are caller-owned. Device state is library-owned.
+ *   - Calls on one graph handle are serialised by a mutex inside the library
+ *     (the reference never overlaps BFS calls).
+ */
+#ifndef LBFS_H
+#define LBFS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LBFS_OK 0
+#define LBFS_EINVAL (-1) /* bad argument: the Python layer raises AssertionError */
+#define LBFS_ECUDA (-2)  /* CUDA runtime / launch failure */
+#define LBFS_ENCCL (-3)  /* collective failure (multi-GPU) */
+#define LBFS_ENOMEM (-4) /* device or pinned-host allocation failed */
+
+/* Unreached-predecessor value; reference traversal.py:22 (SENTINEL). */
+#define LBFS_SENTINEL 0x7FFFFFFF
+
+typedef struct lbfs_graph lbfs_graph; /* device-resident BFS graph        */
+typedef struct lbfs_csr lbfs_csr;     /* device-resident CSR (original ids) */
+
+/* One BFS layer; reference LayerStats, traversal.py:66-70. */
+typedef struct lbfs_layer {
+  int64_t input;      /* frontier vertices entering the layer       */
+  int64_t edges;      /* adjacency entries examined (sum of degree)  */
+  int64_t discovered; /* vertices first reached in this layer        */
+} lbfs_layer;
+
+/* Device-side timing of one BFS (CUDA events on the BFS stream). */
+typedef struct lbfs_timing {
+  double bfs_ms;           /* init kernel start -> end of last level         */
+  double init_ms;          /* K4 init (pred/level fill, bitmap clear, seed)  */
+  double expand_ms;        /* sum over levels of the expansion kernels       */
+  double d2h_ms;           /* host-output variant: pred+level copy to host   */
+  int64_t levels;          /* number of layers (== n_layers)                 */
+  int64_t kernel_launches; /* kernels this BFS launched                      */
+  int64_t edges;           /* traversed_edge_count (sum of layer edges)      */
+  int64_t reached;         /* vertices with a level (sum of layer inputs)    */
+} lbfs_timing;
+
+typedef struct lbfs_device_info {
+  int device;
+  int sm_count;
+  int cc_major;
+  int cc_minor;
+  int64_t l2_bytes;
+  int64_t hbm_bytes;
+  int64_t smem_per_block_optin;
+  char name[256];
+} lbfs_device_info;
+
+/* ---- library ---------------------------------------------------------- */
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* lbfs_last_error(void);
+/* Properties of CUDA device `device`. */
+int lbfs_device_info_get(int device, lbfs_device_info* out);
+/* Number of kernel launches this process has issued through the library. */
+int64_t lbfs_kernel_launch_count(void);
+
+/* ---- graph construction (reference graph.py) -------------------------- */
+
+/* R-MAT endpoint pairs, bit-exact with the reference generate_rmat
+ * (graph.py:68-85): numpy Generator(PCG64).random() draws in the same order.
+ * pcg = {state_hi, state_lo, inc_hi, inc_lo} of default_rng(seed)'s PCG64.
+ * Host outputs src/dst of length m = 2^scale * edgefactor. */
+int lbfs_rmat_edges(int scale, int64_t m, double ab, double a_norm, double c_norm,
+                    const uint64_t pcg[4], uint32_t* src_out, uint32_t* dst_out);
+
+/* Seeded vertex permutation (Feistel bijection on [0,n))
+ * applied in place to both endpoint arrays (host). */
+int lbfs_permute_edges(int64_t n, uint64_t seed, uint32_t* src, uint32_t* dst, int64_t m);
+
+/* CSR from host endpoint arrays; reference build_csr (graph.py:139-160):
+ * symmetrize inserts reverse pairs; dedup sorts each row, drops duplicates
+ * and self-loops; without dedup rows keep stable source order. */
+int lbfs_csr_build(int64_t n, const uint32_t* src, const uint32_t* dst, int64_t m,
+                   int symmetrize, int dedup, lbfs_csr** out);
+/* Whole pipeline on the device: generate_rmat -> (optional) permutation ->
+ * build_csr(symmetrize=True, dedup=True). No host copy of the edge list. */
+int lbfs_csr_build_rmat(int scale, int edgefactor, double ab, double a_norm, double c_norm,
+                        const uint64_t pcg[4], int permute, uint64_t perm_seed, lbfs_csr** out);
+/* 2D 4-neighbour lattice rows x cols (vertex r*cols+c, edges right and down,
+ * no wrap) -> (optional) permutation -> build_csr on the device. */
+int lbfs_csr_build_lattice(int64_t rows, int64_t cols, int permute, uint64_t perm_seed,
+                           lbfs_csr** out);
+int lbfs_csr_info(const lbfs_csr* csr, int64_t* n, int64_t* nnz);
+/* Copy the CSR to host arrays: row_ptr[n+1] (int64), col_idx[nnz] (int32). */
+int lbfs_csr_download(const lbfs_csr* csr, int64_t* row_ptr, int32_t* col_idx);
+void lbfs_csr_destroy(lbfs_csr* csr);
+
+/* ---- BFS graph handle (replaces CsrGraph as seen by run_bfs) ---------- */
+
+/* Copy a host CSR (colstarts int64[n+1], rows int32[nnz]; graph.py:96-136) to
+ * the device and build the traversal layout. ngpus must be 1 in this build
+ * (the partitioned path is driven from Python over torch.distributed). */
+int lbfs_graph_create(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int64_t nnz,
+                      int ngpus, lbfs_graph** out);
+/* Same, from a device CSR (no host round trip). The csr may be destroyed
+ * afterwards. */
+int lbfs_graph_create_from_csr(const lbfs_csr* csr, int ngpus, lbfs_graph** out);
+void lbfs_graph_destroy(lbfs_graph* g);
+int lbfs_graph_info(const lbfs_graph* g, int64_t* n, int64_t* nnz);
+
+/* Top-down BFS from root; synchronous. Replaces run_bfs/bfs_* (traversal.py:
+ * 80-422). pred_out must hold pad32(n) int32 entries (PredecessorArray
+ * storage, traversal.py:42-46): parent id, root -> root, unreached and padding
+ * -> LBFS_SENTINEL. level_out holds n int32 (-1 = unreached). Either output
+ * may be NULL. layers_out receives up to layers_cap layers; *n_layers is the
+ * full count (fetch the rest with lbfs_graph_last_layers). t_out may be NULL. */
+int lbfs_bfs(lbfs_graph* g, int64_t root, int32_t* pred_out, int32_t* level_out,
+             lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers, lbfs_timing* t_out);
+/* Same, writing into DEVICE buffers (e.g. torch CUDA tensors) on the graph's
+ * device; no host copy inside. */
+int lbfs_bfs_device(lbfs_graph* g, int64_t root, int32_t* d_pred, int32_t* d_level,
+                    lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers,
+                    lbfs_timing* t_out);
+/* Layers of the most recent BFS on this handle. */
+int lbfs_graph_last_layers(const lbfs_graph* g, lbfs_layer* out, int64_t cap, int64_t* n_layers);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LBFS_H */

@@ -1,0 +1,378 @@
+// extern "C" boundary of liblbfs (declared in include/lbfs.h). Every entry
+// point converts internal exceptions into LBFS_E* codes plus a thread-local
+// message, mirroring the reference's error split: precondition violations
+// (assert -> AssertionError in traversal.py:84,133,341 / graph.py:33-37) map to
+// LBFS_EINVAL, everything else to a runtime failure.
+#include <cstdio>
+#include <cstring>
+
+#include "bfs_engine.cuh"
+
+namespace lbfs {
+
+std::atomic<int64_t> g_launches{0};
+static thread_local std::string t_err;
+
+void set_error(const std::string& m) { t_err = m; }
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "%s failed: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+  const int code = (e == cudaErrorMemoryAllocation) ? LBFS_ENOMEM : LBFS_ECUDA;
+  throw Failure(code, buf);
+}
+
+int current_sm_count() {
+  int dev = 0, sms = 0;
+  LBFS_CUDA(cudaGetDevice(&dev));
+  LBFS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  return sms;
+}
+
+template <typename F>
+static int guarded(F&& f) {
+  try {
+    f();
+    t_err.clear();
+    return LBFS_OK;
+  } catch (const Failure& e) {
+    t_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    return LBFS_ECUDA;
+  }
+}
+
+static void check_ids(int64_t n) {
+  if (n < 1) throw_inval("num_vertices must be >= 1");
+  if (n > ((int64_t)1 << 31) - 1) throw_inval("num_vertices must fit int32 ids below the sentinel");
+}
+
+struct Stream {  // scratch stream for construction calls
+  cudaStream_t s = nullptr;
+  Stream() { LBFS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~Stream() { cudaStreamDestroy(s); }
+};
+
+}  // namespace lbfs
+
+using namespace lbfs;
+
+extern "C" {
+
+const char* lbfs_last_error(void) { return t_err.c_str(); }
+
+int64_t lbfs_kernel_launch_count(void) { return g_launches.load(); }
+
+int lbfs_device_info_get(int device, lbfs_device_info* out) {
+  return guarded([&] {
+    if (!out) throw_inval("out is NULL");
+    cudaDeviceProp p;
+    LBFS_CUDA(cudaGetDeviceProperties(&p, device));
+    memset(out, 0, sizeof(*out));
+    out->device = device;
+    out->sm_count = p.multiProcessorCount;
+    out->cc_major = p.major;
+    out->cc_minor = p.minor;
+    out->l2_bytes = p.l2CacheSize;
+    out->hbm_bytes = (int64_t)p.totalGlobalMem;
+    out->smem_per_block_optin = (int64_t)p.sharedMemPerBlockOptin;
+    strncpy(out->name, p.name, sizeof(out->name) - 1);
+  });
+}
+
+int lbfs_rmat_edges(int scale, int64_t m, double ab, double a_norm, double c_norm,
+                    const uint64_t pcg[4], uint32_t* src_out, uint32_t* dst_out) {
+  return guarded([&] {
+    if (scale < 1 || scale > 30) throw_inval("scale must be in [1, 30]");
+    if (m < 0 || !pcg || (m > 0 && (!src_out || !dst_out))) throw_inval("bad arguments");
+    if (m == 0) return;
+    Stream s;
+    uint32_t* ds = dev_alloc<uint32_t>((size_t)m);
+    uint32_t* dd = dev_alloc<uint32_t>((size_t)m);
+    try {
+      rmat_edges_device(scale, m, ab, a_norm, c_norm, pcg, ds, dd, s.s);
+      LBFS_CUDA(cudaMemcpy(src_out, ds, sizeof(uint32_t) * (size_t)m, cudaMemcpyDeviceToHost));
+      LBFS_CUDA(cudaMemcpy(dst_out, dd, sizeof(uint32_t) * (size_t)m, cudaMemcpyDeviceToHost));
+    } catch (...) {
+      dev_free(ds);
+      dev_free(dd);
+      throw;
+    }
+    dev_free(ds);
+    dev_free(dd);
+  });
+}
+
+int lbfs_permute_edges(int64_t n, uint64_t seed, uint32_t* src, uint32_t* dst, int64_t m) {
+  return guarded([&] {
+    check_ids(n);
+    if (m < 0 || (m > 0 && (!src || !dst))) throw_inval("bad arguments");
+    if (m == 0) return;
+    Stream s;
+    uint32_t* ds = dev_alloc<uint32_t>((size_t)m);
+    uint32_t* dd = dev_alloc<uint32_t>((size_t)m);
+    try {
+      LBFS_CUDA(cudaMemcpy(ds, src, sizeof(uint32_t) * (size_t)m, cudaMemcpyHostToDevice));
+      LBFS_CUDA(cudaMemcpy(dd, dst, sizeof(uint32_t) * (size_t)m, cudaMemcpyHostToDevice));
+      permute_edges_device(n, seed, ds, dd, m, s.s);
+      LBFS_CUDA(cudaStreamSynchronize(s.s));
+      LBFS_CUDA(cudaMemcpy(src, ds, sizeof(uint32_t) * (size_t)m, cudaMemcpyDeviceToHost));
+      LBFS_CUDA(cudaMemcpy(dst, dd, sizeof(uint32_t) * (size_t)m, cudaMemcpyDeviceToHost));
+    } catch (...) {
+      dev_free(ds);
+      dev_free(dd);
+      throw;
+    }
+    dev_free(ds);
+    dev_free(dd);
+  });
+}
+
+int lbfs_csr_build(int64_t n, const uint32_t* src, const uint32_t* dst, int64_t m, int symmetrize,
+                   int dedup, lbfs_csr** out) {
+  return guarded([&] {
+    check_ids(n);
+    if (!out || m < 0 || (m > 0 && (!src || !dst))) throw_inval("bad arguments");
+    Stream s;
+    uint32_t* ds = dev_alloc<uint32_t>((size_t)m);
+    uint32_t* dd = dev_alloc<uint32_t>((size_t)m);
+    auto* h = new lbfs_csr;
+    try {
+      if (m > 0) {
+        LBFS_CUDA(cudaMemcpy(ds, src, sizeof(uint32_t) * (size_t)m, cudaMemcpyHostToDevice));
+        LBFS_CUDA(cudaMemcpy(dd, dst, sizeof(uint32_t) * (size_t)m, cudaMemcpyHostToDevice));
+      }
+      h->c = build_csr_device(n, ds, dd, m, symmetrize != 0, dedup != 0, s.s);
+    } catch (...) {
+      dev_free(ds);
+      dev_free(dd);
+      delete h;
+      throw;
+    }
+    dev_free(ds);
+    dev_free(dd);
+    *out = h;
+  });
+}
+
+int lbfs_csr_build_rmat(int scale, int edgefactor, double ab, double a_norm, double c_norm,
+                        const uint64_t pcg[4], int permute, uint64_t perm_seed, lbfs_csr** out) {
+  return guarded([&] {
+    if (scale < 1 || scale > 30 || edgefactor < 1 || !pcg || !out) throw_inval("bad arguments");
+    const int64_t n = (int64_t)1 << scale;
+    const int64_t m = n * edgefactor;
+    Stream s;
+    uint32_t* ds = dev_alloc<uint32_t>((size_t)m);
+    uint32_t* dd = dev_alloc<uint32_t>((size_t)m);
+    auto* h = new lbfs_csr;
+    try {
+      rmat_edges_device(scale, m, ab, a_norm, c_norm, pcg, ds, dd, s.s);
+      if (permute) permute_edges_device(n, perm_seed, ds, dd, m, s.s);
+      h->c = build_csr_device(n, ds, dd, m, true, true, s.s);
+    } catch (...) {
+      dev_free(ds);
+      dev_free(dd);
+      delete h;
+      throw;
+    }
+    dev_free(ds);
+    dev_free(dd);
+    *out = h;
+  });
+}
+
+int lbfs_csr_build_lattice(int64_t rows, int64_t cols, int permute, uint64_t perm_seed,
+                           lbfs_csr** out) {
+  return guarded([&] {
+    if (rows < 1 || cols < 1 || !out) throw_inval("bad arguments");
+    const int64_t n = rows * cols;
+    check_ids(n);
+    const int64_t m = rows * (cols - 1) + (rows - 1) * cols;
+    Stream s;
+    uint32_t* ds = dev_alloc<uint32_t>((size_t)m);
+    uint32_t* dd = dev_alloc<uint32_t>((size_t)m);
+    auto* h = new lbfs_csr;
+    try {
+      lattice_edges_device(rows, cols, ds, dd, s.s);
+      if (permute) permute_edges_device(n, perm_seed, ds, dd, m, s.s);
+      h->c = build_csr_device(n, ds, dd, m, true, true, s.s);
+    } catch (...) {
+      dev_free(ds);
+      dev_free(dd);
+      delete h;
+      throw;
+    }
+    dev_free(ds);
+    dev_free(dd);
+    *out = h;
+  });
+}
+
+int lbfs_csr_info(const lbfs_csr* csr, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    if (!csr) throw_inval("csr is NULL");
+    if (n) *n = csr->c.n;
+    if (nnz) *nnz = csr->c.nnz;
+  });
+}
+
+int lbfs_csr_download(const lbfs_csr* csr, int64_t* row_ptr, int32_t* col_idx) {
+  return guarded([&] {
+    if (!csr) throw_inval("csr is NULL");
+    LBFS_CUDA(cudaSetDevice(csr->c.device));
+    if (row_ptr)
+      LBFS_CUDA(cudaMemcpy(row_ptr, csr->c.row_ptr, sizeof(int64_t) * (size_t)(csr->c.n + 1),
+                           cudaMemcpyDeviceToHost));
+    if (col_idx && csr->c.nnz > 0)
+      LBFS_CUDA(cudaMemcpy(col_idx, csr->c.col_idx, sizeof(int32_t) * (size_t)csr->c.nnz,
+                           cudaMemcpyDeviceToHost));
+  });
+}
+
+void lbfs_csr_destroy(lbfs_csr* csr) {
+  if (!csr) return;
+  cudaSetDevice(csr->c.device);
+  free_csr(csr->c);
+  delete csr;
+}
+
+int lbfs_graph_create(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int64_t nnz,
+                      int ngpus, lbfs_graph** out) {
+  return guarded([&] {
+    check_ids(n);
+    if (!out || !row_ptr || nnz < 0 || (nnz > 0 && !col_idx)) throw_inval("bad arguments");
+    if (ngpus != 1) throw_inval("ngpus must be 1 (multi-GPU runs one process per GPU)");
+    if (row_ptr[0] != 0 || row_ptr[n] != nnz) throw_inval("row_ptr must start at 0 and end at nnz");
+    Csr c;
+    LBFS_CUDA(cudaGetDevice(&c.device));
+    c.n = n;
+    c.nnz = nnz;
+    c.row_ptr = dev_alloc<int64_t>((size_t)n + 1);
+    c.col_idx = dev_alloc<int32_t>((size_t)nnz + 4);
+    try {
+      LBFS_CUDA(cudaMemcpy(c.row_ptr, row_ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice));
+      if (nnz > 0)
+        LBFS_CUDA(cudaMemcpy(c.col_idx, col_idx, sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice));
+      auto* g = new lbfs_graph;
+      g->eng = new BfsEngine(c);
+      g->eng->adopt_csr();
+      *out = g;
+    } catch (...) {
+      free_csr(c);
+      throw;
+    }
+  });
+}
+
+int lbfs_graph_create_from_csr(const lbfs_csr* csr, int ngpus, lbfs_graph** out) {
+  return guarded([&] {
+    if (!csr || !out) throw_inval("bad arguments");
+    if (ngpus != 1) throw_inval("ngpus must be 1 (multi-GPU runs one process per GPU)");
+    LBFS_CUDA(cudaSetDevice(csr->c.device));
+    Csr c;
+    c.device = csr->c.device;
+    c.n = csr->c.n;
+    c.nnz = csr->c.nnz;
+    c.row_ptr = dev_alloc<int64_t>((size_t)c.n + 1);
+    c.col_idx = dev_alloc<int32_t>((size_t)c.nnz + 4);
+    try {
+      LBFS_CUDA(cudaMemcpy(c.row_ptr, csr->c.row_ptr, sizeof(int64_t) * (size_t)(c.n + 1),
+                           cudaMemcpyDeviceToDevice));
+      if (c.nnz > 0)
+        LBFS_CUDA(cudaMemcpy(c.col_idx, csr->c.col_idx, sizeof(int32_t) * (size_t)c.nnz,
+                             cudaMemcpyDeviceToDevice));
+      auto* g = new lbfs_graph;
+      g->eng = new BfsEngine(c);
+      g->eng->adopt_csr();
+      *out = g;
+    } catch (...) {
+      free_csr(c);
+      throw;
+    }
+  });
+}
+
+void lbfs_graph_destroy(lbfs_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->eng->device());
+  delete g->eng;
+  delete g;
+}
+
+int lbfs_graph_info(const lbfs_graph* g, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    if (!g) throw_inval("graph is NULL");
+    if (n) *n = g->eng->n();
+    if (nnz) *nnz = g->eng->nnz();
+  });
+}
+
+static void copy_layers(const BfsEngine& e, lbfs_layer* out, int64_t cap, int64_t* n_layers) {
+  const auto& L = e.layers();
+  if (n_layers) *n_layers = (int64_t)L.size();
+  if (out && cap > 0) {
+    const int64_t k = std::min<int64_t>(cap, (int64_t)L.size());
+    memcpy(out, L.data(), sizeof(lbfs_layer) * (size_t)k);
+  }
+}
+
+int lbfs_bfs(lbfs_graph* g, int64_t root, int32_t* pred_out, int32_t* level_out,
+             lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers, lbfs_timing* t_out) {
+  return guarded([&] {
+    if (!g) throw_inval("graph is NULL");
+    BfsEngine& e = *g->eng;
+    std::lock_guard<std::mutex> lk(e.mu);
+    LBFS_CUDA(cudaSetDevice(e.device()));
+    if (root < 0 || root >= e.n()) throw_inval("root out of range");
+    e.ensure_own_outputs();
+    lbfs_timing t{};
+    e.run(root, e.own_pred(), e.own_level(), &t);
+    cudaEvent_t a, b;
+    LBFS_CUDA(cudaEventCreate(&a));
+    LBFS_CUDA(cudaEventCreate(&b));
+    LBFS_CUDA(cudaEventRecord(a, e.stream()));
+    if (pred_out)
+      LBFS_CUDA(cudaMemcpyAsync(pred_out, e.own_pred(), sizeof(int32_t) * (size_t)e.npad(),
+                                cudaMemcpyDeviceToHost, e.stream()));
+    if (level_out)
+      LBFS_CUDA(cudaMemcpyAsync(level_out, e.own_level(), sizeof(int32_t) * (size_t)e.n(),
+                                cudaMemcpyDeviceToHost, e.stream()));
+    LBFS_CUDA(cudaEventRecord(b, e.stream()));
+    LBFS_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    LBFS_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    t.d2h_ms = ms;
+    if (t_out) *t_out = t;
+    copy_layers(e, layers_out, layers_cap, n_layers);
+  });
+}
+
+int lbfs_bfs_device(lbfs_graph* g, int64_t root, int32_t* d_pred, int32_t* d_level,
+                    lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers,
+                    lbfs_timing* t_out) {
+  return guarded([&] {
+    if (!g) throw_inval("graph is NULL");
+    if (!d_pred || !d_level) throw_inval("device outputs must be non-NULL");
+    BfsEngine& e = *g->eng;
+    std::lock_guard<std::mutex> lk(e.mu);
+    LBFS_CUDA(cudaSetDevice(e.device()));
+    if (root < 0 || root >= e.n()) throw_inval("root out of range");
+    lbfs_timing t{};
+    e.run(root, d_pred, d_level, &t);
+    if (t_out) *t_out = t;
+    copy_layers(e, layers_out, layers_cap, n_layers);
+  });
+}
+
+int lbfs_graph_last_layers(const lbfs_graph* g, lbfs_layer* out, int64_t cap, int64_t* n_layers) {
+  return guarded([&] {
+    if (!g) throw_inval("graph is NULL");
+    copy_layers(*g->eng, out, cap, n_layers);
+  });
+}
+
+}  // extern "C"

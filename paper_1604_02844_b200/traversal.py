@@ -1,0 +1,171 @@
+"""Top-down BFS on the B200: the drop-in for the reference traversal.py
+(/root/reference/pkg/src/lanebfs/traversal.py).
+
+``bfs(g, s)`` runs the sm_100a kernels of liblbfs (csrc/bfs.cu) through the
+C ABI and returns the reference's result types, so the reference's own
+``validate_tree`` and ``levels_from_parents`` accept its output unchanged:
+
+* ``predecessors``: PredecessorArray, int32 storage padded to a multiple of
+  32 with SENTINEL (traversal.py:30-50); root -> root, unreached -> SENTINEL;
+* ``layers``: one LayerStats(input, edges, discovered) per frontier,
+  including the last one (discovered == 0) (traversal.py:66-70, 100);
+* ``traversed_edge_count``: sum of layer edges = sum of degree over reached
+  vertices (traversal.py:104; the TEPS numerator, harness.py:269);
+* ``levels`` (new, gap G2): int32 BFS level per vertex, -1 = unreached.
+
+Predecessors are a valid BFS tree; which equal-level parent wins a vertex is
+decided by the device atomic, the benign race the reference documents
+(traversal.py:128-132). Levels and layers are deterministic.
+
+``run_bfs`` keeps the reference dispatch signature (traversal.py:413-422).
+Every mode names the same breadth-first search; here all of them run on the
+device (there is no CPU fallback).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+SENTINEL = 0x7FFFFFFF  # traversal.py:22
+BITS_PER_WORD = 32
+
+MODES = ("gpu", "serial", "parallel_naive", "parallel_restored", "vectorized")
+
+
+class PredecessorArray:
+    """Per-vertex parent ids, SENTINEL for unreached vertices; storage padded
+    to whole 32-entry words (traversal.py:30-50)."""
+
+    __slots__ = ("num_vertices", "storage")
+
+    infinity_sentinel = SENTINEL
+
+    def __init__(self, num_vertices: int, _fill: bool = True):
+        assert num_vertices >= 1
+        padded = (num_vertices + BITS_PER_WORD - 1) // BITS_PER_WORD * BITS_PER_WORD
+        self.num_vertices = num_vertices
+        self.storage = (np.full(padded, SENTINEL, dtype=np.int32) if _fill
+                        else np.empty(padded, dtype=np.int32))
+
+    @property
+    def p(self) -> np.ndarray:
+        return self.storage[:self.num_vertices]
+
+
+@dataclass(frozen=True)
+class LayerPolicy:
+    """Which variant runs (traversal.py:53-63). ``vectorized_layers`` is kept
+    for signature compatibility; the device path treats every layer alike."""
+
+    vectorized_layers: int = 2
+    mode: str = "gpu"
+
+    def __post_init__(self):
+        assert self.vectorized_layers >= 0
+        assert self.mode in MODES
+
+
+@dataclass(frozen=True)
+class LayerStats:
+    input: int       # frontier vertices entering the layer
+    edges: int       # adjacency entries examined
+    discovered: int  # vertices first reached in this layer
+
+
+@dataclass
+class BfsResult:
+    predecessors: PredecessorArray
+    layers: list[LayerStats] = field(default_factory=list)
+    traversed_edge_count: int = 0
+    levels: np.ndarray | None = None
+    timing: dict | None = None
+
+
+# ------------------------------------------------------------- graph handles
+_foreign: dict[int, tuple] = {}
+
+
+def _handle(g) -> int:
+    """Device BFS handle of g. Our CsrGraph owns its handle; a foreign graph
+    object (e.g. the reference's CsrGraph) is uploaded once and cached while
+    its arrays stay the same objects."""
+    if hasattr(g, "device_handle"):
+        return g.device_handle()
+    key = id(g)
+    rows, cs = g.rows, g.colstarts
+    ent = _foreign.get(key)
+    if ent is not None and ent[0] is rows and ent[1] is cs:
+        return ent[2]
+    lib = _lib.load()
+    if ent is not None:
+        lib.lbfs_graph_destroy(ent[2])
+        del _foreign[key]
+    while len(_foreign) >= 2:  # keep at most two foreign graphs resident
+        _, old = _foreign.popitem()
+        lib.lbfs_graph_destroy(old[2])
+    cs64 = np.ascontiguousarray(cs, dtype=np.int64)
+    r32 = np.ascontiguousarray(rows, dtype=np.int32)
+    h = ctypes.c_void_p()
+    _lib.check(lib.lbfs_graph_create(int(g.num_vertices), _lib.ptr(cs64), _lib.ptr(r32) if len(r32) else None,
+                                     len(r32), 1, ctypes.byref(h)))
+    _foreign[key] = (rows, cs, h.value)
+    return h.value
+
+
+def _layers_from(buf, k: int, h: int) -> list[LayerStats]:
+    if k > len(buf):
+        buf = (_lib.Layer * k)()
+        n = ctypes.c_int64()
+        _lib.check(_lib.load().lbfs_graph_last_layers(h, buf, k, ctypes.byref(n)))
+    return [LayerStats(int(buf[i].input), int(buf[i].edges), int(buf[i].discovered)) for i in range(k)]
+
+
+_LAYER_CAP = 256
+
+
+def bfs(g, s: int) -> BfsResult:
+    """Top-down BFS from s on the device; host outputs (one D2H copy of the
+    predecessor and level arrays inside the call)."""
+    n = g.num_vertices
+    assert 0 <= s < n
+    h = _handle(g)
+    pred = PredecessorArray(n, _fill=False)
+    levels = np.empty(n, dtype=np.int32)
+    buf = (_lib.Layer * _LAYER_CAP)()
+    k = ctypes.c_int64()
+    t = _lib.Timing()
+    _lib.check(_lib.load().lbfs_bfs(h, int(s), _lib.ptr(pred.storage), _lib.ptr(levels), buf, _LAYER_CAP,
+                                    ctypes.byref(k), ctypes.byref(t)))
+    layers = _layers_from(buf, k.value, h)
+    return BfsResult(pred, layers, int(t.edges), levels, t.as_dict())
+
+
+def bfs_device(g, s: int, pred_out, level_out) -> BfsResult:
+    """BFS into device buffers (anything with ``data_ptr()``, e.g. torch CUDA
+    int32 tensors of pad32(n) and n entries). No host copy of the outputs;
+    ``predecessors`` of the result is None."""
+    n = g.num_vertices
+    assert 0 <= s < n
+    padded = (n + BITS_PER_WORD - 1) // BITS_PER_WORD * BITS_PER_WORD
+    assert pred_out.numel() >= padded and level_out.numel() >= n
+    h = _handle(g)
+    buf = (_lib.Layer * _LAYER_CAP)()
+    k = ctypes.c_int64()
+    t = _lib.Timing()
+    _lib.check(_lib.load().lbfs_bfs_device(h, int(s), pred_out.data_ptr(), level_out.data_ptr(), buf,
+                                           _LAYER_CAP, ctypes.byref(k), ctypes.byref(t)))
+    return BfsResult(None, _layers_from(buf, k.value, h), int(t.edges), None, t.as_dict())
+
+
+def run_bfs(g, s: int, policy: LayerPolicy | None = None, threads: int = 1,
+            backend=None, chunked: bool = False) -> BfsResult:
+    """Reference dispatch signature (traversal.py:413-422). All modes run the
+    device BFS; ``threads``/``backend``/``chunked`` have no device meaning."""
+    policy = policy or LayerPolicy()
+    assert policy.mode in MODES and threads >= 1
+    return bfs(g, s)

@@ -1,0 +1,93 @@
+"""The BASELINE.json configs on the device, against the reference's golden
+vectors (S16, S20, lattices) and the pinned oracle at full size (S24)."""
+
+import numpy as np
+import pytest
+
+import oracle
+from _util import sha
+from paper_1604_02844_b200 import RmatParams, bfs, build_lattice_graph, build_rmat_graph, pick_roots
+
+pytestmark = pytest.mark.gpu
+
+
+def layers_of(res):
+    return [[l.input, l.edges, l.discovered] for l in res.layers]
+
+
+def test_config_s16_all_roots_bit_exact(golden, golden_arrays):
+    # configs[0]: SCALE 16, 8 roots; levels bit-exact vs the reference's bfs_serial
+    info = golden["S16"]
+    g = build_rmat_graph(RmatParams(scale=16, seed=1))
+    assert pick_roots(g, 8, 1, filter_unconnected=True).tolist() == info["roots"]
+    for r, want in info["bfs"].items():
+        res = bfs(g, int(r))
+        assert np.array_equal(res.levels, golden_arrays[f"S16_levels_{r}"].astype(np.int32))
+        assert layers_of(res) == want["layers"]
+        assert res.traversed_edge_count == want["edges"]
+        code, where = oracle.check_bfs(g.colstarts, g.rows, int(r), res.predecessors.p, res.levels)
+        assert code == 0, (oracle.CHECK_CODES[code], where)
+
+
+def test_config_s20_64_roots(golden):
+    info = golden["S20"]
+    g = build_rmat_graph(RmatParams(scale=20, seed=1))
+    rp, ci = g.colstarts, g.rows
+    roots = pick_roots(g, 64, 1, filter_unconnected=True).tolist()
+    assert roots == info["roots"]
+    for r in roots:
+        res = bfs(g, r)
+        want = info["bfs"].get(str(r))
+        if want:
+            assert layers_of(res) == want["layers"]
+            assert sha(res.levels, "<i4") == want["levels_sha"]
+        code, where = oracle.check_bfs(rp, ci, r, res.predecessors.p, res.levels)
+        assert code == 0, (r, oracle.CHECK_CODES[code], where)
+    # 8 roots against the oracle's own levels
+    for r in roots[:8]:
+        _, lvl, layers = oracle.bfs_parallel(rp, ci, r)
+        res = bfs(g, r)
+        assert np.array_equal(res.levels, lvl) and layers_of(res) == [list(x) for x in layers]
+
+
+def test_config_lattice_small(golden):
+    info = golden["lattice_64x48"]
+    g = build_lattice_graph(64, 48)
+    for r, want in info["bfs"].items():
+        res = bfs(g, int(r))
+        assert layers_of(res) == want["layers"]
+        assert sha(res.levels, "<i4") == want["levels_sha"]
+
+
+def test_config_lattice_4096(golden):
+    info = golden["lattice_4096x4096"]
+    g = build_lattice_graph(4096, 4096)
+    rp, ci = g.colstarts, g.rows
+    roots = pick_roots(g, 16, 1, filter_unconnected=True).tolist()
+    assert roots == info["roots"]
+    for r, want in info["bfs"].items():
+        res = bfs(g, int(r))
+        assert layers_of(res) == want["layers"]
+        assert oracle.check_bfs(rp, ci, int(r), res.predecessors.p, res.levels) == (0, -1)
+    r = roots[5]
+    res = bfs(g, r)
+    _, lvl, layers = oracle.bfs_parallel(rp, ci, r)
+    assert np.array_equal(res.levels, lvl) and layers_of(res) == [list(x) for x in layers]
+
+
+def test_config_s24_against_oracle(golden):
+    g = build_rmat_graph(RmatParams(scale=24, seed=1))
+    rp, ci = g.colstarts, g.rows
+    roots = pick_roots(g, 64, 1, filter_unconnected=True).tolist()
+    info = golden.get("S24")
+    if info:
+        assert roots == info["roots"]
+    for r in roots[:3]:
+        res = bfs(g, r)
+        _, lvl, layers = oracle.bfs_parallel(rp, ci, r)
+        assert np.array_equal(res.levels, lvl)
+        assert layers_of(res) == [list(x) for x in layers]
+        assert oracle.check_bfs(rp, ci, r, res.predecessors.p, res.levels) == (0, -1)
+        if info and str(r) in info["bfs"]:
+            assert layers_of(res) == info["bfs"][str(r)]["layers"]
+            assert sha(res.levels, "<i4") == info["bfs"][str(r)]["levels_sha"]

@@ -1,0 +1,111 @@
+"""Device graph construction vs the reference (golden) and the oracle:
+generate_rmat bit-exact (graph.py:68-85), build_csr exact (graph.py:139-160),
+the seeded permutation and the lattice."""
+
+import numpy as np
+import pytest
+
+import oracle
+from _util import pairs_arrays, sha
+from paper_1604_02844_b200 import (
+    EdgeList,
+    RmatParams,
+    build_csr,
+    build_lattice_graph,
+    build_rmat_graph,
+    generate_rmat,
+    lattice_edges,
+    permute_vertices,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def test_generate_rmat_bit_exact(golden, golden_arrays):
+    for item in golden["rmat_small"]:
+        e = generate_rmat(RmatParams(scale=item["scale"], edgefactor=item["edgefactor"], seed=item["seed"]))
+        assert sha(e.src, "<u4") == item["src_sha"] and sha(e.dst, "<u4") == item["dst_sha"], item
+    for cfg in ("S16", "S20"):
+        info = golden[cfg]
+        e = generate_rmat(RmatParams(scale=int(cfg[1:]), seed=1))
+        assert sha(e.src, "<u4") == info["src_sha"] and sha(e.dst, "<u4") == info["dst_sha"]
+
+
+def test_generate_rmat_odd_sizes_match_oracle():
+    # m not a multiple of the 32-pair thread tile; extreme probabilities
+    for scale, ef, abcd in [(3, 3, (0.57, 0.19, 0.19, 0.05)), (5, 7, (0.25, 0.25, 0.25, 0.25)),
+                            (6, 1, (1.0, 0.0, 0.0, 0.0)), (4, 5, (0.0, 0.0, 0.0, 1.0))]:
+        p = RmatParams(scale=scale, edgefactor=ef, a=abcd[0], b=abcd[1], c=abcd[2], d=abcd[3], seed=9)
+        e = generate_rmat(p)
+        s, d = oracle.rmat_edges(scale, ef, *abcd, seed=9)
+        assert np.array_equal(e.src, s) and np.array_equal(e.dst, d), p
+
+
+def test_permutation_matches_oracle():
+    for n in (1, 7, 33, 1000, 1 << 16, (1 << 16) + 3):
+        rng = np.random.default_rng(n)
+        s = rng.integers(0, n, 5000).astype(np.uint32)
+        d = rng.integers(0, n, 5000).astype(np.uint32)
+        e = permute_vertices(EdgeList(s, d, n), 123)
+        os_, od = oracle.permute_edges(n, 123, s, d)
+        assert np.array_equal(e.src, os_) and np.array_equal(e.dst, od)
+
+
+def test_build_csr_small_all_flags(golden):
+    for name, g in golden["small"].items():
+        s, d = pairs_arrays(g["pairs"])
+        for key, want in g["csr"].items():
+            sym, dd = bool(int(key[0])), bool(int(key[1]))
+            csr = build_csr(EdgeList(s, d, g["n"]), sym, dd)
+            assert csr.colstarts.tolist() == want["colstarts"], (name, key)
+            assert csr.rows.tolist() == want["rows"], (name, key)
+
+
+def test_build_csr_rmat_small(golden):
+    for item in golden["rmat_small"]:
+        p = RmatParams(scale=item["scale"], edgefactor=item["edgefactor"], seed=item["seed"])
+        g = build_csr(generate_rmat(p))
+        assert g.num_edges == item["nnz"]
+        assert sha(g.colstarts, "<i8") == item["colstarts_sha"] and sha(g.rows, "<i4") == item["rows_sha"]
+        g2 = build_rmat_graph(p, permute=False)
+        assert np.array_equal(g2.colstarts, g.colstarts) and np.array_equal(g2.rows, g.rows)
+
+
+@pytest.mark.parametrize("cfg", ["S16", "S20"])
+def test_build_rmat_graph_configs(golden, cfg):
+    info = golden[cfg]
+    g = build_rmat_graph(RmatParams(scale=int(cfg[1:]), seed=1))
+    assert g.num_edges == info["nnz"]
+    assert sha(g.colstarts, "<i8") == info["colstarts_sha"] and sha(g.rows, "<i4") == info["rows_sha"]
+
+
+def test_build_lattice_graphs(golden):
+    for key in ("lattice_64x48", "lattice_4096x4096"):
+        info = golden[key]
+        g = build_lattice_graph(info["rows"], info["cols"], permute=True, perm_seed=1)
+        assert g.num_edges == info["nnz"]
+        assert sha(g.colstarts, "<i8") == info["colstarts_sha"] and sha(g.rows, "<i4") == info["rows_sha"]
+    e = lattice_edges(64, 48)
+    assert sha(e.src, "<u4") == golden["lattice_64x48"]["src_sha"]
+
+
+def test_build_rmat_s24_properties(golden):
+    # full-size construction: structural properties (+ hashes when pinned)
+    g = build_rmat_graph(RmatParams(scale=24, seed=1))
+    cs, rows = g.colstarts, g.rows
+    n = 1 << 24
+    assert len(cs) == n + 1 and cs[0] == 0 and cs[-1] == len(rows)
+    info = golden.get("S24")
+    if info:
+        assert g.num_edges == info["nnz"]
+        assert sha(cs, "<i8") == info["colstarts_sha"] and sha(rows, "<i4") == info["rows_sha"]
+    else:
+        assert g.num_edges == 520763812  # SURVEY G7 [measured with the reference]
+    # symmetric, sorted, no self loops: check on a sample of rows
+    rng = np.random.default_rng(0)
+    for u in rng.integers(0, n, 200):
+        a = rows[cs[u]:cs[u + 1]]
+        assert (np.diff(a) > 0).all() and not (a == u).any()
+        for v in a[:5]:
+            b = rows[cs[v]:cs[v + 1]]
+            assert u in b
