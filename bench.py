@@ -1,0 +1,327 @@
+"""bench.py — GTEPS of the device top-down BFS on R-MAT SCALE 24 (BASELINE.json
+configs[2]: the single-GPU target config and the one sharded at 2/4/8 GPUs).
+
+One step = one BFS from each of the 64 seeded roots (pick_roots(g, 64, seed=1,
+filter_unconnected=True), harness.py:237-246) over the device-resident graph.
+value = harmonic mean over all timed BFS runs of traversed_edge_count / t_bfs
+(harness.py:218-234, 269), t_bfs from CUDA events on the BFS stream (init
+kernel start -> end of the last level). e2e = the same metric through the
+public API bfs(g, root) with host outputs (D2H of pred + level inside the
+call), timed per call like the reference harness (harness.py:263-265).
+
+--impl reference: rank 0 times the reference's CPU path (the oracle port of
+bfs_parallel_naive, traversal.py:128-165, OpenMP over all host cores) on the
+same graph built by the oracle, a bounded sample of roots per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GTEPS (harmonic mean over 64 roots) and % of HBM roofline at 1/2/4/8 B200"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--roots", type=int, default=64)
+    ap.add_argument("--e2e-roots", type=int, default=16, help="roots per step timed through bfs()")
+    ap.add_argument("--cpu-roots", type=int, default=2, help="roots in the CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def hm(values):
+    from paper_1604_02844_b200 import harmonic_mean_teps
+
+    return harmonic_mean_teps(values)[0]
+
+
+def traffic_from_profiles():
+    p = ROOT / "profiles" / "roofline_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return None
+    return None
+
+
+def cpu_baseline_sample(rp, ci, roots, k):
+    """Oracle port of bfs_parallel_naive on all host cores (rank 0, N=1)."""
+    import oracle
+
+    vals = []
+    threads = oracle.max_threads()
+    t_all = time.perf_counter()
+    for r in roots[:k]:
+        t0 = time.perf_counter()
+        pred, lvl, layers = oracle.bfs_parallel(rp, ci, int(r), 0)
+        dt = time.perf_counter() - t0
+        e = sum(l[1] for l in layers)
+        vals.append(e / dt / 1e9 if e else 0.0)
+    return vals, threads, time.perf_counter() - t_all
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+
+    t0 = time.perf_counter()
+    s, d = oracle.rmat_edges(args.scale, 16, seed=1)
+    s, d = oracle.permute_edges(1 << args.scale, 1, s, d)
+    rp, ci = oracle.build_csr(1 << args.scale, s, d)
+    del s, d
+    build_s = time.perf_counter() - t0
+    roots = oracle.pick_roots(np.diff(rp), args.roots, 1, True).tolist()
+    threads = oracle.max_threads()
+    per_step = max(1, args.cpu_roots)
+    vals, step_times = [], []
+    cursor = 0
+    for step in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        step_vals = []
+        for _ in range(per_step):
+            r = roots[cursor % len(roots)]
+            cursor += 1
+            a = time.perf_counter()
+            _, _, layers = oracle.bfs_parallel(rp, ci, int(r), 0)
+            dt = time.perf_counter() - a
+            e = sum(l[1] for l in layers)
+            step_vals.append(e / dt / 1e9 if e else 0.0)
+        if step >= args.warmup:
+            vals += step_vals
+            step_times.append(time.perf_counter() - t)
+    value = hm(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(step_times) / len(step_times), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"rmat-s{args.scale}-ef16-{args.roots}roots", "scale": args.scale,
+                   "edgefactor": 16, "roots": args.roots, "n": len(rp) - 1, "nnz": int(rp[-1]),
+                   "parallelism": f"cpu-openmp-{threads}t", "graph_build_s": round(build_s, 1)},
+        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads, "kind": "port",
+                         "sample": f"{per_step} roots per step of the {args.roots}-root set, oracle "
+                                   "bfs_parallel (restated bfs_parallel_naive, traversal.py:128-165)"},
+        "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    from paper_1604_02844_b200 import RmatParams, _lib, bfs, bfs_device, build_rmat_graph, pick_roots
+    from paper_1604_02844_b200.validate import validate_tree
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t0 = time.perf_counter()
+    g = build_rmat_graph(RmatParams(scale=args.scale, seed=1))
+    n, nnz = g.num_vertices, g.num_edges
+    roots = pick_roots(g, args.roots, 1, filter_unconnected=True).tolist()
+    g.device_handle()
+    build_s = time.perf_counter() - t0
+    npad = (n + 31) // 32 * 32
+    pred = torch.empty(npad, dtype=torch.int32, device="cuda")
+    lvl = torch.empty(n, dtype=torch.int32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        out = []
+        for r in roots:
+            res = bfs_device(g, r, pred, lvl)
+            out.append(res)
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    hbm_gbs, peak_kind = peaks()
+    launches0 = _lib.kernel_launch_count()
+    barrier()
+    w0 = time.perf_counter()
+    results = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            results.append(step())
+        barrier()
+    wall = time.perf_counter() - w0
+    launches = _lib.kernel_launch_count() - launches0
+    runs = [r for s in results for r in s]
+    teps = [r.traversed_edge_count / (r.timing["bfs_ms"] * 1e-3) / 1e9 if r.traversed_edge_count else 0.0
+            for r in runs]
+    dev_ms = sum(r.timing["bfs_ms"] for r in runs)
+    value_local = hm(teps)
+    ms_step_local = dev_ms / args.steps
+    # roofline of the dominant kernel (level expansion), SURVEY §8(d):
+    # expansion bytes per BFS = 8E (col_idx + bitmap probe) + 40V; init = 8n + n/8
+    exp_bytes = sum(8 * r.traversed_edge_count + 40 * r.timing["reached"] for r in runs)
+    exp_ms = sum(r.timing["expand_ms"] for r in runs)
+    exp_launches = sum(r.timing["kernel_launches"] - 2 for r in runs)
+    alg_bytes = sum(8 * r.traversed_edge_count + 40 * r.timing["reached"] + 8 * n + n // 8 for r in runs)
+    bfs_ms = sum(r.timing["bfs_ms"] for r in runs)
+
+    # e2e through the public API with host outputs (D2H inside the call)
+    e2e_vals = []
+    for r in roots[:args.e2e_roots]:
+        a = time.perf_counter()
+        res = bfs(g, r)
+        dt = time.perf_counter() - a
+        e2e_vals.append(res.traversed_edge_count / dt / 1e9 if res.traversed_edge_count else 0.0)
+    e2e = hm(e2e_vals)
+    d2h_bytes = (npad + n) * 4 * args.roots
+    # correctness of the timed configuration (outside the timed region)
+    chk = bfs(g, roots[0])
+    ok = validate_tree(g, roots[0], chk.predecessors).passed
+
+    value, ms_step = value_local, ms_step_local
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms_step_local], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+        # replicas: every rank processes the full root set; aggregate throughput
+        edges_total = sum(r.traversed_edge_count for r in runs) / args.steps
+        value = world * edges_total / (ms_step * 1e-3) / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rp, ci = g.colstarts, g.rows
+        vals, thr, secs = cpu_baseline_sample(rp, ci, roots, args.cpu_roots)
+        cpu = {"value": hm(vals), "unit": "GTEPS", "cores": thr, "kind": "port",
+               "sample": f"{len(vals)} of the {args.roots} roots on the same graph, oracle bfs_parallel "
+                         f"(OpenMP restatement of bfs_parallel_naive), {secs:.1f}s"}
+    traffic = traffic_from_profiles()
+    achieved = exp_bytes / (exp_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic: R-MAT (reference generator, bit-exact) + seeded permutation",
+        "config": {"workload": f"rmat-s{args.scale}-ef16-{args.roots}roots", "scale": args.scale,
+                   "edgefactor": 16, "roots": args.roots, "n": n, "nnz": nnz,
+                   "parallelism": "1gpu" if world == 1 else f"replicas{world}",
+                   "l2": "inputs larger than L2 (CSR %.2f GB vs 126 MB L2); no flush" % ((8 * n + 4 * nnz) / 1e9),
+                   "graph_build_s": round(build_s, 2), "validated": ok},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
+                     "frac": achieved / hbm_gbs, "peak_kind": peak_kind,
+                     "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                     "kernel": "k_expand_* (level expansion, all bins)",
+                     "alg_bytes_per_launch": exp_bytes / max(exp_launches, 1),
+                     "launch_ms": exp_ms / max(exp_launches, 1),
+                     "whole_bfs": {"alg_bytes": alg_bytes / len(runs), "ms": bfs_ms / len(runs),
+                                   "frac_of_peak": alg_bytes / (bfs_ms * 1e-3) / 1e9 / hbm_gbs,
+                                   "frac_of_8TBs": alg_bytes / (bfs_ms * 1e-3) / 8e12}},
+        "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 8 * args.roots,
+                "d2h_bytes_per_step": d2h_bytes, "api": "paper_1604_02844_b200.bfs(g, root), host outputs",
+                "roots_timed": len(e2e_vals)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "wall_s_timed": wall,
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

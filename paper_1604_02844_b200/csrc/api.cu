@@ -245,7 +245,7 @@ int lbfs_graph_create(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
     if (!out || !row_ptr || nnz < 0 || (nnz > 0 && !col_idx)) throw_inval("bad arguments");
     if (ngpus != 1) throw_inval("ngpus must be 1 (multi-GPU runs one process per GPU)");
     if (row_ptr[0] != 0 || row_ptr[n] != nnz) throw_inval("row_ptr must start at 0 and end at nnz");
-    Csr c;
+    Csr c;  // temporary upload in original ids; the engine keeps its own layout
     LBFS_CUDA(cudaGetDevice(&c.device));
     c.n = n;
     c.nnz = nnz;
@@ -256,13 +256,18 @@ int lbfs_graph_create(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
       if (nnz > 0)
         LBFS_CUDA(cudaMemcpy(c.col_idx, col_idx, sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice));
       auto* g = new lbfs_graph;
-      g->eng = new BfsEngine(c);
-      g->eng->adopt_csr();
+      try {
+        g->eng = new BfsEngine(c);
+      } catch (...) {
+        delete g;
+        throw;
+      }
       *out = g;
     } catch (...) {
       free_csr(c);
       throw;
     }
+    free_csr(c);
   });
 }
 
@@ -271,26 +276,14 @@ int lbfs_graph_create_from_csr(const lbfs_csr* csr, int ngpus, lbfs_graph** out)
     if (!csr || !out) throw_inval("bad arguments");
     if (ngpus != 1) throw_inval("ngpus must be 1 (multi-GPU runs one process per GPU)");
     LBFS_CUDA(cudaSetDevice(csr->c.device));
-    Csr c;
-    c.device = csr->c.device;
-    c.n = csr->c.n;
-    c.nnz = csr->c.nnz;
-    c.row_ptr = dev_alloc<int64_t>((size_t)c.n + 1);
-    c.col_idx = dev_alloc<int32_t>((size_t)c.nnz + 4);
+    auto* g = new lbfs_graph;
     try {
-      LBFS_CUDA(cudaMemcpy(c.row_ptr, csr->c.row_ptr, sizeof(int64_t) * (size_t)(c.n + 1),
-                           cudaMemcpyDeviceToDevice));
-      if (c.nnz > 0)
-        LBFS_CUDA(cudaMemcpy(c.col_idx, csr->c.col_idx, sizeof(int32_t) * (size_t)c.nnz,
-                             cudaMemcpyDeviceToDevice));
-      auto* g = new lbfs_graph;
-      g->eng = new BfsEngine(c);
-      g->eng->adopt_csr();
-      *out = g;
+      g->eng = new BfsEngine(csr->c);
     } catch (...) {
-      free_csr(c);
+      delete g;
       throw;
     }
+    *out = g;
   });
 }
 

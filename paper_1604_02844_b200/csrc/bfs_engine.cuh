@@ -1,4 +1,12 @@
 // BFS engine: device layout of one graph and the level driver.
+//
+// Layout (built once per graph): vertices are relabelled in
+// descending-degree order ("internal ids"). The visited bitmap, frontier
+// bins and the traversal CSR use internal ids; predecessor and level outputs
+// are written in the caller's (original) ids through new2old. With this
+// order the degree bins are id ranges and the visited words of the hubs —
+// the targets of most probes in a power-law graph — are a small prefix of
+// the bitmap that stays resident in L1.
 #pragma once
 
 #include "lbfs_internal.cuh"
@@ -7,41 +15,76 @@ namespace lbfs {
 
 constexpr int32_t kSentinel = LBFS_SENTINEL;  // traversal.py:22
 constexpr int kSmallMax = 32;                 // deg < 32: warp-cooperative small bin
-constexpr int kCtaMin = 4096;                 // deg >= 4096: CTA bin
-constexpr int kChunk = 4096;                  // edges per CTA-bin work item
+constexpr int kCtaMin = 1024;                 // deg >= 1024: CTA bin (TMA-staged chunks)
+constexpr int kChunk = 4096;                  // edges per CTA-bin item
 constexpr int kBinSmall = 0, kBinWarp = 1, kBinCta = 2;
 constexpr int kCounterRing = 3;
+constexpr int kExpandThreads = 256;
 
-// Per-level counters (K6). `discovered`/`edges` of level L+1's slot are
-// layers[L].discovered and layers[L+1].edges.
+// Per-level counters (K6). Slot L holds the frontier of level L:
+// discovered = |frontier| (layers[L].input), edges = sum of its degrees
+// (layers[L].edges); bin[] are the bin sizes (entries / items).
 struct alignas(64) Counters {
-  unsigned long long bin[3];  // next-level bin tails (entries / items)
+  unsigned long long bin[3];
   unsigned long long discovered;
-  unsigned long long edges;   // sum of degree over discovered vertices
+  unsigned long long edges;
   unsigned long long pad[3];
 };
 
+struct CtaItem {  // one kChunk-edge slice of a hub's row
+  int32_t v;      // internal id
+  int32_t off;    // offset of the slice in the row
+  int32_t len;    // <= kChunk
+  int32_t v_orig; // original id (the parent id written to pred)
+};
+
+struct Frontier {
+  const int32_t* small;
+  const int32_t* warp;
+  const CtaItem* cta;
+  int64_t n_small, n_warp, n_cta;
+};
+
 struct LevelArgs {
-  const int64_t* row_ptr;
+  const int64_t* row_ptr;   // internal CSR
   const int32_t* col_idx;
+  const int32_t* new2old;
   uint32_t* visited;
-  int32_t* pred;
+  uint32_t* prev;           // visited at the last bitmap-mode boundary
+  int32_t* pred;            // original-id outputs
   int32_t* level;
   int32_t next_level;
+  int32_t t_cta, t_warp, t_nz;  // internal-id bin boundaries
+  // queue-mode outputs (direct append by the winners)
   Counters* next_cnt;
   int32_t* next_small;
   int32_t* next_warp;
-  int4* next_cta;
+  CtaItem* next_cta;
+};
+
+struct CompactArgs {
+  const int64_t* row_ptr;
+  const int32_t* new2old;
+  const uint32_t* visited;
+  uint32_t* prev;           // visited at the previous level boundary
+  int64_t nwords;
+  int32_t* level;
+  int32_t next_level;
+  int32_t t_cta, t_warp, t_nz;
+  Counters* next_cnt;
+  int32_t* next_small;
+  int32_t* next_warp;
+  CtaItem* next_cta;
 };
 
 class BfsEngine {
  public:
-  explicit BfsEngine(const Csr& csr);  // borrows csr arrays (see adopt_csr)
+  // Builds the internal layout from a device CSR in original ids (not kept).
+  explicit BfsEngine(const Csr& csr);
   ~BfsEngine();
   BfsEngine(const BfsEngine&) = delete;
   BfsEngine& operator=(const BfsEngine&) = delete;
 
-  void adopt_csr();  // take ownership of the borrowed CSR arrays
   void ensure_own_outputs();
   // BFS into device buffers d_pred[pad32(n)], d_level[n]; synchronous.
   void run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t);
@@ -58,23 +101,29 @@ class BfsEngine {
   std::mutex mu;
 
  private:
+  void build_layout(const Csr& csr);
+
   int device_ = 0, sm_count_ = 0;
   int64_t n_ = 0, nnz_ = 0, nwords_ = 0, npad_ = 0;
-  int64_t* row_ptr_ = nullptr;
+  int64_t* row_ptr_ = nullptr;   // internal CSR
   int32_t* col_idx_ = nullptr;
-  bool owns_csr_ = false;
+  int32_t* new2old_ = nullptr;
+  int32_t* old2new_ = nullptr;
+  int32_t t_cta_ = 0, t_warp_ = 0, t_nz_ = 0;
   uint32_t* visited_ = nullptr;
+  uint32_t* prev_ = nullptr;
   int32_t* q_small_[2] = {nullptr, nullptr};
   int32_t* q_warp_[2] = {nullptr, nullptr};
-  int4* q_cta_[2] = {nullptr, nullptr};
-  int64_t cap_small_ = 0, cap_warp_ = 0, cap_cta_ = 0;
+  CtaItem* q_cta_[2] = {nullptr, nullptr};
+  int64_t cap_cta_ = 0;
   Counters* cnt_ = nullptr;
   Counters* h_cnt_ = nullptr;
   int32_t* own_pred_ = nullptr;
   int32_t* own_level_ = nullptr;
   cudaStream_t stream_ = nullptr;
-  cudaEvent_t ev_[5] = {};
+  cudaEvent_t ev_[6] = {};
   std::vector<lbfs_layer> layers_;
+  int expand_grid_ = 0;
 };
 
 }  // namespace lbfs

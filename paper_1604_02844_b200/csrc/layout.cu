@@ -1,0 +1,154 @@
+// Traversal layout of a graph (built once, not timed — the analogue of the
+// reference's 64-byte-aligned CsrGraph arrays, graph.py:88-93).
+//
+// Vertices are relabelled by descending degree (ties by original id), rows
+// are gathered in that order with neighbours mapped to internal ids and
+// sorted ascending. Bins become id ranges [0,t_cta) / [t_cta,t_warp) /
+// [t_warp,t_nz), and the visited words of high-degree vertices, which
+// receive most probes, form a small bitmap prefix.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
+
+#include "bfs_engine.cuh"
+
+namespace lbfs {
+
+__global__ void k_degree_keys(const int64_t* __restrict__ rp, int64_t n, uint32_t* __restrict__ key,
+                              int32_t* __restrict__ ids) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = rp[v + 1] - rp[v];
+    key[v] = 0x7FFFFFFFu - (uint32_t)d;  // ascending key == descending degree
+    ids[v] = (int32_t)v;
+  }
+}
+
+__global__ void k_invert(const int32_t* __restrict__ new2old, int64_t n, int32_t* __restrict__ old2new,
+                         const uint32_t* __restrict__ key, int64_t* __restrict__ deg64) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    old2new[new2old[i]] = (int32_t)i;
+    deg64[i] = (int64_t)(0x7FFFFFFFu - key[i]);
+  }
+}
+
+// thresholds over the descending degree sequence: t = #vertices with deg >= X
+__global__ void k_thresholds(const int64_t* __restrict__ deg, int64_t n, int32_t* __restrict__ t3) {
+  const int64_t X[3] = {kCtaMin, kSmallMax, 1};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int k = 0; k < 3; ++k) {
+      const bool here = deg[i] >= X[k];
+      const bool next = (i + 1 < n) && deg[i + 1] >= X[k];
+      if (here && !next) t3[k] = (int32_t)(i + 1);
+    }
+  }
+}
+
+// warp per internal row: gather the original row, map neighbours to internal ids
+__global__ void k_gather_rows(const int64_t* __restrict__ old_rp, const int32_t* __restrict__ old_ci,
+                              const int64_t* __restrict__ new_rp, const int32_t* __restrict__ new2old,
+                              const int32_t* __restrict__ old2new, int64_t n, int32_t* __restrict__ new_ci) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const int64_t o = new2old[r];
+    const int64_t src = old_rp[o], len = old_rp[o + 1] - src, dst = new_rp[r];
+    for (int64_t k = lane; k < len; k += 32) new_ci[dst + k] = old2new[old_ci[src + k]];
+  }
+}
+
+struct SubBase {
+  int64_t base;
+  __host__ __device__ int operator()(int64_t x) const { return (int)(x - base); }
+};
+
+static unsigned grid_of(int64_t work, int threads = 256) {
+  const int64_t cap = (int64_t)current_sm_count() * 32;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + threads - 1) / threads, cap));
+}
+
+void BfsEngine::build_layout(const Csr& csr) {
+  cudaStream_t st = stream_;
+  const int64_t n = csr.n;
+  // 1. degree-descending order
+  uint32_t* key = dev_alloc<uint32_t>((size_t)n);
+  uint32_t* key_s = dev_alloc<uint32_t>((size_t)n);
+  int32_t* ids = dev_alloc<int32_t>((size_t)n);
+  new2old_ = dev_alloc<int32_t>((size_t)n);
+  old2new_ = dev_alloc<int32_t>((size_t)n);
+  LBFS_LAUNCH(k_degree_keys, grid_of(n), 256, 0, st, csr.row_ptr, n, key, ids);
+  size_t tmp_bytes = 0;
+  LBFS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key_s, ids, new2old_, n, 0, 32, st));
+  void* tmp = dev_alloc<uint8_t>(tmp_bytes);
+  LBFS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_s, ids, new2old_, n, 0, 32, st));
+  LBFS_CUDA(cudaStreamSynchronize(st));
+  dev_free(tmp);
+  dev_free(key);
+  dev_free(ids);
+  // 2. inverse map, internal degrees, row_ptr
+  int64_t* deg64 = dev_alloc<int64_t>((size_t)n + 1);
+  LBFS_LAUNCH(k_invert, grid_of(n), 256, 0, st, new2old_, n, old2new_, key_s, deg64);
+  LBFS_CUDA(cudaMemsetAsync(deg64 + n, 0, sizeof(int64_t), st));
+  int32_t* d_t3 = dev_alloc<int32_t>(3);
+  LBFS_CUDA(cudaMemsetAsync(d_t3, 0, 3 * sizeof(int32_t), st));
+  LBFS_LAUNCH(k_thresholds, grid_of(n), 256, 0, st, deg64, n, d_t3);
+  int32_t h_t3[3];
+  LBFS_CUDA(cudaMemcpyAsync(h_t3, d_t3, sizeof(h_t3), cudaMemcpyDeviceToHost, st));
+  row_ptr_ = dev_alloc<int64_t>((size_t)n + 1);
+  tmp_bytes = 0;
+  LBFS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, deg64, row_ptr_, n + 1, st));
+  tmp = dev_alloc<uint8_t>(tmp_bytes);
+  LBFS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, deg64, row_ptr_, n + 1, st));
+  LBFS_CUDA(cudaStreamSynchronize(st));
+  dev_free(tmp);
+  dev_free(deg64);
+  dev_free(key_s);
+  dev_free(d_t3);
+  t_cta_ = h_t3[0];
+  t_warp_ = std::max(h_t3[1], t_cta_);
+  t_nz_ = std::max(h_t3[2], t_warp_);
+  // 3. gather + map rows (16-byte aligned base, padded for int4 over-reads)
+  col_idx_ = dev_alloc<int32_t>((size_t)nnz_ + 8);
+  int32_t* unsorted = dev_alloc<int32_t>((size_t)nnz_ + 8);
+  LBFS_LAUNCH(k_gather_rows, grid_of(n * 32), 256, 0, st, csr.row_ptr, csr.col_idx, row_ptr_, new2old_,
+              old2new_, n, unsorted);
+  // 4. sort every row ascending; CUB's segmented sort takes int sizes, so go
+  //    in row ranges of < 2^30 entries
+  std::vector<int64_t> h_rp((size_t)n + 1);
+  LBFS_CUDA(cudaMemcpyAsync(h_rp.data(), row_ptr_, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost, st));
+  LBFS_CUDA(cudaStreamSynchronize(st));
+  const int64_t kMaxItems = (int64_t)1 << 30;
+  int64_t r0 = 0;
+  while (r0 < n) {
+    int64_t r1 = r0 + 1;
+    // extend the range while it stays below kMaxItems entries (binary search)
+    int64_t lo = r0 + 1, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) / 2;
+      if (h_rp[mid] - h_rp[r0] <= kMaxItems) lo = mid; else hi = mid - 1;
+    }
+    r1 = std::max(lo, r0 + 1);
+    const int64_t base = h_rp[r0];
+    const int items = (int)(h_rp[r1] - base);
+    if (items > 0) {
+      cub::TransformInputIterator<int, SubBase, const int64_t*> beg(row_ptr_ + r0, SubBase{base});
+      cub::TransformInputIterator<int, SubBase, const int64_t*> end(row_ptr_ + r0 + 1, SubBase{base});
+      tmp_bytes = 0;
+      LBFS_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp_bytes, unsorted + base, col_idx_ + base,
+                                                   items, (int)(r1 - r0), beg, end, st));
+      tmp = dev_alloc<uint8_t>(tmp_bytes);
+      LBFS_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp, tmp_bytes, unsorted + base, col_idx_ + base, items,
+                                                   (int)(r1 - r0), beg, end, st));
+      LBFS_CUDA(cudaStreamSynchronize(st));
+      dev_free(tmp);
+    }
+    r0 = r1;
+  }
+  dev_free(unsorted);
+  LBFS_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace lbfs
