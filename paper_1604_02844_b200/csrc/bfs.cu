@@ -5,30 +5,40 @@
 //   K4 k_init / k_seed   PredecessorArray fill + Bitmap clear + root seed
 //                        (traversal.py:42-46, 135-139, 343-347)
 //   K1 k_expand<Mode>    frontier expansion over CSR, degree-binned in one
-//                        launch: CTA bin (hub slices staged in shared memory
-//                        by cp.async.bulk + mbarrier, double-buffered), warp
-//                        bin (warp per vertex, 128-bit col_idx loads with the
-//                        Listing-1 peel/body/remainder split), small bin
-//                        (warp per 32 vertices over their concatenated rows).
+//                        persistent launch (one 1024-thread CTA per SM):
+//                        - CTA bin (deg >= kCtaMin): rows cut into kChunk
+//                          slices; each warp streams slices through a private
+//                          shared-memory double buffer filled by cp.async.bulk
+//                          (mbarrier completion), one chunk ahead;
+//                        - warp bin (32 <= deg < kCtaMin) and small bin
+//                          (deg < 32): a warp takes 32 vertices at once and
+//                          walks their concatenated rows (one row_ptr round
+//                          trip per 32 vertices); small-bin groups of one
+//                          degree class map elements to rows in closed form.
 //                        Replaces _frontier_neighbors + the 16-lane Listing-1
 //                        gather (traversal.py:107-119, 297-332).
-//   K2 claim             visited test-and-set: L1-cached load, then 32-bit
-//                        atomicOr; the unique winner writes pred (and level in
-//                        queue mode). Replaces the unsynchronised OR + negative
-//                        marks + restoration pass (traversal.py:175-279).
-//   K3 next frontier     two forms, chosen per level by the driver:
-//                        - queue mode (small levels): warp-aggregated
-//                          ballot/popc append straight from the winners;
-//                        - bitmap mode (large levels): k_compact turns the
-//                          newly set visited bits into the three bins with
-//                          block-aggregated appends (one atomic per bin per
-//                          block) and writes their levels.
-//                        Replaces the np.unique merge / nonzero-word scans
+//   K2 probe + settle    visited test: words of the hot bitmap prefix from a
+//                        per-SM shared-memory copy, the rest through L1. In
+//                        bitmap mode a clear bit is settled without waiting:
+//                        red.or on the bitmap + the parent into pred_int (any
+//                        equal-level parent is valid, traversal.py:145-147);
+//                        in queue mode atomicOr elects one winner. Replaces
+//                        the unsynchronised OR + negative marks + restoration
+//                        pass (traversal.py:175-279).
+//   K3 next frontier     queue mode (small levels): warp-aggregated
+//                        ballot/popc appends by the winners; bitmap mode
+//                        (large levels): k_compact turns the new visited
+//                        bits into the next frontier bitmap + warp/CTA-bin
+//                        queues with block-aggregated appends, writes levels
+//                        and translates parents to original ids. Replaces the
+//                        np.unique merge / nonzero-word scans
 //                        (traversal.py:157-158, 168-172, 366-384).
 //   K5 BfsEngine::run    level driver (the while loops traversal.py:90,152,366)
 //   K6 Counters          LayerStats(input, edges, discovered) per level
 //                        (traversal.py:66-70, 100, 159, 383)
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include <cub/block/block_reduce.cuh>
@@ -54,13 +64,9 @@ __device__ __forceinline__ int4 ld_stream4(const int32_t* p) {
                : "l"(p));
   return v;
 }
-__device__ __forceinline__ int64_t ld_na64(const int64_t* p) {
-  int64_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.s64 %0, [%1];" : "=l"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // ---------------------------------------------------------------- TMA bulk copy
@@ -96,16 +102,20 @@ struct Acc {  // per-thread K6 accumulators (queue mode), reduced per warp at ex
   unsigned long long edges = 0;
 };
 
-__device__ __forceinline__ bool bit_clear(uint32_t word, int32_t v) { return ((word >> (v & 31)) & 1u) == 0; }
+struct Hot {  // shared-memory copy of the visited words [0, words)
+  uint32_t* s;
+  uint32_t base;  // shared-window address of s
+  int32_t words;
+};
 
-// Bitmap mode: a lane whose probe saw a clear bit tries the atomic; the
-// winner writes the predecessor. Levels are written by k_compact.
-__device__ __forceinline__ void settle_bitmap(const LevelArgs& a, bool cand, int32_t v, int32_t u_orig) {
-  if (cand) {
-    const uint32_t bit = 1u << (v & 31);
-    if ((atomicOr(a.visited + (v >> 5), bit) & bit) == 0) a.pred[__ldg(a.new2old + v)] = u_orig;
-  }
-}
+// Per-warp shared scratch for the group walks.
+struct WarpScratch {
+  int32_t off[33];
+  int32_t vert[32];
+  int64_t start[32];
+};
+
+__device__ __forceinline__ bool bit_clear(uint32_t word, int32_t v) { return ((word >> (v & 31)) & 1u) == 0; }
 
 __device__ __forceinline__ void warp_append(bool take, int32_t val, unsigned long long* tail, int32_t* q,
                                             int lane) {
@@ -118,9 +128,10 @@ __device__ __forceinline__ void warp_append(bool take, int32_t val, unsigned lon
   if (take) q[base + __popc(m & ((1u << lane) - 1u))] = val;
 }
 
-// Queue mode (warp-collective): winners write level + pred, then append to
-// the next level's bin with one atomic per warp per bin.
-__device__ __forceinline__ void settle_queue(const LevelArgs& a, bool cand, int32_t v, int32_t u_orig, int lane,
+// Queue mode (warp-collective): atomicOr elects one winner per vertex, which
+// writes level + pred and appends to the next level's bin with one atomic
+// per warp per bin.
+__device__ __forceinline__ void settle_queue(const LevelArgs& a, bool cand, int32_t v, int32_t u, int lane,
                                              Acc& acc) {
   bool win = false;
   if (cand) {
@@ -128,14 +139,15 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, bool cand, int3
     win = (atomicOr(a.visited + (v >> 5), bit) & bit) == 0;
   }
   if (!__any_sync(kFull, win)) return;
-  int32_t deg = 0;
-  int32_t vo = 0;
+  int32_t deg = 0, vo = 0;
+  int64_t st = 0;
   if (win) {
     atomicOr(a.prev + (v >> 5), 1u << (v & 31));  // keep bitmap-mode compaction exact
     vo = __ldg(a.new2old + v);
     a.level[vo] = a.next_level;
-    a.pred[vo] = u_orig;
-    deg = (int32_t)(a.row_ptr[v + 1] - a.row_ptr[v]);
+    a.pred[vo] = u;  // parents travel as original ids
+    st = a.row_ptr[v];
+    deg = (int32_t)(a.row_ptr[v + 1] - st);
     acc.disc += 1;
     acc.edges += (unsigned long long)deg;
   }
@@ -155,28 +167,88 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, bool cand, int3
     base = __shfl_sync(kFull, base, 31);
     const int off = incl - items;
     for (int k = 0; k < items; ++k)
-      a.next_cta[base + off + k] = CtaItem{v, k * kChunk, min(kChunk, deg - k * kChunk), vo};
+      a.next_cta[base + off + k] = CtaItem{st + (int64_t)k * kChunk, min(kChunk, deg - k * kChunk), vo};
   }
 }
 
-template <int M>
-__device__ __forceinline__ void settle(const LevelArgs& a, bool cand, int32_t v, int32_t u_orig, int lane, Acc& acc) {
-  if constexpr (M == kBitmapOut)
-    settle_bitmap(a, cand, v, u_orig);
-  else
-    settle_queue(a, cand, v, u_orig, lane, acc);
+// Probe a batch of K neighbours. Words of the hot prefix come from the
+// shared copy (a random 32-lane gather costs a few bank cycles there versus
+// ~32 L1 wavefronts); cold words use L1-cached loads. All K loads are issued
+// before any of them is consumed.
+//
+// Bitmap mode settles a clear bit without waiting on memory: any lane whose
+// view (shared copy, L1 line or L2 word — all loaded after the level
+// started) shows v unvisited may record its parent, since every such parent
+// is one level up (the benign race of bfs_parallel_naive,
+// traversal.py:145-147). Lanes hitting the same bitmap word elect one
+// writer: one red.or to the bitmap and one OR into the shared copy per word
+// per warp step; each lane stores its parent (original id) to pred_int[v].
+// Visited word of v's bitmap word wi: from the shared copy when wi is in the
+// hot prefix, else from global memory through L1 — two predicated loads, no
+// branch, no generic addressing.
+__device__ __forceinline__ uint32_t probe_word(const Hot& h, const uint32_t* visited, int32_t wi) {
+  uint32_t w;
+  asm("{\n\t.reg .pred p;\n\t"
+      "setp.lt.s32 p, %1, %2;\n\t"
+      "@p ld.shared.u32 %0, [%3];\n\t"
+      "@!p ld.global.ca.u32 %0, [%4];\n\t}"
+      : "=r"(w)
+      : "r"(wi), "r"(h.words), "r"(h.base + 4u * (uint32_t)wi), "l"(visited + wi));
+  return w;
 }
 
-// Probe a batch of K neighbours: all K bitmap loads are issued before any
-// atomic so each lane keeps K requests in flight.
-template <int M, int K>
-__device__ __forceinline__ void probe_batch(const LevelArgs& a, const int32_t (&nb)[K], const bool (&ok)[K],
-                                            const int32_t (&par)[K], int lane, Acc& acc) {
-  uint32_t w[K];
+// Bitmap mode, candidates in cmask: runs of candidates in one bitmap word
+// (consecutive elements of a lane come from sorted rows) are merged into a
+// single red.or + shared OR; each candidate stores its parent.
+template <int K, typename ParFn>
+__device__ __forceinline__ void settle_bitmap(const LevelArgs& a, const Hot& h, const int32_t (&nb)[K],
+                                              uint32_t cmask, ParFn par) {
+  int32_t run_w = -1;
+  uint32_t run_bits = 0;
 #pragma unroll
-  for (int k = 0; k < K; ++k) w[k] = ok[k] ? __ldca(a.visited + (nb[k] >> 5)) : ~0u;
+  for (int k = 0; k < K; ++k) {
+    if (!((cmask >> k) & 1u)) continue;
+    const int32_t v = nb[k];
+    const int32_t wi = v >> 5;
+    if (wi != run_w) {
+      if (run_bits) {
+        red_or(a.visited + run_w, run_bits);
+        if (run_w < h.words) atomicOr(h.s + run_w, run_bits);
+      }
+      run_w = wi;
+      run_bits = 0;
+    }
+    run_bits |= 1u << (v & 31);
+    a.pred_int[v] = par(k);
+    if (a.dbg) atomicAdd(a.dbg + (wi < h.words ? 0 : 1), 1ull);  // LBFS_COUNT only
+  }
+  red_or(a.visited + run_w, run_bits);
+  if (run_w < h.words) atomicOr(h.s + run_w, run_bits);
+}
+
+// Probe a batch of K neighbours (elements outside okmask must hold a valid
+// id, e.g. 0). All K loads are issued before any is consumed. Bitmap mode
+// settles clear bits without waiting on memory: any lane whose view (shared
+// copy, L1 line or L2 word — all loaded after the level started) shows v
+// unvisited may record its parent, since every such parent is one level up
+// (the benign race of bfs_parallel_naive, traversal.py:145-147). Queue mode
+// elects one winner per vertex with atomicOr.
+template <int M, int K, typename ParFn>
+__device__ __forceinline__ void probe_batch(const LevelArgs& a, const Hot& h, const int32_t (&nb)[K],
+                                            uint32_t okmask, ParFn par, int lane, Acc& acc) {
+  uint32_t cmask = 0;
 #pragma unroll
-  for (int k = 0; k < K; ++k) settle<M>(a, ok[k] && bit_clear(w[k], nb[k]), nb[k], par[k], lane, acc);
+  for (int k = 0; k < K; ++k) {
+    const uint32_t w = probe_word(h, a.visited, nb[k] >> 5);
+    cmask |= ((~w >> (nb[k] & 31)) & 1u) << k;
+  }
+  cmask &= okmask;
+  if constexpr (M == kBitmapOut) {
+    if (cmask) settle_bitmap<K>(a, h, nb, cmask, par);
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) settle_queue(a, (cmask >> k) & 1u, nb[k], par(k), lane, acc);
+  }
 }
 
 template <int M>
@@ -195,159 +267,15 @@ __device__ __forceinline__ void flush_acc(const LevelArgs& a, Acc& acc) {
   }
 }
 
-// ---------------------------------------------------------------- K1
-// Warp-cooperative expansion of row [st, en) of parent u: 128-bit aligned
-// body loads, scalar peel/remainder (Listing-1 split, lane.py:100-108).
-template <int M>
-__device__ __forceinline__ void expand_row_warp(const LevelArgs& a, int32_t u_orig, int64_t st, int64_t en,
-                                                int lane, Acc& acc) {
-  const int64_t al = std::min<int64_t>((st + 3) & ~int64_t(3), en);
-  const int64_t bl = std::max<int64_t>(al, en & ~int64_t(3));
-  {  // peel [st, al) on lanes 0..2 and remainder [bl, en) on lanes 3..5, one batch
-    int64_t j = -1;
-    if (lane < 3 && st + lane < al) j = st + lane;
-    if (lane >= 3 && lane < 6 && bl + (lane - 3) < en) j = bl + (lane - 3);
-    int32_t nb[1] = {j >= 0 ? ld_stream(a.col_idx + j) : 0};
-    bool ok[1] = {j >= 0};
-    int32_t par[1] = {u_orig};
-    probe_batch<M, 1>(a, nb, ok, par, lane, acc);
-  }
-  for (int64_t j0 = al; j0 < bl; j0 += 256) {  // 2 x int4 per lane per step
-    const int64_t j1 = j0 + lane * 4, j2 = j0 + 128 + lane * 4;
-    const bool b1 = j1 < bl, b2 = j2 < bl;
-    int4 x = b1 ? ld_stream4(a.col_idx + j1) : make_int4(0, 0, 0, 0);
-    int4 y = b2 ? ld_stream4(a.col_idx + j2) : make_int4(0, 0, 0, 0);
-    int32_t nb[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
-    bool ok[8] = {b1, b1, b1, b1, b2, b2, b2, b2};
-    int32_t par[8] = {u_orig, u_orig, u_orig, u_orig, u_orig, u_orig, u_orig, u_orig};
-    probe_batch<M, 8>(a, nb, ok, par, lane, acc);
-  }
+// ---------------------------------------------------------------- K1 pieces
+// degree class of a small-region internal id: the d with T[d+1] <= v < T[d]
+__device__ __forceinline__ int degree_class(const int32_t* T, int32_t v) {
+  int d = 1;  // largest d in [1, kSmallMax-1] with T[d] > v (T non-increasing)
+#pragma unroll
+  for (int step = 16; step; step >>= 1)
+    if (d + step <= kSmallMax - 1 && T[d + step] > v) d += step;
+  return d;
 }
-
-struct CtaMeta {
-  int32_t shift;  // first valid element within the staged buffer
-  int32_t len;
-  int32_t u_orig;
-  int32_t nvec;   // int4 slots staged
-};
-
-template <int M>
-__global__ void __launch_bounds__(kExpandThreads, 4) k_expand(LevelArgs a, Frontier f) {
-  __shared__ alignas(128) int32_t s_buf[2][kChunk + 8];
-  __shared__ alignas(8) uint64_t s_bar[2];
-  __shared__ CtaMeta s_meta[2];
-  __shared__ int32_t s_off[kExpandThreads / 32][33];
-  __shared__ int64_t s_start[kExpandThreads / 32][32];
-  __shared__ int32_t s_par[kExpandThreads / 32][32];
-  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-  Acc acc;
-
-  // ---- phase 1: CTA bin, TMA-staged kChunk-edge hub slices ---------------
-  if (f.n_cta > (int64_t)blockIdx.x) {
-    if (tid == 0) {
-      mbar_init(&s_bar[0], 1);
-      mbar_init(&s_bar[1], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    auto issue = [&](int64_t it, int b) {  // thread 0
-      const CtaItem c = f.cta[it];
-      const int64_t st = a.row_ptr[c.v] + c.off;
-      const int64_t a0 = st & ~int64_t(3);
-      const int64_t a1 = (st + c.len + 3) & ~int64_t(3);
-      const uint32_t bytes = (uint32_t)((a1 - a0) * 4);
-      s_meta[b] = CtaMeta{(int32_t)(st - a0), c.len, c.v_orig, (int32_t)((a1 - a0) / 4)};
-      mbar_expect_tx(&s_bar[b], bytes);
-      bulk_g2s(&s_buf[b][0], a.col_idx + a0, bytes, &s_bar[b]);
-    };
-    if (tid == 0) issue(blockIdx.x, 0);
-    __syncthreads();
-    uint32_t ph[2] = {0u, 0u};
-    int b = 0;
-    for (int64_t it = blockIdx.x; it < f.n_cta; it += gridDim.x) {
-      if (tid == 0 && it + gridDim.x < f.n_cta) issue(it + gridDim.x, b ^ 1);
-      mbar_wait(&s_bar[b], ph[b]);
-      ph[b] ^= 1u;
-      const CtaMeta m = s_meta[b];
-      const int4* v4 = reinterpret_cast<const int4*>(&s_buf[b][0]);
-      for (int base = 0; base < m.nvec; base += 2 * kExpandThreads) {
-        const int s1 = base + tid, s2 = base + kExpandThreads + tid;
-        const int4 x = s1 < m.nvec ? v4[s1] : make_int4(0, 0, 0, 0);
-        const int4 y = s2 < m.nvec ? v4[s2] : make_int4(0, 0, 0, 0);
-        int32_t nb[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
-        bool ok[8];
-        int32_t par[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int e = (k < 4 ? s1 * 4 + k : s2 * 4 + (k - 4)) - m.shift;
-          ok[k] = (k < 4 ? s1 < m.nvec : s2 < m.nvec) && e >= 0 && e < m.len;
-          par[k] = m.u_orig;
-        }
-        probe_batch<M, 8>(a, nb, ok, par, lane, acc);
-      }
-      __syncthreads();  // buffer b is free again
-      b ^= 1;
-    }
-  }
-
-  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-
-  // ---- phase 2: warp bin, one warp per vertex ------------------------------
-  for (int64_t i = gwarp; i < f.n_warp; i += nwarps) {
-    const int32_t u = f.warp[i];
-    const int64_t st = a.row_ptr[u], en = a.row_ptr[u + 1];
-    expand_row_warp<M>(a, __ldg(a.new2old + u), st, en, lane, acc);
-  }
-
-  // ---- phase 3: small bin, a warp walks 32 vertices' concatenated rows ----
-  for (int64_t base = gwarp * 32; base < f.n_small; base += nwarps * 32) {
-    const int64_t i = base + lane;
-    int64_t st = 0;
-    int32_t d = 0, uo = 0;
-    if (i < f.n_small) {
-      const int32_t u = f.small[i];
-      st = a.row_ptr[u];
-      d = (int32_t)(a.row_ptr[u + 1] - st);
-      uo = __ldg(a.new2old + u);
-    }
-    int incl = d;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += t;
-    }
-    const int total = __shfl_sync(kFull, incl, 31);
-    s_off[wib][lane] = incl - d;
-    s_start[wib][lane] = st;
-    s_par[wib][lane] = uo;
-    __syncwarp();
-    for (int e0 = 0; e0 < total; e0 += 128) {
-      int32_t nb[4], par[4];
-      bool ok[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int e = e0 + k * 32 + lane;
-        ok[k] = e < total;
-        int lo = 0;
-#pragma unroll
-        for (int step = 16; step; step >>= 1)
-          if (s_off[wib][lo + step] <= e) lo += step;
-        nb[k] = ok[k] ? ld_stream(a.col_idx + s_start[wib][lo] + (e - s_off[wib][lo])) : 0;
-        par[k] = s_par[wib][lo];
-      }
-      probe_batch<M, 4>(a, nb, ok, par, lane, acc);
-    }
-    __syncwarp();
-  }
-  flush_acc<M>(a, acc);
-}
-
-// ---------------------------------------------------------------- K3 compaction
-// One thread per visited word: new = visited & ~prev. Each block scans its
-// per-bin counts, takes one atomic per bin, writes its entries in ascending
-// internal id, writes the new vertices' levels and folds the K6 stats.
-constexpr int kCompactThreads = 256;
 
 __device__ __forceinline__ uint32_t range_mask(int64_t base_v, int64_t lo, int64_t hi) {
   // bits b with lo <= base_v + b < hi
@@ -358,69 +286,423 @@ __device__ __forceinline__ uint32_t range_mask(int64_t base_v, int64_t lo, int64
   return hi_m & ~lo_m;
 }
 
-__global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
-  using Scan = cub::BlockScan<unsigned long long, kCompactThreads>;
-  using Reduce = cub::BlockReduce<unsigned long long, kCompactThreads>;
-  __shared__ typename Scan::TempStorage s_scan;
-  __shared__ typename Reduce::TempStorage s_red;
-  __shared__ unsigned long long s_base[3];
-  const int64_t i = (int64_t)blockIdx.x * kCompactThreads + threadIdx.x;
-  uint32_t nb = 0;
-  if (i < c.nwords) {
-    const uint32_t w = c.visited[i], p = c.prev[i];
-    nb = w & ~p;
-    if (nb) c.prev[i] = w;
+// A warp expands elements [elo, ehi) of the concatenated rows of up to 32
+// vertices (lanes [0, n) own one each): one row_ptr round trip, a degree
+// scan, then 128-element windows in which each lane finds its element's
+// owner by binary search over the group's offsets.
+template <int M>
+__device__ __forceinline__ void expand_group(const LevelArgs& a, const Hot& h, int n, int32_t u, int elo, int ehi,
+                                             int lane, WarpScratch& ws, Acc& acc) {
+  int64_t st = 0;
+  int32_t d = 0, uo = 0;
+  if (lane < n) {
+    st = a.row_ptr[u];
+    d = (int32_t)(a.row_ptr[u + 1] - st);
+    uo = __ldg(a.new2old + u);
   }
-  const int64_t v0 = i * 32;
-  const uint32_t m_cta = nb & range_mask(v0, 0, c.t_cta);
-  const uint32_t m_warp = nb & range_mask(v0, c.t_cta, c.t_warp);
-  const uint32_t m_small = nb & range_mask(v0, c.t_warp, c.t_nz);
-  unsigned long long n_items = 0;
-  for (uint32_t m = m_cta; m; m &= m - 1) {
-    const int64_t v = v0 + __ffs(m) - 1;
-    const int64_t deg = c.row_ptr[v + 1] - c.row_ptr[v];
-    n_items += (unsigned long long)((deg + kChunk - 1) / kChunk);
+  int incl = d;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
   }
-  // pack: items [0,21) | warp [21,42) | small [42,63)
-  const unsigned long long packed =
-      n_items | ((unsigned long long)__popc(m_warp) << 21) | ((unsigned long long)__popc(m_small) << 42);
-  unsigned long long excl, total;
-  Scan(s_scan).ExclusiveSum(packed, excl, total);
-  if (threadIdx.x == 0) {
-    const unsigned long long t_items = total & 0x1FFFFF, t_warp = (total >> 21) & 0x1FFFFF,
-                             t_small = (total >> 42) & 0x1FFFFF;
-    s_base[0] = t_small ? atomicAdd(&c.next_cnt->bin[kBinSmall], t_small) : 0;
-    s_base[1] = t_warp ? atomicAdd(&c.next_cnt->bin[kBinWarp], t_warp) : 0;
-    s_base[2] = t_items ? atomicAdd(&c.next_cnt->bin[kBinCta], t_items) : 0;
+  const int total = __shfl_sync(kFull, incl, 31);
+  const int end = min(ehi, total);
+  __syncwarp();
+  ws.off[lane] = incl - d;
+  ws.start[lane] = st - (incl - d);
+  ws.vert[lane] = uo;
+  __syncwarp();
+  for (int e0 = elo; e0 < end; e0 += 128) {
+    int32_t nb[4], par[4];
+    uint32_t okm = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = e0 + k * 32 + lane;
+      const bool ok = e < end;
+      okm |= (uint32_t)ok << k;
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1)
+        if (ws.off[lo + step] <= e) lo += step;
+      nb[k] = ok ? ld_stream(a.col_idx + ws.start[lo] + e) : 0;
+      par[k] = ws.vert[lo];
+    }
+    probe_batch<M, 4>(a, h, nb, okm, [&](int k) { return par[k]; }, lane, acc);
+  }
+  __syncwarp();
+}
+
+// Elements [elo, ehi) of a group whose vertices all have degree d (lanes
+// [0, n) valid): the rows of class d are contiguous from T/base, so element
+// e belongs to lane e / d at offset e % d — no row_ptr read, no search.
+template <int M>
+__device__ __forceinline__ void expand_class_group(const LevelArgs& a, const Hot& h, int n, int32_t v, int d,
+                                                   int elo, int ehi, const int32_t* T, const int64_t* B, int lane,
+                                                   Acc& acc) {
+  const int32_t roff = (lane < n) ? (v - T[d + 1]) * d : 0;
+  const int32_t vo = (lane < n) ? __ldg(a.new2old + v) : 0;
+  const int32_t* rows = a.col_idx + B[d];
+  const uint32_t rcp = (uint32_t)(0xFFFFFFFFull / (uint32_t)d + 1ull);  // e / d for e < 2^27, d >= 2
+  const int end = min(ehi, n * d);
+  for (int e0 = elo; e0 < end; e0 += 128) {
+    int32_t nb[4], par[4];
+    uint32_t okm = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = e0 + k * 32 + lane;
+      const bool ok = e < end;
+      okm |= (uint32_t)ok << k;
+      const int q = !ok ? 0 : (d == 1 ? e : (int)__umulhi((uint32_t)e, rcp));
+      const int32_t ro = __shfl_sync(kFull, roff, q);
+      par[k] = __shfl_sync(kFull, vo, q);
+      nb[k] = ok ? ld_stream(rows + ro + (e - q * d)) : 0;
+    }
+    probe_batch<M, 4>(a, h, nb, okm, [&](int k) { return par[k]; }, lane, acc);
+  }
+}
+
+// Elements [elo, ehi) of a group of up to 32 vertices (lanes [0, n)):
+// closed-form walk when all lie in one small-region degree class (the common
+// case with degree-ordered ids), generic walk otherwise.
+template <int M>
+__device__ __forceinline__ void expand_range(const LevelArgs& a, const Hot& h, int n, int32_t v, int elo, int ehi,
+                                             const int32_t* T, const int64_t* B, int lane, WarpScratch& ws,
+                                             Acc& acc) {
+  const bool small = (lane < n) && v >= a.t_warp && v < a.t_nz;
+  const int d = small ? degree_class(T, v) : 0;
+  const int d0 = __shfl_sync(kFull, d, 0);
+  if (d0 > 0 && __all_sync(kFull, lane >= n || d == d0))
+    expand_class_group<M>(a, h, n, v, d0, elo, ehi, T, B, lane, acc);
+  else
+    expand_group<M>(a, h, n, v, elo, ehi, lane, ws, acc);
+}
+
+// Valid-element mask of a 256-element chunk whose lane holds elements
+// [4*lane, 4*lane+4) and [128+4*lane, 128+4*lane+4) for a slice covering
+// chunk offsets [lo, hi); invalid elements are zeroed (stale staging data).
+__device__ __forceinline__ uint32_t slice_mask(int32_t (&nb)[8], int lo, int hi, int lane) {
+  if (lo <= 0 && hi >= kWarpChunk) return 0xFFu;  // interior chunk
+  uint32_t okm = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int r = (q < 4 ? lane * 4 + q : 128 + lane * 4 + (q - 4));
+    const bool ok = r >= lo && r < hi;
+    okm |= (uint32_t)ok << q;
+    nb[q] = ok ? nb[q] : 0;
+  }
+  return okm;
+}
+
+struct ChunkMeta {
+  int64_t base;    // col_idx index of the chunk's first staged element
+  int64_t lo, hi;  // valid element range of the owning slice
+  int32_t u;       // internal id of the hub
+};
+
+// One persistent CTA per SM (kExpandWarps warps) holding a shared-memory copy
+// of the hot visited prefix (hot_words words, one bulk copy at kernel start,
+// updated by the CTA's own discoveries). `phases` selects bins (debug split).
+template <int M>
+__global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Frontier f, int32_t hot_words,
+                                                               int phases) {
+  extern __shared__ __align__(128) uint8_t s_dyn[];
+  __shared__ __align__(8) uint64_t s_bar[kExpandWarps][2];
+  __shared__ __align__(8) uint64_t s_hot_bar;
+  __shared__ ChunkMeta s_meta[kExpandWarps][2];
+  __shared__ WarpScratch s_ws[kExpandWarps];
+  __shared__ int32_t s_T[kSmallMax + 2];
+  __shared__ int64_t s_B[kSmallMax + 1];
+  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+  const Hot h{reinterpret_cast<uint32_t*>(s_dyn + kRingBytes), smem_u32(s_dyn + kRingBytes), hot_words};
+  // warp ids interleave the SMs so that the first work units of every phase
+  // land on different SMs
+  const int64_t gwarp = (int64_t)wib * gridDim.x + blockIdx.x;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  WarpScratch& ws = s_ws[wib];
+  Acc acc;
+
+  if (lane == 0) {
+    mbar_init(&s_bar[wib][0], 1);
+    mbar_init(&s_bar[wib][1], 1);
+  }
+  if (tid == 0) {
+    mbar_init(&s_hot_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < kSmallMax + 2) s_T[tid] = a.classes->T[tid];
+  if (tid < kSmallMax + 1) s_B[tid] = a.classes->base[tid];
+  __syncthreads();
+  if (hot_words > 0) {
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)hot_words * 4u;  // multiple of 16 by construction
+      mbar_expect_tx(&s_hot_bar, bytes);
+      bulk_g2s(h.s, a.visited, bytes, &s_hot_bar);
+    }
+    mbar_wait(&s_hot_bar, 0);
+  }
+  uint32_t hot_phase = 0;  // last phase of s_hot_bar issued (warp 0 lane 0)
+  const int refresh_every = hot_words > 0 ? a.refresh_chunks : 0;
+
+  // ---- phase 1: CTA bin, warp-private bulk-copy streams -------------------
+  if ((phases & 1) && gwarp < f.n_cta) {
+    int32_t* wbuf = reinterpret_cast<int32_t*>(s_dyn) + (size_t)wib * 2 * kWarpChunk;
+    // lane-0 stream state: current slice [pos, end) (16-B aligned), next slice prefetched
+    int64_t it = gwarp;
+    CtaItem cur = f.cta[it];
+    CtaItem pre{0, 0, 0};
+    if (it + nwarps < f.n_cta) pre = f.cta[it + nwarps];
+    int64_t pos = cur.start & ~int64_t(3);
+    int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
+    auto issue = [&](int b) -> int {  // lane 0: next chunk into buffer b; 0 when exhausted
+      if (pos >= end) {
+        it += nwarps;
+        if (it >= f.n_cta) return 0;
+        cur = pre;
+        if (it + nwarps < f.n_cta) pre = f.cta[it + nwarps];
+        pos = cur.start & ~int64_t(3);
+        end = (cur.start + cur.len + 3) & ~int64_t(3);
+      }
+      const int64_t cnt = std::min<int64_t>(kWarpChunk, end - pos);
+      s_meta[wib][b] = ChunkMeta{pos, cur.start, cur.start + cur.len, cur.u};
+      mbar_expect_tx(&s_bar[wib][b], (uint32_t)(cnt * 4));
+      bulk_g2s(wbuf + b * kWarpChunk, a.col_idx + pos, (uint32_t)(cnt * 4), &s_bar[wib][b]);
+      pos += cnt;
+      return 1;
+    };
+    int more0 = __shfl_sync(kFull, lane == 0 ? issue(0) : 0, 0);
+    int more1 = __shfl_sync(kFull, lane == 0 ? issue(1) : 0, 0);
+    uint32_t par_bits = 0;
+    int chunks_done = 0;
+    for (int b = 0; b ? more1 : more0; b ^= 1) {
+      mbar_wait(&s_bar[wib][b], (par_bits >> b) & 1u);
+      par_bits ^= 1u << b;
+      const ChunkMeta m = s_meta[wib][b];
+      const int4* v4 = reinterpret_cast<const int4*>(wbuf + b * kWarpChunk);
+      const int4 x = v4[lane], y = v4[lane + 32];
+      __syncwarp();
+      const int mo = __shfl_sync(kFull, lane == 0 ? issue(b) : 0, 0);  // refill b right away
+      if (b) more1 = mo; else more0 = mo;
+      int32_t nb[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+      const uint32_t okm = slice_mask(nb, (int)(m.lo - m.base), (int)(m.hi - m.base), lane);
+      const int32_t pu = m.u;
+      probe_batch<M, 8>(a, h, nb, okm, [&](int) { return pu; }, lane, acc);
+      if (refresh_every > 0 && wib == 0 && ++chunks_done % refresh_every == 0) {
+        // re-learn the hot prefix from L2 (others' discoveries): async bulk
+        // copy over the shared copy; a racing local OR may be lost, which
+        // only costs a redundant write later
+        if (lane == 0) {
+          mbar_wait(&s_hot_bar, hot_phase & 1u);  // previous copy landed
+          ++hot_phase;
+          mbar_expect_tx(&s_hot_bar, (uint32_t)hot_words * 4u);
+          bulk_g2s(h.s, a.visited, (uint32_t)hot_words * 4u, &s_hot_bar);
+        }
+        __syncwarp();
+      }
+    }
+  }
+
+  // ---- phase 1 (variant): hub slices with register double-buffering ------
+  if ((phases & 8) && gwarp < f.n_cta) {
+    // the warp walks its slices in 256-element chunks; the loads of chunk
+    // i+1 are issued before chunk i is probed
+    int64_t it = gwarp;
+    CtaItem cur = f.cta[it];
+    int64_t pos = cur.start & ~int64_t(3);
+    int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
+    int4 x = make_int4(0, 0, 0, 0), y = x;
+    auto load_chunk = [&](int64_t p0, int64_t e0, int4& xa, int4& ya) {
+      const int64_t i1 = p0 + lane * 4, i2 = p0 + 128 + lane * 4;
+      xa = i1 < e0 ? ld_stream4(a.col_idx + i1) : make_int4(0, 0, 0, 0);
+      ya = i2 < e0 ? ld_stream4(a.col_idx + i2) : make_int4(0, 0, 0, 0);
+    };
+    load_chunk(pos, end, x, y);
+    while (true) {
+      const int64_t cbase = pos;
+      const CtaItem ci = cur;
+      pos += kWarpChunk;
+      bool more = true;
+      if (pos >= end) {
+        it += nwarps;
+        if (it < f.n_cta) {
+          cur = f.cta[it];
+          pos = cur.start & ~int64_t(3);
+          end = (cur.start + cur.len + 3) & ~int64_t(3);
+        } else {
+          more = false;
+        }
+      }
+      int4 nx = make_int4(0, 0, 0, 0), ny = nx;
+      if (more) load_chunk(pos, end, nx, ny);
+      int32_t nb[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+      const uint32_t okm = slice_mask(nb, (int)(ci.start - cbase), (int)(ci.start + ci.len - cbase), lane);
+      const int32_t pu = ci.u;
+      probe_batch<M, 8>(a, h, nb, okm, [&](int) { return pu; }, lane, acc);
+      if (!more) break;
+      x = nx;
+      y = ny;
+    }
+  }
+
+  // ---- phase 2: non-hub frontier as balanced group items -----------------
+  for (int64_t it = gwarp; (phases & 2) && it < f.n_items; it += nwarps) {
+    const GroupItem gi = f.items[it];
+    const int32_t v = lane < gi.count ? f.list[gi.list_start + lane] : 0;
+    expand_range<M>(a, h, gi.count, v, gi.elo, gi.ehi, s_T, s_B, lane, ws, acc);
+  }
+
+  // ---- phase 3: raw warp/small queues (after a queue-mode level): a warp
+  // takes one warp-bin vertex or 32 small-bin vertices ---------------------
+  if (phases & 4) {
+    const int64_t ng = f.n_warp + (f.n_small + 31) / 32;
+    for (int64_t g = gwarp; g < ng; g += nwarps) {
+      const bool wb = g < f.n_warp;
+      const int64_t base = wb ? g : (g - f.n_warp) * 32;
+      const int n = wb ? 1 : (int)std::min<int64_t>(32, f.n_small - base);
+      const int32_t v = lane < n ? (wb ? f.warp : f.small)[base + lane] : 0;
+      expand_range<M>(a, h, n, v, 0, 1 << 30, s_T, s_B, lane, ws, acc);
+    }
+  }
+  flush_acc<M>(a, acc);
+}
+
+// ---------------------------------------------------------------- K3 compaction
+// A block owns kCompactVerts consecutive internal ids (kCompactWords visited
+// words): new = visited & ~prev. Hubs become kChunk slices; the other new
+// vertices get list ranks in ascending id (prefix of per-word popcounts), so
+// the list is id-ordered within the block and degree classes stay together;
+// every 32 consecutive list entries form a group cut into kItemElems-element
+// items. One atomic per output per block reserves space. Pass 2 (one vertex
+// per thread per step, so new2old/row_ptr/pred_int reads coalesce) writes
+// levels and parents in original ids and folds the K6 stats.
+constexpr int kCompactThreads = 256;
+constexpr int kCompactVerts = 4096;
+constexpr int kCompactWords = kCompactVerts / 32;
+constexpr int kCompactSteps = kCompactVerts / kCompactThreads;
+
+// exclusive scan of one int per thread over the first 128 threads (all 256
+// threads must call); returns the exclusive prefix, *total the sum
+__device__ __forceinline__ int scan128(int val, int* s_w, int* total) {
+  const int t = threadIdx.x, lane = t & 31;
+  int incl = val;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += x;
   }
   __syncthreads();
-  unsigned long long p_items = s_base[2] + (excl & 0x1FFFFF);
-  unsigned long long p_warp = s_base[1] + ((excl >> 21) & 0x1FFFFF);
-  unsigned long long p_small = s_base[0] + ((excl >> 42) & 0x1FFFFF);
+  if (t < 128 && lane == 31) s_w[t >> 5] = incl;
+  __syncthreads();
+  int before = 0;
+  for (int k = 0; k < (t >> 5) && k < 4; ++k) before += s_w[k];
+  *total = s_w[0] + s_w[1] + s_w[2] + s_w[3];
+  return before + incl - val;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
+  using Reduce = cub::BlockReduce<unsigned long long, kCompactThreads>;
+  __shared__ typename Reduce::TempStorage s_red;
+  __shared__ uint32_t s_new[kCompactWords];
+  __shared__ uint32_t s_lmask[kCompactWords];
+  __shared__ int32_t s_lpre[kCompactWords];
+  __shared__ int32_t s_deg[kCompactVerts];
+  __shared__ int32_t s_gsum[kCompactWords];
+  __shared__ int32_t s_w[4];
+  __shared__ unsigned long long s_base[3];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t w0 = (int64_t)blockIdx.x * kCompactWords;
+  const int64_t v0 = w0 * 32;
+  uint32_t nb = 0, mhub = 0, mlist = 0;
+  int hub_items = 0;
+  if (t < kCompactWords && w0 + t < c.nwords) {
+    const uint32_t w = c.visited[w0 + t], p = c.prev[w0 + t];
+    nb = w & ~p;
+    if (nb) {
+      c.prev[w0 + t] = w;
+      const int64_t vw = (w0 + t) * 32;
+      mhub = nb & range_mask(vw, 0, c.t_cta);
+      mlist = nb & range_mask(vw, c.t_cta, c.t_nz);
+      for (uint32_t m = mhub; m; m &= m - 1) {
+        const int64_t v = vw + __ffs(m) - 1;
+        hub_items += (int)((c.row_ptr[v + 1] - c.row_ptr[v] + kChunk - 1) / kChunk);
+      }
+    }
+  }
+  if (!__syncthreads_or(nb != 0)) return;
+  if (t < kCompactWords) {
+    s_new[t] = nb;
+    s_lmask[t] = mlist;
+  }
+  int n_list = 0, n_hub_items = 0;
+  const int lpre = scan128(__popc(mlist), s_w, &n_list);
+  if (t < kCompactWords) s_lpre[t] = lpre;
+  const int ipre = scan128(hub_items, s_w, &n_hub_items);
+  if (t == 0) {
+    s_base[0] = n_list ? atomicAdd(&c.next_cnt->bin[kBinSmall], (unsigned long long)n_list) : 0;
+    s_base[1] = n_hub_items ? atomicAdd(&c.next_cnt->bin[kBinCta], (unsigned long long)n_hub_items) : 0;
+  }
+  __syncthreads();
+  if (mhub) {  // hub slices, written by the owner thread of each word
+    unsigned long long p = s_base[1] + ipre;
+    for (uint32_t m = mhub; m; m &= m - 1) {
+      const int64_t v = (w0 + t) * 32 + __ffs(m) - 1;
+      const int64_t st = c.row_ptr[v], deg = c.row_ptr[v + 1] - st;
+      for (int64_t k = 0; k * kChunk < deg; ++k)
+        c.next_cta[p++] = CtaItem{st + k * kChunk, (int32_t)std::min<int64_t>(kChunk, deg - k * kChunk),
+                                  c.new2old[v]};
+    }
+  }
+  // pass 2: thread t owns vertices v0 + t + 256 j (bit t&31 of word t/32 + 8 j)
   unsigned long long edges = 0;
-  for (uint32_t m = nb; m; m &= m - 1) {
-    const int b = __ffs(m) - 1;
-    const int64_t v = v0 + b;
+  const int b = t & 31;
+#pragma unroll 4
+  for (int j = 0; j < kCompactSteps; ++j) {
+    const int wl = (t >> 5) + j * (kCompactThreads / 32);
+    if (!((s_new[wl] >> b) & 1u)) continue;
+    const int64_t v = v0 + t + j * kCompactThreads;
     const int32_t vo = c.new2old[v];
     c.level[vo] = c.next_level;
+    c.pred[vo] = c.pred_int[v];
     const int64_t st = c.row_ptr[v];
-    const int64_t deg = c.row_ptr[v + 1] - st;
+    const int32_t deg = (int32_t)(c.row_ptr[v + 1] - st);
     edges += (unsigned long long)deg;
-    const uint32_t bit = 1u << b;
-    if (m_small & bit) {
-      c.next_small[p_small++] = (int32_t)v;
-    } else if (m_warp & bit) {
-      c.next_warp[p_warp++] = (int32_t)v;
-    } else if (m_cta & bit) {
-      for (int64_t k = 0; k * kChunk < deg; ++k)
-        c.next_cta[p_items++] = CtaItem{(int32_t)v, (int32_t)(k * kChunk),
-                                        (int32_t)std::min<int64_t>(kChunk, deg - k * kChunk), vo};
+    const uint32_t lm = s_lmask[wl];
+    if ((lm >> b) & 1u) {
+      const int r = s_lpre[wl] + __popc(lm & ((1u << b) - 1u));
+      c.next_list[s_base[0] + r] = (int32_t)v;
+      s_deg[r] = deg;
     }
+  }
+  __syncthreads();
+  // groups of 32 consecutive list entries -> kItemElems-element items
+  const int ngroups = (n_list + 31) / 32;
+  for (int g = warp; g < ngroups; g += kCompactThreads / 32) {
+    const int r = g * 32 + lane;
+    int x = r < n_list ? s_deg[r] : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+    if (lane == 0) s_gsum[g] = x;
+  }
+  __syncthreads();
+  const int gsum = t < ngroups ? s_gsum[t] : 0;
+  const int nsub = t < ngroups ? std::max(1, (gsum + kItemElems - 1) / kItemElems) : 0;
+  int n_items = 0;
+  const int gpre = scan128(nsub, s_w, &n_items);
+  if (t == 0) s_base[2] = atomicAdd(&c.next_cnt->bin[kBinItems], (unsigned long long)n_items);
+  __syncthreads();
+  for (int k = 0; k < nsub; ++k) {
+    GroupItem gi;
+    gi.list_start = (int64_t)s_base[0] + 32 * t;
+    gi.count = std::min(32, n_list - 32 * t);
+    gi.elo = k * kItemElems;
+    gi.ehi = std::min(gsum, (k + 1) * kItemElems);
+    gi.pad = 0;
+    c.next_items[s_base[2] + gpre + k] = gi;
   }
   const unsigned long long e_tot = Reduce(s_red).Sum(edges);
   __syncthreads();
   const unsigned long long d_tot = Reduce(s_red).Sum((unsigned long long)__popc(nb));
-  if (threadIdx.x == 0) {
+  if (t == 0) {
     if (e_tot) atomicAdd(&c.next_cnt->edges, e_tot);
     if (d_tot) atomicAdd(&c.next_cnt->discovered, d_tot);
   }
@@ -462,7 +744,8 @@ __global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int3
   c.edges = (unsigned long long)deg;
   if (r < a.t_cta) {
     const int items = (deg + kChunk - 1) / kChunk;
-    for (int k = 0; k < items; ++k) a.next_cta[k] = CtaItem{r, k * kChunk, min(kChunk, deg - k * kChunk), root_orig};
+    for (int k = 0; k < items; ++k)
+      a.next_cta[k] = CtaItem{st + (int64_t)k * kChunk, min(kChunk, deg - k * kChunk), root_orig};
     c.bin[kBinCta] = (unsigned long long)items;
   } else if (r < a.t_warp) {
     a.next_warp[0] = r;
@@ -486,19 +769,36 @@ BfsEngine::BfsEngine(const Csr& csr) {
   build_layout(csr);
   visited_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
   prev_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
+  pred_int_ = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_, 1));
+  dbg_ = dev_alloc<unsigned long long>(2);
+  LBFS_CUDA(cudaMemset(dbg_, 0, 2 * sizeof(unsigned long long)));
   // Bins, double-buffered: a vertex enters a bin once per BFS, so n entries
   // bound the small/warp bins; CTA items <= nnz/kChunk + #(deg >= kCtaMin).
   cap_cta_ = nnz_ / kChunk + t_cta_ + 2;
+  // group items: one per started kItemElems of each 32-entry group, per block
+  cap_items_ = nnz_ / kItemElems + n_ / 32 + 2 * ((n_ + kCompactVerts - 1) / kCompactVerts) + 16;
   for (int b = 0; b < 2; ++b) {
     q_small_[b] = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_, 1));
     q_warp_[b] = dev_alloc<int32_t>((size_t)std::max<int64_t>(t_warp_, 1));
     q_cta_[b] = dev_alloc<CtaItem>((size_t)cap_cta_);
+    q_items_[b] = dev_alloc<GroupItem>((size_t)cap_items_);
   }
   cnt_ = dev_alloc<Counters>(kCounterRing);
   LBFS_CUDA(cudaMallocHost(&h_cnt_, sizeof(Counters) * kCounterRing));
   for (auto& e : ev_) LBFS_CUDA(cudaEventCreate(&e));
+  for (auto& e : ev_split_) LBFS_CUDA(cudaEventCreate(&e));
   int occ = 0;
-  LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<kBitmapOut>, kExpandThreads, 0));
+  // shared memory: the TMA ring plus as much of the visited bitmap as fits
+  cudaFuncAttributes fa{};
+  LBFS_CUDA(cudaFuncGetAttributes(&fa, k_expand<kBitmapOut>));
+  int optin = 0;
+  LBFS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device_));
+  const int64_t avail = (int64_t)optin - (int64_t)fa.sharedSizeBytes - kRingBytes - 1024;
+  hot_words_ = (int32_t)std::min<int64_t>(std::max<int64_t>(avail / 4, 0) & ~int64_t(3), (nwords_ + 3) & ~int64_t(3));
+  dyn_smem_ = kRingBytes + hot_words_ * 4;
+  LBFS_CUDA(cudaFuncSetAttribute(k_expand<kBitmapOut>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_));
+  LBFS_CUDA(cudaFuncSetAttribute(k_expand<kQueueOut>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_));
+  LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<kBitmapOut>, kExpandThreads, dyn_smem_));
   expand_grid_ = sm_count_ * std::max(occ, 1);
 }
 
@@ -506,16 +806,21 @@ BfsEngine::~BfsEngine() {
   cudaStreamSynchronize(stream_);
   dev_free(visited_);
   dev_free(prev_);
+  dev_free(pred_int_);
+  dev_free(dbg_);
+  dev_free(classes_);
   for (int b = 0; b < 2; ++b) {
     dev_free(q_small_[b]);
     dev_free(q_warp_[b]);
     dev_free(q_cta_[b]);
+    dev_free(q_items_[b]);
   }
   dev_free(cnt_);
   if (h_cnt_) cudaFreeHost(h_cnt_);
   dev_free(own_pred_);
   dev_free(own_level_);
   for (auto& e : ev_) cudaEventDestroy(e);
+  for (auto& e : ev_split_) cudaEventDestroy(e);
   dev_free(row_ptr_);
   dev_free(col_idx_);
   dev_free(new2old_);
@@ -532,8 +837,17 @@ static unsigned clamp_grid(int64_t blocks, int64_t cap) {
   return (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
 }
 
+static bool env_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && *v && *v != '0';
+}
+
 void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t) {
   if (root < 0 || root >= n_) throw_inval("root out of range");
+  trace_ = env_flag("LBFS_TRACE");  // per-level table on stderr
+  count_ = env_flag("LBFS_COUNT");  // candidate-write counters (slow)
+  split_ = env_flag("LBFS_SPLIT");  // one launch per bin
+  hub_ldg_ = env_flag("LBFS_HUB_LDG");  // experiment: hub bin without TMA staging
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = stream_;
   LBFS_CUDA(cudaEventRecord(ev_[0], st));
@@ -554,6 +868,13 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   a.visited = visited_;
   a.prev = prev_;
   a.pred = d_pred;
+  a.pred_int = pred_int_;
+  a.classes = classes_;
+  a.dbg = count_ ? dbg_ : nullptr;
+  {
+    const char* rf = getenv("LBFS_REFRESH");  // hub chunks between snapshot refreshes (0 = off)
+    a.refresh_chunks = rf ? atoi(rf) : kRefreshChunks;
+  }
   a.level = d_level;
   a.t_cta = t_cta_;
   a.t_warp = t_warp_;
@@ -569,6 +890,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
 
   layers_.clear();
   double expand_ms = 0.0;
+  bool prev_bitmap = false;
   const unsigned long long bitmap_min_edges = (unsigned long long)std::max<int64_t>(1 << 16, n_ / 64);
   int64_t L = 0;
   for (;;) {
@@ -580,35 +902,83 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     a.next_small = q_small_[cur ^ 1];
     a.next_warp = q_warp_[cur ^ 1];
     a.next_cta = q_cta_[cur ^ 1];
-    Frontier f{q_small_[cur], q_warp_[cur], q_cta_[cur], (int64_t)c.bin[kBinSmall], (int64_t)c.bin[kBinWarp],
-               (int64_t)c.bin[kBinCta]};
+    Frontier f{};
+    f.cta = q_cta_[cur];
+    f.n_cta = (int64_t)c.bin[kBinCta];
+    if (prev_bitmap) {  // k_compact produced a list + group items
+      f.list = q_small_[cur];
+      f.items = q_items_[cur];
+      f.n_items = (int64_t)c.bin[kBinItems];
+    } else {  // winners appended to raw queues
+      f.small = q_small_[cur];
+      f.warp = q_warp_[cur];
+      f.n_small = (int64_t)c.bin[kBinSmall];
+      f.n_warp = (int64_t)c.bin[kBinWarp];
+    }
     const bool bitmap = c.edges >= bitmap_min_edges;
-    const int64_t need = std::max({f.n_cta, (f.n_warp + 7) / 8, (f.n_small + 255) / 256, (int64_t)1});
-    const unsigned grid = clamp_grid(need, expand_grid_);
+    const int64_t need = std::max({(f.n_cta + kExpandWarps - 1) / kExpandWarps,
+                                    (f.n_items + kExpandWarps - 1) / kExpandWarps,
+                                    (f.n_warp + (f.n_small + 31) / 32 + kExpandWarps - 1) / kExpandWarps,
+                                    (int64_t)1});
+    const unsigned grid = bitmap ? (unsigned)expand_grid_ : clamp_grid(need, expand_grid_);
     LBFS_CUDA(cudaEventRecord(ev_[2], st));
-    if (f.n_cta + f.n_warp + f.n_small > 0) {
-      if (bitmap) {
-        LBFS_LAUNCH(k_expand<kBitmapOut>, grid, kExpandThreads, 0, st, a, f);
-      } else {
-        LBFS_LAUNCH(k_expand<kQueueOut>, grid, kExpandThreads, 0, st, a, f);
+    float split_ms[3] = {0.f, 0.f, 0.f};
+    if (f.n_cta + f.n_warp + f.n_small + f.n_items > 0) {
+      const int nparts = split_ ? 3 : 1;
+      for (int pi = 0; pi < nparts; ++pi) {
+        int phases = split_ ? (1 << pi) : 7;
+        if (hub_ldg_ && (phases & 1)) phases = (phases & ~1) | 8;
+        if (split_ && env_flag("LBFS_SPLIT_TWICE")) {  // experiment: same phase launched twice
+          if (bitmap) {
+            LBFS_LAUNCH(k_expand<kBitmapOut>, grid, kExpandThreads, dyn_smem_, st, a, f, hot_words_, phases);
+          } else {
+            LBFS_LAUNCH(k_expand<kQueueOut>, grid, kExpandThreads, kRingBytes, st, a, f, 0, phases);
+          }
+        }
+        if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[pi], st));
+        if (bitmap) {
+          LBFS_LAUNCH(k_expand<kBitmapOut>, grid, kExpandThreads, dyn_smem_, st, a, f, hot_words_, phases);
+        } else {
+          LBFS_LAUNCH(k_expand<kQueueOut>, grid, kExpandThreads, kRingBytes, st, a, f, 0, phases);
+        }
       }
+      if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[3], st));
     }
     LBFS_CUDA(cudaEventRecord(ev_[3], st));
+    const bool did_compact = bitmap;
     if (bitmap) {
-      CompactArgs ca{row_ptr_, new2old_, visited_, prev_, nwords_, d_level, (int32_t)(L + 1), t_cta_, t_warp_, t_nz_,
-                     &cnt_[slot], q_small_[cur ^ 1], q_warp_[cur ^ 1], q_cta_[cur ^ 1]};
-      LBFS_LAUNCH(k_compact, (unsigned)((nwords_ + kCompactThreads - 1) / kCompactThreads), kCompactThreads, 0, st,
-                  ca);
+      CompactArgs ca{row_ptr_, new2old_, visited_, prev_, nwords_, d_level, d_pred, pred_int_, (int32_t)(L + 1),
+                     t_cta_, t_warp_, t_nz_, &cnt_[slot], q_small_[cur ^ 1], q_cta_[cur ^ 1], q_items_[cur ^ 1]};
+      LBFS_LAUNCH(k_compact, (unsigned)((n_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
     }
+    LBFS_CUDA(cudaEventRecord(ev_[5], st));
     LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[slot], &cnt_[slot], sizeof(Counters), cudaMemcpyDeviceToHost, st));
     LBFS_CUDA(cudaStreamSynchronize(st));
-    float ms = 0.f;
+    float ms = 0.f, cms = 0.f;
     LBFS_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
+    LBFS_CUDA(cudaEventElapsedTime(&cms, ev_[3], ev_[5]));
     expand_ms += ms;
     const Counters nx = h_cnt_[slot];
+    unsigned long long dbg[2] = {0, 0};
+    if (count_) {
+      LBFS_CUDA(cudaMemcpy(dbg, dbg_, sizeof(dbg), cudaMemcpyDeviceToHost));
+      LBFS_CUDA(cudaMemset(dbg_, 0, sizeof(dbg)));
+      fprintf(stderr, "[lbfs]      candidate writes hot=%llu cold=%llu\n", dbg[0], dbg[1]);
+    }
+    if (split_ && (f.n_cta + f.n_warp + f.n_small + f.n_items > 0)) {
+      for (int pi = 0; pi < 3; ++pi) LBFS_CUDA(cudaEventElapsedTime(&split_ms[pi], ev_split_[pi], ev_split_[pi + 1]));
+      fprintf(stderr, "[lbfs]      split: cta=%.3fms warp=%.3fms small=%.3fms\n", split_ms[0], split_ms[1], split_ms[2]);
+    }
+    if (trace_)
+      fprintf(stderr,
+              "[lbfs] L%-3lld %s in=%-9llu edges=%-10llu bins(s|list/w/c/items)=%llu/%llu/%llu/%llu grid=%u "
+              "expand=%.3fms compact=%.3fms disc=%llu\n",
+              (long long)L, bitmap ? "bitmap" : "queue ", c.discovered, c.edges, c.bin[0], c.bin[1], c.bin[2], c.bin[3],
+              grid, ms, did_compact ? cms : 0.f, nx.discovered);
     layers_.push_back(lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, (int64_t)nx.discovered});
     cur ^= 1;
     ++L;
+    prev_bitmap = bitmap;
     if (nx.discovered == 0) break;
   }
   LBFS_CUDA(cudaEventRecord(ev_[4], st));

@@ -16,33 +16,57 @@ namespace lbfs {
 constexpr int32_t kSentinel = LBFS_SENTINEL;  // traversal.py:22
 constexpr int kSmallMax = 32;                 // deg < 32: warp-cooperative small bin
 constexpr int kCtaMin = 1024;                 // deg >= 1024: CTA bin (TMA-staged chunks)
-constexpr int kChunk = 4096;                  // edges per CTA-bin item
-constexpr int kBinSmall = 0, kBinWarp = 1, kBinCta = 2;
+constexpr int kChunk = 3960;                  // edges per CTA-bin item (<= 992 staged int4 slots)
+constexpr int kBinSmall = 0, kBinWarp = 1, kBinCta = 2, kBinItems = 3;
+constexpr int kItemElems = 512;               // elements per group item (load balance unit)
 constexpr int kCounterRing = 3;
-constexpr int kExpandThreads = 256;
+constexpr int kExpandWarps = 32;
+constexpr int kExpandThreads = 32 * kExpandWarps;
+constexpr int kWarpChunk = 256;
+constexpr int kRefreshChunks = 4;                 // hub chunks (warp 0) between snapshot refreshes                   // elements per warp-private bulk copy
+constexpr int kRingBytes = kExpandWarps * 2 * kWarpChunk * 4;  // warp double buffers
 
 // Per-level counters (K6). Slot L holds the frontier of level L:
 // discovered = |frontier| (layers[L].input), edges = sum of its degrees
 // (layers[L].edges); bin[] are the bin sizes (entries / items).
 struct alignas(64) Counters {
-  unsigned long long bin[3];
+  unsigned long long bin[4];  // small queue | non-hub list, warp queue, CTA items, group items
   unsigned long long discovered;
   unsigned long long edges;
-  unsigned long long pad[3];
+  unsigned long long pad[2];
 };
 
-struct CtaItem {  // one kChunk-edge slice of a hub's row
-  int32_t v;      // internal id
-  int32_t off;    // offset of the slice in the row
-  int32_t len;    // <= kChunk
-  int32_t v_orig; // original id (the parent id written to pred)
+// A balanced unit of non-hub work: up to 32 consecutive entries of the
+// frontier list (ascending internal ids) and the element range [elo, ehi)
+// of their concatenated rows.
+struct alignas(8) GroupItem {
+  int64_t list_start;
+  int32_t count;
+  int32_t elo, ehi;
+  int32_t pad;
+};
+
+struct alignas(16) CtaItem {  // one kChunk-edge slice of a hub's row
+  int64_t start;   // absolute col_idx offset of the slice
+  int32_t len;     // <= kChunk
+  int32_t u;       // original id of the hub (the parent written to pred)
 };
 
 struct Frontier {
-  const int32_t* small;
+  const int32_t* small;    // after a queue-mode level: small/warp-bin queues ...
   const int32_t* warp;
-  const CtaItem* cta;
-  int64_t n_small, n_warp, n_cta;
+  const CtaItem* cta;      // hub slices (both modes)
+  const int32_t* list;     // ... after a bitmap-mode level: non-hub list + group items
+  const GroupItem* items;
+  int64_t n_small, n_warp, n_cta, n_items;
+};
+
+// Degree classes of the small region: internal ids with degree d form the
+// contiguous range [T[d+1], T[d]) whose rows are contiguous in col_idx,
+// starting at base[d]; T[d] = #vertices with degree >= d.
+struct ClassTable {
+  int32_t T[kSmallMax + 2];
+  int64_t base[kSmallMax + 1];
 };
 
 struct LevelArgs {
@@ -52,6 +76,10 @@ struct LevelArgs {
   uint32_t* visited;
   uint32_t* prev;           // visited at the last bitmap-mode boundary
   int32_t* pred;            // original-id outputs
+  int32_t* pred_int;        // bitmap mode: parent (original id) by internal id
+  const ClassTable* classes;
+  unsigned long long* dbg;  // LBFS_COUNT: candidate-write counters (hot, cold)
+  int32_t refresh_chunks;   // hub chunks between hot-snapshot refreshes (warp 0)
   int32_t* level;
   int32_t next_level;
   int32_t t_cta, t_warp, t_nz;  // internal-id bin boundaries
@@ -69,12 +97,14 @@ struct CompactArgs {
   uint32_t* prev;           // visited at the previous level boundary
   int64_t nwords;
   int32_t* level;
+  int32_t* pred;
+  const int32_t* pred_int;
   int32_t next_level;
   int32_t t_cta, t_warp, t_nz;
   Counters* next_cnt;
-  int32_t* next_small;
-  int32_t* next_warp;
+  int32_t* next_list;
   CtaItem* next_cta;
+  GroupItem* next_items;
 };
 
 class BfsEngine {
@@ -110,12 +140,16 @@ class BfsEngine {
   int32_t* new2old_ = nullptr;
   int32_t* old2new_ = nullptr;
   int32_t t_cta_ = 0, t_warp_ = 0, t_nz_ = 0;
+  ClassTable* classes_ = nullptr;
+  unsigned long long* dbg_ = nullptr;
   uint32_t* visited_ = nullptr;
   uint32_t* prev_ = nullptr;
+  int32_t* pred_int_ = nullptr;
   int32_t* q_small_[2] = {nullptr, nullptr};
   int32_t* q_warp_[2] = {nullptr, nullptr};
   CtaItem* q_cta_[2] = {nullptr, nullptr};
-  int64_t cap_cta_ = 0;
+  GroupItem* q_items_[2] = {nullptr, nullptr};
+  int64_t cap_cta_ = 0, cap_items_ = 0;
   Counters* cnt_ = nullptr;
   Counters* h_cnt_ = nullptr;
   int32_t* own_pred_ = nullptr;
@@ -124,6 +158,13 @@ class BfsEngine {
   cudaEvent_t ev_[6] = {};
   std::vector<lbfs_layer> layers_;
   int expand_grid_ = 0;
+  int32_t hot_words_ = 0;  // visited words mirrored in shared memory
+  int dyn_smem_ = 0;
+  bool trace_ = false;  // LBFS_TRACE=1: per-level table on stderr
+  bool count_ = false;
+  bool split_ = false;
+  bool hub_ldg_ = false;  // LBFS_SPLIT=1: one launch per bin, timed separately
+  cudaEvent_t ev_split_[4] = {};  // LBFS_COUNT=1: count bitmap-mode candidate writes (slow)
 };
 
 }  // namespace lbfs

@@ -34,15 +34,17 @@ __global__ void k_invert(const int32_t* __restrict__ new2old, int64_t n, int32_t
   }
 }
 
-// thresholds over the descending degree sequence: t = #vertices with deg >= X
-__global__ void k_thresholds(const int64_t* __restrict__ deg, int64_t n, int32_t* __restrict__ t3) {
-  const int64_t X[3] = {kCtaMin, kSmallMax, 1};
+// thresholds over the descending degree sequence: t[k] = #vertices with
+// deg >= k for k in [1, kSmallMax + 1], t[0] = #vertices with deg >= kCtaMin
+constexpr int kNumThresh = kSmallMax + 2;
+__global__ void k_thresholds(const int64_t* __restrict__ deg, int64_t n, int32_t* __restrict__ t) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    for (int k = 0; k < 3; ++k) {
-      const bool here = deg[i] >= X[k];
-      const bool next = (i + 1 < n) && deg[i + 1] >= X[k];
-      if (here && !next) t3[k] = (int32_t)(i + 1);
+    for (int k = 0; k < kNumThresh; ++k) {
+      const int64_t X = (k == 0) ? kCtaMin : k;
+      const bool here = deg[i] >= X;
+      const bool next = (i + 1 < n) && deg[i + 1] >= X;
+      if (here && !next) t[k] = (int32_t)(i + 1);
     }
   }
 }
@@ -92,11 +94,11 @@ void BfsEngine::build_layout(const Csr& csr) {
   int64_t* deg64 = dev_alloc<int64_t>((size_t)n + 1);
   LBFS_LAUNCH(k_invert, grid_of(n), 256, 0, st, new2old_, n, old2new_, key_s, deg64);
   LBFS_CUDA(cudaMemsetAsync(deg64 + n, 0, sizeof(int64_t), st));
-  int32_t* d_t3 = dev_alloc<int32_t>(3);
-  LBFS_CUDA(cudaMemsetAsync(d_t3, 0, 3 * sizeof(int32_t), st));
+  int32_t* d_t3 = dev_alloc<int32_t>(kNumThresh);
+  LBFS_CUDA(cudaMemsetAsync(d_t3, 0, kNumThresh * sizeof(int32_t), st));
   LBFS_LAUNCH(k_thresholds, grid_of(n), 256, 0, st, deg64, n, d_t3);
-  int32_t h_t3[3];
-  LBFS_CUDA(cudaMemcpyAsync(h_t3, d_t3, sizeof(h_t3), cudaMemcpyDeviceToHost, st));
+  int32_t h_t[kNumThresh];
+  LBFS_CUDA(cudaMemcpyAsync(h_t, d_t3, sizeof(h_t), cudaMemcpyDeviceToHost, st));
   row_ptr_ = dev_alloc<int64_t>((size_t)n + 1);
   tmp_bytes = 0;
   LBFS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, deg64, row_ptr_, n + 1, st));
@@ -107,9 +109,9 @@ void BfsEngine::build_layout(const Csr& csr) {
   dev_free(deg64);
   dev_free(key_s);
   dev_free(d_t3);
-  t_cta_ = h_t3[0];
-  t_warp_ = std::max(h_t3[1], t_cta_);
-  t_nz_ = std::max(h_t3[2], t_warp_);
+  t_cta_ = h_t[0];
+  t_warp_ = std::max(h_t[kSmallMax], t_cta_);
+  t_nz_ = std::max(h_t[1], t_warp_);
   // 3. gather + map rows (16-byte aligned base, padded for int4 over-reads)
   col_idx_ = dev_alloc<int32_t>((size_t)nnz_ + 8);
   int32_t* unsorted = dev_alloc<int32_t>((size_t)nnz_ + 8);
@@ -148,6 +150,13 @@ void BfsEngine::build_layout(const Csr& csr) {
     r0 = r1;
   }
   dev_free(unsorted);
+  // 5. degree classes of the small region (deg in [1, kSmallMax))
+  ClassTable ct{};
+  for (int d = 1; d <= kSmallMax + 1; ++d) ct.T[d] = h_t[d];
+  ct.T[0] = (int32_t)n;
+  for (int d = 1; d <= kSmallMax; ++d) ct.base[d] = h_rp[(size_t)(d <= kSmallMax ? h_t[std::min(d + 1, kSmallMax + 1)] : 0)];
+  classes_ = dev_alloc<ClassTable>(1);
+  LBFS_CUDA(cudaMemcpyAsync(classes_, &ct, sizeof(ct), cudaMemcpyHostToDevice, st));
   LBFS_CUDA(cudaStreamSynchronize(st));
 }
 
