@@ -7,6 +7,7 @@ it does. A missing library or a missing GPU raises immediately.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -79,7 +80,7 @@ def load(path: Path | str | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        p = Path(path) if path else Path(os.environ.get("LBFS_LIB", LIB_PATH))
         if not p.exists():
             raise RuntimeError(f"{p} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`"
                                " (there is no CPU fallback)")

@@ -313,8 +313,9 @@ __device__ __forceinline__ void expand_group(const LevelArgs& a, const Hot& h, i
   ws.start[lane] = st - (incl - d);
   ws.vert[lane] = uo;
   __syncwarp();
-  for (int e0 = elo; e0 < end; e0 += 128) {
-    int32_t nb[4], par[4];
+  // software-pipelined 128-element windows: window i+1's col_idx loads are
+  // in flight while window i is probed
+  auto load_win = [&](int e0, int32_t (&nb)[4], int32_t (&par)[4]) -> uint32_t {
     uint32_t okm = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -328,7 +329,19 @@ __device__ __forceinline__ void expand_group(const LevelArgs& a, const Hot& h, i
       nb[k] = ok ? ld_stream(a.col_idx + ws.start[lo] + e) : 0;
       par[k] = ws.vert[lo];
     }
-    probe_batch<M, 4>(a, h, nb, okm, [&](int k) { return par[k]; }, lane, acc);
+    return okm;
+  };
+  int32_t nbA[4], parA[4], nbB[4], parB[4];
+  uint32_t okA = elo < end ? load_win(elo, nbA, parA) : 0u;
+  for (int e0 = elo; e0 < end; e0 += 128) {
+    const uint32_t okB = (e0 + 128 < end) ? load_win(e0 + 128, nbB, parB) : 0u;
+    probe_batch<M, 4>(a, h, nbA, okA, [&](int k) { return parA[k]; }, lane, acc);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      nbA[k] = nbB[k];
+      parA[k] = parB[k];
+    }
+    okA = okB;
   }
   __syncwarp();
 }
@@ -345,8 +358,7 @@ __device__ __forceinline__ void expand_class_group(const LevelArgs& a, const Hot
   const int32_t* rows = a.col_idx + B[d];
   const uint32_t rcp = (uint32_t)(0xFFFFFFFFull / (uint32_t)d + 1ull);  // e / d for e < 2^27, d >= 2
   const int end = min(ehi, n * d);
-  for (int e0 = elo; e0 < end; e0 += 128) {
-    int32_t nb[4], par[4];
+  auto load_win = [&](int e0, int32_t (&nb)[4], int32_t (&par)[4]) -> uint32_t {
     uint32_t okm = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -358,7 +370,19 @@ __device__ __forceinline__ void expand_class_group(const LevelArgs& a, const Hot
       par[k] = __shfl_sync(kFull, vo, q);
       nb[k] = ok ? ld_stream(rows + ro + (e - q * d)) : 0;
     }
-    probe_batch<M, 4>(a, h, nb, okm, [&](int k) { return par[k]; }, lane, acc);
+    return okm;
+  };
+  int32_t nbA[4], parA[4], nbB[4], parB[4];
+  uint32_t okA = elo < end ? load_win(elo, nbA, parA) : 0u;
+  for (int e0 = elo; e0 < end; e0 += 128) {
+    const uint32_t okB = (e0 + 128 < end) ? load_win(e0 + 128, nbB, parB) : 0u;
+    probe_batch<M, 4>(a, h, nbA, okA, [&](int k) { return parA[k]; }, lane, acc);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      nbA[k] = nbB[k];
+      parA[k] = parB[k];
+    }
+    okA = okB;
   }
 }
 
@@ -394,6 +418,57 @@ __device__ __forceinline__ uint32_t slice_mask(int32_t (&nb)[8], int lo, int hi,
   return okm;
 }
 
+// A warp walks row slices (grid-stride over items) in 128-element chunks of
+// one 128-bit load per lane; the loads of chunk i+1 are issued before chunk
+// i is probed.
+template <int M>
+__device__ __forceinline__ void stream_slices(const LevelArgs& a, const Hot& h, const CtaItem* items, int64_t n,
+                                              int64_t gwarp, int64_t nwarps, int lane, Acc& acc) {
+  if (gwarp >= n) return;
+  int64_t it = gwarp;
+  CtaItem cur = items[it];
+  int64_t pos = cur.start & ~int64_t(3);
+  int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
+  auto load = [&](int64_t p0, int64_t e0) {
+    const int64_t i1 = p0 + lane * 4;
+    return i1 < e0 ? ld_stream4(a.col_idx + i1) : make_int4(0, 0, 0, 0);
+  };
+  int4 x = load(pos, end);
+  while (true) {
+    const int64_t cbase = pos;
+    const CtaItem ci = cur;
+    pos += 128;
+    bool more = true;
+    if (pos >= end) {
+      it += nwarps;
+      if (it < n) {
+        cur = items[it];
+        pos = cur.start & ~int64_t(3);
+        end = (cur.start + cur.len + 3) & ~int64_t(3);
+      } else {
+        more = false;
+      }
+    }
+    const int4 nx = more ? load(pos, end) : make_int4(0, 0, 0, 0);
+    int32_t nb[4] = {x.x, x.y, x.z, x.w};
+    const int lo = (int)(ci.start - cbase) - lane * 4, hi = (int)(ci.start + ci.len - cbase) - lane * 4;
+    uint32_t okm = 0xFu;
+    if (lo > 0 || hi < 4) {  // first/last chunk of a slice
+      okm = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool ok = q >= lo && q < hi;
+        okm |= (uint32_t)ok << q;
+        nb[q] = ok ? nb[q] : 0;
+      }
+    }
+    const int32_t pu = ci.u;
+    probe_batch<M, 4>(a, h, nb, okm, [&](int) { return pu; }, lane, acc);
+    if (!more) break;
+    x = nx;
+  }
+}
+
 struct ChunkMeta {
   int64_t base;    // col_idx index of the chunk's first staged element
   int64_t lo, hi;  // valid element range of the owning slice
@@ -403,9 +478,9 @@ struct ChunkMeta {
 // One persistent CTA per SM (kExpandWarps warps) holding a shared-memory copy
 // of the hot visited prefix (hot_words words, one bulk copy at kernel start,
 // updated by the CTA's own discoveries). `phases` selects bins (debug split).
-template <int M>
-__global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Frontier f, int32_t hot_words,
-                                                               int phases) {
+template <int M, int kPhases>
+__global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Frontier f, int32_t hot_words) {
+  constexpr int phases = kPhases;
   extern __shared__ __align__(128) uint8_t s_dyn[];
   __shared__ __align__(8) uint64_t s_bar[kExpandWarps][2];
   __shared__ __align__(8) uint64_t s_hot_bar;
@@ -502,47 +577,11 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
     }
   }
 
-  // ---- phase 1 (variant): hub slices with register double-buffering ------
-  if ((phases & 8) && gwarp < f.n_cta) {
-    // the warp walks its slices in 256-element chunks; the loads of chunk
-    // i+1 are issued before chunk i is probed
-    int64_t it = gwarp;
-    CtaItem cur = f.cta[it];
-    int64_t pos = cur.start & ~int64_t(3);
-    int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
-    int4 x = make_int4(0, 0, 0, 0), y = x;
-    auto load_chunk = [&](int64_t p0, int64_t e0, int4& xa, int4& ya) {
-      const int64_t i1 = p0 + lane * 4, i2 = p0 + 128 + lane * 4;
-      xa = i1 < e0 ? ld_stream4(a.col_idx + i1) : make_int4(0, 0, 0, 0);
-      ya = i2 < e0 ? ld_stream4(a.col_idx + i2) : make_int4(0, 0, 0, 0);
-    };
-    load_chunk(pos, end, x, y);
-    while (true) {
-      const int64_t cbase = pos;
-      const CtaItem ci = cur;
-      pos += kWarpChunk;
-      bool more = true;
-      if (pos >= end) {
-        it += nwarps;
-        if (it < f.n_cta) {
-          cur = f.cta[it];
-          pos = cur.start & ~int64_t(3);
-          end = (cur.start + cur.len + 3) & ~int64_t(3);
-        } else {
-          more = false;
-        }
-      }
-      int4 nx = make_int4(0, 0, 0, 0), ny = nx;
-      if (more) load_chunk(pos, end, nx, ny);
-      int32_t nb[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
-      const uint32_t okm = slice_mask(nb, (int)(ci.start - cbase), (int)(ci.start + ci.len - cbase), lane);
-      const int32_t pu = ci.u;
-      probe_batch<M, 8>(a, h, nb, okm, [&](int) { return pu; }, lane, acc);
-      if (!more) break;
-      x = nx;
-      y = ny;
-    }
-  }
+  // ---- phase 1 (variant): hub slices through registers instead of TMA ----
+  if (phases & 8) stream_slices<M>(a, h, f.cta, f.n_cta, gwarp, nwarps, lane, acc);
+
+  // ---- phase 2a: warp-bin rows (32 <= deg < kCtaMin), one slice each -----
+  if (phases & 16) stream_slices<M>(a, h, f.wslice, f.n_wslice, gwarp, nwarps, lane, acc);
 
   // ---- phase 2: non-hub frontier as balanced group items -----------------
   for (int64_t it = gwarp; (phases & 2) && it < f.n_items; it += nwarps) {
@@ -605,14 +644,16 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
   __shared__ uint32_t s_new[kCompactWords];
   __shared__ uint32_t s_lmask[kCompactWords];
   __shared__ int32_t s_lpre[kCompactWords];
+  __shared__ uint32_t s_wmask[kCompactWords];
+  __shared__ int32_t s_wpre[kCompactWords];
   __shared__ int32_t s_deg[kCompactVerts];
   __shared__ int32_t s_gsum[kCompactWords];
   __shared__ int32_t s_w[4];
-  __shared__ unsigned long long s_base[3];
+  __shared__ unsigned long long s_base[4];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t w0 = (int64_t)blockIdx.x * kCompactWords;
   const int64_t v0 = w0 * 32;
-  uint32_t nb = 0, mhub = 0, mlist = 0;
+  uint32_t nb = 0, mhub = 0, mlist = 0, mwarp = 0;
   int hub_items = 0;
   if (t < kCompactWords && w0 + t < c.nwords) {
     const uint32_t w = c.visited[w0 + t], p = c.prev[w0 + t];
@@ -621,7 +662,8 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
       c.prev[w0 + t] = w;
       const int64_t vw = (w0 + t) * 32;
       mhub = nb & range_mask(vw, 0, c.t_cta);
-      mlist = nb & range_mask(vw, c.t_cta, c.t_nz);
+      mwarp = nb & range_mask(vw, c.t_cta, c.t_warp);
+      mlist = nb & range_mask(vw, c.t_warp, c.t_nz);
       for (uint32_t m = mhub; m; m &= m - 1) {
         const int64_t v = vw + __ffs(m) - 1;
         hub_items += (int)((c.row_ptr[v + 1] - c.row_ptr[v] + kChunk - 1) / kChunk);
@@ -632,14 +674,18 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
   if (t < kCompactWords) {
     s_new[t] = nb;
     s_lmask[t] = mlist;
+    s_wmask[t] = mwarp;
   }
-  int n_list = 0, n_hub_items = 0;
+  int n_list = 0, n_hub_items = 0, n_wsl = 0;
   const int lpre = scan128(__popc(mlist), s_w, &n_list);
   if (t < kCompactWords) s_lpre[t] = lpre;
+  const int wpre = scan128(__popc(mwarp), s_w, &n_wsl);
+  if (t < kCompactWords) s_wpre[t] = wpre;
   const int ipre = scan128(hub_items, s_w, &n_hub_items);
   if (t == 0) {
     s_base[0] = n_list ? atomicAdd(&c.next_cnt->bin[kBinSmall], (unsigned long long)n_list) : 0;
     s_base[1] = n_hub_items ? atomicAdd(&c.next_cnt->bin[kBinCta], (unsigned long long)n_hub_items) : 0;
+    s_base[3] = n_wsl ? atomicAdd(&c.next_cnt->bin[kBinWSlice], (unsigned long long)n_wsl) : 0;
   }
   __syncthreads();
   if (mhub) {  // hub slices, written by the owner thread of each word
@@ -666,6 +712,9 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
     const int64_t st = c.row_ptr[v];
     const int32_t deg = (int32_t)(c.row_ptr[v + 1] - st);
     edges += (unsigned long long)deg;
+    const uint32_t wm = s_wmask[wl];
+    if ((wm >> b) & 1u)
+      c.next_wslice[s_base[3] + s_wpre[wl] + __popc(wm & ((1u << b) - 1u))] = CtaItem{st, deg, vo};
     const uint32_t lm = s_lmask[wl];
     if ((lm >> b) & 1u) {
       const int r = s_lpre[wl] + __popc(lm & ((1u << b) - 1u));
@@ -782,6 +831,7 @@ BfsEngine::BfsEngine(const Csr& csr) {
     q_warp_[b] = dev_alloc<int32_t>((size_t)std::max<int64_t>(t_warp_, 1));
     q_cta_[b] = dev_alloc<CtaItem>((size_t)cap_cta_);
     q_items_[b] = dev_alloc<GroupItem>((size_t)cap_items_);
+    q_wslice_[b] = dev_alloc<CtaItem>((size_t)std::max<int64_t>(t_warp_ - t_cta_, 1));
   }
   cnt_ = dev_alloc<Counters>(kCounterRing);
   LBFS_CUDA(cudaMallocHost(&h_cnt_, sizeof(Counters) * kCounterRing));
@@ -789,16 +839,25 @@ BfsEngine::BfsEngine(const Csr& csr) {
   for (auto& e : ev_split_) LBFS_CUDA(cudaEventCreate(&e));
   int occ = 0;
   // shared memory: the TMA ring plus as much of the visited bitmap as fits
-  cudaFuncAttributes fa{};
-  LBFS_CUDA(cudaFuncGetAttributes(&fa, k_expand<kBitmapOut>));
+  // (static shared memory differs per phase kernel: take the largest)
+  const void* kernels[] = {(const void*)k_expand<kBitmapOut, 1>,  (const void*)k_expand<kBitmapOut, 2>,
+                           (const void*)k_expand<kBitmapOut, 4>,  (const void*)k_expand<kBitmapOut, 8>,
+                           (const void*)k_expand<kBitmapOut, 16>, (const void*)k_expand<kQueueOut, 1>,
+                           (const void*)k_expand<kQueueOut, 2>,   (const void*)k_expand<kQueueOut, 4>,
+                           (const void*)k_expand<kQueueOut, 8>,   (const void*)k_expand<kQueueOut, 16>};
+  size_t max_static = 0;
+  for (auto fn : kernels) {
+    cudaFuncAttributes fa{};
+    LBFS_CUDA(cudaFuncGetAttributes(&fa, fn));
+    max_static = std::max(max_static, fa.sharedSizeBytes);
+  }
   int optin = 0;
   LBFS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device_));
-  const int64_t avail = (int64_t)optin - (int64_t)fa.sharedSizeBytes - kRingBytes - 1024;
+  const int64_t avail = (int64_t)optin - (int64_t)max_static - kRingBytes - 1024;
   hot_words_ = (int32_t)std::min<int64_t>(std::max<int64_t>(avail / 4, 0) & ~int64_t(3), (nwords_ + 3) & ~int64_t(3));
   dyn_smem_ = kRingBytes + hot_words_ * 4;
-  LBFS_CUDA(cudaFuncSetAttribute(k_expand<kBitmapOut>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_));
-  LBFS_CUDA(cudaFuncSetAttribute(k_expand<kQueueOut>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_));
-  LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<kBitmapOut>, kExpandThreads, dyn_smem_));
+  for (auto fn : kernels) LBFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_));
+  LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<kBitmapOut, 2>, kExpandThreads, dyn_smem_));
   expand_grid_ = sm_count_ * std::max(occ, 1);
 }
 
@@ -814,6 +873,7 @@ BfsEngine::~BfsEngine() {
     dev_free(q_warp_[b]);
     dev_free(q_cta_[b]);
     dev_free(q_items_[b]);
+    dev_free(q_wslice_[b]);
   }
   dev_free(cnt_);
   if (h_cnt_) cudaFreeHost(h_cnt_);
@@ -835,6 +895,32 @@ void BfsEngine::ensure_own_outputs() {
 
 static unsigned clamp_grid(int64_t blocks, int64_t cap) {
   return (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
+}
+
+template <int M>
+static void launch_expand_m(int pi, unsigned grid, int smem, const LevelArgs& a, const Frontier& f, int32_t hot,
+                            bool hub_ldg, cudaStream_t st) {
+  if (pi == 0) {
+    if (hub_ldg) {
+      LBFS_LAUNCH((k_expand<M, 8>), grid, kExpandThreads, smem, st, a, f, hot);
+    } else {
+      LBFS_LAUNCH((k_expand<M, 1>), grid, kExpandThreads, smem, st, a, f, hot);
+    }
+  } else if (pi == 1) {
+    LBFS_LAUNCH((k_expand<M, 2>), grid, kExpandThreads, smem, st, a, f, hot);
+  } else if (pi == 3) {
+    LBFS_LAUNCH((k_expand<M, 16>), grid, kExpandThreads, smem, st, a, f, hot);
+  } else {
+    LBFS_LAUNCH((k_expand<M, 4>), grid, kExpandThreads, smem, st, a, f, hot);
+  }
+}
+
+void BfsEngine::launch_expand(bool bitmap, int pi, unsigned grid, const LevelArgs& a, const Frontier& f,
+                              cudaStream_t st) {
+  if (bitmap)
+    launch_expand_m<kBitmapOut>(pi, grid, dyn_smem_, a, f, hot_words_, hub_ldg_, st);
+  else
+    launch_expand_m<kQueueOut>(pi, grid, kRingBytes, a, f, 0, hub_ldg_, st);
 }
 
 static bool env_flag(const char* name) {
@@ -909,6 +995,8 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       f.list = q_small_[cur];
       f.items = q_items_[cur];
       f.n_items = (int64_t)c.bin[kBinItems];
+      f.wslice = q_wslice_[cur];
+      f.n_wslice = (int64_t)c.bin[kBinWSlice];
     } else {  // winners appended to raw queues
       f.small = q_small_[cur];
       f.warp = q_warp_[cur];
@@ -917,38 +1005,30 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     }
     const bool bitmap = c.edges >= bitmap_min_edges;
     const int64_t need = std::max({(f.n_cta + kExpandWarps - 1) / kExpandWarps,
+                                    (f.n_wslice + kExpandWarps - 1) / kExpandWarps,
                                     (f.n_items + kExpandWarps - 1) / kExpandWarps,
                                     (f.n_warp + (f.n_small + 31) / 32 + kExpandWarps - 1) / kExpandWarps,
                                     (int64_t)1});
     const unsigned grid = bitmap ? (unsigned)expand_grid_ : clamp_grid(need, expand_grid_);
     LBFS_CUDA(cudaEventRecord(ev_[2], st));
-    float split_ms[3] = {0.f, 0.f, 0.f};
-    if (f.n_cta + f.n_warp + f.n_small + f.n_items > 0) {
-      const int nparts = split_ ? 3 : 1;
-      for (int pi = 0; pi < nparts; ++pi) {
-        int phases = split_ ? (1 << pi) : 7;
-        if (hub_ldg_ && (phases & 1)) phases = (phases & ~1) | 8;
-        if (split_ && env_flag("LBFS_SPLIT_TWICE")) {  // experiment: same phase launched twice
-          if (bitmap) {
-            LBFS_LAUNCH(k_expand<kBitmapOut>, grid, kExpandThreads, dyn_smem_, st, a, f, hot_words_, phases);
-          } else {
-            LBFS_LAUNCH(k_expand<kQueueOut>, grid, kExpandThreads, kRingBytes, st, a, f, 0, phases);
-          }
-        }
+    float split_ms[4] = {0.f, 0.f, 0.f, 0.f};
+    if (f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice > 0) {
+      // one launch per non-empty bin: each phase kernel gets its own register
+      // allocation (the fused kernel was capped at 64 registers by 1024 threads)
+      const bool has[4] = {f.n_cta > 0, f.n_items > 0, f.n_warp + f.n_small > 0, f.n_wslice > 0};
+      for (int pi = 0; pi < 4; ++pi) {
         if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[pi], st));
-        if (bitmap) {
-          LBFS_LAUNCH(k_expand<kBitmapOut>, grid, kExpandThreads, dyn_smem_, st, a, f, hot_words_, phases);
-        } else {
-          LBFS_LAUNCH(k_expand<kQueueOut>, grid, kExpandThreads, kRingBytes, st, a, f, 0, phases);
-        }
+        if (!has[pi]) continue;
+        launch_expand(bitmap, pi, grid, a, f, st);
       }
-      if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[3], st));
+      if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[4], st));
     }
     LBFS_CUDA(cudaEventRecord(ev_[3], st));
     const bool did_compact = bitmap;
     if (bitmap) {
       CompactArgs ca{row_ptr_, new2old_, visited_, prev_, nwords_, d_level, d_pred, pred_int_, (int32_t)(L + 1),
-                     t_cta_, t_warp_, t_nz_, &cnt_[slot], q_small_[cur ^ 1], q_cta_[cur ^ 1], q_items_[cur ^ 1]};
+                     t_cta_, t_warp_, t_nz_, &cnt_[slot], q_small_[cur ^ 1], q_cta_[cur ^ 1], q_items_[cur ^ 1],
+                     q_wslice_[cur ^ 1]};
       LBFS_LAUNCH(k_compact, (unsigned)((n_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
     }
     LBFS_CUDA(cudaEventRecord(ev_[5], st));
@@ -965,9 +1045,10 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       LBFS_CUDA(cudaMemset(dbg_, 0, sizeof(dbg)));
       fprintf(stderr, "[lbfs]      candidate writes hot=%llu cold=%llu\n", dbg[0], dbg[1]);
     }
-    if (split_ && (f.n_cta + f.n_warp + f.n_small + f.n_items > 0)) {
-      for (int pi = 0; pi < 3; ++pi) LBFS_CUDA(cudaEventElapsedTime(&split_ms[pi], ev_split_[pi], ev_split_[pi + 1]));
-      fprintf(stderr, "[lbfs]      split: cta=%.3fms warp=%.3fms small=%.3fms\n", split_ms[0], split_ms[1], split_ms[2]);
+    if (split_ && (f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice > 0)) {
+      for (int pi = 0; pi < 4; ++pi) LBFS_CUDA(cudaEventElapsedTime(&split_ms[pi], ev_split_[pi], ev_split_[pi + 1]));
+      fprintf(stderr, "[lbfs]      split: hub=%.3fms items=%.3fms queues=%.3fms wslice=%.3fms\n", split_ms[0],
+              split_ms[1], split_ms[2], split_ms[3]);
     }
     if (trace_)
       fprintf(stderr,

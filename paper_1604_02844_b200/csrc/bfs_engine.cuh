@@ -17,23 +17,26 @@ constexpr int32_t kSentinel = LBFS_SENTINEL;  // traversal.py:22
 constexpr int kSmallMax = 32;                 // deg < 32: warp-cooperative small bin
 constexpr int kCtaMin = 1024;                 // deg >= 1024: CTA bin (TMA-staged chunks)
 constexpr int kChunk = 3960;                  // edges per CTA-bin item (<= 992 staged int4 slots)
-constexpr int kBinSmall = 0, kBinWarp = 1, kBinCta = 2, kBinItems = 3;
+constexpr int kBinSmall = 0, kBinWarp = 1, kBinCta = 2, kBinItems = 3, kBinWSlice = 4;
 constexpr int kItemElems = 512;               // elements per group item (load balance unit)
 constexpr int kCounterRing = 3;
-constexpr int kExpandWarps = 32;
+#ifndef LBFS_EXPAND_WARPS
+#define LBFS_EXPAND_WARPS 32
+#endif
+constexpr int kExpandWarps = LBFS_EXPAND_WARPS;
 constexpr int kExpandThreads = 32 * kExpandWarps;
-constexpr int kWarpChunk = 256;
-constexpr int kRefreshChunks = 4;                 // hub chunks (warp 0) between snapshot refreshes                   // elements per warp-private bulk copy
+constexpr int kWarpChunk = 256;                   // elements per warp-private bulk copy
+constexpr int kRefreshChunks = 4;                 // hub chunks (warp 0) between snapshot refreshes
 constexpr int kRingBytes = kExpandWarps * 2 * kWarpChunk * 4;  // warp double buffers
 
 // Per-level counters (K6). Slot L holds the frontier of level L:
 // discovered = |frontier| (layers[L].input), edges = sum of its degrees
 // (layers[L].edges); bin[] are the bin sizes (entries / items).
 struct alignas(64) Counters {
-  unsigned long long bin[4];  // small queue | non-hub list, warp queue, CTA items, group items
+  unsigned long long bin[5];  // small queue | small list, warp queue, hub slices, group items, warp slices
   unsigned long long discovered;
   unsigned long long edges;
-  unsigned long long pad[2];
+  unsigned long long pad[1];
 };
 
 // A balanced unit of non-hub work: up to 32 consecutive entries of the
@@ -56,9 +59,10 @@ struct Frontier {
   const int32_t* small;    // after a queue-mode level: small/warp-bin queues ...
   const int32_t* warp;
   const CtaItem* cta;      // hub slices (both modes)
+  const CtaItem* wslice;   // warp-bin rows as slices (after a bitmap-mode level)
   const int32_t* list;     // ... after a bitmap-mode level: non-hub list + group items
   const GroupItem* items;
-  int64_t n_small, n_warp, n_cta, n_items;
+  int64_t n_small, n_warp, n_cta, n_items, n_wslice;
 };
 
 // Degree classes of the small region: internal ids with degree d form the
@@ -105,6 +109,7 @@ struct CompactArgs {
   int32_t* next_list;
   CtaItem* next_cta;
   GroupItem* next_items;
+  CtaItem* next_wslice;
 };
 
 class BfsEngine {
@@ -132,6 +137,7 @@ class BfsEngine {
 
  private:
   void build_layout(const Csr& csr);
+  void launch_expand(bool bitmap, int pi, unsigned grid, const LevelArgs& a, const Frontier& f, cudaStream_t st);
 
   int device_ = 0, sm_count_ = 0;
   int64_t n_ = 0, nnz_ = 0, nwords_ = 0, npad_ = 0;
@@ -149,6 +155,7 @@ class BfsEngine {
   int32_t* q_warp_[2] = {nullptr, nullptr};
   CtaItem* q_cta_[2] = {nullptr, nullptr};
   GroupItem* q_items_[2] = {nullptr, nullptr};
+  CtaItem* q_wslice_[2] = {nullptr, nullptr};
   int64_t cap_cta_ = 0, cap_items_ = 0;
   Counters* cnt_ = nullptr;
   Counters* h_cnt_ = nullptr;
@@ -164,7 +171,7 @@ class BfsEngine {
   bool count_ = false;
   bool split_ = false;
   bool hub_ldg_ = false;  // LBFS_SPLIT=1: one launch per bin, timed separately
-  cudaEvent_t ev_split_[4] = {};  // LBFS_COUNT=1: count bitmap-mode candidate writes (slow)
+  cudaEvent_t ev_split_[5] = {};  // LBFS_COUNT=1: count bitmap-mode candidate writes (slow)
 };
 
 }  // namespace lbfs
