@@ -38,13 +38,14 @@ FALLBACK_HBM_GBS = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--roots", type=int, default=64)
     ap.add_argument("--e2e-roots", type=int, default=16, help="roots per step timed through bfs()")
-    ap.add_argument("--cpu-roots", type=int, default=2, help="roots in the CPU-baseline sample")
+    ap.add_argument("--cpu-roots", type=int, default=2, help="roots per step of the --impl reference arm")
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU-baseline sampling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -125,14 +126,17 @@ def traffic_from_profiles():
     return None
 
 
-def cpu_baseline_sample(rp, ci, roots, k):
-    """Oracle port of bfs_parallel_naive on all host cores (rank 0, N=1)."""
+def cpu_baseline_sample(rp, ci, roots, budget_s):
+    """Oracle port of bfs_parallel_naive on all host cores (rank 0, N=1):
+    roots in order until ~budget_s seconds of CPU work (at least 2)."""
     import oracle
 
     vals = []
     threads = oracle.max_threads()
     t_all = time.perf_counter()
-    for r in roots[:k]:
+    for i, r in enumerate(roots):
+        if i >= 2 and time.perf_counter() - t_all > budget_s:
+            break
         t0 = time.perf_counter()
         pred, lvl, layers = oracle.bfs_parallel(rp, ci, int(r), 0)
         dt = time.perf_counter() - t0
@@ -274,7 +278,7 @@ def run_ours(args, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rp, ci = g.colstarts, g.rows
-        vals, thr, secs = cpu_baseline_sample(rp, ci, roots, args.cpu_roots)
+        vals, thr, secs = cpu_baseline_sample(rp, ci, roots, args.cpu_budget)
         cpu = {"value": hm(vals), "unit": "GTEPS", "cores": thr, "kind": "port",
                "sample": f"{len(vals)} of the {args.roots} roots on the same graph, oracle bfs_parallel "
                          f"(OpenMP restatement of bfs_parallel_naive), {secs:.1f}s"}

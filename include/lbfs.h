@@ -74,6 +74,10 @@ const char* lbfs_last_error(void);
 int lbfs_device_info_get(int device, lbfs_device_info* out);
 /* Number of kernel launches this process has issued through the library. */
 int64_t lbfs_kernel_launch_count(void);
+/* Page-locked host memory for BFS outputs (D2H at full PCIe rate); the
+ * Python layer pools these buffers behind the numpy arrays it returns. */
+int lbfs_host_alloc(int64_t bytes, void** out);
+void lbfs_host_free(void* p);
 
 /* ---- graph construction (reference graph.py) -------------------------- */
 

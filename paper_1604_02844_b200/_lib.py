@@ -51,6 +51,8 @@ SIGNATURES = {
     "lbfs_last_error": (ctypes.c_char_p, []),
     "lbfs_device_info_get": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(DeviceInfo)]),
     "lbfs_kernel_launch_count": (_i64, []),
+    "lbfs_host_alloc": (ctypes.c_int, [_i64, ctypes.POINTER(_p)]),
+    "lbfs_host_free": (None, [_p]),
     "lbfs_rmat_edges": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_double, ctypes.c_double,
                                        ctypes.c_double, _p, _p, _p]),
     "lbfs_permute_edges": (ctypes.c_int, [_i64, ctypes.c_uint64, _p, _p, _i64]),
@@ -123,3 +125,37 @@ def device_info(device: int = 0) -> DeviceInfo:
 
 def kernel_launch_count() -> int:
     return int(load().lbfs_kernel_launch_count())
+
+
+# ---------------------------------------------------------------- pinned pool
+_pool: dict[int, list[int]] = {}
+_pool_lock = threading.Lock()
+_POOL_KEEP = 4  # free buffers kept per size
+
+
+def _pool_put(nbytes: int, addr: int) -> None:
+    with _pool_lock:
+        lst = _pool.setdefault(nbytes, [])
+        if len(lst) < _POOL_KEEP:
+            lst.append(addr)
+            return
+    load().lbfs_host_free(addr)
+
+
+def pinned_empty(count: int, dtype=np.int32) -> np.ndarray:
+    """numpy array backed by page-locked memory from a small pool; the buffer
+    returns to the pool when the array (and its views) are garbage."""
+    import weakref
+
+    dt = np.dtype(dtype)
+    nbytes = max(int(count) * dt.itemsize, 16)
+    with _pool_lock:
+        lst = _pool.get(nbytes)
+        addr = lst.pop() if lst else None
+    if addr is None:
+        out = ctypes.c_void_p()
+        check(load().lbfs_host_alloc(nbytes, ctypes.byref(out)))
+        addr = out.value
+    raw = (ctypes.c_byte * nbytes).from_address(addr)
+    weakref.finalize(raw, _pool_put, nbytes, addr)
+    return np.frombuffer(raw, dtype=dt, count=int(count))

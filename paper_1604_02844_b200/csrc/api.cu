@@ -65,6 +65,23 @@ const char* lbfs_last_error(void) { return t_err.c_str(); }
 
 int64_t lbfs_kernel_launch_count(void) { return g_launches.load(); }
 
+int lbfs_host_alloc(int64_t bytes, void** out) {
+  return guarded([&] {
+    if (!out || bytes < 0) throw_inval("bad arguments");
+    void* p = nullptr;
+    cudaError_t e = cudaHostAlloc(&p, (size_t)std::max<int64_t>(bytes, 16), cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      throw Failure(LBFS_ENOMEM, std::string("cudaHostAlloc failed: ") + cudaGetErrorString(e));
+    }
+    *out = p;
+  });
+}
+
+void lbfs_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int lbfs_device_info_get(int device, lbfs_device_info* out) {
   return guarded([&] {
     if (!out) throw_inval("out is NULL");

@@ -45,12 +45,16 @@ class PredecessorArray:
 
     infinity_sentinel = SENTINEL
 
-    def __init__(self, num_vertices: int, _fill: bool = True):
+    def __init__(self, num_vertices: int, _fill: bool = True, _storage: np.ndarray | None = None):
         assert num_vertices >= 1
         padded = (num_vertices + BITS_PER_WORD - 1) // BITS_PER_WORD * BITS_PER_WORD
         self.num_vertices = num_vertices
-        self.storage = (np.full(padded, SENTINEL, dtype=np.int32) if _fill
-                        else np.empty(padded, dtype=np.int32))
+        if _storage is not None:
+            assert len(_storage) == padded
+            self.storage = _storage
+        else:
+            self.storage = (np.full(padded, SENTINEL, dtype=np.int32) if _fill
+                            else np.empty(padded, dtype=np.int32))
 
     @property
     def p(self) -> np.ndarray:
@@ -134,8 +138,11 @@ def bfs(g, s: int) -> BfsResult:
     n = g.num_vertices
     assert 0 <= s < n
     h = _handle(g)
-    pred = PredecessorArray(n, _fill=False)
-    levels = np.empty(n, dtype=np.int32)
+    padded = (n + BITS_PER_WORD - 1) // BITS_PER_WORD * BITS_PER_WORD
+    # outputs land in page-locked memory (pooled), so the D2H copy inside the
+    # call runs at full link rate
+    pred = PredecessorArray(n, _storage=_lib.pinned_empty(padded))
+    levels = _lib.pinned_empty(n)
     buf = (_lib.Layer * _LAYER_CAP)()
     k = ctypes.c_int64()
     t = _lib.Timing()
