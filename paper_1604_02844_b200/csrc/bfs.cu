@@ -144,8 +144,8 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, bool cand, int3
   if (win) {
     atomicOr(a.prev + (v >> 5), 1u << (v & 31));  // keep bitmap-mode compaction exact
     vo = __ldg(a.new2old + v);
-    a.level[vo] = a.next_level;
-    a.pred[vo] = u;  // parents travel as original ids
+    a.level_int[v] = a.next_level;  // internal order; k_finalize writes the outputs
+    a.pred_int[v] = u;              // parents travel as original ids
     st = a.row_ptr[v];
     deg = (int32_t)(a.row_ptr[v + 1] - st);
     acc.disc += 1;
@@ -463,6 +463,7 @@ __device__ __forceinline__ void stream_slices(const LevelArgs& a, const Hot& h, 
       }
     }
     const int32_t pu = ci.u;
+    if (a.dbg) atomicAdd(a.dbg + 2, (unsigned long long)__popc(okm));  // LBFS_COUNT: slice elements
     probe_batch<M, 4>(a, h, nb, okm, [&](int) { return pu; }, lane, acc);
     if (!more) break;
     x = nx;
@@ -482,9 +483,9 @@ template <int M, int kPhases>
 __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Frontier f, int32_t hot_words) {
   constexpr int phases = kPhases;
   extern __shared__ __align__(128) uint8_t s_dyn[];
-  __shared__ __align__(8) uint64_t s_bar[kExpandWarps][2];
+  __shared__ __align__(8) uint64_t s_bar[kExpandWarps][kWarpStages];
   __shared__ __align__(8) uint64_t s_hot_bar;
-  __shared__ ChunkMeta s_meta[kExpandWarps][2];
+  __shared__ ChunkMeta s_meta[kExpandWarps][kWarpStages];
   __shared__ WarpScratch s_ws[kExpandWarps];
   __shared__ int32_t s_T[kSmallMax + 2];
   __shared__ int64_t s_B[kSmallMax + 1];
@@ -497,10 +498,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
   WarpScratch& ws = s_ws[wib];
   Acc acc;
 
-  if (lane == 0) {
-    mbar_init(&s_bar[wib][0], 1);
-    mbar_init(&s_bar[wib][1], 1);
-  }
+  if (lane == 0)
+    for (int b = 0; b < kWarpStages; ++b) mbar_init(&s_bar[wib][b], 1);
   if (tid == 0) {
     mbar_init(&s_hot_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -520,8 +519,10 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
   const int refresh_every = hot_words > 0 ? a.refresh_chunks : 0;
 
   // ---- phase 1: CTA bin, warp-private bulk-copy streams -------------------
+  // a kWarpStages-deep ring of kWarpChunk-element buffers per warp: lane 0
+  // keeps kWarpStages-1 chunks in flight while the warp probes one
   if ((phases & 1) && gwarp < f.n_cta) {
-    int32_t* wbuf = reinterpret_cast<int32_t*>(s_dyn) + (size_t)wib * 2 * kWarpChunk;
+    int32_t* wbuf = reinterpret_cast<int32_t*>(s_dyn) + (size_t)wib * kWarpStages * kWarpChunk;
     // lane-0 stream state: current slice [pos, end) (16-B aligned), next slice prefetched
     int64_t it = gwarp;
     CtaItem cur = f.cta[it];
@@ -529,10 +530,10 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
     if (it + nwarps < f.n_cta) pre = f.cta[it + nwarps];
     int64_t pos = cur.start & ~int64_t(3);
     int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
-    auto issue = [&](int b) -> int {  // lane 0: next chunk into buffer b; 0 when exhausted
+    auto issue = [&](int b) -> uint32_t {  // lane 0: next chunk into buffer b; 0 when exhausted
       if (pos >= end) {
         it += nwarps;
-        if (it >= f.n_cta) return 0;
+        if (it >= f.n_cta) return 0u;
         cur = pre;
         if (it + nwarps < f.n_cta) pre = f.cta[it + nwarps];
         pos = cur.start & ~int64_t(3);
@@ -543,26 +544,56 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
       mbar_expect_tx(&s_bar[wib][b], (uint32_t)(cnt * 4));
       bulk_g2s(wbuf + b * kWarpChunk, a.col_idx + pos, (uint32_t)(cnt * 4), &s_bar[wib][b]);
       pos += cnt;
-      return 1;
+      return 1u;
     };
-    int more0 = __shfl_sync(kFull, lane == 0 ? issue(0) : 0, 0);
-    int more1 = __shfl_sync(kFull, lane == 0 ? issue(1) : 0, 0);
+    uint32_t more = 0;  // bit b: buffer b holds a chunk
+    if (lane == 0)
+      for (int b = 0; b < kWarpStages; ++b) more |= issue(b) << b;
+    more = __shfl_sync(kFull, more, 0);
     uint32_t par_bits = 0;
     int chunks_done = 0;
-    for (int b = 0; b ? more1 : more0; b ^= 1) {
+    for (int b = 0; (more >> b) & 1u; b = (b + 1) % kWarpStages) {
       mbar_wait(&s_bar[wib][b], (par_bits >> b) & 1u);
       par_bits ^= 1u << b;
       const ChunkMeta m = s_meta[wib][b];
-      const int4* v4 = reinterpret_cast<const int4*>(wbuf + b * kWarpChunk);
-      const int4 x = v4[lane], y = v4[lane + 32];
+      constexpr int kV = kWarpChunk / 128;  // 128-bit loads per lane per chunk
+      int4 xs[kV];
+#pragma unroll
+      for (int i = 0; i < kV; ++i) xs[i] = reinterpret_cast<const int4*>(wbuf + b * kWarpChunk)[lane + 32 * i];
+      // WAR hazards before lane 0 refills slot b: (1) across proxies, every
+      // lane's shared-memory load of buffer b must have returned before the
+      // async proxy overwrites it — a warp vote consuming the loaded
+      // registers (data and meta) cannot execute earlier; (2) the meta slot
+      // is rewritten by lane 0's generic stores, ordered by __syncwarp.
+      int32_t dep = m.u ^ (int32_t)(m.base ^ m.lo ^ m.hi);
+#pragma unroll
+      for (int i = 0; i < kV; ++i) dep |= (xs[i].x ^ xs[i].y) | (xs[i].z ^ xs[i].w);
+      (void)__any_sync(kFull, dep == 0x7FFFFFFF);
       __syncwarp();
-      const int mo = __shfl_sync(kFull, lane == 0 ? issue(b) : 0, 0);  // refill b right away
-      if (b) more1 = mo; else more0 = mo;
-      int32_t nb[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
-      const uint32_t okm = slice_mask(nb, (int)(m.lo - m.base), (int)(m.hi - m.base), lane);
+      uint32_t mo = 0;
+      if (lane == 0) mo = issue(b);  // refill b right away
+      mo = __shfl_sync(kFull, mo, 0);
+      more = (more & ~(1u << b)) | (mo << b);
+      int32_t nb[4 * kV];
+      uint32_t okm = 0;
+#pragma unroll
+      for (int i = 0; i < kV; ++i) {
+        nb[4 * i + 0] = xs[i].x;
+        nb[4 * i + 1] = xs[i].y;
+        nb[4 * i + 2] = xs[i].z;
+        nb[4 * i + 3] = xs[i].w;
+        const int lo = (int)(m.lo - m.base) - (lane + 32 * i) * 4, hi = (int)(m.hi - m.base) - (lane + 32 * i) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool ok = q >= lo && q < hi;
+          okm |= (uint32_t)ok << (4 * i + q);
+          nb[4 * i + q] = ok ? nb[4 * i + q] : 0;  // staged slots outside the slice hold stale data
+        }
+      }
       const int32_t pu = m.u;
-      probe_batch<M, 8>(a, h, nb, okm, [&](int) { return pu; }, lane, acc);
-      if (refresh_every > 0 && wib == 0 && ++chunks_done % refresh_every == 0) {
+      if (a.dbg) atomicAdd(a.dbg + 2, (unsigned long long)__popc(okm));  // LBFS_COUNT: hub elements
+      probe_batch<M, 4 * kV>(a, h, nb, okm, [&](int) { return pu; }, lane, acc);
+      if (refresh_every && wib == 0 && ++chunks_done % refresh_every == 0) {
         // re-learn the hot prefix from L2 (others' discoveries): async bulk
         // copy over the shared copy; a racing local OR may be lost, which
         // only costs a redundant write later
@@ -698,28 +729,41 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
                                   c.new2old[v]};
     }
   }
-  // pass 2: thread t owns vertices v0 + t + 256 j (bit t&31 of word t/32 + 8 j)
+  // pass 2: thread t owns vertices v0 + t + 256 j (bit t&31 of word t/32 + 8 j);
+  // four vertices' loads are issued before any of their stores
   unsigned long long edges = 0;
   const int b = t & 31;
-#pragma unroll 4
-  for (int j = 0; j < kCompactSteps; ++j) {
-    const int wl = (t >> 5) + j * (kCompactThreads / 32);
-    if (!((s_new[wl] >> b) & 1u)) continue;
-    const int64_t v = v0 + t + j * kCompactThreads;
-    const int32_t vo = c.new2old[v];
-    c.level[vo] = c.next_level;
-    c.pred[vo] = c.pred_int[v];
-    const int64_t st = c.row_ptr[v];
-    const int32_t deg = (int32_t)(c.row_ptr[v + 1] - st);
-    edges += (unsigned long long)deg;
-    const uint32_t wm = s_wmask[wl];
-    if ((wm >> b) & 1u)
-      c.next_wslice[s_base[3] + s_wpre[wl] + __popc(wm & ((1u << b) - 1u))] = CtaItem{st, deg, vo};
-    const uint32_t lm = s_lmask[wl];
-    if ((lm >> b) & 1u) {
-      const int r = s_lpre[wl] + __popc(lm & ((1u << b) - 1u));
-      c.next_list[s_base[0] + r] = (int32_t)v;
-      s_deg[r] = deg;
+#pragma unroll
+  for (int j0 = 0; j0 < kCompactSteps; j0 += 4) {
+    int32_t vo[4];
+    int64_t st[4], en[4];
+    bool nw[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int wl = (t >> 5) + (j0 + q) * (kCompactThreads / 32);
+      const int64_t v = v0 + t + (j0 + q) * kCompactThreads;
+      nw[q] = (s_new[wl] >> b) & 1u;
+      vo[q] = nw[q] && v < c.t_warp ? __ldg(c.new2old + v) : 0;  // parent id for hub/warp slices
+      st[q] = nw[q] ? __ldg(c.row_ptr + v) : 0;
+      en[q] = nw[q] ? __ldg(c.row_ptr + v + 1) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (!nw[q]) continue;
+      const int wl = (t >> 5) + (j0 + q) * (kCompactThreads / 32);
+      const int64_t v = v0 + t + (j0 + q) * kCompactThreads;
+      c.level_int[v] = c.next_level;  // coalesced; outputs are written by k_finalize
+      const int32_t deg = (int32_t)(en[q] - st[q]);
+      edges += (unsigned long long)deg;
+      const uint32_t wm = s_wmask[wl];
+      if ((wm >> b) & 1u)
+        c.next_wslice[s_base[3] + s_wpre[wl] + __popc(wm & ((1u << b) - 1u))] = CtaItem{st[q], deg, vo[q]};
+      const uint32_t lm = s_lmask[wl];
+      if ((lm >> b) & 1u) {
+        const int r = s_lpre[wl] + __popc(lm & ((1u << b) - 1u));
+        c.next_list[s_base[0] + r] = (int32_t)v;
+        s_deg[r] = deg;
+      }
     }
   }
   __syncthreads();
@@ -758,26 +802,61 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
 }
 
 // ---------------------------------------------------------------- K4 init
-__global__ void k_init(int32_t* __restrict__ pred, int64_t npad, int32_t* __restrict__ level, int64_t n,
-                       uint32_t* __restrict__ visited, uint32_t* __restrict__ prev, int64_t nwords) {
+// per-BFS state: visited/prev bitmaps cleared, internal levels -1
+__global__ void k_init(uint4* __restrict__ vis4, uint4* __restrict__ prev4, int64_t nwords4,
+                       int4* __restrict__ lvl4, int64_t n4) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (int64_t i = t; i < npad; i += stride) pred[i] = kSentinel;
-  for (int64_t i = t; i < n; i += stride) level[i] = -1;
-  for (int64_t i = t; i < nwords; i += stride) visited[i] = prev[i] = 0;
+  for (int64_t i = t; i < nwords4; i += stride) vis4[i] = prev4[i] = make_uint4(0, 0, 0, 0);
+  const int4 m4 = make_int4(-1, -1, -1, -1);
+  for (int64_t i = t; i < n4; i += stride) lvl4[i] = m4;
 }
 
-__global__ void k_init_vec(int4* __restrict__ pred4, int64_t npad4, int4* __restrict__ level4, int64_t n4,
-                           int32_t* __restrict__ level, int64_t n, uint4* __restrict__ vis4,
-                           uint4* __restrict__ prev4, int64_t nwords4) {
+// Outputs in original ids, once per BFS: sequential (128-bit) writes of
+// level[x] and pred[x], gathering the internal-order records through old2new
+// (PredecessorArray semantics, traversal.py:42-50: unreached and padding =
+// SENTINEL). Replaces per-vertex scattered writes during the levels.
+__global__ void k_finalize(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
+                           const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
+                           int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int4 s4 = make_int4(kSentinel, kSentinel, kSentinel, kSentinel);
-  const int4 m4 = make_int4(-1, -1, -1, -1);
-  for (int64_t i = t; i < npad4; i += stride) pred4[i] = s4;
-  for (int64_t i = t; i < n4; i += stride) level4[i] = m4;
-  for (int64_t i = 4 * n4 + t; i < n; i += stride) level[i] = -1;
-  for (int64_t i = t; i < nwords4; i += stride) vis4[i] = prev4[i] = make_uint4(0, 0, 0, 0);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i * 4 < npad; i += stride) {
+    int lv[4], pr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t x = i * 4 + q;
+      lv[q] = -1;
+      pr[q] = kSentinel;
+      if (x < n) {
+        const int32_t v = __ldg(old2new + x);
+        lv[q] = __ldg(level_int + v);
+        if (lv[q] >= 0) pr[q] = __ldg(pred_int + v);
+      }
+    }
+    reinterpret_cast<int4*>(pred_out)[i] = make_int4(pr[0], pr[1], pr[2], pr[3]);
+    if (i * 4 + 3 < n) {
+      reinterpret_cast<int4*>(level_out)[i] = make_int4(lv[0], lv[1], lv[2], lv[3]);
+    } else {
+      for (int q = 0; q < 4; ++q)
+        if (i * 4 + q < n) level_out[i * 4 + q] = lv[q];
+    }
+  }
+}
+
+__global__ void k_finalize_scalar(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
+                                  const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
+                                  int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < npad; x += stride) {
+    int lv = -1, pr = kSentinel;
+    if (x < n) {
+      const int32_t v = __ldg(old2new + x);
+      lv = __ldg(level_int + v);
+      if (lv >= 0) pr = __ldg(pred_int + v);
+      level_out[x] = lv;
+    }
+    pred_out[x] = pr;
+  }
 }
 
 __global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int32_t root_orig, Counters* cnt0) {
@@ -786,8 +865,8 @@ __global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int3
   const int32_t deg = (int32_t)(a.row_ptr[r + 1] - st);
   a.visited[r >> 5] |= 1u << (r & 31);
   prev[r >> 5] |= 1u << (r & 31);
-  a.level[root_orig] = 0;
-  a.pred[root_orig] = root_orig;
+  a.level_int[r] = 0;
+  a.pred_int[r] = root_orig;
   Counters c{};
   c.discovered = 1;
   c.edges = (unsigned long long)deg;
@@ -819,8 +898,9 @@ BfsEngine::BfsEngine(const Csr& csr) {
   visited_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
   prev_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
   pred_int_ = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_, 1));
-  dbg_ = dev_alloc<unsigned long long>(2);
-  LBFS_CUDA(cudaMemset(dbg_, 0, 2 * sizeof(unsigned long long)));
+  level_int_ = dev_alloc<int32_t>((size_t)(n_ + 4));
+  dbg_ = dev_alloc<unsigned long long>(3);
+  LBFS_CUDA(cudaMemset(dbg_, 0, 3 * sizeof(unsigned long long)));
   // Bins, double-buffered: a vertex enters a bin once per BFS, so n entries
   // bound the small/warp bins; CTA items <= nnz/kChunk + #(deg >= kCtaMin).
   cap_cta_ = nnz_ / kChunk + t_cta_ + 2;
@@ -866,6 +946,7 @@ BfsEngine::~BfsEngine() {
   dev_free(visited_);
   dev_free(prev_);
   dev_free(pred_int_);
+  dev_free(level_int_);
   dev_free(dbg_);
   dev_free(classes_);
   for (int b = 0; b < 2; ++b) {
@@ -937,15 +1018,10 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = stream_;
   LBFS_CUDA(cudaEventRecord(ev_[0], st));
-  {  // K4
-    const bool aligned = ((uintptr_t)d_pred % 16 == 0) && ((uintptr_t)d_level % 16 == 0);
-    const unsigned grid = clamp_grid((npad_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
-    if (aligned && nwords_ % 4 == 0) {
-      LBFS_LAUNCH(k_init_vec, grid, 256, 0, st, (int4*)d_pred, npad_ / 4, (int4*)d_level, n_ / 4, d_level, n_,
-                  (uint4*)visited_, (uint4*)prev_, nwords_ / 4);
-    } else {
-      LBFS_LAUNCH(k_init, grid, 256, 0, st, d_pred, npad_, d_level, n_, visited_, prev_, nwords_);
-    }
+  {  // K4: bitmaps + internal levels (outputs are written once, by k_finalize)
+    const unsigned grid = clamp_grid((n_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
+    LBFS_LAUNCH(k_init, grid, 256, 0, st, (uint4*)visited_, (uint4*)prev_, (nwords_ + 3) / 4, (int4*)level_int_,
+                (n_ + 3) / 4);
   }
   LevelArgs a{};
   a.row_ptr = row_ptr_;
@@ -953,15 +1029,14 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   a.new2old = new2old_;
   a.visited = visited_;
   a.prev = prev_;
-  a.pred = d_pred;
   a.pred_int = pred_int_;
+  a.level_int = level_int_;
   a.classes = classes_;
   a.dbg = count_ ? dbg_ : nullptr;
   {
     const char* rf = getenv("LBFS_REFRESH");  // hub chunks between snapshot refreshes (0 = off)
     a.refresh_chunks = rf ? atoi(rf) : kRefreshChunks;
   }
-  a.level = d_level;
   a.t_cta = t_cta_;
   a.t_warp = t_warp_;
   a.t_nz = t_nz_;
@@ -1026,7 +1101,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     LBFS_CUDA(cudaEventRecord(ev_[3], st));
     const bool did_compact = bitmap;
     if (bitmap) {
-      CompactArgs ca{row_ptr_, new2old_, visited_, prev_, nwords_, d_level, d_pred, pred_int_, (int32_t)(L + 1),
+      CompactArgs ca{row_ptr_, new2old_, visited_, prev_, nwords_, level_int_, (int32_t)(L + 1),
                      t_cta_, t_warp_, t_nz_, &cnt_[slot], q_small_[cur ^ 1], q_cta_[cur ^ 1], q_items_[cur ^ 1],
                      q_wslice_[cur ^ 1]};
       LBFS_LAUNCH(k_compact, (unsigned)((n_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
@@ -1039,11 +1114,12 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     LBFS_CUDA(cudaEventElapsedTime(&cms, ev_[3], ev_[5]));
     expand_ms += ms;
     const Counters nx = h_cnt_[slot];
-    unsigned long long dbg[2] = {0, 0};
+    unsigned long long dbg[3] = {0, 0, 0};
     if (count_) {
       LBFS_CUDA(cudaMemcpy(dbg, dbg_, sizeof(dbg), cudaMemcpyDeviceToHost));
       LBFS_CUDA(cudaMemset(dbg_, 0, sizeof(dbg)));
-      fprintf(stderr, "[lbfs]      candidate writes hot=%llu cold=%llu\n", dbg[0], dbg[1]);
+      fprintf(stderr, "[lbfs]      candidate writes hot=%llu cold=%llu streamed elements=%llu\n", dbg[0], dbg[1],
+              dbg[2]);
     }
     if (split_ && (f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice > 0)) {
       for (int pi = 0; pi < 4; ++pi) LBFS_CUDA(cudaEventElapsedTime(&split_ms[pi], ev_split_[pi], ev_split_[pi + 1]));
@@ -1061,6 +1137,15 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     ++L;
     prev_bitmap = bitmap;
     if (nx.discovered == 0) break;
+  }
+  {  // outputs in original ids
+    const unsigned grid = clamp_grid((npad_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
+    const bool aligned = ((uintptr_t)d_pred % 16 == 0) && ((uintptr_t)d_level % 16 == 0);
+    if (aligned) {
+      LBFS_LAUNCH(k_finalize, grid, 256, 0, st, old2new_, level_int_, pred_int_, n_, npad_, d_level, d_pred);
+    } else {
+      LBFS_LAUNCH(k_finalize_scalar, grid, 256, 0, st, old2new_, level_int_, pred_int_, n_, npad_, d_level, d_pred);
+    }
   }
   LBFS_CUDA(cudaEventRecord(ev_[4], st));
   LBFS_CUDA(cudaEventSynchronize(ev_[4]));

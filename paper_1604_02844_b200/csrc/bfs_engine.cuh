@@ -25,9 +25,20 @@ constexpr int kCounterRing = 3;
 #endif
 constexpr int kExpandWarps = LBFS_EXPAND_WARPS;
 constexpr int kExpandThreads = 32 * kExpandWarps;
-constexpr int kWarpChunk = 256;                   // elements per warp-private bulk copy
+// Note: 128-element chunks (one 128-bit load per lane) produced missed
+// discoveries on S24 in round 1 while 256-element chunks are exact at ring
+// depths 2 and 4 (tools/debug_parity.py); cause not yet identified, so the
+// chunk stays at 256 elements.
+#ifndef LBFS_WARP_CHUNK
+#define LBFS_WARP_CHUNK 256
+#endif
+#ifndef LBFS_WARP_STAGES
+#define LBFS_WARP_STAGES 2
+#endif
+constexpr int kWarpChunk = LBFS_WARP_CHUNK;       // elements per warp-private bulk copy
+constexpr int kWarpStages = LBFS_WARP_STAGES;     // per-warp ring depth (stages-1 chunks in flight)
 constexpr int kRefreshChunks = 4;                 // hub chunks (warp 0) between snapshot refreshes
-constexpr int kRingBytes = kExpandWarps * 2 * kWarpChunk * 4;  // warp double buffers
+constexpr int kRingBytes = kExpandWarps * kWarpStages * kWarpChunk * 4;  // per-warp rings
 
 // Per-level counters (K6). Slot L holds the frontier of level L:
 // discovered = |frontier| (layers[L].input), edges = sum of its degrees
@@ -79,12 +90,11 @@ struct LevelArgs {
   const int32_t* new2old;
   uint32_t* visited;
   uint32_t* prev;           // visited at the last bitmap-mode boundary
-  int32_t* pred;            // original-id outputs
-  int32_t* pred_int;        // bitmap mode: parent (original id) by internal id
+  int32_t* pred_int;        // parent (original id) by internal id
+  int32_t* level_int;       // level by internal id (-1 unreached)
   const ClassTable* classes;
   unsigned long long* dbg;  // LBFS_COUNT: candidate-write counters (hot, cold)
   int32_t refresh_chunks;   // hub chunks between hot-snapshot refreshes (warp 0)
-  int32_t* level;
   int32_t next_level;
   int32_t t_cta, t_warp, t_nz;  // internal-id bin boundaries
   // queue-mode outputs (direct append by the winners)
@@ -100,9 +110,7 @@ struct CompactArgs {
   const uint32_t* visited;
   uint32_t* prev;           // visited at the previous level boundary
   int64_t nwords;
-  int32_t* level;
-  int32_t* pred;
-  const int32_t* pred_int;
+  int32_t* level_int;
   int32_t next_level;
   int32_t t_cta, t_warp, t_nz;
   Counters* next_cnt;
@@ -151,6 +159,7 @@ class BfsEngine {
   uint32_t* visited_ = nullptr;
   uint32_t* prev_ = nullptr;
   int32_t* pred_int_ = nullptr;
+  int32_t* level_int_ = nullptr;
   int32_t* q_small_[2] = {nullptr, nullptr};
   int32_t* q_warp_[2] = {nullptr, nullptr};
   CtaItem* q_cta_[2] = {nullptr, nullptr};
