@@ -621,6 +621,100 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
     expand_range<M>(a, h, gi.count, v, gi.elo, gi.ehi, s_T, s_B, lane, ws, acc);
   }
 
+  // ---- phase 2b: dense small region (after a bitmap-mode level whose
+  // frontier covers most small-degree vertices): the rows of the whole small
+  // region are one contiguous col_idx range, cut at layout time into tasks
+  // inside one degree class d; a warp streams a task with 128-bit loads and
+  // keeps an element when its owner v = lo_d + (p - base_d) / d is in the
+  // frontier bitmap. No list, no per-vertex row_ptr read.
+  if (phases & 32) {
+    for (int64_t it = gwarp; it < f.n_dense; it += nwarps) {
+      const DenseTask dt = f.dense[it];
+      const int d = dt.d;
+      const int32_t lo = s_T[d + 1];
+      const int64_t base = s_B[d];
+      const uint32_t rcp = (uint32_t)(0xFFFFFFFFull / (uint32_t)d + 1ull);
+      const int64_t a0 = dt.p0 & ~int64_t(3), a1 = dt.p0 + dt.len;
+      for (int64_t c0 = a0; c0 < a1; c0 += 128) {
+        const int64_t p = c0 + lane * 4;
+        const int4 x = p < a1 ? ld_stream4(a.col_idx + p) : make_int4(0, 0, 0, 0);
+        int32_t nb[4] = {x.x, x.y, x.z, x.w};
+        int32_t own[4];
+        uint32_t okm = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t pq = p + q;
+          const uint32_t rel = (uint32_t)(pq - base);
+          own[q] = lo + (d == 1 ? (int32_t)rel : (int32_t)__umulhi(rel, rcp));
+          const bool in_task = pq >= dt.p0 && pq < a1;
+          const bool in_front = in_task && ((__ldca(f.front + (own[q] >> 5)) >> (own[q] & 31)) & 1u);
+          okm |= (uint32_t)in_front << q;
+          nb[q] = in_front ? nb[q] : 0;
+        }
+        probe_batch<M, 4>(a, h, nb, okm, [&](int k) { return __ldg(a.new2old + own[k]); }, lane, acc);
+      }
+    }
+  }
+
+  // ---- phase 2c: dense warp-bin region (32 <= deg < kCtaMin): a warp takes
+  // 32 consecutive rows (contiguous in col_idx), skips the group when none of
+  // them is in the frontier, else streams the group with 128-bit loads. The
+  // owner of an element comes from a 128-bit mask of row starts in the
+  // window (four redux.or) and a prefix popcount — no search, no list.
+  if (phases & 64) {
+    const int64_t ngroups = (a.t_warp - a.t_cta + 31) / 32;
+    for (int64_t g = gwarp; g < ngroups; g += nwarps) {
+      const int64_t v0 = a.t_cta + 32 * g;
+      const int nrow = (int)std::min<int64_t>(32, a.t_warp - v0);
+      // frontier bits of rows v0 .. v0+31 (two words when v0 is unaligned)
+      const uint32_t sh = (uint32_t)(v0 & 31);
+      const uint32_t wlo = __ldca(f.front + (v0 >> 5));
+      const uint32_t whi = sh ? __ldca(f.front + (v0 >> 5) + 1) : 0u;
+      uint32_t fw = sh ? ((wlo >> sh) | (whi << (32 - sh))) : wlo;
+      fw &= (nrow == 32) ? kFull : ((1u << nrow) - 1u);
+      if (!fw) continue;
+      if (a.dbg && lane == 0) atomicAdd(a.dbg + 3, (unsigned long long)__popc(fw));  // LBFS_COUNT: frontier rows
+      const int64_t rs = lane < nrow ? __ldg(a.row_ptr + v0 + lane) : 0;  // row starts
+      const int64_t e_beg = __shfl_sync(kFull, rs, 0);
+      const int64_t e_end = __ldg(a.row_ptr + v0 + nrow);  // (a 33rd lane does not exist)
+      const int32_t uo = (lane < nrow && ((fw >> lane) & 1u)) ? __ldg(a.new2old + v0 + lane) : 0;
+      for (int64_t c0 = e_beg & ~int64_t(3); c0 < e_end; c0 += 128) {
+        const int64_t p = c0 + lane * 4;
+        const int4 x = p < e_end ? ld_stream4(a.col_idx + p) : make_int4(0, 0, 0, 0);
+        // row starts inside [c0, c0+128) as a 128-bit mask
+        const int64_t off = rs - c0;
+        const bool inwin = lane < nrow && off >= 0 && off < 128;
+        uint32_t Mk[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          Mk[k] = __reduce_or_sync(kFull, (inwin && (off >> 5) == k) ? (1u << (off & 31)) : 0u);
+        const int before = __popc(__ballot_sync(kFull, lane < nrow && off < 0));  // rows starting before c0
+        const int wk = lane >> 3;  // this lane's 4 elements sit in mask word wk
+        int pre = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pre += (k < wk) ? __popc(Mk[k]) : 0;
+        const uint32_t mw = wk == 0 ? Mk[0] : (wk == 1 ? Mk[1] : (wk == 2 ? Mk[2] : Mk[3]));
+        int32_t nb[4] = {x.x, x.y, x.z, x.w};
+        int own[4];
+        uint32_t okm = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int o = lane * 4 + q;
+          own[q] = before + pre + __popc(mw & ((2u << (o & 31)) - 1u)) - 1;  // row index within the group
+          const bool ok = (p + q) >= e_beg && (p + q) < e_end && own[q] >= 0 && ((fw >> (own[q] & 31)) & 1u);
+          okm |= (uint32_t)ok << q;
+          nb[q] = ok ? nb[q] : 0;
+          own[q] &= 31;
+        }
+        int32_t par[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) par[q] = __shfl_sync(kFull, uo, own[q]);
+        if (a.dbg) atomicAdd(a.dbg + 2, (unsigned long long)__popc(okm));  // LBFS_COUNT: kept elements
+        probe_batch<M, 4>(a, h, nb, okm, [&](int k) { return par[k]; }, lane, acc);
+      }
+    }
+  }
+
   // ---- phase 3: raw warp/small queues (after a queue-mode level): a warp
   // takes one warp-bin vertex or 32 small-bin vertices ---------------------
   if (phases & 4) {
@@ -689,6 +783,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
   if (t < kCompactWords && w0 + t < c.nwords) {
     const uint32_t w = c.visited[w0 + t], p = c.prev[w0 + t];
     nb = w & ~p;
+    c.front[w0 + t] = nb;  // next frontier as a bitmap (dense small-region path)
     if (nb) {
       c.prev[w0 + t] = w;
       const int64_t vw = (w0 + t) * 32;
@@ -899,8 +994,9 @@ BfsEngine::BfsEngine(const Csr& csr) {
   prev_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
   pred_int_ = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_, 1));
   level_int_ = dev_alloc<int32_t>((size_t)(n_ + 4));
-  dbg_ = dev_alloc<unsigned long long>(3);
-  LBFS_CUDA(cudaMemset(dbg_, 0, 3 * sizeof(unsigned long long)));
+  front_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
+  dbg_ = dev_alloc<unsigned long long>(4);
+  LBFS_CUDA(cudaMemset(dbg_, 0, 4 * sizeof(unsigned long long)));
   // Bins, double-buffered: a vertex enters a bin once per BFS, so n entries
   // bound the small/warp bins; CTA items <= nnz/kChunk + #(deg >= kCtaMin).
   cap_cta_ = nnz_ / kChunk + t_cta_ + 2;
@@ -922,9 +1018,11 @@ BfsEngine::BfsEngine(const Csr& csr) {
   // (static shared memory differs per phase kernel: take the largest)
   const void* kernels[] = {(const void*)k_expand<kBitmapOut, 1>,  (const void*)k_expand<kBitmapOut, 2>,
                            (const void*)k_expand<kBitmapOut, 4>,  (const void*)k_expand<kBitmapOut, 8>,
-                           (const void*)k_expand<kBitmapOut, 16>, (const void*)k_expand<kQueueOut, 1>,
+                           (const void*)k_expand<kBitmapOut, 16>, (const void*)k_expand<kBitmapOut, 32>,
+                           (const void*)k_expand<kBitmapOut, 64>, (const void*)k_expand<kQueueOut, 1>,
                            (const void*)k_expand<kQueueOut, 2>,   (const void*)k_expand<kQueueOut, 4>,
-                           (const void*)k_expand<kQueueOut, 8>,   (const void*)k_expand<kQueueOut, 16>};
+                           (const void*)k_expand<kQueueOut, 8>,   (const void*)k_expand<kQueueOut, 16>,
+                           (const void*)k_expand<kQueueOut, 32>,  (const void*)k_expand<kQueueOut, 64>};
   size_t max_static = 0;
   for (auto fn : kernels) {
     cudaFuncAttributes fa{};
@@ -947,6 +1045,8 @@ BfsEngine::~BfsEngine() {
   dev_free(prev_);
   dev_free(pred_int_);
   dev_free(level_int_);
+  dev_free(front_);
+  dev_free(dense_tasks_);
   dev_free(dbg_);
   dev_free(classes_);
   for (int b = 0; b < 2; ++b) {
@@ -991,6 +1091,10 @@ static void launch_expand_m(int pi, unsigned grid, int smem, const LevelArgs& a,
     LBFS_LAUNCH((k_expand<M, 2>), grid, kExpandThreads, smem, st, a, f, hot);
   } else if (pi == 3) {
     LBFS_LAUNCH((k_expand<M, 16>), grid, kExpandThreads, smem, st, a, f, hot);
+  } else if (pi == 4) {
+    LBFS_LAUNCH((k_expand<M, 32>), grid, kExpandThreads, smem, st, a, f, hot);
+  } else if (pi == 5) {
+    LBFS_LAUNCH((k_expand<M, 64>), grid, kExpandThreads, smem, st, a, f, hot);
   } else {
     LBFS_LAUNCH((k_expand<M, 4>), grid, kExpandThreads, smem, st, a, f, hot);
   }
@@ -1014,6 +1118,8 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   trace_ = env_flag("LBFS_TRACE");  // per-level table on stderr
   count_ = env_flag("LBFS_COUNT");  // candidate-write counters (slow)
   split_ = env_flag("LBFS_SPLIT");  // one launch per bin
+  dense_off_ = env_flag("LBFS_NO_DENSE");  // experiment: always use the small-bin list
+  dense_warp_ = env_flag("LBFS_DENSE_WARP");  // experiment: dense warp-bin region
   hub_ldg_ = env_flag("LBFS_HUB_LDG");  // experiment: hub bin without TMA staging
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = stream_;
@@ -1072,6 +1178,22 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       f.n_items = (int64_t)c.bin[kBinItems];
       f.wslice = q_wslice_[cur];
       f.n_wslice = (int64_t)c.bin[kBinWSlice];
+      // dense small region: stream it whole when most of it is in the frontier
+      const int64_t small_region = (int64_t)t_nz_ - t_warp_;
+      if (small_region > 0 && (int64_t)c.bin[kBinSmall] * kDenseDenom > small_region * kDenseNum && !dense_off_) {
+        f.n_items = 0;
+        f.front = front_;
+        f.dense = dense_tasks_;
+        f.n_dense = n_dense_tasks_;
+      }
+      const int64_t warp_region = (int64_t)t_warp_ - t_cta_;
+      // (opt-in: measured slower than warp slices on S24, 0.55 vs 0.36 ms)
+      if (warp_region > 0 && (int64_t)c.bin[kBinWSlice] * kDenseDenom > warp_region * kDenseNum && !dense_off_ &&
+          dense_warp_) {
+        f.n_wslice = 0;
+        f.front = front_;
+        f.dense_warp = true;
+      }
     } else {  // winners appended to raw queues
       f.small = q_small_[cur];
       f.warp = q_warp_[cur];
@@ -1079,31 +1201,33 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       f.n_warp = (int64_t)c.bin[kBinWarp];
     }
     const bool bitmap = c.edges >= bitmap_min_edges;
-    const int64_t need = std::max({(f.n_cta + kExpandWarps - 1) / kExpandWarps,
+    const int64_t need = std::max({(f.n_cta + kExpandWarps - 1) / kExpandWarps, f.dense_warp ? (int64_t)1 << 30 : 0,
+                                    (f.n_dense + kExpandWarps - 1) / kExpandWarps,
                                     (f.n_wslice + kExpandWarps - 1) / kExpandWarps,
                                     (f.n_items + kExpandWarps - 1) / kExpandWarps,
                                     (f.n_warp + (f.n_small + 31) / 32 + kExpandWarps - 1) / kExpandWarps,
                                     (int64_t)1});
     const unsigned grid = bitmap ? (unsigned)expand_grid_ : clamp_grid(need, expand_grid_);
     LBFS_CUDA(cudaEventRecord(ev_[2], st));
-    float split_ms[4] = {0.f, 0.f, 0.f, 0.f};
-    if (f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice > 0) {
+    float split_ms[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice + f.n_dense > 0 || f.dense_warp) {
       // one launch per non-empty bin: each phase kernel gets its own register
       // allocation (the fused kernel was capped at 64 registers by 1024 threads)
-      const bool has[4] = {f.n_cta > 0, f.n_items > 0, f.n_warp + f.n_small > 0, f.n_wslice > 0};
-      for (int pi = 0; pi < 4; ++pi) {
+      const bool has[6] = {f.n_cta > 0, f.n_items > 0, f.n_warp + f.n_small > 0, f.n_wslice > 0, f.n_dense > 0,
+                           f.dense_warp};
+      for (int pi = 0; pi < 6; ++pi) {
         if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[pi], st));
         if (!has[pi]) continue;
         launch_expand(bitmap, pi, grid, a, f, st);
       }
-      if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[4], st));
+      if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[6], st));
     }
     LBFS_CUDA(cudaEventRecord(ev_[3], st));
     const bool did_compact = bitmap;
     if (bitmap) {
       CompactArgs ca{row_ptr_, new2old_, visited_, prev_, nwords_, level_int_, (int32_t)(L + 1),
                      t_cta_, t_warp_, t_nz_, &cnt_[slot], q_small_[cur ^ 1], q_cta_[cur ^ 1], q_items_[cur ^ 1],
-                     q_wslice_[cur ^ 1]};
+                     q_wslice_[cur ^ 1], front_};
       LBFS_LAUNCH(k_compact, (unsigned)((n_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
     }
     LBFS_CUDA(cudaEventRecord(ev_[5], st));
@@ -1114,17 +1238,19 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     LBFS_CUDA(cudaEventElapsedTime(&cms, ev_[3], ev_[5]));
     expand_ms += ms;
     const Counters nx = h_cnt_[slot];
-    unsigned long long dbg[3] = {0, 0, 0};
+    unsigned long long dbg[4] = {0, 0, 0, 0};
     if (count_) {
       LBFS_CUDA(cudaMemcpy(dbg, dbg_, sizeof(dbg), cudaMemcpyDeviceToHost));
       LBFS_CUDA(cudaMemset(dbg_, 0, sizeof(dbg)));
-      fprintf(stderr, "[lbfs]      candidate writes hot=%llu cold=%llu streamed elements=%llu\n", dbg[0], dbg[1],
-              dbg[2]);
+      fprintf(stderr, "[lbfs]      candidate writes hot=%llu cold=%llu streamed elements=%llu dwarp rows=%llu\n",
+              dbg[0], dbg[1], dbg[2], dbg[3]);
+
     }
-    if (split_ && (f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice > 0)) {
-      for (int pi = 0; pi < 4; ++pi) LBFS_CUDA(cudaEventElapsedTime(&split_ms[pi], ev_split_[pi], ev_split_[pi + 1]));
-      fprintf(stderr, "[lbfs]      split: hub=%.3fms items=%.3fms queues=%.3fms wslice=%.3fms\n", split_ms[0],
-              split_ms[1], split_ms[2], split_ms[3]);
+    if (split_ && (f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice + f.n_dense > 0 || f.dense_warp)) {
+      for (int pi = 0; pi < 6; ++pi) LBFS_CUDA(cudaEventElapsedTime(&split_ms[pi], ev_split_[pi], ev_split_[pi + 1]));
+      fprintf(stderr,
+              "[lbfs]      split: hub=%.3fms items=%.3fms queues=%.3fms wslice=%.3fms dense=%.3fms dwarp=%.3fms\n",
+              split_ms[0], split_ms[1], split_ms[2], split_ms[3], split_ms[4], split_ms[5]);
     }
     if (trace_)
       fprintf(stderr,

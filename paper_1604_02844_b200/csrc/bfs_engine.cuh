@@ -66,6 +66,15 @@ struct alignas(16) CtaItem {  // one kChunk-edge slice of a hub's row
   int32_t u;       // original id of the hub (the parent written to pred)
 };
 
+// A contiguous element range of the small region inside one degree class.
+struct alignas(16) DenseTask {
+  int64_t p0;   // first col_idx index
+  int32_t len;
+  int32_t d;    // degree class
+};
+constexpr int kDenseTask = 4096;  // elements per dense task
+constexpr int kDenseNum = 1, kDenseDenom = 2;  // dense when list > region/2
+
 struct Frontier {
   const int32_t* small;    // after a queue-mode level: small/warp-bin queues ...
   const int32_t* warp;
@@ -74,6 +83,10 @@ struct Frontier {
   const int32_t* list;     // ... after a bitmap-mode level: non-hub list + group items
   const GroupItem* items;
   int64_t n_small, n_warp, n_cta, n_items, n_wslice;
+  const uint32_t* front;   // frontier bitmap (dense small-region path)
+  const DenseTask* dense;
+  int64_t n_dense;
+  bool dense_warp;         // stream the warp-bin region from the frontier bitmap
 };
 
 // Degree classes of the small region: internal ids with degree d form the
@@ -118,6 +131,7 @@ struct CompactArgs {
   CtaItem* next_cta;
   GroupItem* next_items;
   CtaItem* next_wslice;
+  uint32_t* front;
 };
 
 class BfsEngine {
@@ -160,6 +174,11 @@ class BfsEngine {
   uint32_t* prev_ = nullptr;
   int32_t* pred_int_ = nullptr;
   int32_t* level_int_ = nullptr;
+  uint32_t* front_ = nullptr;
+  DenseTask* dense_tasks_ = nullptr;
+  int64_t n_dense_tasks_ = 0;
+  bool dense_off_ = false;
+  bool dense_warp_ = false;
   int32_t* q_small_[2] = {nullptr, nullptr};
   int32_t* q_warp_[2] = {nullptr, nullptr};
   CtaItem* q_cta_[2] = {nullptr, nullptr};
@@ -180,7 +199,7 @@ class BfsEngine {
   bool count_ = false;
   bool split_ = false;
   bool hub_ldg_ = false;  // LBFS_SPLIT=1: one launch per bin, timed separately
-  cudaEvent_t ev_split_[5] = {};  // LBFS_COUNT=1: count bitmap-mode candidate writes (slow)
+  cudaEvent_t ev_split_[7] = {};  // LBFS_COUNT=1: count bitmap-mode candidate writes (slow)
 };
 
 }  // namespace lbfs

@@ -157,6 +157,19 @@ void BfsEngine::build_layout(const Csr& csr) {
   for (int d = 1; d <= kSmallMax; ++d) ct.base[d] = h_rp[(size_t)(d <= kSmallMax ? h_t[std::min(d + 1, kSmallMax + 1)] : 0)];
   classes_ = dev_alloc<ClassTable>(1);
   LBFS_CUDA(cudaMemcpyAsync(classes_, &ct, sizeof(ct), cudaMemcpyHostToDevice, st));
+  // 6. dense tasks over the small region: kDenseTask-element ranges inside a class
+  std::vector<DenseTask> tasks;
+  for (int d = kSmallMax - 1; d >= 1; --d) {
+    const int64_t lo = ct.T[d + 1], hi = ct.T[d];
+    if (hi <= lo) continue;
+    const int64_t e0 = ct.base[d], e1 = ct.base[d] + (hi - lo) * d;
+    for (int64_t p = e0; p < e1; p += kDenseTask)
+      tasks.push_back(DenseTask{p, (int32_t)std::min<int64_t>(kDenseTask, e1 - p), d});
+  }
+  n_dense_tasks_ = (int64_t)tasks.size();
+  dense_tasks_ = dev_alloc<DenseTask>(std::max<size_t>(tasks.size(), 1));
+  if (!tasks.empty())
+    LBFS_CUDA(cudaMemcpyAsync(dense_tasks_, tasks.data(), sizeof(DenseTask) * tasks.size(), cudaMemcpyHostToDevice, st));
   LBFS_CUDA(cudaStreamSynchronize(st));
 }
 
