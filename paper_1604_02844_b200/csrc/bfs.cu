@@ -49,7 +49,9 @@
 namespace lbfs {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-enum Mode : int { kBitmapOut = 0, kQueueOut = 1 };
+// kQueueDirect: queue mode without the visited pre-probe (k_levels: small
+// frontiers, where the probe's round trip costs more than extra atomics)
+enum Mode : int { kBitmapOut = 0, kQueueOut = 1, kQueueDirect = 2 };
 
 // ---------------------------------------------------------------- memory ops
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
@@ -117,57 +119,87 @@ struct WarpScratch {
 
 __device__ __forceinline__ bool bit_clear(uint32_t word, int32_t v) { return ((word >> (v & 31)) & 1u) == 0; }
 
-__device__ __forceinline__ void warp_append(bool take, int32_t val, unsigned long long* tail, int32_t* q,
-                                            int lane) {
-  const unsigned m = __ballot_sync(kFull, take);
-  if (!m) return;
-  const int leader = __ffs(m) - 1;
-  unsigned long long base = 0;
-  if (lane == leader) base = atomicAdd(tail, (unsigned long long)__popc(m));
-  base = __shfl_sync(kFull, base, leader);
-  if (take) q[base + __popc(m & ((1u << lane) - 1u))] = val;
-}
-
-// Queue mode (warp-collective): atomicOr elects one winner per vertex, which
-// writes level + pred and appends to the next level's bin with one atomic
-// per warp per bin.
-__device__ __forceinline__ void settle_queue(const LevelArgs& a, bool cand, int32_t v, int32_t u, int lane,
-                                             Acc& acc) {
-  bool win = false;
-  if (cand) {
-    const uint32_t bit = 1u << (v & 31);
-    win = (atomicOr(a.visited + (v >> 5), bit) & bit) == 0;
+// Queue mode (warp-collective), a batch of K candidates per lane: the K
+// atomicOr elections are in flight together; winners write level + pred and
+// are appended to the next level's bins with one atomic per bin per warp for
+// the whole batch (a packed warp scan of the per-lane counts). Hub winners
+// (rare) also emit kChunk slices.
+template <int K, typename ParFn>
+__device__ __forceinline__ void settle_queue(const LevelArgs& a, const int32_t (&nb)[K], uint32_t cmask, ParFn par,
+                                             int lane, Acc& acc) {
+  uint32_t old[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    old[k] = ((cmask >> k) & 1u) ? atomicOr(a.visited + (nb[k] >> 5), 1u << (nb[k] & 31)) : kFull;
+  uint32_t win = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) win |= (((old[k] >> (nb[k] & 31)) & 1u) ^ 1u) << k;
+  if (!__any_sync(kFull, win != 0)) return;
+  int64_t st[K];
+  int32_t deg[K];
+  uint32_t ns = 0, nw = 0;
+  bool hub = false;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    st[k] = 0;
+    deg[k] = 0;
+    if ((win >> k) & 1u) {
+      const int32_t v = nb[k];
+      st[k] = a.row_ptr[v];
+      deg[k] = (int32_t)(a.row_ptr[v + 1] - st[k]);
+      ns += (v >= a.t_warp && v < a.t_nz);
+      nw += (v >= a.t_cta && v < a.t_warp);
+      hub |= v < a.t_cta;
+    }
   }
-  if (!__any_sync(kFull, win)) return;
-  int32_t deg = 0, vo = 0;
-  int64_t st = 0;
-  if (win) {
+  // exclusive offsets of this lane's small (low half) and warp (high half) appends
+  uint32_t incl = ns | (nw << 16);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const uint32_t tot = __shfl_sync(kFull, incl, 31);
+  unsigned long long bs = 0, bw = 0;
+  if (lane == 0) {
+    if (tot & 0xFFFFu) bs = atomicAdd(&a.next_cnt->bin[kBinSmall], (unsigned long long)(tot & 0xFFFFu));
+    if (tot >> 16) bw = atomicAdd(&a.next_cnt->bin[kBinWarp], (unsigned long long)(tot >> 16));
+  }
+  const uint32_t excl = incl - (ns | (nw << 16));
+  unsigned long long os = __shfl_sync(kFull, bs, 0) + (excl & 0xFFFFu);
+  unsigned long long ow = __shfl_sync(kFull, bw, 0) + (excl >> 16);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (!((win >> k) & 1u)) continue;
+    const int32_t v = nb[k];
     atomicOr(a.prev + (v >> 5), 1u << (v & 31));  // keep bitmap-mode compaction exact
-    vo = __ldg(a.new2old + v);
-    a.level_int[v] = a.next_level;  // internal order; k_finalize writes the outputs
-    a.pred_int[v] = u;              // parents travel as original ids
-    st = a.row_ptr[v];
-    deg = (int32_t)(a.row_ptr[v + 1] - st);
+    a.level_int[v] = a.next_level;                 // internal order; k_finalize writes the outputs
+    a.pred_int[v] = par(k);                        // parents travel as original ids
+    if (v >= a.t_warp && v < a.t_nz) a.next_small[os++] = v;
+    if (v >= a.t_cta && v < a.t_warp) a.next_warp[ow++] = v;
     acc.disc += 1;
-    acc.edges += (unsigned long long)deg;
+    acc.edges += (unsigned long long)deg[k];
   }
-  warp_append(win && v >= a.t_warp && v < a.t_nz, v, &a.next_cnt->bin[kBinSmall], a.next_small, lane);
-  warp_append(win && v >= a.t_cta && v < a.t_warp, v, &a.next_cnt->bin[kBinWarp], a.next_warp, lane);
-  const int items = (win && v < a.t_cta) ? (deg + kChunk - 1) / kChunk : 0;
-  if (__any_sync(kFull, items > 0)) {
-    int incl = items;
+  if (!__any_sync(kFull, hub)) return;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const bool w = ((win >> k) & 1u) && nb[k] < a.t_cta;
+    if (!__any_sync(kFull, w)) continue;
+    const int items = w ? (deg[k] + kChunk - 1) / kChunk : 0;
+    const int32_t vo = w ? __ldg(a.new2old + nb[k]) : 0;
+    int inc = items;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += t;
+      const int t = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += t;
     }
-    const int total = __shfl_sync(kFull, incl, 31);
+    const int total = __shfl_sync(kFull, inc, 31);
     unsigned long long base = 0;
     if (lane == 31) base = atomicAdd(&a.next_cnt->bin[kBinCta], (unsigned long long)total);
     base = __shfl_sync(kFull, base, 31);
-    const int off = incl - items;
-    for (int k = 0; k < items; ++k)
-      a.next_cta[base + off + k] = CtaItem{st + (int64_t)k * kChunk, min(kChunk, deg - k * kChunk), vo};
+    const int off = inc - items;
+    for (int j = 0; j < items; ++j)
+      a.next_cta[base + off + j] = CtaItem{st[k] + (int64_t)j * kChunk, min(kChunk, deg[k] - j * kChunk), vo};
   }
 }
 
@@ -237,23 +269,26 @@ template <int M, int K, typename ParFn>
 __device__ __forceinline__ void probe_batch(const LevelArgs& a, const Hot& h, const int32_t (&nb)[K],
                                             uint32_t okmask, ParFn par, int lane, Acc& acc) {
   uint32_t cmask = 0;
+  if constexpr (M == kQueueDirect) {
+    cmask = okmask;
+  } else {
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const uint32_t w = probe_word(h, a.visited, nb[k] >> 5);
-    cmask |= ((~w >> (nb[k] & 31)) & 1u) << k;
+    for (int k = 0; k < K; ++k) {
+      const uint32_t w = probe_word(h, a.visited, nb[k] >> 5);
+      cmask |= ((~w >> (nb[k] & 31)) & 1u) << k;
+    }
+    cmask &= okmask;
   }
-  cmask &= okmask;
   if constexpr (M == kBitmapOut) {
     if (cmask) settle_bitmap<K>(a, h, nb, cmask, par);
   } else {
-#pragma unroll
-    for (int k = 0; k < K; ++k) settle_queue(a, (cmask >> k) & 1u, nb[k], par(k), lane, acc);
+    settle_queue<K>(a, nb, cmask, par, lane, acc);
   }
 }
 
 template <int M>
 __device__ __forceinline__ void flush_acc(const LevelArgs& a, Acc& acc) {
-  if constexpr (M == kQueueOut) {
+  if constexpr (M != kBitmapOut) {
     unsigned long long d = acc.disc, e = acc.edges;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -291,13 +326,19 @@ __device__ __forceinline__ uint32_t range_mask(int64_t base_v, int64_t lo, int64
 // scan, then 128-element windows in which each lane finds its element's
 // owner by binary search over the group's offsets.
 template <int M>
-__device__ __forceinline__ void expand_group(const LevelArgs& a, const Hot& h, int n, int32_t u, int elo, int ehi,
-                                             int lane, WarpScratch& ws, Acc& acc) {
+__device__ __forceinline__ void expand_group(const LevelArgs& a, const Hot& h, int n, int32_t u, int dcls, int elo,
+                                             int ehi, const int32_t* T, const int64_t* B, int lane, WarpScratch& ws,
+                                             Acc& acc) {
   int64_t st = 0;
   int32_t d = 0, uo = 0;
   if (lane < n) {
-    st = a.row_ptr[u];
-    d = (int32_t)(a.row_ptr[u + 1] - st);
+    if (dcls > 0) {  // small region: row from the degree-class table, no row_ptr read
+      d = dcls;
+      st = B[dcls] + (int64_t)(u - T[dcls + 1]) * dcls;
+    } else {
+      st = a.row_ptr[u];
+      d = (int32_t)(a.row_ptr[u + 1] - st);
+    }
     uo = __ldg(a.new2old + u);
   }
   int incl = d;
@@ -399,7 +440,7 @@ __device__ __forceinline__ void expand_range(const LevelArgs& a, const Hot& h, i
   if (d0 > 0 && __all_sync(kFull, lane >= n || d == d0))
     expand_class_group<M>(a, h, n, v, d0, elo, ehi, T, B, lane, acc);
   else
-    expand_group<M>(a, h, n, v, elo, ehi, lane, ws, acc);
+    expand_group<M>(a, h, n, v, d, elo, ehi, T, B, lane, ws, acc);
 }
 
 // Valid-element mask of a 256-element chunk whose lane holds elements
@@ -418,6 +459,17 @@ __device__ __forceinline__ uint32_t slice_mask(int32_t (&nb)[8], int lo, int hi,
   return okm;
 }
 
+// Slice descriptors through L2 (k_levels rewrites a queue buffer every other
+// level within one launch; L1 is not coherent).
+__device__ __forceinline__ CtaItem ld_item(const CtaItem* p) {
+  const int4 r = __ldcg(reinterpret_cast<const int4*>(p));
+  CtaItem c;
+  c.start = (int64_t)(((uint64_t)(uint32_t)r.y << 32) | (uint32_t)r.x);
+  c.len = r.z;
+  c.u = r.w;
+  return c;
+}
+
 // A warp walks row slices (grid-stride over items) in 128-element chunks of
 // one 128-bit load per lane; the loads of chunk i+1 are issued before chunk
 // i is probed.
@@ -426,7 +478,7 @@ __device__ __forceinline__ void stream_slices(const LevelArgs& a, const Hot& h, 
                                               int64_t gwarp, int64_t nwarps, int lane, Acc& acc) {
   if (gwarp >= n) return;
   int64_t it = gwarp;
-  CtaItem cur = items[it];
+  CtaItem cur = ld_item(items + it);
   int64_t pos = cur.start & ~int64_t(3);
   int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
   auto load = [&](int64_t p0, int64_t e0) {
@@ -442,7 +494,7 @@ __device__ __forceinline__ void stream_slices(const LevelArgs& a, const Hot& h, 
     if (pos >= end) {
       it += nwarps;
       if (it < n) {
-        cur = items[it];
+        cur = ld_item(items + it);
         pos = cur.start & ~int64_t(3);
         end = (cur.start + cur.len + 3) & ~int64_t(3);
       } else {
@@ -728,6 +780,124 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
     }
   }
   flush_acc<M>(a, acc);
+}
+
+// ---------------------------------------------------------------- K5 on the device
+// Grid-wide barrier for a co-resident grid (cooperative launch): one arrival
+// atomic per CTA, the last arrival bumps the generation word. The fences
+// make the CTA's writes of this level (queue entries, counters, bitmap)
+// visible to every CTA after the barrier.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned r;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
+  asm volatile("red.add.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// g: this CTA's copy of the generation word (read once at kernel start; it
+// cannot advance before every CTA has arrived), advanced here.
+__device__ __forceinline__ void grid_sync(unsigned* count, unsigned* gen, unsigned& g,
+                                          unsigned long long* last_arrival) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atom_add_acq_rel(count, 1u) == gridDim.x - 1) {
+      if (last_arrival) *last_arrival = gtimer();
+      *(volatile unsigned*)count = 0u;  // ordered before the release below
+      red_add_release(gen, 1u);
+    } else {
+      while (ld_acquire(gen) == g) {
+      }
+    }
+  }
+  ++g;
+  __syncthreads();
+}
+
+__device__ __forceinline__ Counters ld_counters(const Counters* p) {
+  Counters c;
+  const ulonglong2* s = reinterpret_cast<const ulonglong2*>(p);
+  ulonglong2* d = reinterpret_cast<ulonglong2*>(&c);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Counters) / 16); ++i) d[i] = __ldcg(s + i);
+  return c;
+}
+
+// Consecutive queue-mode levels in one launch (the level loop of
+// traversal.py:90 moved onto the device for small frontiers): per level, the
+// frontier queues of slot L%2 are expanded with winner election + appends
+// into slot (L+1)%2 exactly as k_expand<kQueueOut> does, then one grid
+// barrier. Counters live in the same 3-slot ring as the host loop uses; slot
+// (L+2)%3 is cleared during level L (nobody reads it then). The loop returns
+// to the host when the next frontier is empty, needs bitmap mode
+// (edges >= bitmap_min_edges) or the layer buffer is full. Queue entries and
+// counters are re-read through L2 (__ldcg): L1 is not coherent within a
+// launch and a queue buffer is reused every other level.
+__global__ void __launch_bounds__(kLoopThreads, 1) k_levels(LevelArgs a, LoopArgs p) {
+  __shared__ WarpScratch s_ws[kLoopThreads / 32];
+  __shared__ int32_t s_T[kSmallMax + 2];
+  __shared__ int64_t s_B[kSmallMax + 1];
+  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+  if (tid < kSmallMax + 2) s_T[tid] = a.classes->T[tid];
+  if (tid < kSmallMax + 1) s_B[tid] = a.classes->base[tid];
+  __syncthreads();
+  const Hot h{nullptr, 0u, 0};
+  const int64_t gwarp = (int64_t)wib * gridDim.x + blockIdx.x;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  WarpScratch& ws = s_ws[wib];
+  int64_t L = p.L0;
+  unsigned long long t0 = 0;
+  unsigned gen = tid == 0 ? ld_acquire(&p.state->bar_gen) : 0u;
+  Counters c = ld_counters(&p.ring[L % kCounterRing]);
+  for (;;) {
+    if (p.prof && blockIdx.x == 0 && tid == 0) t0 = gtimer();
+    const int cur = (int)(L & 1);
+    if (blockIdx.x == 0 && tid < (int)(sizeof(Counters) / 8))
+      reinterpret_cast<unsigned long long*>(&p.ring[(L + 2) % kCounterRing])[tid] = 0ull;
+    a.next_level = (int32_t)(L + 1);
+    a.next_cnt = &p.ring[(L + 1) % kCounterRing];
+    a.next_small = p.q_small[cur ^ 1];
+    a.next_warp = p.q_warp[cur ^ 1];
+    a.next_cta = p.q_cta[cur ^ 1];
+    Acc acc;
+    stream_slices<kQueueDirect>(a, h, p.q_cta[cur], (int64_t)c.bin[kBinCta], gwarp, nwarps, lane, acc);
+    const int64_t n_warp = (int64_t)c.bin[kBinWarp], n_small = (int64_t)c.bin[kBinSmall];
+    const int32_t* qw = p.q_warp[cur];
+    const int32_t* qs = p.q_small[cur];
+    const int64_t ng = n_warp + (n_small + 31) / 32;
+    for (int64_t g = gwarp; g < ng; g += nwarps) {
+      const bool wb = g < n_warp;
+      const int64_t base = wb ? g : (g - n_warp) * 32;
+      const int n = wb ? 1 : (int)std::min<int64_t>(32, n_small - base);
+      const int32_t v = lane < n ? __ldcg((wb ? qw : qs) + base + lane) : 0;
+      expand_range<kQueueDirect>(a, h, n, v, 0, 1 << 30, s_T, s_B, lane, ws, acc);
+    }
+    flush_acc<kQueueDirect>(a, acc);
+    grid_sync(&p.state->bar_count, &p.state->bar_gen, gen, p.prof ? p.prof + 3 : nullptr);
+    if (p.prof && blockIdx.x == 0 && tid == 0) {  // LBFS_LOOP_PROF: expansion / barrier split
+      const unsigned long long t2 = gtimer(), t1 = *(volatile unsigned long long*)(p.prof + 3);
+      p.prof[0] += t1 - t0;
+      p.prof[1] += t2 - t1;
+      p.prof[2] += 1;
+    }
+    const Counters nx = ld_counters(a.next_cnt);
+    if (blockIdx.x == 0 && tid == 0)
+      p.layers[L - p.L0] = lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, (int64_t)nx.discovered};
+    ++L;
+    if (nx.discovered == 0 || nx.edges >= p.bitmap_min_edges || L - p.L0 >= p.max_levels) break;
+    c = nx;
+  }
+  if (blockIdx.x == 0 && tid == 0) p.state->L_end = L;
 }
 
 // ---------------------------------------------------------------- K3 compaction
@@ -1037,6 +1207,16 @@ BfsEngine::BfsEngine(const Csr& csr) {
   for (auto fn : kernels) LBFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_));
   LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<kBitmapOut, 2>, kExpandThreads, dyn_smem_));
   expand_grid_ = sm_count_ * std::max(occ, 1);
+  // device-side level loop: one co-resident CTA per SM (cooperative launch)
+  int coop = 0, locc = 0;
+  LBFS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device_));
+  LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&locc, k_levels, kLoopThreads, 0));
+  loop_grid_ = (coop && locc > 0) ? sm_count_ : 0;
+  d_layers_ = dev_alloc<lbfs_layer>((size_t)kLoopCap);
+  loop_ = dev_alloc<LoopState>(1);
+  LBFS_CUDA(cudaMemset(loop_, 0, sizeof(LoopState)));
+  LBFS_CUDA(cudaMallocHost(&h_layers_, sizeof(lbfs_layer) * kLoopCap));
+  LBFS_CUDA(cudaMallocHost(&h_loop_, sizeof(LoopState)));
 }
 
 BfsEngine::~BfsEngine() {
@@ -1058,6 +1238,10 @@ BfsEngine::~BfsEngine() {
   }
   dev_free(cnt_);
   if (h_cnt_) cudaFreeHost(h_cnt_);
+  dev_free(d_layers_);
+  dev_free(loop_);
+  if (h_layers_) cudaFreeHost(h_layers_);
+  if (h_loop_) cudaFreeHost(h_loop_);
   dev_free(own_pred_);
   dev_free(own_level_);
   for (auto& e : ev_) cudaEventDestroy(e);
@@ -1121,6 +1305,8 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   dense_off_ = env_flag("LBFS_NO_DENSE");  // experiment: always use the small-bin list
   dense_warp_ = env_flag("LBFS_DENSE_WARP");  // experiment: dense warp-bin region
   hub_ldg_ = env_flag("LBFS_HUB_LDG");  // experiment: hub bin without TMA staging
+  loop_off_ = env_flag("LBFS_NO_LOOP");  // experiment: host-driven queue-mode levels
+  loop_prof_ = env_flag("LBFS_LOOP_PROF");
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = stream_;
   LBFS_CUDA(cudaEventRecord(ev_[0], st));
@@ -1160,10 +1346,66 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   bool prev_bitmap = false;
   const unsigned long long bitmap_min_edges = (unsigned long long)std::max<int64_t>(1 << 16, n_ / 64);
   int64_t L = 0;
+  const bool dev_loop = loop_grid_ > 0 && !loop_off_ && !split_ && !count_;
   for (;;) {
     const Counters c = h_cnt_[L % kCounterRing];
     const int slot = (int)((L + 1) % kCounterRing);
     LBFS_CUDA(cudaMemsetAsync(&cnt_[slot], 0, sizeof(Counters), st));
+    if (dev_loop && !prev_bitmap && c.edges < bitmap_min_edges) {
+      // a run of queue-mode levels on the device (k_levels), one launch
+      LoopArgs p{};
+      for (int b = 0; b < 2; ++b) {
+        p.q_small[b] = q_small_[b];
+        p.q_warp[b] = q_warp_[b];
+        p.q_cta[b] = q_cta_[b];
+      }
+      p.ring = cnt_;
+      p.layers = d_layers_;
+      p.state = loop_;
+      p.L0 = L;
+      p.max_levels = kLoopCap;
+      p.bitmap_min_edges = bitmap_min_edges;
+      if (loop_prof_) {
+        LBFS_CUDA(cudaMemsetAsync(dbg_, 0, 4 * sizeof(unsigned long long), st));
+        p.prof = dbg_;
+      }
+      // queue slot parity must match the level parity the kernel assumes
+      if (cur != (int)(L & 1)) throw Failure(LBFS_EINVAL, "internal: queue parity");
+      LBFS_CUDA(cudaEventRecord(ev_[2], st));
+      void* args[] = {(void*)&a, (void*)&p};
+      LBFS_CUDA(cudaLaunchCooperativeKernel((const void*)k_levels, dim3(loop_grid_), dim3(kLoopThreads), args, 0, st));
+      g_launches.fetch_add(1);
+      LBFS_CUDA(cudaEventRecord(ev_[3], st));
+      LBFS_CUDA(cudaMemcpyAsync(h_cnt_, cnt_, sizeof(Counters) * kCounterRing, cudaMemcpyDeviceToHost, st));
+      LBFS_CUDA(cudaMemcpyAsync(h_loop_, loop_, sizeof(LoopState), cudaMemcpyDeviceToHost, st));
+      LBFS_CUDA(cudaMemcpyAsync(h_layers_, d_layers_, sizeof(lbfs_layer) * 64, cudaMemcpyDeviceToHost, st));
+      LBFS_CUDA(cudaStreamSynchronize(st));
+      const int64_t L_end = h_loop_->L_end, k = L_end - L;
+      if (k < 1 || k > kLoopCap) throw Failure(LBFS_ECUDA, "internal: device level loop state");
+      if (k > 64) {
+        LBFS_CUDA(cudaMemcpyAsync(h_layers_ + 64, d_layers_ + 64, sizeof(lbfs_layer) * (k - 64),
+                                  cudaMemcpyDeviceToHost, st));
+        LBFS_CUDA(cudaStreamSynchronize(st));
+      }
+      float ms = 0.f;
+      LBFS_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
+      expand_ms += ms;
+      for (int64_t i = 0; i < k; ++i) layers_.push_back(h_layers_[i]);
+      if (loop_prof_) {
+        unsigned long long pr[4];
+        LBFS_CUDA(cudaMemcpy(pr, dbg_, sizeof(pr), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[lbfs] device loop %llu levels: expand %.2f us/level, barrier %.2f us/level\n", pr[2],
+                pr[2] ? pr[0] * 1e-3 / pr[2] : 0.0, pr[2] ? pr[1] * 1e-3 / pr[2] : 0.0);
+      }
+      if (trace_)
+        fprintf(stderr, "[lbfs] L%-3lld..L%-3lld device loop (%lld levels) %.3fms, last disc=%lld\n", (long long)L,
+                (long long)(L_end - 1), (long long)k, ms, (long long)h_layers_[k - 1].discovered);
+      cur ^= (int)(k & 1);
+      L = L_end;
+      prev_bitmap = false;
+      if (h_layers_[k - 1].discovered == 0) break;
+      continue;
+    }
     a.next_level = (int32_t)(L + 1);
     a.next_cnt = &cnt_[slot];
     a.next_small = q_small_[cur ^ 1];

@@ -134,6 +134,28 @@ struct CompactArgs {
   uint32_t* front;
 };
 
+// Device-side level loop (k_levels): cooperative launch, one CTA per SM.
+constexpr int kLoopThreads = 512;
+constexpr int64_t kLoopCap = 1 << 16;  // layers per k_levels launch
+
+struct LoopState {
+  long long L_end;   // first level not run by the last k_levels launch
+  unsigned bar_count;
+  unsigned bar_gen;
+};
+
+struct LoopArgs {
+  int32_t* q_small[2];
+  int32_t* q_warp[2];
+  CtaItem* q_cta[2];
+  Counters* ring;            // kCounterRing slots, slot L%3 = frontier of level L
+  lbfs_layer* layers;        // layers[L - L0]
+  LoopState* state;
+  int64_t L0, max_levels;
+  unsigned long long bitmap_min_edges;
+  unsigned long long* prof;  // LBFS_LOOP_PROF: {expand ns, barrier ns, levels, scratch}
+};
+
 class BfsEngine {
  public:
   // Builds the internal layout from a device CSR in original ids (not kept).
@@ -193,6 +215,13 @@ class BfsEngine {
   cudaEvent_t ev_[6] = {};
   std::vector<lbfs_layer> layers_;
   int expand_grid_ = 0;
+  int loop_grid_ = 0;             // k_levels CTAs (0: device loop unavailable)
+  bool loop_off_ = false;         // LBFS_NO_LOOP=1: host-driven queue levels
+  bool loop_prof_ = false;        // LBFS_LOOP_PROF=1: time split of k_levels on stderr
+  lbfs_layer* d_layers_ = nullptr;
+  lbfs_layer* h_layers_ = nullptr;  // pinned
+  LoopState* loop_ = nullptr;
+  LoopState* h_loop_ = nullptr;     // pinned
   int32_t hot_words_ = 0;  // visited words mirrored in shared memory
   int dyn_smem_ = 0;
   bool trace_ = false;  // LBFS_TRACE=1: per-level table on stderr
