@@ -70,6 +70,9 @@ typedef struct lbfs_device_info {
 
 /* Thread-local message of the last failing call ("" if none). */
 const char* lbfs_last_error(void);
+/* Make `device` the calling thread's device for subsequent construction
+ * calls (one process per GPU: the local rank's device). */
+int lbfs_set_device(int device);
 /* Properties of CUDA device `device`. */
 int lbfs_device_info_get(int device, lbfs_device_info* out);
 /* Number of kernel launches this process has issued through the library. */
@@ -138,6 +141,43 @@ int lbfs_bfs_device(lbfs_graph* g, int64_t root, int32_t* d_pred, int32_t* d_lev
                     lbfs_timing* t_out);
 /* Layers of the most recent BFS on this handle. */
 int lbfs_graph_last_layers(const lbfs_graph* g, lbfs_layer* out, int64_t cap, int64_t* n_layers);
+
+/* ---- partitioned BFS (multi-GPU) --------------------------
+ * One process per GPU; rank g of P (a power of two) owns the internal ids of
+ * bitmap words w with w % P == g and their rows. The level loop
+ * (traversal.py:90/152/366 made level-synchronous across ranks) is driven by
+ * the caller, who runs the three collectives between the steps on the same
+ * stream (paper_1604_02844_b200/distributed.py does this over
+ * torch.distributed/NCCL). Per level, with W = nwords / P:
+ *   lbfs_part_expand                      owned frontier -> visited / marks
+ *   lbfs_part_pack(send[P*W])             marks by owner       -> all_to_all(send, recv)
+ *   lbfs_part_merge(recv[P*W], fsend[W], red[2])
+ *                                         remote discoveries + parents, next
+ *                                         frontier              -> all_gather(fsend, fgath[P*W]),
+ *                                                                  all_reduce_sum(red)
+ *   lbfs_part_sync(fgath)                 replicated frontier / visited
+ *   lbfs_part_level_done(red)             layer + termination (host sync)
+ * lbfs_part_start(root, red) is followed by all_reduce_sum(red) and one
+ * lbfs_part_level_done (which emits no layer). Buffers are device pointers
+ * on the partition's device; `stream` is the caller's cudaStream_t, used as
+ * given (NULL = the legacy default stream), so the steps are ordered with the
+ * collectives the caller issues on the same stream. */
+int lbfs_part_create(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int64_t nnz, int rank,
+                     int nparts, lbfs_graph** out);
+int lbfs_part_create_from_csr(const lbfs_csr* csr, int rank, int nparts, lbfs_graph** out);
+int lbfs_part_info(const lbfs_graph* g, int* rank, int* nparts, int64_t* nwords, int64_t* n_local,
+                   int64_t* nnz_local);
+int lbfs_part_start(lbfs_graph* g, int64_t root, uint64_t* red, void* stream);
+int lbfs_part_expand(lbfs_graph* g, void* stream);
+int lbfs_part_pack(lbfs_graph* g, uint32_t* send, void* stream);
+int lbfs_part_merge(lbfs_graph* g, const uint32_t* recv, uint32_t* fsend, uint64_t* red, void* stream);
+int lbfs_part_sync(lbfs_graph* g, const uint32_t* fgath, void* stream);
+int lbfs_part_level_done(lbfs_graph* g, const uint64_t* red_global, lbfs_layer* layer, int* done);
+/* Owned vertices' pred (pad32(n)) / level (n) in original ids; every other
+ * entry is LBFS_SENTINEL / -1, so the ranks' outputs combine by min / max. */
+int lbfs_part_finish(lbfs_graph* g, int32_t* d_pred, int32_t* d_level, void* stream);
+/* Adjacency entries read by parent resolution since lbfs_part_start. */
+int lbfs_part_resolve_count(lbfs_graph* g, int64_t* out);
 
 #ifdef __cplusplus
 }

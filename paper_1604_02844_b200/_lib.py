@@ -73,6 +73,19 @@ SIGNATURES = {
     "lbfs_bfs_device": (ctypes.c_int, [_p, _i64, _p, _p, ctypes.POINTER(Layer), _i64,
                                        ctypes.POINTER(_i64), ctypes.POINTER(Timing)]),
     "lbfs_graph_last_layers": (ctypes.c_int, [_p, ctypes.POINTER(Layer), _i64, ctypes.POINTER(_i64)]),
+    "lbfs_set_device": (ctypes.c_int, [ctypes.c_int]),
+    "lbfs_part_create": (ctypes.c_int, [_i64, _p, _p, _i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_p)]),
+    "lbfs_part_create_from_csr": (ctypes.c_int, [_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_p)]),
+    "lbfs_part_info": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                      ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "lbfs_part_start": (ctypes.c_int, [_p, _i64, _p, _p]),
+    "lbfs_part_expand": (ctypes.c_int, [_p, _p]),
+    "lbfs_part_pack": (ctypes.c_int, [_p, _p, _p]),
+    "lbfs_part_merge": (ctypes.c_int, [_p, _p, _p, _p, _p]),
+    "lbfs_part_sync": (ctypes.c_int, [_p, _p, _p]),
+    "lbfs_part_level_done": (ctypes.c_int, [_p, _p, ctypes.POINTER(Layer), ctypes.POINTER(ctypes.c_int)]),
+    "lbfs_part_finish": (ctypes.c_int, [_p, _p, _p, _p]),
+    "lbfs_part_resolve_count": (ctypes.c_int, [_p, ctypes.POINTER(_i64)]),
 }
 
 

@@ -82,6 +82,15 @@ void lbfs_host_free(void* p) {
   if (p) cudaFreeHost(p);
 }
 
+int lbfs_set_device(int device) {
+  return guarded([&] {
+    int count = 0;
+    LBFS_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw_inval("device out of range");
+    LBFS_CUDA(cudaSetDevice(device));
+  });
+}
+
 int lbfs_device_info_get(int device, lbfs_device_info* out) {
   return guarded([&] {
     if (!out) throw_inval("out is NULL");
@@ -382,6 +391,150 @@ int lbfs_graph_last_layers(const lbfs_graph* g, lbfs_layer* out, int64_t cap, in
   return guarded([&] {
     if (!g) throw_inval("graph is NULL");
     copy_layers(*g->eng, out, cap, n_layers);
+  });
+}
+
+
+/* ---- partitioned (multi-GPU) BFS: one partition per process ----------- */
+
+static BfsEngine& part_engine(lbfs_graph* g) {
+  if (!g) throw_inval("graph is NULL");
+  LBFS_CUDA(cudaSetDevice(g->eng->device()));
+  return *g->eng;
+}
+
+int lbfs_part_create_from_csr(const lbfs_csr* csr, int rank, int nparts, lbfs_graph** out) {
+  return guarded([&] {
+    if (!csr || !out) throw_inval("bad arguments");
+    LBFS_CUDA(cudaSetDevice(csr->c.device));
+    auto* g = new lbfs_graph;
+    try {
+      g->eng = new BfsEngine(csr->c, rank, nparts);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int lbfs_part_create(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int64_t nnz, int rank,
+                     int nparts, lbfs_graph** out) {
+  return guarded([&] {
+    check_ids(n);
+    if (!out || !row_ptr || nnz < 0 || (nnz > 0 && !col_idx)) throw_inval("bad arguments");
+    if (row_ptr[0] != 0 || row_ptr[n] != nnz) throw_inval("row_ptr must start at 0 and end at nnz");
+    Csr c;
+    LBFS_CUDA(cudaGetDevice(&c.device));
+    c.n = n;
+    c.nnz = nnz;
+    c.row_ptr = dev_alloc<int64_t>((size_t)n + 1);
+    c.col_idx = dev_alloc<int32_t>((size_t)nnz + 4);
+    try {
+      LBFS_CUDA(cudaMemcpy(c.row_ptr, row_ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice));
+      if (nnz > 0)
+        LBFS_CUDA(cudaMemcpy(c.col_idx, col_idx, sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice));
+      auto* g = new lbfs_graph;
+      try {
+        g->eng = new BfsEngine(c, rank, nparts);
+      } catch (...) {
+        delete g;
+        throw;
+      }
+      *out = g;
+    } catch (...) {
+      free_csr(c);
+      throw;
+    }
+    free_csr(c);
+  });
+}
+
+int lbfs_part_info(const lbfs_graph* g, int* rank, int* nparts, int64_t* nwords, int64_t* n_local,
+                   int64_t* nnz_local) {
+  return guarded([&] {
+    if (!g) throw_inval("graph is NULL");
+    const BfsEngine& e = *g->eng;
+    if (rank) *rank = e.part_rank();
+    if (nparts) *nparts = e.nparts();
+    if (nwords) *nwords = e.nwords();
+    if (n_local) *n_local = e.n_local();
+    if (nnz_local) *nnz_local = e.nnz_local();
+  });
+}
+
+// the caller's stream as given: NULL is the legacy default stream (torch's
+// default stream reports cuda_stream == 0), never the library's own stream,
+// so the steps stay ordered with the caller's collectives
+static cudaStream_t as_stream(lbfs_graph*, void* stream) { return (cudaStream_t)stream; }
+
+int lbfs_part_start(lbfs_graph* g, int64_t root, uint64_t* red, void* stream) {
+  return guarded([&] {
+    BfsEngine& e = part_engine(g);
+    if (!red) throw_inval("red is NULL");
+    std::lock_guard<std::mutex> lk(e.mu);
+    e.part_start(root, as_stream(g, stream), (unsigned long long*)red);
+  });
+}
+
+int lbfs_part_expand(lbfs_graph* g, void* stream) {
+  return guarded([&] {
+    BfsEngine& e = part_engine(g);
+    std::lock_guard<std::mutex> lk(e.mu);
+    e.part_expand(as_stream(g, stream));
+  });
+}
+
+int lbfs_part_pack(lbfs_graph* g, uint32_t* send, void* stream) {
+  return guarded([&] {
+    BfsEngine& e = part_engine(g);
+    if (!send) throw_inval("send is NULL");
+    std::lock_guard<std::mutex> lk(e.mu);
+    e.part_pack(send, as_stream(g, stream));
+  });
+}
+
+int lbfs_part_merge(lbfs_graph* g, const uint32_t* recv, uint32_t* fsend, uint64_t* red, void* stream) {
+  return guarded([&] {
+    BfsEngine& e = part_engine(g);
+    if (!recv || !fsend || !red) throw_inval("NULL buffer");
+    std::lock_guard<std::mutex> lk(e.mu);
+    e.part_merge(recv, fsend, (unsigned long long*)red, as_stream(g, stream));
+  });
+}
+
+int lbfs_part_sync(lbfs_graph* g, const uint32_t* fgath, void* stream) {
+  return guarded([&] {
+    BfsEngine& e = part_engine(g);
+    if (!fgath) throw_inval("fgath is NULL");
+    std::lock_guard<std::mutex> lk(e.mu);
+    e.part_sync(fgath, as_stream(g, stream));
+  });
+}
+
+int lbfs_part_level_done(lbfs_graph* g, const uint64_t* red_global, lbfs_layer* layer, int* done) {
+  return guarded([&] {
+    BfsEngine& e = part_engine(g);
+    if (!red_global) throw_inval("red_global is NULL");
+    std::lock_guard<std::mutex> lk(e.mu);
+    e.part_level_done((const unsigned long long*)red_global, layer, done);
+  });
+}
+
+int lbfs_part_finish(lbfs_graph* g, int32_t* d_pred, int32_t* d_level, void* stream) {
+  return guarded([&] {
+    BfsEngine& e = part_engine(g);
+    std::lock_guard<std::mutex> lk(e.mu);
+    e.part_finish(d_pred, d_level, as_stream(g, stream));
+  });
+}
+
+int lbfs_part_resolve_count(lbfs_graph* g, int64_t* out) {
+  return guarded([&] {
+    BfsEngine& e = part_engine(g);
+    if (!out) throw_inval("out is NULL");
+    std::lock_guard<std::mutex> lk(e.mu);
+    *out = (int64_t)e.resolve_scanned();
   });
 }
 

@@ -119,6 +119,7 @@ struct WarpScratch {
 
 __device__ __forceinline__ bool bit_clear(uint32_t word, int32_t v) { return ((word >> (v & 31)) & 1u) == 0; }
 
+// (single-partition runs only: ids are local == global)
 // Queue mode (warp-collective), a batch of K candidates per lane: the K
 // atomicOr elections are in flight together; winners write level + pred and
 // are appended to the next level's bins with one atomic per bin per warp for
@@ -251,7 +252,9 @@ __device__ __forceinline__ void settle_bitmap(const LevelArgs& a, const Hot& h, 
       run_bits = 0;
     }
     run_bits |= 1u << (v & 31);
-    a.pred_int[v] = par(k);
+    // partitioned: a neighbour owned by another rank is only marked; its
+    // owner resolves the parent after the exchange (partition.cu)
+    if (part_owned(v, a.part_log, a.part_rank)) a.pred_int[part_local(v, a.part_log)] = par(k);
     if (a.dbg) atomicAdd(a.dbg + (wi < h.words ? 0 : 1), 1ull);  // LBFS_COUNT only
   }
   red_or(a.visited + run_w, run_bits);
@@ -951,11 +954,13 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
   uint32_t nb = 0, mhub = 0, mlist = 0, mwarp = 0;
   int hub_items = 0;
   if (t < kCompactWords && w0 + t < c.nwords) {
-    const uint32_t w = c.visited[w0 + t], p = c.prev[w0 + t];
+    const int64_t gw = ((w0 + t) << c.part_log) | c.part_rank;  // global word of owned word w0+t
+    const uint32_t w = c.visited[gw], p = c.prev[gw];
     nb = w & ~p;
     c.front[w0 + t] = nb;  // next frontier as a bitmap (dense small-region path)
+    if (c.fsend) c.fsend[w0 + t] = nb;
     if (nb) {
-      c.prev[w0 + t] = w;
+      c.prev[gw] = w;
       const int64_t vw = (w0 + t) * 32;
       mhub = nb & range_mask(vw, 0, c.t_cta);
       mwarp = nb & range_mask(vw, c.t_cta, c.t_warp);
@@ -1124,56 +1129,82 @@ __global__ void k_finalize_scalar(const int32_t* __restrict__ old2new, const int
   }
 }
 
-__global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int32_t root_orig, Counters* cnt0) {
+// Root of a BFS (traversal.py:135-139, 343-347): its bit in visited/prev
+// (and in the replicated frontier bitmap when partitioned) on every rank;
+// the owner records level 0 / pred = root and seeds its bins. red, when
+// given, receives the (frontier, edges) counts for the cross-rank sum.
+__global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int32_t root_orig, Counters* cnt0,
+                       uint32_t* fglob, unsigned long long* red) {
   const int32_t r = old2new[root_orig];
-  const int64_t st = a.row_ptr[r];
-  const int32_t deg = (int32_t)(a.row_ptr[r + 1] - st);
   a.visited[r >> 5] |= 1u << (r & 31);
   prev[r >> 5] |= 1u << (r & 31);
-  a.level_int[r] = 0;
-  a.pred_int[r] = root_orig;
+  if (fglob) fglob[r >> 5] |= 1u << (r & 31);
   Counters c{};
-  c.discovered = 1;
-  c.edges = (unsigned long long)deg;
-  if (r < a.t_cta) {
-    const int items = (deg + kChunk - 1) / kChunk;
-    for (int k = 0; k < items; ++k)
-      a.next_cta[k] = CtaItem{st + (int64_t)k * kChunk, min(kChunk, deg - k * kChunk), root_orig};
-    c.bin[kBinCta] = (unsigned long long)items;
-  } else if (r < a.t_warp) {
-    a.next_warp[0] = r;
-    c.bin[kBinWarp] = 1;
-  } else if (r < a.t_nz) {
-    a.next_small[0] = r;
-    c.bin[kBinSmall] = 1;
+  if (part_owned(r, a.part_log, a.part_rank)) {
+    const int32_t l = part_local(r, a.part_log);
+    const int64_t st = a.row_ptr[l];
+    const int32_t deg = (int32_t)(a.row_ptr[l + 1] - st);
+    a.level_int[l] = 0;
+    a.pred_int[l] = root_orig;
+    c.discovered = 1;
+    c.edges = (unsigned long long)deg;
+    if (l < a.t_cta) {
+      const int items = (deg + kChunk - 1) / kChunk;
+      for (int k = 0; k < items; ++k)
+        a.next_cta[k] = CtaItem{st + (int64_t)k * kChunk, min(kChunk, deg - k * kChunk), root_orig};
+      c.bin[kBinCta] = (unsigned long long)items;
+    } else if (l < a.t_warp) {
+      a.next_warp[0] = l;
+      c.bin[kBinWarp] = 1;
+    } else if (l < a.t_nz) {
+      a.next_small[0] = l;
+      c.bin[kBinSmall] = 1;
+    }
   }
   *cnt0 = c;
+  if (red) {
+    red[0] = c.discovered;
+    red[1] = c.edges;
+  }
 }
 
 // ---------------------------------------------------------------- engine
-BfsEngine::BfsEngine(const Csr& csr) {
+BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
+  if (nparts < 1 || (nparts & (nparts - 1)) != 0 || nparts > 64) throw_inval("nparts must be a power of two <= 64");
+  if (rank < 0 || rank >= nparts) throw_inval("rank out of range");
   LBFS_CUDA(cudaGetDevice(&device_));
   sm_count_ = current_sm_count();
+  nparts_ = nparts;
+  part_rank_ = rank;
+  while ((1 << part_log_) < nparts_) ++part_log_;
   n_ = csr.n;
   nnz_ = csr.nnz;
-  nwords_ = (n_ + 31) / 32;
+  // bitmap words rounded up to whole partition rounds; rank g owns words g, g+P, ...
+  nwords_ = ((n_ + 31) / 32 + nparts_ - 1) / nparts_ * nparts_;
+  nwl_ = nwords_ / nparts_;
+  n_loc_ = nparts_ == 1 ? n_ : nwl_ * 32;
   npad_ = pad32(n_);
   LBFS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   build_layout(csr);
   visited_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
   prev_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
-  pred_int_ = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_, 1));
-  level_int_ = dev_alloc<int32_t>((size_t)(n_ + 4));
-  front_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
+  pred_int_ = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_loc_, 1));
+  level_int_ = dev_alloc<int32_t>((size_t)(n_loc_ + 4));
+  front_ = dev_alloc<uint32_t>((size_t)nwl_ + 4);
   dbg_ = dev_alloc<unsigned long long>(4);
   LBFS_CUDA(cudaMemset(dbg_, 0, 4 * sizeof(unsigned long long)));
+  if (nparts_ > 1) {
+    fglob_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
+    resolve_cnt_ = dev_alloc<unsigned long long>(1);
+    LBFS_CUDA(cudaMemset(resolve_cnt_, 0, sizeof(unsigned long long)));
+  }
   // Bins, double-buffered: a vertex enters a bin once per BFS, so n entries
   // bound the small/warp bins; CTA items <= nnz/kChunk + #(deg >= kCtaMin).
-  cap_cta_ = nnz_ / kChunk + t_cta_ + 2;
+  cap_cta_ = nnz_loc_ / kChunk + t_cta_ + 2;
   // group items: one per started kItemElems of each 32-entry group, per block
-  cap_items_ = nnz_ / kItemElems + n_ / 32 + 2 * ((n_ + kCompactVerts - 1) / kCompactVerts) + 16;
+  cap_items_ = nnz_loc_ / kItemElems + n_loc_ / 32 + 2 * ((n_loc_ + kCompactVerts - 1) / kCompactVerts) + 16;
   for (int b = 0; b < 2; ++b) {
-    q_small_[b] = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_, 1));
+    q_small_[b] = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_loc_, 1));
     q_warp_[b] = dev_alloc<int32_t>((size_t)std::max<int64_t>(t_warp_, 1));
     q_cta_[b] = dev_alloc<CtaItem>((size_t)cap_cta_);
     q_items_[b] = dev_alloc<GroupItem>((size_t)cap_items_);
@@ -1248,7 +1279,11 @@ BfsEngine::~BfsEngine() {
   for (auto& e : ev_split_) cudaEventDestroy(e);
   dev_free(row_ptr_);
   dev_free(col_idx_);
+  if (new2old_loc_ != new2old_) dev_free(new2old_loc_);
   dev_free(new2old_);
+  dev_free(fglob_);
+  if (h_red_) cudaFreeHost(h_red_);
+  dev_free(resolve_cnt_);
   dev_free(old2new_);
   cudaStreamDestroy(stream_);
 }
@@ -1258,7 +1293,7 @@ void BfsEngine::ensure_own_outputs() {
   if (!own_level_) own_level_ = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_, 1));
 }
 
-static unsigned clamp_grid(int64_t blocks, int64_t cap) {
+unsigned clamp_grid(int64_t blocks, int64_t cap) {
   return (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
 }
 
@@ -1292,13 +1327,102 @@ void BfsEngine::launch_expand(bool bitmap, int pi, unsigned grid, const LevelArg
     launch_expand_m<kQueueOut>(pi, grid, kRingBytes, a, f, 0, hub_ldg_, st);
 }
 
-static bool env_flag(const char* name) {
+bool env_flag(const char* name) {
   const char* v = getenv(name);
   return v && *v && *v != '0';
 }
 
-void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t) {
-  if (root < 0 || root >= n_) throw_inval("root out of range");
+LevelArgs BfsEngine::level_args() const {
+  LevelArgs a{};
+  a.row_ptr = row_ptr_;
+  a.col_idx = col_idx_;
+  a.new2old = new2old_loc_;
+  a.visited = visited_;
+  a.prev = prev_;
+  a.pred_int = pred_int_;
+  a.level_int = level_int_;
+  a.classes = classes_;
+  a.dbg = count_ ? dbg_ : nullptr;
+  const char* rf = getenv("LBFS_REFRESH");  // hub chunks between snapshot refreshes (0 = off)
+  a.refresh_chunks = rf ? atoi(rf) : kRefreshChunks;
+  a.t_cta = t_cta_;
+  a.t_warp = t_warp_;
+  a.t_nz = t_nz_;
+  a.part_log = part_log_;
+  a.part_rank = part_rank_;
+  return a;
+}
+
+unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, bool bitmap, bool prev_bitmap, int cur, int64_t L,
+                                 cudaStream_t st) {
+  a.next_level = (int32_t)(L + 1);
+  a.next_cnt = &cnt_[(L + 1) % kCounterRing];
+  a.next_small = q_small_[cur ^ 1];
+  a.next_warp = q_warp_[cur ^ 1];
+  a.next_cta = q_cta_[cur ^ 1];
+  Frontier f{};
+  f.cta = q_cta_[cur];
+  f.n_cta = (int64_t)c.bin[kBinCta];
+  if (prev_bitmap) {  // k_compact produced a list + group items
+    f.list = q_small_[cur];
+    f.items = q_items_[cur];
+    f.n_items = (int64_t)c.bin[kBinItems];
+    f.wslice = q_wslice_[cur];
+    f.n_wslice = (int64_t)c.bin[kBinWSlice];
+    // dense small region: stream it whole when most of it is in the frontier
+    const int64_t small_region = (int64_t)t_nz_ - t_warp_;
+    if (small_region > 0 && (int64_t)c.bin[kBinSmall] * kDenseDenom > small_region * kDenseNum && !dense_off_) {
+      f.n_items = 0;
+      f.front = front_;
+      f.dense = dense_tasks_;
+      f.n_dense = n_dense_tasks_;
+    }
+    const int64_t warp_region = (int64_t)t_warp_ - t_cta_;
+    // (opt-in: measured slower than warp slices on S24, 0.55 vs 0.36 ms)
+    if (warp_region > 0 && (int64_t)c.bin[kBinWSlice] * kDenseDenom > warp_region * kDenseNum && !dense_off_ &&
+        dense_warp_) {
+      f.n_wslice = 0;
+      f.front = front_;
+      f.dense_warp = true;
+    }
+  } else {  // winners appended to raw queues
+    f.small = q_small_[cur];
+    f.warp = q_warp_[cur];
+    f.n_small = (int64_t)c.bin[kBinSmall];
+    f.n_warp = (int64_t)c.bin[kBinWarp];
+  }
+  const int64_t need = std::max({(f.n_cta + kExpandWarps - 1) / kExpandWarps, f.dense_warp ? (int64_t)1 << 30 : 0,
+                                  (f.n_dense + kExpandWarps - 1) / kExpandWarps,
+                                  (f.n_wslice + kExpandWarps - 1) / kExpandWarps,
+                                  (f.n_items + kExpandWarps - 1) / kExpandWarps,
+                                  (f.n_warp + (f.n_small + 31) / 32 + kExpandWarps - 1) / kExpandWarps,
+                                  (int64_t)1});
+  const unsigned grid = bitmap ? (unsigned)expand_grid_ : clamp_grid(need, expand_grid_);
+  const bool any = f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice + f.n_dense > 0 || f.dense_warp;
+  if (any) {
+    // one launch per non-empty bin: each phase kernel gets its own register
+    // allocation (the fused kernel was capped at 64 registers by 1024 threads)
+    const bool has[6] = {f.n_cta > 0, f.n_items > 0, f.n_warp + f.n_small > 0, f.n_wslice > 0, f.n_dense > 0,
+                         f.dense_warp};
+    for (int pi = 0; pi < 6; ++pi) {
+      if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[pi], st));
+      if (!has[pi]) continue;
+      launch_expand(bitmap, pi, grid, a, f, st);
+    }
+    if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[6], st));
+  }
+  split_any_ = any;
+  return grid;
+}
+
+void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st) {
+  CompactArgs ca{row_ptr_, new2old_loc_, visited_, prev_, nwl_, level_int_, (int32_t)(L + 1),
+                 t_cta_, t_warp_, t_nz_, &cnt_[(L + 1) % kCounterRing], q_small_[cur ^ 1], q_cta_[cur ^ 1],
+                 q_items_[cur ^ 1], q_wslice_[cur ^ 1], front_, part_log_, part_rank_, fsend};
+  LBFS_LAUNCH(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
+}
+
+void BfsEngine::read_env() {
   trace_ = env_flag("LBFS_TRACE");  // per-level table on stderr
   count_ = env_flag("LBFS_COUNT");  // candidate-write counters (slow)
   split_ = env_flag("LBFS_SPLIT");  // one launch per bin
@@ -1307,6 +1431,12 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   hub_ldg_ = env_flag("LBFS_HUB_LDG");  // experiment: hub bin without TMA staging
   loop_off_ = env_flag("LBFS_NO_LOOP");  // experiment: host-driven queue-mode levels
   loop_prof_ = env_flag("LBFS_LOOP_PROF");
+}
+
+void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t) {
+  if (root < 0 || root >= n_) throw_inval("root out of range");
+  if (nparts_ != 1) throw_inval("partitioned graph: use the lbfs_part_* level steps");
+  read_env();
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = stream_;
   LBFS_CUDA(cudaEventRecord(ev_[0], st));
@@ -1315,28 +1445,12 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     LBFS_LAUNCH(k_init, grid, 256, 0, st, (uint4*)visited_, (uint4*)prev_, (nwords_ + 3) / 4, (int4*)level_int_,
                 (n_ + 3) / 4);
   }
-  LevelArgs a{};
-  a.row_ptr = row_ptr_;
-  a.col_idx = col_idx_;
-  a.new2old = new2old_;
-  a.visited = visited_;
-  a.prev = prev_;
-  a.pred_int = pred_int_;
-  a.level_int = level_int_;
-  a.classes = classes_;
-  a.dbg = count_ ? dbg_ : nullptr;
-  {
-    const char* rf = getenv("LBFS_REFRESH");  // hub chunks between snapshot refreshes (0 = off)
-    a.refresh_chunks = rf ? atoi(rf) : kRefreshChunks;
-  }
-  a.t_cta = t_cta_;
-  a.t_warp = t_warp_;
-  a.t_nz = t_nz_;
+  LevelArgs a = level_args();
   int cur = 0;
   a.next_small = q_small_[cur];
   a.next_warp = q_warp_[cur];
   a.next_cta = q_cta_[cur];
-  LBFS_LAUNCH(k_seed, 1, 1, 0, st, a, prev_, old2new_, (int32_t)root, &cnt_[0]);
+  LBFS_LAUNCH(k_seed, 1, 1, 0, st, a, prev_, old2new_, (int32_t)root, &cnt_[0], nullptr, nullptr);
   LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[0], &cnt_[0], sizeof(Counters), cudaMemcpyDeviceToHost, st));
   LBFS_CUDA(cudaEventRecord(ev_[1], st));
   LBFS_CUDA(cudaStreamSynchronize(st));
@@ -1406,72 +1520,11 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       if (h_layers_[k - 1].discovered == 0) break;
       continue;
     }
-    a.next_level = (int32_t)(L + 1);
-    a.next_cnt = &cnt_[slot];
-    a.next_small = q_small_[cur ^ 1];
-    a.next_warp = q_warp_[cur ^ 1];
-    a.next_cta = q_cta_[cur ^ 1];
-    Frontier f{};
-    f.cta = q_cta_[cur];
-    f.n_cta = (int64_t)c.bin[kBinCta];
-    if (prev_bitmap) {  // k_compact produced a list + group items
-      f.list = q_small_[cur];
-      f.items = q_items_[cur];
-      f.n_items = (int64_t)c.bin[kBinItems];
-      f.wslice = q_wslice_[cur];
-      f.n_wslice = (int64_t)c.bin[kBinWSlice];
-      // dense small region: stream it whole when most of it is in the frontier
-      const int64_t small_region = (int64_t)t_nz_ - t_warp_;
-      if (small_region > 0 && (int64_t)c.bin[kBinSmall] * kDenseDenom > small_region * kDenseNum && !dense_off_) {
-        f.n_items = 0;
-        f.front = front_;
-        f.dense = dense_tasks_;
-        f.n_dense = n_dense_tasks_;
-      }
-      const int64_t warp_region = (int64_t)t_warp_ - t_cta_;
-      // (opt-in: measured slower than warp slices on S24, 0.55 vs 0.36 ms)
-      if (warp_region > 0 && (int64_t)c.bin[kBinWSlice] * kDenseDenom > warp_region * kDenseNum && !dense_off_ &&
-          dense_warp_) {
-        f.n_wslice = 0;
-        f.front = front_;
-        f.dense_warp = true;
-      }
-    } else {  // winners appended to raw queues
-      f.small = q_small_[cur];
-      f.warp = q_warp_[cur];
-      f.n_small = (int64_t)c.bin[kBinSmall];
-      f.n_warp = (int64_t)c.bin[kBinWarp];
-    }
     const bool bitmap = c.edges >= bitmap_min_edges;
-    const int64_t need = std::max({(f.n_cta + kExpandWarps - 1) / kExpandWarps, f.dense_warp ? (int64_t)1 << 30 : 0,
-                                    (f.n_dense + kExpandWarps - 1) / kExpandWarps,
-                                    (f.n_wslice + kExpandWarps - 1) / kExpandWarps,
-                                    (f.n_items + kExpandWarps - 1) / kExpandWarps,
-                                    (f.n_warp + (f.n_small + 31) / 32 + kExpandWarps - 1) / kExpandWarps,
-                                    (int64_t)1});
-    const unsigned grid = bitmap ? (unsigned)expand_grid_ : clamp_grid(need, expand_grid_);
     LBFS_CUDA(cudaEventRecord(ev_[2], st));
-    float split_ms[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice + f.n_dense > 0 || f.dense_warp) {
-      // one launch per non-empty bin: each phase kernel gets its own register
-      // allocation (the fused kernel was capped at 64 registers by 1024 threads)
-      const bool has[6] = {f.n_cta > 0, f.n_items > 0, f.n_warp + f.n_small > 0, f.n_wslice > 0, f.n_dense > 0,
-                           f.dense_warp};
-      for (int pi = 0; pi < 6; ++pi) {
-        if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[pi], st));
-        if (!has[pi]) continue;
-        launch_expand(bitmap, pi, grid, a, f, st);
-      }
-      if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[6], st));
-    }
+    const unsigned grid = expand_level(a, c, bitmap, prev_bitmap, cur, L, st);
     LBFS_CUDA(cudaEventRecord(ev_[3], st));
-    const bool did_compact = bitmap;
-    if (bitmap) {
-      CompactArgs ca{row_ptr_, new2old_, visited_, prev_, nwords_, level_int_, (int32_t)(L + 1),
-                     t_cta_, t_warp_, t_nz_, &cnt_[slot], q_small_[cur ^ 1], q_cta_[cur ^ 1], q_items_[cur ^ 1],
-                     q_wslice_[cur ^ 1], front_};
-      LBFS_LAUNCH(k_compact, (unsigned)((n_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
-    }
+    if (bitmap) compact_level(cur, L, nullptr, st);
     LBFS_CUDA(cudaEventRecord(ev_[5], st));
     LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[slot], &cnt_[slot], sizeof(Counters), cudaMemcpyDeviceToHost, st));
     LBFS_CUDA(cudaStreamSynchronize(st));
@@ -1480,15 +1533,15 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     LBFS_CUDA(cudaEventElapsedTime(&cms, ev_[3], ev_[5]));
     expand_ms += ms;
     const Counters nx = h_cnt_[slot];
-    unsigned long long dbg[4] = {0, 0, 0, 0};
     if (count_) {
+      unsigned long long dbg[4] = {0, 0, 0, 0};
       LBFS_CUDA(cudaMemcpy(dbg, dbg_, sizeof(dbg), cudaMemcpyDeviceToHost));
       LBFS_CUDA(cudaMemset(dbg_, 0, sizeof(dbg)));
       fprintf(stderr, "[lbfs]      candidate writes hot=%llu cold=%llu streamed elements=%llu dwarp rows=%llu\n",
               dbg[0], dbg[1], dbg[2], dbg[3]);
-
     }
-    if (split_ && (f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice + f.n_dense > 0 || f.dense_warp)) {
+    if (split_ && split_any_) {
+      float split_ms[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       for (int pi = 0; pi < 6; ++pi) LBFS_CUDA(cudaEventElapsedTime(&split_ms[pi], ev_split_[pi], ev_split_[pi + 1]));
       fprintf(stderr,
               "[lbfs]      split: hub=%.3fms items=%.3fms queues=%.3fms wslice=%.3fms dense=%.3fms dwarp=%.3fms\n",
@@ -1499,7 +1552,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
               "[lbfs] L%-3lld %s in=%-9llu edges=%-10llu bins(s|list/w/c/items)=%llu/%llu/%llu/%llu grid=%u "
               "expand=%.3fms compact=%.3fms disc=%llu\n",
               (long long)L, bitmap ? "bitmap" : "queue ", c.discovered, c.edges, c.bin[0], c.bin[1], c.bin[2], c.bin[3],
-              grid, ms, did_compact ? cms : 0.f, nx.discovered);
+              grid, ms, bitmap ? cms : 0.f, nx.discovered);
     layers_.push_back(lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, (int64_t)nx.discovered});
     cur ^= 1;
     ++L;

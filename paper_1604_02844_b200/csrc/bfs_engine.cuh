@@ -109,7 +109,11 @@ struct LevelArgs {
   unsigned long long* dbg;  // LBFS_COUNT: candidate-write counters (hot, cold)
   int32_t refresh_chunks;   // hub chunks between hot-snapshot refreshes (warp 0)
   int32_t next_level;
-  int32_t t_cta, t_warp, t_nz;  // internal-id bin boundaries
+  int32_t t_cta, t_warp, t_nz;  // internal-id bin boundaries (local rows)
+  // partitioned run (nparts = 1 << part_log > 1): this rank owns the ids of
+  // bitmap words w with w % nparts == part_rank; pred_int/level_int, rows and
+  // frontier entries use local row ids, bitmaps and neighbours global ids
+  int32_t part_log, part_rank;
   // queue-mode outputs (direct append by the winners)
   Counters* next_cnt;
   int32_t* next_small;
@@ -122,7 +126,7 @@ struct CompactArgs {
   const int32_t* new2old;
   const uint32_t* visited;
   uint32_t* prev;           // visited at the previous level boundary
-  int64_t nwords;
+  int64_t nwords;           // local (owned) words
   int32_t* level_int;
   int32_t next_level;
   int32_t t_cta, t_warp, t_nz;
@@ -132,7 +136,20 @@ struct CompactArgs {
   GroupItem* next_items;
   CtaItem* next_wslice;
   uint32_t* front;
+  int32_t part_log, part_rank;
+  uint32_t* fsend;          // partitioned: owned words of the next frontier (all-gather input)
 };
+
+// Owner / local id of a global internal id (word-cyclic partition).
+__host__ __device__ __forceinline__ bool part_owned(int32_t v, int32_t part_log, int32_t part_rank) {
+  return ((v >> 5) & ((1 << part_log) - 1)) == part_rank;
+}
+__host__ __device__ __forceinline__ int32_t part_local(int32_t v, int32_t part_log) {
+  return (((v >> 5) >> part_log) << 5) | (v & 31);
+}
+__host__ __device__ __forceinline__ int64_t part_global(int64_t l, int32_t part_log, int32_t part_rank) {
+  return ((((l >> 5) << part_log) | part_rank) << 5) | (l & 31);
+}
 
 // Device-side level loop (k_levels): cooperative launch, one CTA per SM.
 constexpr int kLoopThreads = 512;
@@ -156,10 +173,18 @@ struct LoopArgs {
   unsigned long long* prof;  // LBFS_LOOP_PROF: {expand ns, barrier ns, levels, scratch}
 };
 
+bool env_flag(const char* name);
+__global__ void k_init(uint4* vis4, uint4* prev4, int64_t nwords4, int4* lvl4, int64_t n4);
+__global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int32_t root_orig, Counters* cnt0,
+                       uint32_t* fglob, unsigned long long* red);
+unsigned clamp_grid(int64_t blocks, int64_t cap);
+
 class BfsEngine {
  public:
   // Builds the internal layout from a device CSR in original ids (not kept).
-  explicit BfsEngine(const Csr& csr);
+  // nparts > 1 (a power of two): the partition of rank `rank` only
+  // (multi-GPU, partition.cu); run() needs nparts == 1.
+  explicit BfsEngine(const Csr& csr, int rank = 0, int nparts = 1);
   ~BfsEngine();
   BfsEngine(const BfsEngine&) = delete;
   BfsEngine& operator=(const BfsEngine&) = delete;
@@ -168,6 +193,21 @@ class BfsEngine {
   // BFS into device buffers d_pred[pad32(n)], d_level[n]; synchronous.
   void run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t);
 
+  // ---- partitioned BFS, one level step at a time (partition.cu); the
+  // collectives between the steps are issued by the caller on `st`
+  void part_start(int64_t root, cudaStream_t st, unsigned long long* red);
+  void part_expand(cudaStream_t st);
+  void part_pack(uint32_t* send, cudaStream_t st);
+  void part_merge(const uint32_t* recv, uint32_t* fsend, unsigned long long* red, cudaStream_t st);
+  void part_sync(const uint32_t* fgath, cudaStream_t st);
+  void part_level_done(const unsigned long long* red_global, lbfs_layer* layer, int* done);
+  void part_finish(int32_t* d_pred, int32_t* d_level, cudaStream_t st);
+  int nparts() const { return nparts_; }
+  int part_rank() const { return part_rank_; }
+  int64_t nwords() const { return nwords_; }
+  int64_t n_local() const { return n_loc_; }
+  int64_t nnz_local() const { return nnz_loc_; }
+  unsigned long long resolve_scanned() const;
   int64_t n() const { return n_; }
   int64_t nnz() const { return nnz_; }
   int64_t npad() const { return npad_; }
@@ -182,9 +222,28 @@ class BfsEngine {
  private:
   void build_layout(const Csr& csr);
   void launch_expand(bool bitmap, int pi, unsigned grid, const LevelArgs& a, const Frontier& f, cudaStream_t st);
+  LevelArgs level_args() const;
+  // frontier of level L (queue slot cur, counters c) -> launches; returns the grid
+  unsigned expand_level(LevelArgs& a, const Counters& c, bool bitmap, bool prev_bitmap, int cur, int64_t L,
+                        cudaStream_t st);
+  void compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st);
+  void read_env();
+  bool split_any_ = false;
 
   int device_ = 0, sm_count_ = 0;
-  int64_t n_ = 0, nnz_ = 0, nwords_ = 0, npad_ = 0;
+  int64_t n_ = 0, nnz_ = 0, nwords_ = 0, npad_ = 0;  // global: vertices, entries, bitmap words, pad32(n)
+  int nparts_ = 1, part_rank_ = 0, part_log_ = 0;
+  int64_t n_loc_ = 0, nwl_ = 0, nnz_loc_ = 0;       // this rank: rows, owned words, entries
+  int32_t* new2old_loc_ = nullptr;                  // local row -> original id (== new2old_ if nparts 1)
+  // partitioned state
+  uint32_t* fglob_ = nullptr;                       // replicated frontier bitmap of the current level
+  unsigned long long* resolve_cnt_ = nullptr;       // adjacency entries read by parent resolution
+  int64_t part_L_ = 0;
+  int part_cur_ = 0;
+  bool part_prev_bitmap_ = false;
+  cudaStream_t part_st_ = nullptr;
+  unsigned long long part_in_ = 0, part_edges_ = 0;  // global counts of the current frontier
+  unsigned long long* h_red_ = nullptr;              // pinned: global (discovered, edges)
   int64_t* row_ptr_ = nullptr;   // internal CSR
   int32_t* col_idx_ = nullptr;
   int32_t* new2old_ = nullptr;

@@ -49,6 +49,21 @@ __global__ void k_thresholds(const int64_t* __restrict__ deg, int64_t n, int32_t
   }
 }
 
+// Partitioned layout (nparts > 1): rank g owns the internal ids of bitmap
+// words w with w % nparts == g; its local row l is internal id
+// ((l/32)*nparts + g)*32 + l%32. Local degrees / original ids of the owned
+// rows (rows past n are empty padding).
+__global__ void k_local_rows(const int64_t* __restrict__ deg64, const int32_t* __restrict__ new2old, int64_t n,
+                             int64_t n_loc, int part_log, int rank, int64_t* __restrict__ deg_loc,
+                             int32_t* __restrict__ new2old_loc) {
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n_loc;
+       l += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = ((((l >> 5) << part_log) | rank) << 5) | (l & 31);
+    deg_loc[l] = v < n ? deg64[v] : 0;
+    new2old_loc[l] = v < n ? new2old[v] : 0;
+  }
+}
+
 // warp per internal row: gather the original row, map neighbours to internal ids
 __global__ void k_gather_rows(const int64_t* __restrict__ old_rp, const int32_t* __restrict__ old_ci,
                               const int64_t* __restrict__ new_rp, const int32_t* __restrict__ new2old,
@@ -75,6 +90,7 @@ static unsigned grid_of(int64_t work, int threads = 256) {
 void BfsEngine::build_layout(const Csr& csr) {
   cudaStream_t st = stream_;
   const int64_t n = csr.n;
+  const int64_t nl = n_loc_;  // rows of this rank (== n unpartitioned)
   // 1. degree-descending order
   uint32_t* key = dev_alloc<uint32_t>((size_t)n);
   uint32_t* key_s = dev_alloc<uint32_t>((size_t)n);
@@ -94,40 +110,53 @@ void BfsEngine::build_layout(const Csr& csr) {
   int64_t* deg64 = dev_alloc<int64_t>((size_t)n + 1);
   LBFS_LAUNCH(k_invert, grid_of(n), 256, 0, st, new2old_, n, old2new_, key_s, deg64);
   LBFS_CUDA(cudaMemsetAsync(deg64 + n, 0, sizeof(int64_t), st));
+  dev_free(key_s);
+  // 2b. the rows this rank owns (all rows when unpartitioned)
+  int64_t* deg_loc = deg64;
+  if (nparts_ > 1) {
+    deg_loc = dev_alloc<int64_t>((size_t)nl + 1);
+    new2old_loc_ = dev_alloc<int32_t>((size_t)nl);
+    LBFS_LAUNCH(k_local_rows, grid_of(nl), 256, 0, st, deg64, new2old_, n, nl, part_log_, part_rank_, deg_loc,
+                new2old_loc_);
+    LBFS_CUDA(cudaMemsetAsync(deg_loc + nl, 0, sizeof(int64_t), st));
+  } else {
+    new2old_loc_ = new2old_;
+  }
   int32_t* d_t3 = dev_alloc<int32_t>(kNumThresh);
   LBFS_CUDA(cudaMemsetAsync(d_t3, 0, kNumThresh * sizeof(int32_t), st));
-  LBFS_LAUNCH(k_thresholds, grid_of(n), 256, 0, st, deg64, n, d_t3);
+  LBFS_LAUNCH(k_thresholds, grid_of(nl), 256, 0, st, deg_loc, nl, d_t3);
   int32_t h_t[kNumThresh];
   LBFS_CUDA(cudaMemcpyAsync(h_t, d_t3, sizeof(h_t), cudaMemcpyDeviceToHost, st));
-  row_ptr_ = dev_alloc<int64_t>((size_t)n + 1);
+  row_ptr_ = dev_alloc<int64_t>((size_t)nl + 1);
   tmp_bytes = 0;
-  LBFS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, deg64, row_ptr_, n + 1, st));
+  LBFS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, deg_loc, row_ptr_, nl + 1, st));
   tmp = dev_alloc<uint8_t>(tmp_bytes);
-  LBFS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, deg64, row_ptr_, n + 1, st));
+  LBFS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, deg_loc, row_ptr_, nl + 1, st));
   LBFS_CUDA(cudaStreamSynchronize(st));
   dev_free(tmp);
+  if (deg_loc != deg64) dev_free(deg_loc);
   dev_free(deg64);
-  dev_free(key_s);
   dev_free(d_t3);
   t_cta_ = h_t[0];
   t_warp_ = std::max(h_t[kSmallMax], t_cta_);
   t_nz_ = std::max(h_t[1], t_warp_);
+  std::vector<int64_t> h_rp((size_t)nl + 1);
+  LBFS_CUDA(cudaMemcpyAsync(h_rp.data(), row_ptr_, sizeof(int64_t) * (size_t)(nl + 1), cudaMemcpyDeviceToHost, st));
+  LBFS_CUDA(cudaStreamSynchronize(st));
+  nnz_loc_ = h_rp[(size_t)nl];
   // 3. gather + map rows (16-byte aligned base, padded for int4 over-reads)
-  col_idx_ = dev_alloc<int32_t>((size_t)nnz_ + 8);
-  int32_t* unsorted = dev_alloc<int32_t>((size_t)nnz_ + 8);
-  LBFS_LAUNCH(k_gather_rows, grid_of(n * 32), 256, 0, st, csr.row_ptr, csr.col_idx, row_ptr_, new2old_,
-              old2new_, n, unsorted);
+  col_idx_ = dev_alloc<int32_t>((size_t)nnz_loc_ + 8);
+  int32_t* unsorted = dev_alloc<int32_t>((size_t)nnz_loc_ + 8);
+  LBFS_LAUNCH(k_gather_rows, grid_of(nl * 32), 256, 0, st, csr.row_ptr, csr.col_idx, row_ptr_, new2old_loc_,
+              old2new_, nl, unsorted);
   // 4. sort every row ascending; CUB's segmented sort takes int sizes, so go
   //    in row ranges of < 2^30 entries
-  std::vector<int64_t> h_rp((size_t)n + 1);
-  LBFS_CUDA(cudaMemcpyAsync(h_rp.data(), row_ptr_, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost, st));
-  LBFS_CUDA(cudaStreamSynchronize(st));
   const int64_t kMaxItems = (int64_t)1 << 30;
   int64_t r0 = 0;
-  while (r0 < n) {
+  while (r0 < nl) {
     int64_t r1 = r0 + 1;
     // extend the range while it stays below kMaxItems entries (binary search)
-    int64_t lo = r0 + 1, hi = n;
+    int64_t lo = r0 + 1, hi = nl;
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) / 2;
       if (h_rp[mid] - h_rp[r0] <= kMaxItems) lo = mid; else hi = mid - 1;
@@ -153,7 +182,7 @@ void BfsEngine::build_layout(const Csr& csr) {
   // 5. degree classes of the small region (deg in [1, kSmallMax))
   ClassTable ct{};
   for (int d = 1; d <= kSmallMax + 1; ++d) ct.T[d] = h_t[d];
-  ct.T[0] = (int32_t)n;
+  ct.T[0] = (int32_t)nl;
   for (int d = 1; d <= kSmallMax; ++d) ct.base[d] = h_rp[(size_t)(d <= kSmallMax ? h_t[std::min(d + 1, kSmallMax + 1)] : 0)];
   classes_ = dev_alloc<ClassTable>(1);
   LBFS_CUDA(cudaMemcpyAsync(classes_, &ct, sizeof(ct), cudaMemcpyHostToDevice, st));

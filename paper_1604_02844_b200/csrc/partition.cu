@@ -1,0 +1,235 @@
+// Partitioned top-down BFS: one rank per GPU, 1D word-cyclic
+// partition of the degree-ordered internal ids. Rank g owns the ids of
+// bitmap words w with w % P == g (every rank gets a share of the hubs, whose
+// ids form the bitmap prefix) and stores their rows (neighbours as global
+// internal ids). The visited bitmap and the frontier bitmap are replicated.
+//
+// One level, all on the caller's stream (the collectives between the steps
+// are issued by the caller, e.g. torch.distributed over NCCL):
+//   expand   the owned frontier with the single-GPU kernels in bitmap mode
+//            (K1/K2, bfs.cu); a clear neighbour owned elsewhere is only
+//            marked in the local visited bitmap (no parent)
+//   pack     the marks of each peer's words (visited & ~prev) into that
+//            peer's contiguous send slice                   -> all_to_all
+//   merge    OR of the received slices, minus what is already visited, is
+//            this rank's remote discoveries: set visited, parent = the first
+//            neighbour of v in the replicated frontier F_L (v's row is local
+//            and the graph symmetric, so one exists and lies one level up),
+//            then k_compact over the owned words -> next frontier bins, levels,
+//            the owned words of F_{L+1} and the local counts
+//                                                -> all_gather, all_reduce
+//   sync     F_{L+1} in global word order; visited |= F_{L+1}; prev = visited
+//   done     host reads the summed counts: the layer (input, edges,
+//            discovered) and termination, identical on every rank
+// The level structure is the reference's level-synchronous loop
+// (traversal.py:90, 152, 366); the exchange replaces nothing in the
+// reference (it is single-node CPU) and follows SURVEY §8e.
+#include <algorithm>
+
+#include "bfs_engine.cuh"
+
+namespace lbfs {
+
+// send[h*nwl + j] = marks of peer h's owned word j (global word j*P + h)
+__global__ void k_part_pack(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ prev,
+                            uint32_t* __restrict__ send, int64_t nwl, int part_log, int rank) {
+  const int64_t total = nwl << part_log;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = i / nwl, j = i - h * nwl;
+    const int64_t gw = (j << part_log) | h;
+    send[i] = (h == rank) ? 0u : (visited[gw] & ~prev[gw]);
+  }
+}
+
+// Warp per owned word (lane = bit): remote discoveries of this level and
+// their parents. recv[p*nwl + j] is peer p's marks for owned word j.
+__global__ void k_part_merge(const uint32_t* __restrict__ recv, int64_t nwl, int part_log, int rank,
+                             uint32_t* __restrict__ visited, const uint32_t* __restrict__ fglob,
+                             const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                             const int32_t* __restrict__ new2old, int32_t* __restrict__ pred_int,
+                             unsigned long long* __restrict__ scanned) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long cnt = 0;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nwl; j += nw) {
+    uint32_t inc = 0;
+    for (int p = 0; p < (1 << part_log); ++p)
+      if (p != rank) inc |= __ldg(recv + (int64_t)p * nwl + j);
+    if (!inc) continue;  // warp-uniform
+    const int64_t gw = (j << part_log) | rank;
+    const uint32_t vis = visited[gw];
+    const uint32_t nb = inc & ~vis;
+    __syncwarp();
+    if (lane == 0 && nb) visited[gw] = vis | nb;
+    if ((nb >> lane) & 1u) {
+      const int64_t l = j * 32 + lane;
+      const int64_t e0 = row_ptr[l], e1 = row_ptr[l + 1];
+      int32_t par = kSentinel;
+      for (int64_t e = e0; e < e1; ++e) {
+        const int32_t u = __ldg(col_idx + e);
+        ++cnt;
+        if ((__ldg(fglob + (u >> 5)) >> (u & 31)) & 1u) {
+          par = __ldg(new2old + u);
+          break;
+        }
+      }
+      pred_int[l] = par;  // always found: a marking peer expanded a neighbour in F_L
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+  if (lane == 0 && cnt) atomicAdd(scanned, cnt);
+}
+
+// local counts of the next frontier -> red (cross-rank sum input)
+__global__ void k_part_counts(const Counters* __restrict__ c, unsigned long long* __restrict__ red) {
+  red[0] = c->discovered;
+  red[1] = c->edges;
+}
+
+// fgath[h*nwl + j] = rank h's owned word j of F_{L+1}
+__global__ void k_part_sync(const uint32_t* __restrict__ fgath, uint32_t* __restrict__ fglob,
+                            uint32_t* __restrict__ visited, uint32_t* __restrict__ prev, int64_t nwords, int64_t nwl,
+                            int part_log) {
+  const int64_t mask = (1 << part_log) - 1;
+  for (int64_t gw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gw < nwords;
+       gw += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = fgath[(gw & mask) * nwl + (gw >> part_log)];
+    fglob[gw] = f;
+    const uint32_t v = visited[gw] | f;
+    visited[gw] = v;
+    prev[gw] = v;
+  }
+}
+
+__global__ void k_fill2(int32_t* __restrict__ a, int64_t na, int32_t va, int32_t* __restrict__ b, int64_t nb,
+                        int32_t vb) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < std::max(na, nb);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < na) a[i] = va;
+    if (i < nb) b[i] = vb;
+  }
+}
+
+// owned records -> outputs in original ids (scatter); other entries keep
+// the fill (SENTINEL / -1), so the ranks' outputs combine by min / max
+__global__ void k_part_finalize(const int32_t* __restrict__ new2old_loc, const int32_t* __restrict__ level_int,
+                                const int32_t* __restrict__ pred_int, int64_t n_loc, int64_t n, int part_log,
+                                int rank, int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out) {
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n_loc; l += (int64_t)gridDim.x * blockDim.x) {
+    if (part_global(l, part_log, rank) >= n) continue;
+    const int32_t lv = level_int[l];
+    if (lv < 0) continue;
+    const int32_t o = new2old_loc[l];
+    if (level_out) level_out[o] = lv;
+    if (pred_out) pred_out[o] = pred_int[l];
+  }
+}
+
+static unsigned grid_for(int64_t work, int sm_count) { return clamp_grid((work + 255) / 256, (int64_t)sm_count * 8); }
+
+void BfsEngine::part_start(int64_t root, cudaStream_t st, unsigned long long* red) {
+  if (root < 0 || root >= n_) throw_inval("root out of range");
+  read_env();
+  part_st_ = st;
+  if (!h_red_) LBFS_CUDA(cudaMallocHost(&h_red_, 2 * sizeof(unsigned long long)));
+  LBFS_LAUNCH(k_init, grid_for(std::max(nwords_, n_loc_) / 4, sm_count_), 256, 0, st, (uint4*)visited_,
+              (uint4*)prev_, (nwords_ + 3) / 4, (int4*)level_int_, (n_loc_ + 3) / 4);
+  if (fglob_) LBFS_CUDA(cudaMemsetAsync(fglob_, 0, sizeof(uint32_t) * (size_t)nwords_, st));
+  if (resolve_cnt_) LBFS_CUDA(cudaMemsetAsync(resolve_cnt_, 0, sizeof(unsigned long long), st));
+  LBFS_CUDA(cudaMemsetAsync(cnt_, 0, sizeof(Counters) * kCounterRing, st));
+  LevelArgs a = level_args();
+  a.next_small = q_small_[0];
+  a.next_warp = q_warp_[0];
+  a.next_cta = q_cta_[0];
+  LBFS_LAUNCH(k_seed, 1, 1, 0, st, a, prev_, old2new_, (int32_t)root, &cnt_[0], fglob_, red);
+  LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[0], &cnt_[0], sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  layers_.clear();
+  part_L_ = -1;  // until part_level_done has the summed root counts
+  part_cur_ = 0;
+  part_prev_bitmap_ = false;
+}
+
+void BfsEngine::part_expand(cudaStream_t st) {
+  if (part_L_ < 0) throw_inval("part_expand before the start counts were summed");
+  part_st_ = st;
+  const int64_t L = part_L_;
+  const Counters c = h_cnt_[L % kCounterRing];
+  LBFS_CUDA(cudaMemsetAsync(&cnt_[(L + 1) % kCounterRing], 0, sizeof(Counters), st));
+  LevelArgs a = level_args();
+  // always bitmap mode: the exchange works on bitmaps, and queue-mode
+  // settling would elect winners for vertices this rank does not own
+  expand_level(a, c, true, part_prev_bitmap_, part_cur_, L, st);
+}
+
+void BfsEngine::part_pack(uint32_t* send, cudaStream_t st) {
+  part_st_ = st;
+  LBFS_LAUNCH(k_part_pack, grid_for(nwords_, sm_count_), 256, 0, st, visited_, prev_, send, nwl_, part_log_,
+              part_rank_);
+}
+
+void BfsEngine::part_merge(const uint32_t* recv, uint32_t* fsend, unsigned long long* red, cudaStream_t st) {
+  part_st_ = st;
+  const int64_t L = part_L_;
+  if (nparts_ > 1)
+    LBFS_LAUNCH(k_part_merge, grid_for(nwl_ * 32, sm_count_), 256, 0, st, recv, nwl_, part_log_, part_rank_,
+                visited_, fglob_, row_ptr_, col_idx_, new2old_, pred_int_, resolve_cnt_);
+  compact_level(part_cur_, L, fsend, st);
+  LBFS_LAUNCH(k_part_counts, 1, 1, 0, st, &cnt_[(L + 1) % kCounterRing], red);
+}
+
+void BfsEngine::part_sync(const uint32_t* fgath, cudaStream_t st) {
+  part_st_ = st;
+  // (one partition: visited and prev are already complete after k_compact)
+  if (nparts_ > 1)
+    LBFS_LAUNCH(k_part_sync, grid_for(nwords_, sm_count_), 256, 0, st, fgath, fglob_, visited_, prev_, nwords_, nwl_,
+                part_log_);
+}
+
+void BfsEngine::part_level_done(const unsigned long long* red_global, lbfs_layer* layer, int* done) {
+  cudaStream_t st = part_st_;
+  const int64_t L = part_L_;
+  const int slot = (int)((L + 1) % kCounterRing);
+  if (L >= 0) LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[slot], &cnt_[slot], sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  LBFS_CUDA(cudaMemcpyAsync(h_red_, red_global, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  LBFS_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long disc = h_red_[0], edges = h_red_[1];
+  if (L < 0) {  // start: the summed root counts (1, deg(root)) become frontier 0
+    part_in_ = disc;
+    part_edges_ = edges;
+    part_L_ = 0;
+    if (layer) *layer = lbfs_layer{0, 0, 0};
+    if (done) *done = disc == 0;
+    return;
+  }
+  const lbfs_layer ly{(int64_t)part_in_, (int64_t)part_edges_, (int64_t)disc};
+  layers_.push_back(ly);
+  if (trace_)
+    fprintf(stderr, "[lbfs] rank %d L%-3lld in=%-9llu edges=%-10llu local bins %llu/%llu/%llu/%llu disc=%llu\n",
+            part_rank_, (long long)L, part_in_, part_edges_, h_cnt_[slot].bin[0], h_cnt_[slot].bin[1],
+            h_cnt_[slot].bin[2], h_cnt_[slot].bin[3], disc);
+  if (layer) *layer = ly;
+  if (done) *done = disc == 0;
+  part_in_ = disc;
+  part_edges_ = edges;
+  part_L_ = L + 1;
+  part_cur_ ^= 1;
+  part_prev_bitmap_ = true;
+}
+
+void BfsEngine::part_finish(int32_t* d_pred, int32_t* d_level, cudaStream_t st) {
+  part_st_ = st;
+  LBFS_LAUNCH(k_fill2, grid_for(npad_, sm_count_), 256, 0, st, d_pred, d_pred ? npad_ : 0, kSentinel, d_level,
+              d_level ? n_ : 0, -1);
+  LBFS_LAUNCH(k_part_finalize, grid_for(n_loc_, sm_count_), 256, 0, st, new2old_loc_, level_int_, pred_int_, n_loc_,
+              n_, part_log_, part_rank_, d_level, d_pred);
+}
+
+unsigned long long BfsEngine::resolve_scanned() const {
+  if (!resolve_cnt_) return 0;
+  unsigned long long v = 0;
+  LBFS_CUDA(cudaMemcpy(&v, resolve_cnt_, sizeof(v), cudaMemcpyDeviceToHost));
+  return v;
+}
+
+}  // namespace lbfs
