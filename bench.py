@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--cpu-roots", type=int, default=2, help="roots per step of the --impl reference arm")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU-baseline sampling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="use the partitioned (multi-GPU) driver even at N=1 (one NCCL rank)")
     return ap.parse_args()
 
 
@@ -192,6 +194,128 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_partitioned(args, rank, world, local):
+    """N > 1: the graph 1D-partitioned over the N GPUs (one rank each), one
+    BFS = the level loop of distributed.bfs_partitioned with three NCCL
+    collectives per level. Every rank builds the same graph on
+    its GPU (deterministic device generator) and keeps only its partition's
+    rows. Per-BFS time = max over ranks of the CUDA-event time on each
+    rank's stream; value = harmonic mean over roots of E / t (whole job)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1604_02844_b200 import RmatParams, _lib, build_rmat_graph, pick_roots
+    from paper_1604_02844_b200.distributed import PartitionedGraph, TorchExchange, bfs_partitioned
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t0 = time.perf_counter()
+    g = build_rmat_graph(RmatParams(scale=args.scale, seed=1))
+    n, nnz = g.num_vertices, g.num_edges
+    roots = pick_roots(g, args.roots, 1, filter_unconnected=True).tolist()
+    part = PartitionedGraph(g, rank, world, device=local)
+    host_csr = (g.colstarts, g.rows) if rank == 0 else None  # for the tree check
+    del g  # only this rank's rows stay on the GPU
+    build_s = time.perf_counter() - t0
+    ex = TorchExchange()
+    bufs = [part.new_buffers()]
+    outs = [part.new_outputs()]
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def one(r, gather=False):
+        ev0.record()
+        res = bfs_partitioned([part], r, ex, bufs=bufs, outputs=outs, gather=gather)
+        ev1.record()
+        ev1.synchronize()
+        return res, ev0.elapsed_time(ev1)
+
+    for _ in range(args.warmup):
+        for r in roots:
+            one(r)
+    launches0 = _lib.kernel_launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    times, edges, nlevels, reached = [], [], [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            for r in roots:
+                res, ms = one(r)
+                times.append(ms)
+                edges.append(res.traversed_edge_count)
+                nlevels.append(len(res.layers))
+                reached.append(sum(l.input for l in res.layers))
+        dist.barrier()
+        torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    launches = _lib.kernel_launch_count() - launches0
+    t = torch.tensor(times, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tmax = t.cpu().numpy()
+    teps = [e / (ms * 1e-3) / 1e9 if e else 0.0 for e, ms in zip(edges, tmax)]
+    value = hm(teps)
+    ms_step = float(tmax.sum()) / args.steps
+    # e2e: public driver with the gathered outputs, rank 0 reads pred+level to host
+    pred_h = torch.empty(outs[0][0].numel(), dtype=torch.int32, pin_memory=True)
+    lvl_h = torch.empty(outs[0][1].numel(), dtype=torch.int32, pin_memory=True)
+    e2e_vals = []
+    for r in roots[:args.e2e_roots]:
+        dist.barrier()
+        a = time.perf_counter()
+        res = bfs_partitioned([part], r, ex, bufs=bufs, outputs=outs, gather=True)
+        if rank == 0:
+            pred_h.copy_(outs[0][0])
+            lvl_h.copy_(outs[0][1])
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - a], dtype=torch.float64, device="cuda")
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e_vals.append(res.traversed_edge_count / float(dt.item()) / 1e9)
+    e2e = hm(e2e_vals)
+    # correctness of the timed configuration (outside the timed region): the
+    # gathered tree of the last e2e root through the package validator
+    ok = None
+    if rank == 0 and e2e_vals:
+        from paper_1604_02844_b200 import CsrGraph, PredecessorArray
+        from paper_1604_02844_b200.validate import validate_tree
+
+        gh = CsrGraph(n, host_csr[1], host_csr[0])
+        ok = validate_tree(gh, roots[len(e2e_vals) - 1], PredecessorArray(n, _storage=pred_h.numpy())).passed
+    hbm_gbs, peak_kind = peaks()
+    E = float(np.mean(edges))
+    alg = 8 * E + 40 * float(np.mean(reached)) + 8 * n + n // 8  # SURVEY §8(d) B_alg
+    X = float(np.mean(nlevels))
+    words = (n + 31) // 32
+    nvl_bytes = X * 2 * (world - 1) * ((words + world - 1) // world) * 4
+    t_meas = float(np.mean(tmax)) * 1e-3
+    t_roof = max(alg / (world * hbm_gbs * 1e9), nvl_bytes / 9e11)
+    line = {
+        "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic: R-MAT (reference generator, bit-exact) + seeded permutation",
+        "config": {"workload": f"rmat-s{args.scale}-ef16-{args.roots}roots", "scale": args.scale,
+                   "edgefactor": 16, "roots": args.roots, "n": n, "nnz": nnz,
+                   "parallelism": f"1d-partition-{world}gpu-nccl",
+                   "l2": "inputs larger than L2; no flush", "graph_build_s": round(build_s, 2),
+                   "validated": ok},
+        "roofline": {"bound": "hbm", "achieved": alg / world / t_meas / 1e9, "peak": hbm_gbs, "unit": "GB/s",
+                     "frac": t_roof / t_meas, "peak_kind": peak_kind, "traffic": None,
+                     "kernel": "whole BFS per GPU (SURVEY §8e t_roof(P) formula)",
+                     "t_roof_ms": t_roof * 1e3, "t_measured_ms": t_meas * 1e3,
+                     "nvlink_bytes_per_gpu": nvl_bytes, "levels": X},
+        "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 8 * args.roots,
+                "d2h_bytes_per_step": (outs[0][0].numel() + n) * 4 * args.roots,
+                "api": "distributed.bfs_partitioned(gather=True) + rank-0 D2H", "roots_timed": len(e2e_vals)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "wall_s_timed": wall,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    part.close()
+    dist.destroy_process_group()
+
+
 def run_ours(args, rank, world, local):
     import torch
 
@@ -323,6 +447,8 @@ def main():
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif world > 1 or args.partitioned:
+        run_partitioned(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)
 
