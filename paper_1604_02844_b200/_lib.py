@@ -95,7 +95,7 @@ def load(path: Path | str | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path else Path(os.environ.get("LBFS_LIB", LIB_PATH))
+        p = Path(path) if path else Path(os.environ.get("LBFS_LIB") or LIB_PATH)
         if not p.exists():
             raise RuntimeError(f"{p} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`"
                                " (there is no CPU fallback)")

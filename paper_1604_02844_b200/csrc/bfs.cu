@@ -268,25 +268,46 @@ __device__ __forceinline__ void settle_bitmap(const LevelArgs& a, const Hot& h, 
 // unvisited may record its parent, since every such parent is one level up
 // (the benign race of bfs_parallel_naive, traversal.py:145-147). Queue mode
 // elects one winner per vertex with atomicOr.
-template <int M, int K, typename ParFn>
-__device__ __forceinline__ void probe_batch(const LevelArgs& a, const Hot& h, const int32_t (&nb)[K],
-                                            uint32_t okmask, ParFn par, int lane, Acc& acc) {
+// Where a batch's visited words are known to lie (warp-uniform): sorted
+// interior chunks of a row are classified once by their first/last element.
+enum Where : int { kMixed = 0, kAllHot = 1, kAllCold = 2 };
+
+// Candidate mask of a batch: bit k set when nb[k] (valid per okmask) reads
+// as unvisited.
+template <int M, int K, int W = kMixed>
+__device__ __forceinline__ uint32_t probe_mask(const LevelArgs& a, const Hot& h, const int32_t (&nb)[K],
+                                               uint32_t okmask) {
+  if constexpr (M == kQueueDirect) return okmask;
   uint32_t cmask = 0;
-  if constexpr (M == kQueueDirect) {
-    cmask = okmask;
-  } else {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t w = probe_word(h, a.visited, nb[k] >> 5);
-      cmask |= ((~w >> (nb[k] & 31)) & 1u) << k;
-    }
-    cmask &= okmask;
+  for (int k = 0; k < K; ++k) {
+    uint32_t w;
+    if constexpr (W == kAllHot)
+      w = h.s[nb[k] >> 5];
+    else if constexpr (W == kAllCold)
+      w = __ldca(a.visited + (nb[k] >> 5));
+    else
+      w = probe_word(h, a.visited, nb[k] >> 5);
+    cmask |= ((~w >> (nb[k] & 31)) & 1u) << k;
   }
+  return cmask & okmask;
+}
+
+// Settle the candidates of a batch (queue modes: warp-collective).
+template <int M, int K, typename ParFn>
+__device__ __forceinline__ void settle(const LevelArgs& a, const Hot& h, const int32_t (&nb)[K], uint32_t cmask,
+                                       ParFn par, int lane, Acc& acc) {
   if constexpr (M == kBitmapOut) {
     if (cmask) settle_bitmap<K>(a, h, nb, cmask, par);
   } else {
     settle_queue<K>(a, nb, cmask, par, lane, acc);
   }
+}
+
+template <int M, int K, typename ParFn, int W = kMixed>
+__device__ __forceinline__ void probe_batch(const LevelArgs& a, const Hot& h, const int32_t (&nb)[K],
+                                            uint32_t okmask, ParFn par, int lane, Acc& acc) {
+  settle<M, K>(a, h, nb, probe_mask<M, K, W>(a, h, nb, okmask), par, lane, acc);
 }
 
 template <int M>
@@ -482,6 +503,9 @@ __device__ __forceinline__ void stream_slices(const LevelArgs& a, const Hot& h, 
   if (gwarp >= n) return;
   int64_t it = gwarp;
   CtaItem cur = ld_item(items + it);
+  // the descriptor after cur is loaded one row ahead, so a row switch never
+  // waits on it before issuing the row's first col_idx load
+  CtaItem nxt = it + nwarps < n ? ld_item(items + it + nwarps) : CtaItem{0, 0, 0};
   int64_t pos = cur.start & ~int64_t(3);
   int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
   auto load = [&](int64_t p0, int64_t e0) {
@@ -497,7 +521,8 @@ __device__ __forceinline__ void stream_slices(const LevelArgs& a, const Hot& h, 
     if (pos >= end) {
       it += nwarps;
       if (it < n) {
-        cur = ld_item(items + it);
+        cur = nxt;
+        if (it + nwarps < n) nxt = ld_item(items + it + nwarps);
         pos = cur.start & ~int64_t(3);
         end = (cur.start + cur.len + 3) & ~int64_t(3);
       } else {
@@ -630,24 +655,42 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
       mo = __shfl_sync(kFull, mo, 0);
       more = (more & ~(1u << b)) | (mo << b);
       int32_t nb[4 * kV];
-      uint32_t okm = 0;
 #pragma unroll
       for (int i = 0; i < kV; ++i) {
         nb[4 * i + 0] = xs[i].x;
         nb[4 * i + 1] = xs[i].y;
         nb[4 * i + 2] = xs[i].z;
         nb[4 * i + 3] = xs[i].w;
-        const int lo = (int)(m.lo - m.base) - (lane + 32 * i) * 4, hi = (int)(m.hi - m.base) - (lane + 32 * i) * 4;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const bool ok = q >= lo && q < hi;
-          okm |= (uint32_t)ok << (4 * i + q);
-          nb[4 * i + q] = ok ? nb[4 * i + q] : 0;  // staged slots outside the slice hold stale data
-        }
       }
       const int32_t pu = m.u;
-      if (a.dbg) atomicAdd(a.dbg + 2, (unsigned long long)__popc(okm));  // LBFS_COUNT: hub elements
-      probe_batch<M, 4 * kV>(a, h, nb, okm, [&](int) { return pu; }, lane, acc);
+      auto par = [&](int) { return pu; };
+      if (m.lo <= m.base && m.hi >= m.base + kWarpChunk) {
+        // interior chunk: all staged elements valid, ascending (a sorted row
+        // segment) from lane 0's first to lane 31's last element
+        constexpr uint32_t kAll = (1u << (4 * kV)) - 1u;
+        const int32_t first = __shfl_sync(kFull, nb[0], 0), last = __shfl_sync(kFull, nb[4 * kV - 1], 31);
+        if (a.dbg) atomicAdd(a.dbg + 2, (unsigned long long)(4 * kV));  // LBFS_COUNT: hub elements
+        if ((last >> 5) < h.words)
+          probe_batch<M, 4 * kV, decltype(par), kAllHot>(a, h, nb, kAll, par, lane, acc);
+        else if ((first >> 5) >= h.words)
+          probe_batch<M, 4 * kV, decltype(par), kAllCold>(a, h, nb, kAll, par, lane, acc);
+        else
+          probe_batch<M, 4 * kV>(a, h, nb, kAll, par, lane, acc);
+      } else {
+        uint32_t okm = 0;
+#pragma unroll
+        for (int i = 0; i < kV; ++i) {
+          const int lo = (int)(m.lo - m.base) - (lane + 32 * i) * 4, hi = (int)(m.hi - m.base) - (lane + 32 * i) * 4;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool ok = q >= lo && q < hi;
+            okm |= (uint32_t)ok << (4 * i + q);
+            nb[4 * i + q] = ok ? nb[4 * i + q] : 0;  // staged slots outside the slice hold stale data
+          }
+        }
+        if (a.dbg) atomicAdd(a.dbg + 2, (unsigned long long)__popc(okm));  // LBFS_COUNT: hub elements
+        probe_batch<M, 4 * kV>(a, h, nb, okm, par, lane, acc);
+      }
       if (refresh_every && wib == 0 && ++chunks_done % refresh_every == 0) {
         // re-learn the hot prefix from L2 (others' discoveries): async bulk
         // copy over the shared copy; a racing local OR may be lost, which
@@ -951,8 +994,9 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t w0 = (int64_t)blockIdx.x * kCompactWords;
   const int64_t v0 = w0 * 32;
+  __shared__ int32_t s_hitems[kCompactWords];  // hub slices per word, then their word offsets
   uint32_t nb = 0, mhub = 0, mlist = 0, mwarp = 0;
-  int hub_items = 0;
+  if (t < kCompactWords) s_hitems[t] = 0;
   if (t < kCompactWords && w0 + t < c.nwords) {
     const int64_t gw = ((w0 + t) << c.part_log) | c.part_rank;  // global word of owned word w0+t
     const uint32_t w = c.visited[gw], p = c.prev[gw];
@@ -965,78 +1009,88 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
       mhub = nb & range_mask(vw, 0, c.t_cta);
       mwarp = nb & range_mask(vw, c.t_cta, c.t_warp);
       mlist = nb & range_mask(vw, c.t_warp, c.t_nz);
-      for (uint32_t m = mhub; m; m &= m - 1) {
-        const int64_t v = vw + __ffs(m) - 1;
-        hub_items += (int)((c.row_ptr[v + 1] - c.row_ptr[v] + kChunk - 1) / kChunk);
-      }
     }
   }
+  const int any_hub = __syncthreads_or(mhub != 0);  // (also orders s_hitems' zeroing)
   if (!__syncthreads_or(nb != 0)) return;
   if (t < kCompactWords) {
     s_new[t] = nb;
     s_lmask[t] = mlist;
     s_wmask[t] = mwarp;
   }
-  int n_list = 0, n_hub_items = 0, n_wsl = 0;
+  int n_list = 0, n_wsl = 0;
   const int lpre = scan128(__popc(mlist), s_w, &n_list);
   if (t < kCompactWords) s_lpre[t] = lpre;
   const int wpre = scan128(__popc(mwarp), s_w, &n_wsl);
   if (t < kCompactWords) s_wpre[t] = wpre;
-  const int ipre = scan128(hub_items, s_w, &n_hub_items);
   if (t == 0) {
     s_base[0] = n_list ? atomicAdd(&c.next_cnt->bin[kBinSmall], (unsigned long long)n_list) : 0;
-    s_base[1] = n_hub_items ? atomicAdd(&c.next_cnt->bin[kBinCta], (unsigned long long)n_hub_items) : 0;
     s_base[3] = n_wsl ? atomicAdd(&c.next_cnt->bin[kBinWSlice], (unsigned long long)n_wsl) : 0;
   }
   __syncthreads();
-  if (mhub) {  // hub slices, written by the owner thread of each word
-    unsigned long long p = s_base[1] + ipre;
-    for (uint32_t m = mhub; m; m &= m - 1) {
-      const int64_t v = (w0 + t) * 32 + __ffs(m) - 1;
-      const int64_t st = c.row_ptr[v], deg = c.row_ptr[v + 1] - st;
-      for (int64_t k = 0; k * kChunk < deg; ++k)
-        c.next_cta[p++] = CtaItem{st + k * kChunk, (int32_t)std::min<int64_t>(kChunk, deg - k * kChunk),
-                                  c.new2old[v]};
-    }
-  }
   // pass 2: thread t owns vertices v0 + t + 256 j (bit t&31 of word t/32 + 8 j);
   // four vertices' loads are issued before any of their stores
   unsigned long long edges = 0;
   const int b = t & 31;
 #pragma unroll
   for (int j0 = 0; j0 < kCompactSteps; j0 += 4) {
-    int32_t vo[4];
     int64_t st[4], en[4];
+    int32_t vo[4];
     bool nw[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int wl = (t >> 5) + (j0 + q) * (kCompactThreads / 32);
       const int64_t v = v0 + t + (j0 + q) * kCompactThreads;
       nw[q] = (s_new[wl] >> b) & 1u;
-      vo[q] = nw[q] && v < c.t_warp ? __ldg(c.new2old + v) : 0;  // parent id for hub/warp slices
+      vo[q] = nw[q] && v >= c.t_cta && v < c.t_warp ? __ldg(c.new2old + v) : 0;  // warp-slice parent
       st[q] = nw[q] ? __ldg(c.row_ptr + v) : 0;
       en[q] = nw[q] ? __ldg(c.row_ptr + v + 1) : 0;
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      if (!nw[q]) continue;
       const int wl = (t >> 5) + (j0 + q) * (kCompactThreads / 32);
       const int64_t v = v0 + t + (j0 + q) * kCompactThreads;
+      if (!nw[q]) continue;
       c.level_int[v] = c.next_level;  // coalesced; outputs are written by k_finalize
       const int32_t deg = (int32_t)(en[q] - st[q]);
       edges += (unsigned long long)deg;
       const uint32_t wm = s_wmask[wl];
-      if ((wm >> b) & 1u)
-        c.next_wslice[s_base[3] + s_wpre[wl] + __popc(wm & ((1u << b) - 1u))] = CtaItem{st[q], deg, vo[q]};
+      if ((wm >> b) & 1u)  // warp-bin row: one slice, parent = the row's vertex
+        c.next_wslice[s_base[3] + s_wpre[wl] + __popc(wm & ((1u << b) - 1u))] =
+            CtaItem{st[q], deg, vo[q]};
       const uint32_t lm = s_lmask[wl];
       if ((lm >> b) & 1u) {
         const int r = s_lpre[wl] + __popc(lm & ((1u << b) - 1u));
         c.next_list[s_base[0] + r] = (int32_t)v;
         s_deg[r] = deg;
       }
+      if (v < c.t_cta) atomicAdd(&s_hitems[wl], (deg + kChunk - 1) / kChunk);
     }
   }
   __syncthreads();
+  if (any_hub) {
+    // hub slices: word offsets from one scan, slots inside a word claimed
+    // with shared atomics (slice order is free); one vertex per thread per
+    // step, so the row_ptr reads stay parallel (they hit L1: read above)
+    int n_hub_items = 0;
+    const int hi = t < kCompactWords ? s_hitems[t] : 0;
+    const int ipre = scan128(hi, s_w, &n_hub_items);
+    __syncthreads();
+    if (t < kCompactWords) s_hitems[t] = ipre;
+    if (t == 0) s_base[1] = atomicAdd(&c.next_cnt->bin[kBinCta], (unsigned long long)n_hub_items);
+    __syncthreads();
+    for (int j = 0; j < kCompactSteps; ++j) {
+      const int wl = (t >> 5) + j * (kCompactThreads / 32);
+      const int64_t v = v0 + t + j * kCompactThreads;
+      if (v >= c.t_cta || !((s_new[wl] >> b) & 1u)) continue;
+      const int64_t st = __ldg(c.row_ptr + v), deg = __ldg(c.row_ptr + v + 1) - st;
+      const int items = (int)((deg + kChunk - 1) / kChunk);
+      const int32_t vo = __ldg(c.new2old + v);
+      unsigned long long p = s_base[1] + atomicAdd(&s_hitems[wl], items);
+      for (int64_t k = 0; k < items; ++k)
+        c.next_cta[p++] = CtaItem{st + k * kChunk, (int32_t)std::min<int64_t>(kChunk, deg - k * kChunk), vo};
+    }
+  }
   // groups of 32 consecutive list entries -> kItemElems-element items
   const int ngroups = (n_list + 31) / 32;
   for (int g = warp; g < ngroups; g += kCompactThreads / 32) {
