@@ -37,6 +37,7 @@
 //   K6 Counters          LayerStats(input, edges, discovered) per level
 //                        (traversal.py:66-70, 100, 159, 383)
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1222,6 +1223,42 @@ __global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int3
   }
 }
 
+// End of a host-driven level: the next frontier's counters go to the host
+// mailbox (mapped pinned memory) behind a sequence number, and the ring slot
+// the following level writes is cleared.
+__global__ void k_publish(Counters* ring, int slot, int zero_slot, Counters* mail, unsigned long long* seq,
+                          unsigned long long value) {
+  const int t = threadIdx.x;
+  constexpr int kWords = (int)(sizeof(Counters) / 8);
+  if (t < kWords) {
+    reinterpret_cast<volatile unsigned long long*>(mail)[t] = reinterpret_cast<unsigned long long*>(&ring[slot])[t];
+    reinterpret_cast<unsigned long long*>(&ring[zero_slot])[t] = 0ull;
+  }
+  __syncwarp();
+  if (t == 0) {
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(seq) = value;
+  }
+}
+
+void BfsEngine::publish_and_wait(int slot, int zero_slot, cudaStream_t st) {
+  const unsigned long long want = ++seq_;
+  LBFS_LAUNCH(k_publish, 1, 32, 0, st, cnt_, slot, zero_slot, h_mail_, h_seq_, want);
+  // spin: a blocking stream sync costs tens of microseconds of wake-up per level
+  volatile unsigned long long* p = h_seq_;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spins = 1; *p < want; ++spins) {
+    if ((spins & 0x3FFF) == 0) {
+      const cudaError_t e = cudaStreamQuery(st);
+      if (e != cudaSuccess && e != cudaErrorNotReady) throw_cuda(e, "level kernels", __FILE__, __LINE__);
+      if (e == cudaSuccess && *p < want) throw Failure(LBFS_ECUDA, "internal: level mailbox not written");
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+        throw Failure(LBFS_ECUDA, "level did not complete within 120 s");
+    }
+  }
+  h_cnt_[slot] = *const_cast<const Counters*>(h_mail_);
+}
+
 // ---------------------------------------------------------------- engine
 BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   if (nparts < 1 || (nparts & (nparts - 1)) != 0 || nparts > 64) throw_inval("nparts must be a power of two <= 64");
@@ -1266,6 +1303,13 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   }
   cnt_ = dev_alloc<Counters>(kCounterRing);
   LBFS_CUDA(cudaMallocHost(&h_cnt_, sizeof(Counters) * kCounterRing));
+  {
+    void* m = nullptr;
+    LBFS_CUDA(cudaHostAlloc(&m, sizeof(Counters) + 64, cudaHostAllocMapped));
+    memset(m, 0, sizeof(Counters) + 64);
+    h_mail_ = reinterpret_cast<Counters*>(m);
+    h_seq_ = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(m) + sizeof(Counters));
+  }
   for (auto& e : ev_) LBFS_CUDA(cudaEventCreate(&e));
   for (auto& e : ev_split_) LBFS_CUDA(cudaEventCreate(&e));
   int occ = 0;
@@ -1323,6 +1367,7 @@ BfsEngine::~BfsEngine() {
   }
   dev_free(cnt_);
   if (h_cnt_) cudaFreeHost(h_cnt_);
+  if (h_mail_) cudaFreeHost(h_mail_);
   dev_free(d_layers_);
   dev_free(loop_);
   if (h_layers_) cudaFreeHost(h_layers_);
@@ -1504,6 +1549,8 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   a.next_small = q_small_[cur];
   a.next_warp = q_warp_[cur];
   a.next_cta = q_cta_[cur];
+  // ring invariant: at the start of level L, slot (L+1)%3 is zero
+  LBFS_CUDA(cudaMemsetAsync(cnt_, 0, sizeof(Counters) * kCounterRing, st));
   LBFS_LAUNCH(k_seed, 1, 1, 0, st, a, prev_, old2new_, (int32_t)root, &cnt_[0], nullptr, nullptr);
   LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[0], &cnt_[0], sizeof(Counters), cudaMemcpyDeviceToHost, st));
   LBFS_CUDA(cudaEventRecord(ev_[1], st));
@@ -1518,7 +1565,6 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   for (;;) {
     const Counters c = h_cnt_[L % kCounterRing];
     const int slot = (int)((L + 1) % kCounterRing);
-    LBFS_CUDA(cudaMemsetAsync(&cnt_[slot], 0, sizeof(Counters), st));
     if (dev_loop && !prev_bitmap && c.edges < bitmap_min_edges) {
       // a run of queue-mode levels on the device (k_levels), one launch
       LoopArgs p{};
@@ -1580,8 +1626,8 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     LBFS_CUDA(cudaEventRecord(ev_[3], st));
     if (bitmap) compact_level(cur, L, nullptr, st);
     LBFS_CUDA(cudaEventRecord(ev_[5], st));
-    LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[slot], &cnt_[slot], sizeof(Counters), cudaMemcpyDeviceToHost, st));
-    LBFS_CUDA(cudaStreamSynchronize(st));
+    publish_and_wait(slot, (int)((L + 2) % kCounterRing), st);
+    LBFS_CUDA(cudaEventSynchronize(ev_[5]));
     float ms = 0.f, cms = 0.f;
     LBFS_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
     LBFS_CUDA(cudaEventElapsedTime(&cms, ev_[3], ev_[5]));

@@ -268,6 +268,12 @@ class BfsEngine {
   int64_t cap_cta_ = 0, cap_items_ = 0;
   Counters* cnt_ = nullptr;
   Counters* h_cnt_ = nullptr;
+  // per-level mailbox in mapped pinned memory: k_publish copies a level's
+  // counters here and bumps the sequence word; the host spins on it
+  Counters* h_mail_ = nullptr;
+  unsigned long long* h_seq_ = nullptr;
+  unsigned long long seq_ = 0;
+  void publish_and_wait(int slot, int zero_slot, cudaStream_t st);
   int32_t* own_pred_ = nullptr;
   int32_t* own_level_ = nullptr;
   cudaStream_t stream_ = nullptr;
