@@ -557,47 +557,79 @@ struct ChunkMeta {
   int32_t u;       // internal id of the hub
 };
 
-// One persistent CTA per SM (kExpandWarps warps) holding a shared-memory copy
-// of the hot visited prefix (hot_words words, one bulk copy at kernel start,
-// updated by the CTA's own discoveries). `phases` selects bins (debug split).
-template <int M, int kPhases>
-__global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Frontier f, int32_t hot_words) {
-  constexpr int phases = kPhases;
-  extern __shared__ __align__(128) uint8_t s_dyn[];
-  __shared__ __align__(8) uint64_t s_bar[kExpandWarps][kWarpStages];
-  __shared__ __align__(8) uint64_t s_hot_bar;
-  __shared__ ChunkMeta s_meta[kExpandWarps][kWarpStages];
-  __shared__ WarpScratch s_ws[kExpandWarps];
-  __shared__ int32_t s_T[kSmallMax + 2];
-  __shared__ int64_t s_B[kSmallMax + 1];
+// Static shared memory of an expansion CTA (kExpandWarps warps); the
+// dynamic part holds the per-warp bulk-copy rings (kRingBytes) and the hot
+// snapshot of the visited prefix behind them.
+struct ExpandSmem {
+  uint64_t bar[kExpandWarps][kWarpStages];  // per-warp ring slots (mbarriers)
+  uint64_t hot_bar;                         // hot snapshot copies
+  ChunkMeta meta[kExpandWarps][kWarpStages];
+  WarpScratch ws[kExpandWarps];
+  int32_t T[kSmallMax + 2];
+  int64_t B[kSmallMax + 1];
+  uint32_t hot_issued;  // snapshot copies issued so far (thread 0 only issues)
+};
+
+__device__ __forceinline__ void expand_init(ExpandSmem& s, const LevelArgs& a) {
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-  const Hot h{reinterpret_cast<uint32_t*>(s_dyn + kRingBytes), smem_u32(s_dyn + kRingBytes), hot_words};
+  if (lane == 0)
+    for (int b = 0; b < kWarpStages; ++b) mbar_init(&s.bar[wib][b], 1);
+  if (tid == 0) {
+    mbar_init(&s.hot_bar, 1);
+    s.hot_issued = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < kSmallMax + 2) s.T[tid] = a.classes->T[tid];
+  if (tid < kSmallMax + 1) s.B[tid] = a.classes->base[tid];
+  __syncthreads();
+}
+
+// (thread 0) wait until the last snapshot copy has landed
+__device__ __forceinline__ void hot_wait_last(ExpandSmem& s) {
+  if (s.hot_issued) mbar_wait(&s.hot_bar, (s.hot_issued - 1) & 1u);
+}
+// (thread 0) issue a snapshot copy of the visited prefix
+__device__ __forceinline__ void hot_issue(ExpandSmem& s, const Hot& h, const uint32_t* visited) {
+  const uint32_t bytes = (uint32_t)h.words * 4u;  // multiple of 16 by construction
+  mbar_expect_tx(&s.hot_bar, bytes);
+  bulk_g2s(h.s, visited, bytes, &s.hot_bar);
+  ++s.hot_issued;
+}
+// (all threads) load the snapshot and wait for it
+__device__ __forceinline__ void hot_load(ExpandSmem& s, const Hot& h, const uint32_t* visited) {
+  if (h.words <= 0) return;
+  __syncthreads();  // nobody still reads the old snapshot
+  if (threadIdx.x == 0) {
+    hot_wait_last(s);
+    hot_issue(s, h, visited);
+  }
+  __syncthreads();
+  mbar_wait(&s.hot_bar, (s.hot_issued - 1) & 1u);
+}
+// (all threads) no snapshot copy in flight (before reusing or leaving the smem)
+__device__ __forceinline__ void hot_drain(ExpandSmem& s) {
+  if (threadIdx.x == 0) hot_wait_last(s);
+  __syncthreads();
+}
+
+// The expansion of one level's frontier by one persistent CTA per SM,
+// bins selected by kPhases. par_bits carries the per-warp ring parities
+// across calls (the mbarriers live as long as the CTA).
+template <int M, int kPhases>
+__device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier& f, ExpandSmem& s, uint8_t* s_dyn,
+                                              const Hot& h, uint32_t& par_bits, Acc& acc) {
+  constexpr int phases = kPhases;
+  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   // warp ids interleave the SMs so that the first work units of every phase
   // land on different SMs
   const int64_t gwarp = (int64_t)wib * gridDim.x + blockIdx.x;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  WarpScratch& ws = s_ws[wib];
-  Acc acc;
-
-  if (lane == 0)
-    for (int b = 0; b < kWarpStages; ++b) mbar_init(&s_bar[wib][b], 1);
-  if (tid == 0) {
-    mbar_init(&s_hot_bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (tid < kSmallMax + 2) s_T[tid] = a.classes->T[tid];
-  if (tid < kSmallMax + 1) s_B[tid] = a.classes->base[tid];
-  __syncthreads();
-  if (hot_words > 0) {
-    if (tid == 0) {
-      const uint32_t bytes = (uint32_t)hot_words * 4u;  // multiple of 16 by construction
-      mbar_expect_tx(&s_hot_bar, bytes);
-      bulk_g2s(h.s, a.visited, bytes, &s_hot_bar);
-    }
-    mbar_wait(&s_hot_bar, 0);
-  }
-  uint32_t hot_phase = 0;  // last phase of s_hot_bar issued (warp 0 lane 0)
-  const int refresh_every = hot_words > 0 ? a.refresh_chunks : 0;
+  WarpScratch& ws = s.ws[wib];
+  const int32_t* s_T = s.T;
+  const int64_t* s_B = s.B;
+  const int refresh_every = h.words > 0 ? a.refresh_chunks : 0;
+  auto& s_bar = s.bar;
+  auto& s_meta = s.meta;
 
   // ---- phase 1: CTA bin, warp-private bulk-copy streams -------------------
   // a kWarpStages-deep ring of kWarpChunk-element buffers per warp: lane 0
@@ -606,9 +638,9 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
     int32_t* wbuf = reinterpret_cast<int32_t*>(s_dyn) + (size_t)wib * kWarpStages * kWarpChunk;
     // lane-0 stream state: current slice [pos, end) (16-B aligned), next slice prefetched
     int64_t it = gwarp;
-    CtaItem cur = f.cta[it];
+    CtaItem cur = ld_item(f.cta + it);
     CtaItem pre{0, 0, 0};
-    if (it + nwarps < f.n_cta) pre = f.cta[it + nwarps];
+    if (it + nwarps < f.n_cta) pre = ld_item(f.cta + it + nwarps);
     int64_t pos = cur.start & ~int64_t(3);
     int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
     auto issue = [&](int b) -> uint32_t {  // lane 0: next chunk into buffer b; 0 when exhausted
@@ -616,7 +648,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
         it += nwarps;
         if (it >= f.n_cta) return 0u;
         cur = pre;
-        if (it + nwarps < f.n_cta) pre = f.cta[it + nwarps];
+        if (it + nwarps < f.n_cta) pre = ld_item(f.cta + it + nwarps);
         pos = cur.start & ~int64_t(3);
         end = (cur.start + cur.len + 3) & ~int64_t(3);
       }
@@ -631,7 +663,6 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
     if (lane == 0)
       for (int b = 0; b < kWarpStages; ++b) more |= issue(b) << b;
     more = __shfl_sync(kFull, more, 0);
-    uint32_t par_bits = 0;
     int chunks_done = 0;
     for (int b = 0; (more >> b) & 1u; b = (b + 1) % kWarpStages) {
       mbar_wait(&s_bar[wib][b], (par_bits >> b) & 1u);
@@ -696,11 +727,9 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
         // re-learn the hot prefix from L2 (others' discoveries): async bulk
         // copy over the shared copy; a racing local OR may be lost, which
         // only costs a redundant write later
-        if (lane == 0) {
-          mbar_wait(&s_hot_bar, hot_phase & 1u);  // previous copy landed
-          ++hot_phase;
-          mbar_expect_tx(&s_hot_bar, (uint32_t)hot_words * 4u);
-          bulk_g2s(h.s, a.visited, (uint32_t)hot_words * 4u, &s_hot_bar);
+        if (lane == 0) {  // (warp 0 lane 0 is thread 0, the only issuer)
+          hot_wait_last(s);  // previous copy landed
+          hot_issue(s, h, a.visited);
         }
         __syncwarp();
       }
@@ -715,8 +744,16 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
 
   // ---- phase 2: non-hub frontier as balanced group items -----------------
   for (int64_t it = gwarp; (phases & 2) && it < f.n_items; it += nwarps) {
-    const GroupItem gi = f.items[it];
-    const int32_t v = lane < gi.count ? f.list[gi.list_start + lane] : 0;
+    GroupItem gi;
+    {  // through L2: written within the same launch by k_bfs (24-byte items: 8-byte loads)
+      const int2* r = reinterpret_cast<const int2*>(f.items + it);
+      const int2 r0 = __ldcg(r), r1 = __ldcg(r + 1), r2 = __ldcg(r + 2);
+      gi.list_start = (int64_t)(((uint64_t)(uint32_t)r0.y << 32) | (uint32_t)r0.x);
+      gi.count = r1.x;
+      gi.elo = r1.y;
+      gi.ehi = r2.x;
+    }
+    const int32_t v = lane < gi.count ? __ldcg(f.list + gi.list_start + lane) : 0;
     expand_range<M>(a, h, gi.count, v, gi.elo, gi.ehi, s_T, s_B, lane, ws, acc);
   }
 
@@ -746,7 +783,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
           const uint32_t rel = (uint32_t)(pq - base);
           own[q] = lo + (d == 1 ? (int32_t)rel : (int32_t)__umulhi(rel, rcp));
           const bool in_task = pq >= dt.p0 && pq < a1;
-          const bool in_front = in_task && ((__ldca(f.front + (own[q] >> 5)) >> (own[q] & 31)) & 1u);
+          const bool in_front = in_task && ((__ldcg(f.front + (own[q] >> 5)) >> (own[q] & 31)) & 1u);
           okm |= (uint32_t)in_front << q;
           nb[q] = in_front ? nb[q] : 0;
         }
@@ -822,11 +859,25 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
       const bool wb = g < f.n_warp;
       const int64_t base = wb ? g : (g - f.n_warp) * 32;
       const int n = wb ? 1 : (int)std::min<int64_t>(32, f.n_small - base);
-      const int32_t v = lane < n ? (wb ? f.warp : f.small)[base + lane] : 0;
+      const int32_t v = lane < n ? __ldcg((wb ? f.warp : f.small) + base + lane) : 0;
       expand_range<M>(a, h, n, v, 0, 1 << 30, s_T, s_B, lane, ws, acc);
     }
   }
+}
+
+// One launch per level and bin set (host-driven level loop).
+template <int M, int kPhases>
+__global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Frontier f, int32_t hot_words) {
+  extern __shared__ __align__(128) uint8_t s_dyn[];
+  __shared__ ExpandSmem s;
+  expand_init(s, a);
+  const Hot h{reinterpret_cast<uint32_t*>(s_dyn + kRingBytes), smem_u32(s_dyn + kRingBytes), hot_words};
+  hot_load(s, h, a.visited);
+  uint32_t par_bits = 0;
+  Acc acc;
+  expand_phases<M, kPhases>(a, f, s, s_dyn, h, par_bits, acc);
   flush_acc<M>(a, acc);
+  hot_drain(s);
 }
 
 // ---------------------------------------------------------------- K5 on the device
@@ -961,41 +1012,74 @@ constexpr int kCompactVerts = 4096;
 constexpr int kCompactWords = kCompactVerts / 32;
 constexpr int kCompactSteps = kCompactVerts / kCompactThreads;
 
-// exclusive scan of one int per thread over the first 128 threads (all 256
-// threads must call); returns the exclusive prefix, *total the sum
-__device__ __forceinline__ int scan128(int val, int* s_w, int* total) {
-  const int t = threadIdx.x, lane = t & 31;
+// A compaction group is 256 threads synchronised on named barrier `bar`
+// (a whole CTA in k_compact; a quarter of a k_bfs CTA).
+__device__ __forceinline__ void gsync(int bar) {
+  asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(kCompactThreads) : "memory");
+}
+__device__ __forceinline__ int gsync_or(int bar, bool pred) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.s32 p, %2, 0;\n\t"
+      "bar.red.or.pred q, %1, %3, p;\n\t"
+      "selp.s32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"(bar), "r"((int)pred), "r"(kCompactThreads)
+      : "memory");
+  return r;
+}
+
+// exclusive scan of one int per thread over the first 128 threads of the
+// group (all 256 must call); returns the exclusive prefix, *total the sum
+__device__ __forceinline__ int scan128(int t, int bar, int val, int* s_w, int* total) {
+  const int lane = t & 31;
   int incl = val;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int x = __shfl_up_sync(kFull, incl, o);
     if (lane >= o) incl += x;
   }
-  __syncthreads();
+  gsync(bar);
   if (t < 128 && lane == 31) s_w[t >> 5] = incl;
-  __syncthreads();
+  gsync(bar);
   int before = 0;
   for (int k = 0; k < (t >> 5) && k < 4; ++k) before += s_w[k];
   *total = s_w[0] + s_w[1] + s_w[2] + s_w[3];
   return before + incl - val;
 }
 
-__global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
-  using Reduce = cub::BlockReduce<unsigned long long, kCompactThreads>;
-  __shared__ typename Reduce::TempStorage s_red;
-  __shared__ uint32_t s_new[kCompactWords];
-  __shared__ uint32_t s_lmask[kCompactWords];
-  __shared__ int32_t s_lpre[kCompactWords];
-  __shared__ uint32_t s_wmask[kCompactWords];
-  __shared__ int32_t s_wpre[kCompactWords];
-  __shared__ int32_t s_deg[kCompactVerts];
-  __shared__ int32_t s_gsum[kCompactWords];
-  __shared__ int32_t s_w[4];
-  __shared__ unsigned long long s_base[4];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int64_t w0 = (int64_t)blockIdx.x * kCompactWords;
+struct CompactSmem {
+  unsigned long long base[4];
+  unsigned long long red[2][kCompactThreads / 32];
+  uint32_t new_[kCompactWords];
+  uint32_t lmask[kCompactWords];
+  int32_t lpre[kCompactWords];
+  uint32_t wmask[kCompactWords];
+  int32_t wpre[kCompactWords];
+  int32_t gsum[kCompactWords];
+  int32_t hitems[kCompactWords];  // hub slices per word, then their word offsets
+  int32_t w[4];
+  int32_t deg[kCompactVerts];
+};
+
+// One compaction block (kCompactVerts ids) by a 256-thread group: thread t
+// of the group, named barrier `bar`, shared scratch sm.
+__device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk, CompactSmem& sm, int t, int bar) {
+  uint32_t* s_new = sm.new_;
+  uint32_t* s_lmask = sm.lmask;
+  int32_t* s_lpre = sm.lpre;
+  uint32_t* s_wmask = sm.wmask;
+  int32_t* s_wpre = sm.wpre;
+  int32_t* s_deg = sm.deg;
+  int32_t* s_gsum = sm.gsum;
+  int32_t* s_w = sm.w;
+  unsigned long long* s_base = sm.base;
+  int32_t* s_hitems = sm.hitems;
+  const int lane = t & 31, warp = t >> 5;
+  const int64_t w0 = blk * kCompactWords;
   const int64_t v0 = w0 * 32;
-  __shared__ int32_t s_hitems[kCompactWords];  // hub slices per word, then their word offsets
+  gsync(bar);  // the previous block's readers of sm are done
   uint32_t nb = 0, mhub = 0, mlist = 0, mwarp = 0;
   if (t < kCompactWords) s_hitems[t] = 0;
   if (t < kCompactWords && w0 + t < c.nwords) {
@@ -1012,23 +1096,23 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
       mlist = nb & range_mask(vw, c.t_warp, c.t_nz);
     }
   }
-  const int any_hub = __syncthreads_or(mhub != 0);  // (also orders s_hitems' zeroing)
-  if (!__syncthreads_or(nb != 0)) return;
+  const int any_hub = gsync_or(bar, mhub != 0);  // (also orders s_hitems' zeroing)
+  if (!gsync_or(bar, nb != 0)) return;
   if (t < kCompactWords) {
     s_new[t] = nb;
     s_lmask[t] = mlist;
     s_wmask[t] = mwarp;
   }
   int n_list = 0, n_wsl = 0;
-  const int lpre = scan128(__popc(mlist), s_w, &n_list);
+  const int lpre = scan128(t, bar, __popc(mlist), s_w, &n_list);
   if (t < kCompactWords) s_lpre[t] = lpre;
-  const int wpre = scan128(__popc(mwarp), s_w, &n_wsl);
+  const int wpre = scan128(t, bar, __popc(mwarp), s_w, &n_wsl);
   if (t < kCompactWords) s_wpre[t] = wpre;
   if (t == 0) {
     s_base[0] = n_list ? atomicAdd(&c.next_cnt->bin[kBinSmall], (unsigned long long)n_list) : 0;
     s_base[3] = n_wsl ? atomicAdd(&c.next_cnt->bin[kBinWSlice], (unsigned long long)n_wsl) : 0;
   }
-  __syncthreads();
+  gsync(bar);
   // pass 2: thread t owns vertices v0 + t + 256 j (bit t&31 of word t/32 + 8 j);
   // four vertices' loads are issued before any of their stores
   unsigned long long edges = 0;
@@ -1068,18 +1152,18 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
       if (v < c.t_cta) atomicAdd(&s_hitems[wl], (deg + kChunk - 1) / kChunk);
     }
   }
-  __syncthreads();
+  gsync(bar);
   if (any_hub) {
     // hub slices: word offsets from one scan, slots inside a word claimed
     // with shared atomics (slice order is free); one vertex per thread per
     // step, so the row_ptr reads stay parallel (they hit L1: read above)
     int n_hub_items = 0;
     const int hi = t < kCompactWords ? s_hitems[t] : 0;
-    const int ipre = scan128(hi, s_w, &n_hub_items);
-    __syncthreads();
+    const int ipre = scan128(t, bar, hi, s_w, &n_hub_items);
+    gsync(bar);
     if (t < kCompactWords) s_hitems[t] = ipre;
     if (t == 0) s_base[1] = atomicAdd(&c.next_cnt->bin[kBinCta], (unsigned long long)n_hub_items);
-    __syncthreads();
+    gsync(bar);
     for (int j = 0; j < kCompactSteps; ++j) {
       const int wl = (t >> 5) + j * (kCompactThreads / 32);
       const int64_t v = v0 + t + j * kCompactThreads;
@@ -1101,13 +1185,13 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
     for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
     if (lane == 0) s_gsum[g] = x;
   }
-  __syncthreads();
+  gsync(bar);
   const int gsum = t < ngroups ? s_gsum[t] : 0;
   const int nsub = t < ngroups ? std::max(1, (gsum + kItemElems - 1) / kItemElems) : 0;
   int n_items = 0;
-  const int gpre = scan128(nsub, s_w, &n_items);
+  const int gpre = scan128(t, bar, nsub, s_w, &n_items);
   if (t == 0) s_base[2] = atomicAdd(&c.next_cnt->bin[kBinItems], (unsigned long long)n_items);
-  __syncthreads();
+  gsync(bar);
   for (int k = 0; k < nsub; ++k) {
     GroupItem gi;
     gi.list_start = (int64_t)s_base[0] + 32 * t;
@@ -1117,14 +1201,34 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
     gi.pad = 0;
     c.next_items[s_base[2] + gpre + k] = gi;
   }
-  const unsigned long long e_tot = Reduce(s_red).Sum(edges);
-  __syncthreads();
-  const unsigned long long d_tot = Reduce(s_red).Sum((unsigned long long)__popc(nb));
+  unsigned long long e = edges, d = (unsigned long long)__popc(nb);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    e += __shfl_xor_sync(kFull, e, o);
+    d += __shfl_xor_sync(kFull, d, o);
+  }
+  if (lane == 0) {
+    sm.red[0][warp] = e;
+    sm.red[1][warp] = d;
+  }
+  gsync(bar);
   if (t == 0) {
+    unsigned long long e_tot = 0, d_tot = 0;
+    for (int k = 0; k < kCompactThreads / 32; ++k) {
+      e_tot += sm.red[0][k];
+      d_tot += sm.red[1][k];
+    }
     if (e_tot) atomicAdd(&c.next_cnt->edges, e_tot);
     if (d_tot) atomicAdd(&c.next_cnt->discovered, d_tot);
   }
 }
+
+__global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
+  __shared__ CompactSmem sm;
+  compact_block(c, blockIdx.x, sm, threadIdx.x, 1);
+}
+
+
 
 // ---------------------------------------------------------------- K4 init
 // per-BFS state: visited/prev bitmaps cleared, internal levels -1
