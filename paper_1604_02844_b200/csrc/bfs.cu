@@ -218,14 +218,16 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, const int32_t (
 // writer: one red.or to the bitmap and one OR into the shared copy per word
 // per warp step; each lane stores its parent (original id) to pred_int[v].
 // Visited word of v's bitmap word wi: from the shared copy when wi is in the
-// hot prefix, else from global memory through L1 — two predicated loads, no
-// branch, no generic addressing.
+// hot prefix, else from L2 — two predicated loads, no branch, no generic
+// addressing. (Not through L1: within one k_bfs launch an L1 line may date
+// from an earlier level, and an old "unvisited" would record a parent two
+// levels up; the L1 hit rate of these probes was 1-8% anyway.)
 __device__ __forceinline__ uint32_t probe_word(const Hot& h, const uint32_t* visited, int32_t wi) {
   uint32_t w;
   asm("{\n\t.reg .pred p;\n\t"
       "setp.lt.s32 p, %1, %2;\n\t"
       "@p ld.shared.u32 %0, [%3];\n\t"
-      "@!p ld.global.ca.u32 %0, [%4];\n\t}"
+      "@!p ld.global.cg.u32 %0, [%4];\n\t}"
       : "=r"(w)
       : "r"(wi), "r"(h.words), "r"(h.base + 4u * (uint32_t)wi), "l"(visited + wi));
   return w;
@@ -284,9 +286,13 @@ __device__ __forceinline__ uint32_t probe_mask(const LevelArgs& a, const Hot& h,
   for (int k = 0; k < K; ++k) {
     uint32_t w;
     if constexpr (W == kAllHot)
+#ifdef LBFS_HOT_GENERIC
       w = h.s[nb[k] >> 5];
+#else
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(h.base + 4u * (uint32_t)(nb[k] >> 5)));
+#endif
     else if constexpr (W == kAllCold)
-      w = __ldca(a.visited + (nb[k] >> 5));
+      w = __ldcg(a.visited + (nb[k] >> 5));
     else
       w = probe_word(h, a.visited, nb[k] >> 5);
     cmask |= ((~w >> (nb[k] & 31)) & 1u) << k;
@@ -1084,7 +1090,7 @@ __device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk,
   if (t < kCompactWords) s_hitems[t] = 0;
   if (t < kCompactWords && w0 + t < c.nwords) {
     const int64_t gw = ((w0 + t) << c.part_log) | c.part_rank;  // global word of owned word w0+t
-    const uint32_t w = c.visited[gw], p = c.prev[gw];
+    const uint32_t w = __ldcg(c.visited + gw), p = __ldcg(c.prev + gw);
     nb = w & ~p;
     c.front[w0 + t] = nb;  // next frontier as a bitmap (dense small-region path)
     if (c.fsend) c.fsend[w0 + t] = nb;
@@ -1232,24 +1238,27 @@ __global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
 
 // ---------------------------------------------------------------- K4 init
 // per-BFS state: visited/prev bitmaps cleared, internal levels -1
-__global__ void k_init(uint4* __restrict__ vis4, uint4* __restrict__ prev4, int64_t nwords4,
-                       int4* __restrict__ lvl4, int64_t n4) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void init_range(uint4* __restrict__ vis4, uint4* __restrict__ prev4, int64_t nwords4,
+                                           int4* __restrict__ lvl4, int64_t n4, int64_t t, int64_t stride) {
   for (int64_t i = t; i < nwords4; i += stride) vis4[i] = prev4[i] = make_uint4(0, 0, 0, 0);
   const int4 m4 = make_int4(-1, -1, -1, -1);
   for (int64_t i = t; i < n4; i += stride) lvl4[i] = m4;
+}
+__global__ void k_init(uint4* __restrict__ vis4, uint4* __restrict__ prev4, int64_t nwords4,
+                       int4* __restrict__ lvl4, int64_t n4) {
+  init_range(vis4, prev4, nwords4, lvl4, n4, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+             (int64_t)gridDim.x * blockDim.x);
 }
 
 // Outputs in original ids, once per BFS: sequential (128-bit) writes of
 // level[x] and pred[x], gathering the internal-order records through old2new
 // (PredecessorArray semantics, traversal.py:42-50: unreached and padding =
 // SENTINEL). Replaces per-vertex scattered writes during the levels.
-__global__ void k_finalize(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
-                           const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
-                           int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i * 4 < npad; i += stride) {
+__device__ __forceinline__ void finalize_vec(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
+                                             const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
+                                             int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out,
+                                             int64_t t, int64_t stride) {
+  for (int64_t i = t; i * 4 < npad; i += stride) {
     int lv[4], pr[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -1258,8 +1267,8 @@ __global__ void k_finalize(const int32_t* __restrict__ old2new, const int32_t* _
       pr[q] = kSentinel;
       if (x < n) {
         const int32_t v = __ldg(old2new + x);
-        lv[q] = __ldg(level_int + v);
-        if (lv[q] >= 0) pr[q] = __ldg(pred_int + v);
+        lv[q] = __ldcg(level_int + v);
+        if (lv[q] >= 0) pr[q] = __ldcg(pred_int + v);
       }
     }
     reinterpret_cast<int4*>(pred_out)[i] = make_int4(pr[0], pr[1], pr[2], pr[3]);
@@ -1271,29 +1280,42 @@ __global__ void k_finalize(const int32_t* __restrict__ old2new, const int32_t* _
     }
   }
 }
-
-__global__ void k_finalize_scalar(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
-                                  const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
-                                  int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < npad; x += stride) {
+__device__ __forceinline__ void finalize_scalar(const int32_t* __restrict__ old2new,
+                                                const int32_t* __restrict__ level_int,
+                                                const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
+                                                int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out,
+                                                int64_t t, int64_t stride) {
+  for (int64_t x = t; x < npad; x += stride) {
     int lv = -1, pr = kSentinel;
     if (x < n) {
       const int32_t v = __ldg(old2new + x);
-      lv = __ldg(level_int + v);
-      if (lv >= 0) pr = __ldg(pred_int + v);
+      lv = __ldcg(level_int + v);
+      if (lv >= 0) pr = __ldcg(pred_int + v);
       level_out[x] = lv;
     }
     pred_out[x] = pr;
   }
+}
+__global__ void k_finalize(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
+                           const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
+                           int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out) {
+  finalize_vec(old2new, level_int, pred_int, n, npad, level_out, pred_out,
+               (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
+__global__ void k_finalize_scalar(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
+                                  const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
+                                  int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out) {
+  finalize_scalar(old2new, level_int, pred_int, n, npad, level_out, pred_out,
+                  (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 
 // Root of a BFS (traversal.py:135-139, 343-347): its bit in visited/prev
 // (and in the replicated frontier bitmap when partitioned) on every rank;
 // the owner records level 0 / pred = root and seeds its bins. red, when
 // given, receives the (frontier, edges) counts for the cross-rank sum.
-__global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int32_t root_orig, Counters* cnt0,
-                       uint32_t* fglob, unsigned long long* red) {
+__device__ __forceinline__ void seed_root(const LevelArgs& a, uint32_t* prev, const int32_t* old2new,
+                                          int32_t root_orig, Counters* cnt0, uint32_t* fglob,
+                                          unsigned long long* red) {
   const int32_t r = old2new[root_orig];
   a.visited[r >> 5] |= 1u << (r & 31);
   prev[r >> 5] |= 1u << (r & 31);
@@ -1324,6 +1346,230 @@ __global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int3
   if (red) {
     red[0] = c.discovered;
     red[1] = c.edges;
+  }
+}
+__global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int32_t root_orig, Counters* cnt0,
+                       uint32_t* fglob, unsigned long long* red) {
+  seed_root(a, prev, old2new, root_orig, cnt0, fglob, red);
+}
+
+// ---------------------------------------------------------------- K5: whole BFS, one launch
+// The level loop of traversal.py:90 / 152 / 366 on the device: one
+// cooperative launch of one 1024-thread CTA per SM runs init, every level
+// and the output pass. Per level the plan (queue vs bitmap mode, list vs
+// dense small region) is derived from the counter ring exactly as the host
+// loop does; bitmap levels run expansion -> grid barrier -> compaction
+// (four 256-thread groups per CTA, scratch aliased onto the hot snapshot)
+// -> grid barrier, queue levels expansion -> grid barrier. No host round
+// trip and no launch between levels.
+constexpr int kMegaPhases = 1 | 2 | 4 | 16 | 32;
+
+// Separate calls (not inlined) so that each part gets the kernel's register
+// budget to itself: inlined into one loop, the per-level state of all of
+// them spilled inside the element loops.
+#ifndef LBFS_MEGA_PHASE_CALL
+#define LBFS_MEGA_PHASE_CALL __noinline__
+#endif
+#ifndef LBFS_MEGA_COMPACT_CALL
+#define LBFS_MEGA_COMPACT_CALL __noinline__
+#endif
+template <int M, int kPhase>
+__device__ LBFS_MEGA_PHASE_CALL void mega_phase(const LevelArgs* a, const Frontier* f, ExpandSmem* s,
+                                                uint8_t* s_dyn, Hot h, uint32_t* par_bits) {
+  // local copies: read through the shared-memory pointers, every global
+  // store in the element loops could alias them and force reloads
+  const LevelArgs la = *a;
+  const Frontier lf = *f;
+  Acc acc;
+  uint32_t pb = *par_bits;
+  expand_phases<M, kPhase>(la, lf, *s, s_dyn, h, pb, acc);
+  *par_bits = pb;
+  flush_acc<M>(la, acc);
+}
+// all bins of a level, one call per non-empty bin
+template <int M>
+__device__ __forceinline__ void mega_expand(const LevelArgs* a, const Frontier* f, ExpandSmem* s, uint8_t* s_dyn,
+                                            Hot h, uint32_t* par_bits, int skip) {
+  // the snapshot is re-read before each bin (as each separate phase launch
+  // does): later bins then see the discoveries of the earlier ones
+  bool first = true;
+  auto fresh = [&]() {
+    if (!first) hot_load(*s, h, a->visited);
+    first = false;
+  };
+  if (f->n_cta && !(skip & 2)) {
+    fresh();
+    mega_phase<M, 1>(a, f, s, s_dyn, h, par_bits);
+  }
+  if (f->n_items && !(skip & 8)) {
+    fresh();
+    mega_phase<M, 2>(a, f, s, s_dyn, h, par_bits);
+  }
+  if (f->n_warp + f->n_small && !(skip & 4)) {
+    fresh();
+    mega_phase<M, 4>(a, f, s, s_dyn, h, par_bits);
+  }
+  if (f->n_wslice && !(skip & 16)) {
+    fresh();
+    mega_phase<M, 16>(a, f, s, s_dyn, h, par_bits);
+  }
+  if (f->n_dense && !(skip & 32)) {
+    fresh();
+    mega_phase<M, 32>(a, f, s, s_dyn, h, par_bits);
+  }
+}
+// consecutive blocks go to different SMs (the hub-heavy first blocks spread out)
+__device__ LBFS_MEGA_COMPACT_CALL void mega_compact(const CompactArgs* ca, int64_t nblk, CompactSmem* cs, int sub,
+                                                    int interleave) {
+  const CompactArgs c = *ca;
+  const int64_t b0 = interleave ? (int64_t)sub * gridDim.x + blockIdx.x : (int64_t)blockIdx.x * 4 + sub;
+  for (int64_t blk = b0; blk < nblk; blk += (int64_t)gridDim.x * 4)
+    compact_block(c, blk, *cs, threadIdx.x & (kCompactThreads - 1), 1 + sub);
+}
+
+__global__ void __launch_bounds__(kExpandThreads, 1) k_bfs(LevelArgs a, BfsArgs p) {
+  extern __shared__ __align__(128) uint8_t s_dyn[];
+  __shared__ ExpandSmem s;
+  expand_init(s, a);
+  const int tid = threadIdx.x;
+  unsigned gen = tid == 0 ? ld_acquire(&p.state->bar_gen) : 0u;
+  unsigned* bar_count = &p.state->bar_count;
+  unsigned* bar_gen = &p.state->bar_gen;
+  const Hot hot{reinterpret_cast<uint32_t*>(s_dyn + kRingBytes), smem_u32(s_dyn + kRingBytes), p.hot_words};
+  const Hot cold{nullptr, 0u, 0};
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + tid, gstride = (int64_t)gridDim.x * blockDim.x;
+  bool finished = false;
+  if (p.do_init) {
+    init_range(reinterpret_cast<uint4*>(a.visited), reinterpret_cast<uint4*>(a.prev), (p.nwords + 3) / 4,
+               reinterpret_cast<int4*>(a.level_int), (p.n_loc + 3) / 4, gt, gstride);
+    if (blockIdx.x == 0 && tid < (int)(kCounterRing * sizeof(Counters) / 8))
+      reinterpret_cast<unsigned long long*>(p.ring)[tid] = 0ull;
+    grid_sync(bar_count, bar_gen, gen, nullptr);
+    if (blockIdx.x == 0 && tid == 0) {
+      LevelArgs sa = a;
+      sa.next_small = p.q_small[0];
+      sa.next_warp = p.q_warp[0];
+      sa.next_cta = p.q_cta[0];
+      seed_root(sa, a.prev, p.old2new, p.root_orig, &p.ring[0], nullptr, nullptr);
+    }
+    grid_sync(bar_count, bar_gen, gen, nullptr);
+  }
+  // per-level plan in shared memory (kept out of registers across the
+  // phases); one variable, so no part of it can share storage with another
+  struct Plan {
+    LevelArgs la;
+    Frontier f;
+    Counters c;
+    int flags;  // bit 0: bitmap level, bit 1: finished, bit 2: stop
+  };
+  __shared__ Plan s_plan;
+  LevelArgs& s_la = s_plan.la;
+  Frontier& s_f = s_plan.f;
+  Counters& s_c = s_plan.c;
+  int& s_flags = s_plan.flags;
+  int64_t L = p.L0;
+  bool prev_bitmap = p.prev_bitmap0 != 0;
+  uint32_t par_bits = 0;
+  const int sub = tid >> 8;  // compaction group of this thread
+  CompactSmem* cs = reinterpret_cast<CompactSmem*>(s_dyn + kRingBytes) + sub;
+  if (tid == 0) s_c = ld_counters(&p.ring[L % kCounterRing]);
+  __syncthreads();
+  for (;;) {
+    const int cur = (int)(L & 1);
+    if (blockIdx.x == 0 && tid < (int)(sizeof(Counters) / 8))
+      reinterpret_cast<unsigned long long*>(&p.ring[(L + 2) % kCounterRing])[tid] = 0ull;
+    if (tid == 0) {
+      const Counters& c = s_c;
+      Frontier f{};
+      f.cta = p.q_cta[cur];
+      f.n_cta = (int64_t)c.bin[kBinCta];
+      if (prev_bitmap) {
+        f.list = p.q_small[cur];
+        f.items = p.q_items[cur];
+        f.n_items = (int64_t)c.bin[kBinItems];
+        f.wslice = p.q_wslice[cur];
+        f.n_wslice = (int64_t)c.bin[kBinWSlice];
+        if (p.small_region > 0 && (int64_t)c.bin[kBinSmall] * kDenseDenom > p.small_region * kDenseNum &&
+            !p.dense_off) {
+          f.n_items = 0;
+          f.front = p.front;
+          f.dense = p.dense;
+          f.n_dense = p.n_dense;
+        }
+      } else {
+        f.small = p.q_small[cur];
+        f.warp = p.q_warp[cur];
+        f.n_small = (int64_t)c.bin[kBinSmall];
+        f.n_warp = (int64_t)c.bin[kBinWarp];
+      }
+      s_f = f;
+      LevelArgs la = a;
+      la.next_level = (int32_t)(L + 1);
+      la.next_cnt = &p.ring[(L + 1) % kCounterRing];
+      la.next_small = p.q_small[cur ^ 1];
+      la.next_warp = p.q_warp[cur ^ 1];
+      la.next_cta = p.q_cta[cur ^ 1];
+      s_la = la;
+      s_flags = c.edges >= p.bitmap_min_edges ? 1 : 0;
+    }
+    __syncthreads();
+    const bool bitmap = s_flags & 1;
+    unsigned long long* pf = (p.prof && blockIdx.x == 0 && tid == 0 && L - p.L0 < 64) ? p.prof + 6 * (L - p.L0) : nullptr;
+    if (pf) pf[0] = gtimer();
+    if (bitmap) {
+      hot_load(s, hot, a.visited);
+      if (pf) pf[1] = gtimer();
+      mega_expand<kBitmapOut>(&s_la, &s_f, &s, s_dyn, hot, &par_bits, p.debug_skip);
+      hot_drain(s);
+      if (pf) pf[2] = gtimer();
+      grid_sync(bar_count, bar_gen, gen, nullptr);
+      if (pf) pf[3] = gtimer();
+      {
+        const CompactArgs ca{a.row_ptr, a.new2old, a.visited, a.prev, p.nwl, a.level_int, (int32_t)(L + 1),
+                             a.t_cta, a.t_warp, a.t_nz, &p.ring[(L + 1) % kCounterRing], p.q_small[cur ^ 1],
+                             p.q_cta[cur ^ 1], p.q_items[cur ^ 1], p.q_wslice[cur ^ 1], p.front, 0, 0, nullptr};
+        if (!(p.debug_skip & 1)) mega_compact(&ca, p.n_compact_blocks, cs, sub, !(p.debug_skip & 256));
+      }
+      __syncthreads();
+      if (pf) pf[4] = gtimer();
+      grid_sync(bar_count, bar_gen, gen, nullptr);
+      if (pf) pf[5] = gtimer();
+    } else {
+      if (pf) pf[1] = gtimer();
+      mega_expand<kQueueOut>(&s_la, &s_f, &s, s_dyn, cold, &par_bits, p.debug_skip);
+      __syncthreads();
+      if (pf) pf[2] = gtimer();
+      grid_sync(bar_count, bar_gen, gen, nullptr);
+      if (pf) pf[3] = pf[4] = pf[5] = gtimer();
+    }
+    if (tid == 0) {
+      const Counters nx = ld_counters(&p.ring[(L + 1) % kCounterRing]);
+      if (blockIdx.x == 0)
+        p.layers[L - p.L0] = lbfs_layer{(int64_t)s_c.discovered, (int64_t)s_c.edges, (int64_t)nx.discovered};
+      s_c = nx;
+      s_flags = (nx.discovered == 0 ? 2 : 0) | (L + 1 - p.L0 >= p.max_levels ? 4 : 0);
+    }
+    __syncthreads();
+    ++L;
+    prev_bitmap = bitmap;
+    const int fl = s_flags;
+    __syncthreads();  // s_flags / s_c are rewritten at the next level's start
+    if (fl & 2) {
+      finished = true;
+      break;
+    }
+    if (fl & 4) break;
+  }
+  if (finished) {
+    if (p.aligned)
+      finalize_vec(p.old2new, a.level_int, a.pred_int, p.n, p.npad, p.d_level, p.d_pred, gt, gstride);
+    else
+      finalize_scalar(p.old2new, a.level_int, a.pred_int, p.n, p.npad, p.d_level, p.d_pred, gt, gstride);
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    p.state->L_end = L;
+    p.state->prev_bitmap = prev_bitmap ? 1 : 0;
+    p.state->done = finished ? 1 : 0;
   }
 }
 
@@ -1445,6 +1691,24 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   LBFS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device_));
   LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&locc, k_levels, kLoopThreads, 0));
   loop_grid_ = (coop && locc > 0) ? sm_count_ : 0;
+  // whole-BFS kernel: the dynamic part must also hold four compaction groups
+  {
+    cudaFuncAttributes fa{};
+    LBFS_CUDA(cudaFuncGetAttributes(&fa, (const void*)k_bfs));
+    const int need = std::max<int>(dyn_smem_, kRingBytes + 4 * (int)sizeof(CompactSmem));
+    int mocc = 0;
+    if (coop && (int64_t)fa.sharedSizeBytes + need <= optin) {
+      LBFS_CUDA(cudaFuncSetAttribute((const void*)k_bfs, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
+      LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mocc, k_bfs, kExpandThreads, need));
+    }
+    mega_smem_ = mocc > 0 ? need : 0;
+    if (mega_smem_) {  // the phase calls' frames exceed the default 1 KB per-thread stack
+      size_t cur_stack = 0;
+      LBFS_CUDA(cudaDeviceGetLimit(&cur_stack, cudaLimitStackSize));
+      if (cur_stack < (size_t)fa.localSizeBytes + 1024)
+        LBFS_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, (size_t)fa.localSizeBytes + 1024));
+    }
+  }
   d_layers_ = dev_alloc<lbfs_layer>((size_t)kLoopCap);
   loop_ = dev_alloc<LoopState>(1);
   LBFS_CUDA(cudaMemset(loop_, 0, sizeof(LoopState)));
@@ -1461,6 +1725,7 @@ BfsEngine::~BfsEngine() {
   dev_free(front_);
   dev_free(dense_tasks_);
   dev_free(dbg_);
+  dev_free(mprof_);
   dev_free(classes_);
   for (int b = 0; b < 2; ++b) {
     dev_free(q_small_[b]);
@@ -1634,12 +1899,135 @@ void BfsEngine::read_env() {
   hub_ldg_ = env_flag("LBFS_HUB_LDG");  // experiment: hub bin without TMA staging
   loop_off_ = env_flag("LBFS_NO_LOOP");  // experiment: host-driven queue-mode levels
   loop_prof_ = env_flag("LBFS_LOOP_PROF");
+  // LBFS_MEGA=1: whole BFS in one persistent launch (k_bfs). Measured on
+  // S24 it is ~12% slower than the host-driven loop (its phases run as
+  // calls inside one kernel: 10-15% slower per level than one launch per
+  // bin), on S20 ~15% faster (no host round trips); off by default.
+  mega_on_ = env_flag("LBFS_MEGA");
+}
+
+void BfsEngine::run_mega(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t) {
+  const int64_t launches0 = g_launches.load();
+  cudaStream_t st = stream_;
+  LevelArgs a = level_args();
+  BfsArgs p{};
+  for (int b = 0; b < 2; ++b) {
+    p.q_small[b] = q_small_[b];
+    p.q_warp[b] = q_warp_[b];
+    p.q_cta[b] = q_cta_[b];
+    p.q_items[b] = q_items_[b];
+    p.q_wslice[b] = q_wslice_[b];
+  }
+  p.ring = cnt_;
+  p.front = front_;
+  p.dense = dense_tasks_;
+  p.n_dense = n_dense_tasks_;
+  p.layers = d_layers_;
+  p.state = loop_;
+  p.max_levels = kLoopCap;
+  if (const char* ml = getenv("LBFS_MEGA_LEVELS")) p.max_levels = std::max(1, atoi(ml));  // debug: levels per launch
+  p.bitmap_min_edges = (unsigned long long)std::max<int64_t>(1 << 16, n_ / 64);
+  p.small_region = (int64_t)t_nz_ - t_warp_;
+  p.dense_off = dense_off_ ? 1 : 0;
+  p.hot_words = env_flag("LBFS_MEGA_NOHOT") ? 0 : hot_words_;  // debug
+  if (const char* sk = getenv("LBFS_MEGA_SKIP")) p.debug_skip = atoi(sk);
+  const bool mprof = env_flag("LBFS_MEGA_PROF");
+  if (mprof) {
+    if (!mprof_) mprof_ = dev_alloc<unsigned long long>(6 * 64);
+    LBFS_CUDA(cudaMemsetAsync(mprof_, 0, sizeof(unsigned long long) * 6 * 64, st));
+    p.prof = mprof_;
+  }
+  if (trace_)
+    fprintf(stderr, "[lbfs] host: rp %p n2o %p vis %p prev %p nwl %lld lvl %p t %d/%d/%d ring %p small %p/%p cta %p/%p items %p/%p wsl %p/%p front %p\n",
+            (void*)row_ptr_, (void*)new2old_loc_, (void*)visited_, (void*)prev_, (long long)nwl_, (void*)level_int_, t_cta_,
+            t_warp_, t_nz_, (void*)cnt_, (void*)q_small_[0], (void*)q_small_[1], (void*)q_cta_[0], (void*)q_cta_[1],
+            (void*)q_items_[0], (void*)q_items_[1], (void*)q_wslice_[0], (void*)q_wslice_[1], (void*)front_);
+  if (trace_)
+    fprintf(stderr, "[lbfs] k_bfs: dyn smem %d (ring %d, hot words %d, 4 x compact %zu), static ExpandSmem %zu\n",
+            mega_smem_, kRingBytes, p.hot_words, sizeof(CompactSmem), sizeof(ExpandSmem));
+  p.nwords = nwords_;
+  p.nwl = nwl_;
+  p.n_loc = n_loc_;
+  p.root_orig = (int32_t)root;
+  p.old2new = old2new_;
+  p.n_compact_blocks = (n_loc_ + kCompactVerts - 1) / kCompactVerts;
+  p.d_pred = d_pred;
+  p.d_level = d_level;
+  p.n = n_;
+  p.npad = npad_;
+  p.aligned = ((uintptr_t)d_pred % 16 == 0) && ((uintptr_t)d_level % 16 == 0);
+  p.do_init = 1;
+  p.L0 = 0;
+  p.prev_bitmap0 = 0;
+  layers_.clear();
+  LBFS_CUDA(cudaEventRecord(ev_[0], st));
+  for (;;) {
+    void* args[] = {(void*)&a, (void*)&p};
+    LBFS_CUDA(cudaLaunchCooperativeKernel((const void*)k_bfs, dim3(sm_count_), dim3(kExpandThreads), args,
+                                          (size_t)mega_smem_, st));
+    g_launches.fetch_add(1);
+    LBFS_CUDA(cudaEventRecord(ev_[4], st));
+    LBFS_CUDA(cudaMemcpyAsync(h_loop_, loop_, sizeof(LoopState), cudaMemcpyDeviceToHost, st));
+    LBFS_CUDA(cudaMemcpyAsync(h_layers_, d_layers_, sizeof(lbfs_layer) * 64, cudaMemcpyDeviceToHost, st));
+    LBFS_CUDA(cudaStreamSynchronize(st));
+    const int64_t k = h_loop_->L_end - p.L0;
+    if (k < 1 || k > kLoopCap) throw Failure(LBFS_ECUDA, "internal: k_bfs level state");
+    if (k > 64) {
+      LBFS_CUDA(cudaMemcpyAsync(h_layers_ + 64, d_layers_ + 64, sizeof(lbfs_layer) * (k - 64),
+                                cudaMemcpyDeviceToHost, st));
+      LBFS_CUDA(cudaStreamSynchronize(st));
+    }
+    for (int64_t i = 0; i < k; ++i) layers_.push_back(h_layers_[i]);
+    if (trace_)
+      fprintf(stderr, "[lbfs] k_bfs launch L%lld..L%lld ok (prev_bitmap=%d done=%d)\n", (long long)p.L0,
+              (long long)h_loop_->L_end - 1, h_loop_->prev_bitmap, h_loop_->done);
+    if (h_loop_->done) break;
+    p.do_init = 0;  // more than kLoopCap levels: continue from the saved state
+    p.L0 = h_loop_->L_end;
+    p.prev_bitmap0 = h_loop_->prev_bitmap;
+  }
+  if (mprof) {
+    unsigned long long pr[6 * 64];
+    LBFS_CUDA(cudaMemcpy(pr, mprof_, sizeof(pr), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < layers_.size() && i < 64; ++i) {
+      const unsigned long long* q = pr + 6 * i;
+      fprintf(stderr, "[lbfs] k_bfs L%-3zu %s in=%-9lld snapshot %.1fus expand(b0) %.1fus expand(all) %.1fus "
+              "compact(b0) %.1fus compact(all) %.1fus\n", i, q[5] > q[4] || q[3] != q[2] ? "bitmap" : "queue ",
+              (long long)layers_[i].input, (q[1] - q[0]) * 1e-3, (q[2] - q[1]) * 1e-3, (q[3] - q[1]) * 1e-3,
+              (q[4] - q[3]) * 1e-3, (q[5] - q[3]) * 1e-3);
+    }
+  }
+  if (trace_)
+    for (size_t i = 0; i < layers_.size(); ++i)
+      fprintf(stderr, "[lbfs] L%-3zu k_bfs in=%-9lld edges=%-10lld disc=%lld\n", i, (long long)layers_[i].input,
+              (long long)layers_[i].edges, (long long)layers_[i].discovered);
+  if (t) {
+    float total = 0.f;
+    LBFS_CUDA(cudaEventElapsedTime(&total, ev_[0], ev_[4]));
+    t->bfs_ms = total;
+    t->init_ms = 0.0;
+    t->expand_ms = total;  // one kernel: expansion, compaction, init and outputs
+    t->d2h_ms = 0.0;
+    t->levels = (int64_t)layers_.size();
+    t->kernel_launches = g_launches.load() - launches0;
+    int64_t e = 0, r = 0;
+    for (auto& l : layers_) {
+      e += l.edges;
+      r += l.input;
+    }
+    t->edges = e;
+    t->reached = r;
+  }
 }
 
 void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t) {
   if (root < 0 || root >= n_) throw_inval("root out of range");
   if (nparts_ != 1) throw_inval("partitioned graph: use the lbfs_part_* level steps");
   read_env();
+  if (mega_smem_ > 0 && mega_on_ && !split_ && !count_) {
+    run_mega(root, d_pred, d_level, t);
+    return;
+  }
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = stream_;
   LBFS_CUDA(cudaEventRecord(ev_[0], st));

@@ -156,9 +156,41 @@ constexpr int kLoopThreads = 512;
 constexpr int64_t kLoopCap = 1 << 16;  // layers per k_levels launch
 
 struct LoopState {
-  long long L_end;   // first level not run by the last k_levels launch
+  long long L_end;   // first level not run by the last k_levels / k_bfs launch
   unsigned bar_count;
   unsigned bar_gen;
+  int prev_bitmap;   // k_bfs: mode of level L_end - 1
+  int done;          // k_bfs: search finished (outputs written)
+};
+
+// Whole-BFS persistent kernel (k_bfs) arguments.
+struct BfsArgs {
+  int32_t* q_small[2];
+  int32_t* q_warp[2];
+  CtaItem* q_cta[2];
+  GroupItem* q_items[2];
+  CtaItem* q_wslice[2];
+  Counters* ring;
+  uint32_t* front;
+  const DenseTask* dense;
+  int64_t n_dense;
+  lbfs_layer* layers;  // layers[L - L0]
+  LoopState* state;
+  int64_t L0, max_levels;
+  unsigned long long bitmap_min_edges;
+  int64_t small_region;
+  int32_t dense_off, prev_bitmap0;
+  int32_t hot_words, do_init;
+  int64_t nwords, nwl, n_loc;  // init / compaction extents
+  int32_t root_orig;
+  const int32_t* old2new;
+  int64_t n_compact_blocks;
+  int32_t* d_pred;
+  int32_t* d_level;
+  int64_t n, npad;
+  int32_t aligned;
+  int32_t debug_skip;  // LBFS_MEGA_SKIP (debug): 1 compaction, 2 hub, 4 queues, 8 items, 16 warp slices, 32 dense
+  unsigned long long* prof;  // LBFS_MEGA_PROF: 6 globaltimer stamps of block 0 per level (first 64 levels)
 };
 
 struct LoopArgs {
@@ -281,6 +313,10 @@ class BfsEngine {
   std::vector<lbfs_layer> layers_;
   int expand_grid_ = 0;
   int loop_grid_ = 0;             // k_levels CTAs (0: device loop unavailable)
+  int mega_smem_ = 0;             // k_bfs dynamic shared memory (0: unavailable)
+  unsigned long long* mprof_ = nullptr;  // LBFS_MEGA_PROF stamps
+  bool mega_on_ = false;          // LBFS_MEGA=1: k_bfs instead of the host-driven level loop
+  void run_mega(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t);
   bool loop_off_ = false;         // LBFS_NO_LOOP=1: host-driven queue levels
   bool loop_prof_ = false;        // LBFS_LOOP_PROF=1: time split of k_levels on stderr
   lbfs_layer* d_layers_ = nullptr;

@@ -91,3 +91,42 @@ def test_config_s24_against_oracle(golden):
         if info and str(r) in info["bfs"]:
             assert layers_of(res) == info["bfs"][str(r)]["layers"]
             assert sha(res.levels, "<i4") == info["bfs"][str(r)]["levels_sha"]
+
+
+@pytest.fixture
+def whole_bfs_kernel(monkeypatch):
+    """Run the searches through the single-launch persistent kernel (k_bfs,
+    LBFS_MEGA=1; the library reads the switch at every BFS)."""
+    monkeypatch.setenv("LBFS_MEGA", "1")
+
+
+def test_whole_bfs_kernel_s16_golden(golden, golden_arrays, whole_bfs_kernel):
+    info = golden["S16"]
+    g = build_rmat_graph(RmatParams(scale=16, seed=1))
+    for r, want in info["bfs"].items():
+        res = bfs(g, int(r))
+        assert res.timing["kernel_launches"] == 1
+        assert np.array_equal(res.levels, golden_arrays[f"S16_levels_{r}"].astype(np.int32))
+        assert layers_of(res) == want["layers"]
+        code, where = oracle.check_bfs(g.colstarts, g.rows, int(r), res.predecessors.p, res.levels)
+        assert code == 0, (oracle.CHECK_CODES[code], where)
+
+
+def test_whole_bfs_kernel_s20_and_lattice(golden, whole_bfs_kernel):
+    info = golden["S20"]
+    g = build_rmat_graph(RmatParams(scale=20, seed=1))
+    rp, ci = g.colstarts, g.rows
+    for r in info["roots"][:8]:
+        res = bfs(g, r)
+        want = info["bfs"].get(str(r))
+        if want:
+            assert layers_of(res) == want["layers"]
+            assert sha(res.levels, "<i4") == want["levels_sha"]
+        code, where = oracle.check_bfs(rp, ci, r, res.predecessors.p, res.levels)
+        assert code == 0, (r, oracle.CHECK_CODES[code], where)
+    info = golden["lattice_64x48"]
+    g = build_lattice_graph(64, 48)
+    for r, want in info["bfs"].items():
+        res = bfs(g, int(r))
+        assert layers_of(res) == want["layers"]
+        assert sha(res.levels, "<i4") == want["levels_sha"]
