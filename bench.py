@@ -258,6 +258,8 @@ def run_partitioned(args, rank, world, local):
     # e2e: public driver with the gathered outputs, rank 0 reads pred+level to host
     pred_h = torch.empty(outs[0][0].numel(), dtype=torch.int32, pin_memory=True)
     lvl_h = torch.empty(outs[0][1].numel(), dtype=torch.int32, pin_memory=True)
+    for r in roots[:2]:  # untimed warm-up
+        bfs_partitioned([part], r, ex, bufs=bufs, outputs=outs, gather=True)
     e2e_vals = []
     for r in roots[:args.e2e_roots]:
         dist.barrier()
@@ -303,8 +305,8 @@ def run_partitioned(args, rank, world, local):
                      "kernel": "whole BFS per GPU (SURVEY §8e t_roof(P) formula)",
                      "t_roof_ms": t_roof * 1e3, "t_measured_ms": t_meas * 1e3,
                      "nvlink_bytes_per_gpu": nvl_bytes, "levels": X},
-        "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 8 * args.roots,
-                "d2h_bytes_per_step": (outs[0][0].numel() + n) * 4 * args.roots,
+        "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 8,
+                "d2h_bytes_per_step": (outs[0][0].numel() + n) * 4, "step": "one BFS (harmonic mean over roots)",
                 "api": "distributed.bfs_partitioned(gather=True) + rank-0 D2H", "roots_timed": len(e2e_vals)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -376,7 +378,10 @@ def run_ours(args, rank, world, local):
     alg_bytes = sum(8 * r.traversed_edge_count + 40 * r.timing["reached"] + 8 * n + n // 8 for r in runs)
     bfs_ms = sum(r.timing["bfs_ms"] for r in runs)
 
-    # e2e through the public API with host outputs (D2H inside the call)
+    # e2e through the public API with host outputs (D2H inside the call);
+    # untimed warm-up calls first (they fill the page-locked output pool)
+    for r in roots[:3]:
+        bfs(g, r)
     e2e_vals = []
     for r in roots[:args.e2e_roots]:
         a = time.perf_counter()
@@ -384,7 +389,7 @@ def run_ours(args, rank, world, local):
         dt = time.perf_counter() - a
         e2e_vals.append(res.traversed_edge_count / dt / 1e9 if res.traversed_edge_count else 0.0)
     e2e = hm(e2e_vals)
-    d2h_bytes = (npad + n) * 4 * args.roots
+    d2h_bytes = (npad + n) * 4  # one e2e step = one BFS: pred (pad32) + level to host
     # correctness of the timed configuration (outside the timed region)
     chk = bfs(g, roots[0])
     ok = validate_tree(g, roots[0], chk.predecessors).passed
@@ -427,9 +432,9 @@ def run_ours(args, rank, world, local):
                      "whole_bfs": {"alg_bytes": alg_bytes / len(runs), "ms": bfs_ms / len(runs),
                                    "frac_of_peak": alg_bytes / (bfs_ms * 1e-3) / 1e9 / hbm_gbs,
                                    "frac_of_8TBs": alg_bytes / (bfs_ms * 1e-3) / 8e12}},
-        "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 8 * args.roots,
-                "d2h_bytes_per_step": d2h_bytes, "api": "paper_1604_02844_b200.bfs(g, root), host outputs",
-                "roots_timed": len(e2e_vals)},
+        "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 8,
+                "d2h_bytes_per_step": d2h_bytes, "step": "one bfs(g, root) call (harmonic mean over roots)",
+                "api": "paper_1604_02844_b200.bfs(g, root), host outputs", "roots_timed": len(e2e_vals)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "wall_s_timed": wall,

@@ -8,7 +8,7 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "lts__throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.max.pct_of_peak_sustained_elapsed",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size",
            "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio"]
-SHORT = ["ms", "dram_rd", "dram_wr", "L2hit%", "L1hit%", "warp_eff", "warps%", "L2sect", "L2thr%", "L2max%",
+SHORT = ["ms", "dram_rd", "dram_wr", "L2hit%", "L1hit%", "thr/inst", "warps%", "L2sect", "L2thr%", "L2max%",
          "dram%", "grid", "lsb"]
 
 
