@@ -322,7 +322,7 @@ def run_ours(args, rank, world, local):
     import torch
 
     from paper_1604_02844_b200 import RmatParams, _lib, bfs, bfs_device, build_rmat_graph, pick_roots
-    from paper_1604_02844_b200.validate import validate_tree
+    from paper_1604_02844_b200.validate import validate_tree_device
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -392,7 +392,7 @@ def run_ours(args, rank, world, local):
     d2h_bytes = (npad + n) * 4  # one e2e step = one BFS: pred (pad32) + level to host
     # correctness of the timed configuration (outside the timed region)
     chk = bfs(g, roots[0])
-    ok = validate_tree(g, roots[0], chk.predecessors).passed
+    ok = validate_tree_device(g, roots[0], chk.predecessors).passed
 
     value, ms_step = value_local, ms_step_local
     if world > 1:

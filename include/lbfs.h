@@ -142,6 +142,15 @@ int lbfs_bfs_device(lbfs_graph* g, int64_t root, int32_t* d_pred, int32_t* d_lev
 /* Layers of the most recent BFS on this handle. */
 int lbfs_graph_last_layers(const lbfs_graph* g, lbfs_layer* out, int64_t cap, int64_t* n_layers);
 
+/* ---- tree validation (replaces validate_tree, validate.py:50-155) ------
+ * The reference's five checks on a parent array in original ids (n int32;
+ * SENTINEL = unreached), with its report semantics: report[0..4] = passed
+ * flags of root_self_parent, reachability_closure, tree_edge_existence,
+ * level_consistency, cycle_freedom; report[5..9] = the first offender of
+ * each (the reference's details), -1 when passed. Unpartitioned handles. */
+int lbfs_validate_tree(lbfs_graph* g, int64_t root, const int32_t* pred, int64_t report[10]);
+int lbfs_validate_tree_device(lbfs_graph* g, int64_t root, const int32_t* d_pred, int64_t report[10]);
+
 /* ---- partitioned BFS (multi-GPU) --------------------------
  * One process per GPU; rank g of P (a power of two) owns the internal ids of
  * bitmap words w with w % P == g and their rows. The level loop

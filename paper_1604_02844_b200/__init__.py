@@ -41,7 +41,14 @@ from .traversal import (
     bfs_device,
     run_bfs,
 )
-from .validate import Certificate, ValidationReport, bfs_certificate, levels_from_parents, validate_tree
+from .validate import (
+    Certificate,
+    ValidationReport,
+    bfs_certificate,
+    levels_from_parents,
+    validate_tree,
+    validate_tree_device,
+)
 
 __all__ = [
     "MAX_SCALE", "CsrGraph", "EdgeList", "RmatParams", "build_csr", "build_lattice_graph",
@@ -49,7 +56,7 @@ __all__ = [
     "read_edge_list", "write_edge_list", "ExperimentConfig", "RootRun", "RunStats", "emit_results",
     "harmonic_mean_teps", "pick_roots", "run_experiment", "MODES", "SENTINEL", "BfsResult",
     "LayerPolicy", "LayerStats", "PredecessorArray", "bfs", "bfs_device", "run_bfs", "Certificate",
-    "ValidationReport", "bfs_certificate", "levels_from_parents", "validate_tree",
+    "ValidationReport", "bfs_certificate", "levels_from_parents", "validate_tree", "validate_tree_device",
 ]
 
 __version__ = "0.1.0"

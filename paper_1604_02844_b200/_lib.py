@@ -74,6 +74,8 @@ SIGNATURES = {
                                        ctypes.POINTER(_i64), ctypes.POINTER(Timing)]),
     "lbfs_graph_last_layers": (ctypes.c_int, [_p, ctypes.POINTER(Layer), _i64, ctypes.POINTER(_i64)]),
     "lbfs_set_device": (ctypes.c_int, [ctypes.c_int]),
+    "lbfs_validate_tree": (ctypes.c_int, [_p, _i64, _p, _p]),
+    "lbfs_validate_tree_device": (ctypes.c_int, [_p, _i64, _p, _p]),
     "lbfs_part_create": (ctypes.c_int, [_i64, _p, _p, _i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_p)]),
     "lbfs_part_create_from_csr": (ctypes.c_int, [_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_p)]),
     "lbfs_part_info": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),

@@ -395,6 +395,36 @@ int lbfs_graph_last_layers(const lbfs_graph* g, lbfs_layer* out, int64_t cap, in
 }
 
 
+/* ---- tree validation on the device ------------------------------------ */
+
+int lbfs_validate_tree_device(lbfs_graph* g, int64_t root, const int32_t* d_pred, int64_t report[10]) {
+  return guarded([&] {
+    if (!g || !d_pred || !report) throw_inval("bad arguments");
+    BfsEngine& e = *g->eng;
+    std::lock_guard<std::mutex> lk(e.mu);
+    LBFS_CUDA(cudaSetDevice(e.device()));
+    e.validate_tree(root, d_pred, report);
+  });
+}
+
+int lbfs_validate_tree(lbfs_graph* g, int64_t root, const int32_t* pred, int64_t report[10]) {
+  return guarded([&] {
+    if (!g || !pred || !report) throw_inval("bad arguments");
+    BfsEngine& e = *g->eng;
+    std::lock_guard<std::mutex> lk(e.mu);
+    LBFS_CUDA(cudaSetDevice(e.device()));
+    int32_t* d = dev_alloc<int32_t>((size_t)std::max<int64_t>(e.n(), 1));
+    try {
+      LBFS_CUDA(cudaMemcpy(d, pred, sizeof(int32_t) * (size_t)e.n(), cudaMemcpyHostToDevice));
+      e.validate_tree(root, d, report);
+    } catch (...) {
+      dev_free(d);
+      throw;
+    }
+    dev_free(d);
+  });
+}
+
 /* ---- partitioned (multi-GPU) BFS: one partition per process ----------- */
 
 static BfsEngine& part_engine(lbfs_graph* g) {

@@ -240,6 +240,9 @@ class BfsEngine {
   int64_t n_local() const { return n_loc_; }
   int64_t nnz_local() const { return nnz_loc_; }
   unsigned long long resolve_scanned() const;
+  // validate_tree (validate.py:50-155) on a device parent array in original
+  // ids: out[0..4] passed flags, out[5..9] details (-1 when passed)
+  void validate_tree(int64_t root, const int32_t* d_pred, int64_t out[10]);
   int64_t n() const { return n_; }
   int64_t nnz() const { return nnz_; }
   int64_t npad() const { return npad_; }

@@ -177,6 +177,34 @@ def validate_tree(g, s: int, pred) -> ValidationReport:
     return ValidationReport(ok_root, ok_closure, ok_edges, ok_levels, ok_acyclic, details)
 
 
+def validate_tree_device(g, s: int, pred) -> ValidationReport:
+    """``validate_tree`` on the GPU (csrc/validate.cu): the same five checks
+    and first offenders; the parent array goes to the device once and the
+    memoised chases become pointer jumping. ``g`` is any graph ``bfs``
+    accepts; ``pred`` a PredecessorArray, an int array of n entries, or a
+    device tensor (anything with ``data_ptr()`` on the graph's device)."""
+    import ctypes
+
+    from . import _lib
+    from .traversal import _handle
+
+    n = g.num_vertices
+    assert 0 <= s < n
+    h = _handle(g)
+    rep = (ctypes.c_int64 * 10)()
+    lib = _lib.load()
+    if hasattr(pred, "data_ptr") and getattr(pred, "is_cuda", False):
+        assert pred.numel() >= n
+        _lib.check(lib.lbfs_validate_tree_device(h, int(s), pred.data_ptr(), rep))
+    else:
+        p = np.ascontiguousarray(_parent_array(pred)[:n], dtype=np.int32)
+        assert len(p) == n
+        _lib.check(lib.lbfs_validate_tree(h, int(s), _lib.ptr(p), rep))
+    flags = [bool(rep[k]) for k in range(5)]
+    details = {name: int(rep[5 + k]) for k, name in enumerate(ValidationReport.CHECKS) if not flags[k]}
+    return ValidationReport(*flags, details)
+
+
 def levels_from_parents(p, s: int) -> np.ndarray:
     """Per-vertex level implied by a parent array, -1 where undefined
     (validate.py:158-177): the length of v's parent chain to a self-parented
