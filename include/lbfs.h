@@ -160,14 +160,14 @@ int lbfs_validate_tree_device(lbfs_graph* g, int64_t root, const int32_t* d_pred
  * torch.distributed/NCCL). Per level, with W = nwords / P:
  *   lbfs_part_expand                      owned frontier -> visited / marks
  *   lbfs_part_pack(send[P*W])             marks by owner       -> all_to_all(send, recv)
- *   lbfs_part_merge(recv[P*W], fsend[W], red[2])
- *                                         remote discoveries + parents, next
- *                                         frontier              -> all_gather(fsend, fgath[P*W]),
- *                                                                  all_reduce_sum(red)
- *   lbfs_part_sync(fgath)                 replicated frontier / visited
- *   lbfs_part_level_done(red)             layer + termination (host sync)
+ *   lbfs_part_merge(recv[P*W], fsend[W+4]) remote discoveries + parents, next
+ *                                         frontier: W owned words + this
+ *                                         rank's counts (2 x u64) -> all_gather(fsend, fgath[P*(W+4)])
+ *   lbfs_part_sync(fgath)                 replicated frontier / visited,
+ *                                         counts summed on the device
+ *   lbfs_part_level_done(NULL)            layer + termination (host sync)
  * lbfs_part_start(root, red) is followed by all_reduce_sum(red) and one
- * lbfs_part_level_done (which emits no layer). Buffers are device pointers
+ * lbfs_part_level_done(red) (which emits no layer). Buffers are device pointers
  * on the partition's device; `stream` is the caller's cudaStream_t, used as
  * given (NULL = the legacy default stream), so the steps are ordered with the
  * collectives the caller issues on the same stream. */
@@ -179,8 +179,9 @@ int lbfs_part_info(const lbfs_graph* g, int* rank, int* nparts, int64_t* nwords,
 int lbfs_part_start(lbfs_graph* g, int64_t root, uint64_t* red, void* stream);
 int lbfs_part_expand(lbfs_graph* g, void* stream);
 int lbfs_part_pack(lbfs_graph* g, uint32_t* send, void* stream);
-int lbfs_part_merge(lbfs_graph* g, const uint32_t* recv, uint32_t* fsend, uint64_t* red, void* stream);
+int lbfs_part_merge(lbfs_graph* g, const uint32_t* recv, uint32_t* fsend, void* stream);
 int lbfs_part_sync(lbfs_graph* g, const uint32_t* fgath, void* stream);
+/* red_global: the summed start counts after lbfs_part_start; NULL after a level */
 int lbfs_part_level_done(lbfs_graph* g, const uint64_t* red_global, lbfs_layer* layer, int* done);
 /* Owned vertices' pred (pad32(n)) / level (n) in original ids; every other
  * entry is LBFS_SENTINEL / -1, so the ranks' outputs combine by min / max. */

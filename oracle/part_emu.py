@@ -60,7 +60,7 @@ class EmuPart:
     def new_buffers(self) -> dict:
         W, P = self.words_per_peer, self.nparts
         return {"send": torch.zeros(P * W, dtype=torch.int32), "recv": torch.zeros(P * W, dtype=torch.int32),
-                "fsend": torch.zeros(W, dtype=torch.int32), "fgath": torch.zeros(P * W, dtype=torch.int32),
+                "fsend": torch.zeros(W + 4, dtype=torch.int32), "fgath": torch.zeros(P * (W + 4), dtype=torch.int32),
                 "red": torch.zeros(2, dtype=torch.int64)}
 
     def new_outputs(self):
@@ -108,7 +108,7 @@ class EmuPart:
         ids = np.arange(self.nbits)
         return (ids >> 5) % self.nparts == self.rank
 
-    def merge(self, recv, fsend, red) -> None:
+    def merge(self, recv, fsend) -> None:
         W = self.words_per_peer
         rv = recv.numpy().view("<u4")
         inc_w = np.zeros(W, dtype="<u4")
@@ -132,20 +132,21 @@ class EmuPart:
         self.level[new] = self.L + 1
         self.frontier = list(np.nonzero(new)[0])
         fs = _words(new)[np.arange(W) * self.nparts + self.rank]
-        fsend.copy_(torch.from_numpy(fs.view(np.int32)))
-        red.copy_(torch.tensor((len(self.frontier), int(self.deg[new[:self.num_vertices]].sum())),
-                               dtype=torch.int64))
+        counts = np.array([len(self.frontier), int(self.deg[new[:self.num_vertices]].sum())], dtype="<u8")
+        fsend.copy_(torch.from_numpy(np.concatenate([fs, counts.view("<u4")]).view(np.int32)))
 
     def sync(self, fgath) -> None:
-        g = fgath.numpy().view("<u4")
-        words = g[self.slot]
+        W, P = self.words_per_peer, self.nparts
+        g = fgath.numpy().view("<u4").reshape(P, W + 4)
+        self.summed = tuple(int(x) for x in g[:, W:].copy().view("<u8").sum(axis=0))
+        words = g[:, :W].reshape(-1)[self.slot]
         self.F = _bits(words)
         self.visited |= self.F
         self.prev = self.visited.copy()
 
-    def level_done(self, red):
+    def level_done(self, red=None):
         from paper_1604_02844_b200.traversal import LayerStats
-        disc, edges = (int(x) for x in red.tolist())
+        disc, edges = (int(x) for x in red.tolist()) if red is not None else self.summed
         if self.L < 0:
             self.L = 0
             self.cur = (disc, edges)

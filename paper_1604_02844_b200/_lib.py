@@ -83,7 +83,7 @@ SIGNATURES = {
     "lbfs_part_start": (ctypes.c_int, [_p, _i64, _p, _p]),
     "lbfs_part_expand": (ctypes.c_int, [_p, _p]),
     "lbfs_part_pack": (ctypes.c_int, [_p, _p, _p]),
-    "lbfs_part_merge": (ctypes.c_int, [_p, _p, _p, _p, _p]),
+    "lbfs_part_merge": (ctypes.c_int, [_p, _p, _p, _p]),
     "lbfs_part_sync": (ctypes.c_int, [_p, _p, _p]),
     "lbfs_part_level_done": (ctypes.c_int, [_p, _p, ctypes.POINTER(Layer), ctypes.POINTER(ctypes.c_int)]),
     "lbfs_part_finish": (ctypes.c_int, [_p, _p, _p, _p]),

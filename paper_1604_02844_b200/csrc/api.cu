@@ -524,12 +524,12 @@ int lbfs_part_pack(lbfs_graph* g, uint32_t* send, void* stream) {
   });
 }
 
-int lbfs_part_merge(lbfs_graph* g, const uint32_t* recv, uint32_t* fsend, uint64_t* red, void* stream) {
+int lbfs_part_merge(lbfs_graph* g, const uint32_t* recv, uint32_t* fsend, void* stream) {
   return guarded([&] {
     BfsEngine& e = part_engine(g);
-    if (!recv || !fsend || !red) throw_inval("NULL buffer");
+    if (!recv || !fsend) throw_inval("NULL buffer");
     std::lock_guard<std::mutex> lk(e.mu);
-    e.part_merge(recv, fsend, (unsigned long long*)red, as_stream(g, stream));
+    e.part_merge(recv, fsend, as_stream(g, stream));
   });
 }
 
@@ -545,7 +545,6 @@ int lbfs_part_sync(lbfs_graph* g, const uint32_t* fgath, void* stream) {
 int lbfs_part_level_done(lbfs_graph* g, const uint64_t* red_global, lbfs_layer* layer, int* done) {
   return guarded([&] {
     BfsEngine& e = part_engine(g);
-    if (!red_global) throw_inval("red_global is NULL");
     std::lock_guard<std::mutex> lk(e.mu);
     e.part_level_done((const unsigned long long*)red_global, layer, done);
   });

@@ -1751,6 +1751,7 @@ BfsEngine::~BfsEngine() {
   dev_free(new2old_);
   dev_free(fglob_);
   if (h_red_) cudaFreeHost(h_red_);
+  dev_free(red_dev_);
   dev_free(resolve_cnt_);
   dev_free(old2new_);
   cudaStreamDestroy(stream_);

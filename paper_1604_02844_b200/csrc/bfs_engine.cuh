@@ -230,7 +230,7 @@ class BfsEngine {
   void part_start(int64_t root, cudaStream_t st, unsigned long long* red);
   void part_expand(cudaStream_t st);
   void part_pack(uint32_t* send, cudaStream_t st);
-  void part_merge(const uint32_t* recv, uint32_t* fsend, unsigned long long* red, cudaStream_t st);
+  void part_merge(const uint32_t* recv, uint32_t* fsend, cudaStream_t st);
   void part_sync(const uint32_t* fgath, cudaStream_t st);
   void part_level_done(const unsigned long long* red_global, lbfs_layer* layer, int* done);
   void part_finish(int32_t* d_pred, int32_t* d_level, cudaStream_t st);
@@ -279,6 +279,7 @@ class BfsEngine {
   cudaStream_t part_st_ = nullptr;
   unsigned long long part_in_ = 0, part_edges_ = 0;  // global counts of the current frontier
   unsigned long long* h_red_ = nullptr;              // pinned: global (discovered, edges)
+  unsigned long long* red_dev_ = nullptr;            // summed counts of the gathered slices
   int64_t* row_ptr_ = nullptr;   // internal CSR
   int32_t* col_idx_ = nullptr;
   int32_t* new2old_ = nullptr;

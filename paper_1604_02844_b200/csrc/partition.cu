@@ -16,9 +16,10 @@
 //            neighbour of v in the replicated frontier F_L (v's row is local
 //            and the graph symmetric, so one exists and lies one level up),
 //            then k_compact over the owned words -> next frontier bins, levels,
-//            the owned words of F_{L+1} and the local counts
-//                                                -> all_gather, all_reduce
-//   sync     F_{L+1} in global word order; visited |= F_{L+1}; prev = visited
+//            the owned words of F_{L+1}, followed by the local counts
+//            (4 words)                                   -> all_gather
+//   sync     F_{L+1} in global word order; visited |= F_{L+1}; prev = visited;
+//            the gathered counts summed on the device
 //   done     host reads the summed counts: the layer (input, edges,
 //            discovered) and termination, identical on every rank
 // The level structure is the reference's level-synchronous loop
@@ -81,20 +82,35 @@ __global__ void k_part_merge(const uint32_t* __restrict__ recv, int64_t nwl, int
   if (lane == 0 && cnt) atomicAdd(scanned, cnt);
 }
 
-// local counts of the next frontier -> red (cross-rank sum input)
-__global__ void k_part_counts(const Counters* __restrict__ c, unsigned long long* __restrict__ red) {
-  red[0] = c->discovered;
-  red[1] = c->edges;
+// local counts of the next frontier -> the 4 words after the frontier words
+// of the all-gather slice (two little-endian 64-bit values)
+__global__ void k_part_counts(const Counters* __restrict__ c, uint32_t* __restrict__ tail) {
+  tail[0] = (uint32_t)c->discovered;
+  tail[1] = (uint32_t)(c->discovered >> 32);
+  tail[2] = (uint32_t)c->edges;
+  tail[3] = (uint32_t)(c->edges >> 32);
+}
+// sum of the P gathered count tails -> red
+__global__ void k_part_sum(const uint32_t* __restrict__ fgath, int nparts, int64_t stride, int64_t nwl,
+                           unsigned long long* __restrict__ red) {
+  unsigned long long d = 0, e = 0;
+  for (int p = 0; p < nparts; ++p) {
+    const uint32_t* t = fgath + p * stride + nwl;
+    d += (unsigned long long)t[0] | ((unsigned long long)t[1] << 32);
+    e += (unsigned long long)t[2] | ((unsigned long long)t[3] << 32);
+  }
+  red[0] = d;
+  red[1] = e;
 }
 
-// fgath[h*nwl + j] = rank h's owned word j of F_{L+1}
+// fgath[h*stride + j] = rank h's owned word j of F_{L+1} (stride = nwl + 4)
 __global__ void k_part_sync(const uint32_t* __restrict__ fgath, uint32_t* __restrict__ fglob,
-                            uint32_t* __restrict__ visited, uint32_t* __restrict__ prev, int64_t nwords, int64_t nwl,
+                            uint32_t* __restrict__ visited, uint32_t* __restrict__ prev, int64_t nwords, int64_t stride,
                             int part_log) {
   const int64_t mask = (1 << part_log) - 1;
   for (int64_t gw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gw < nwords;
        gw += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t f = fgath[(gw & mask) * nwl + (gw >> part_log)];
+    const uint32_t f = fgath[(gw & mask) * stride + (gw >> part_log)];
     fglob[gw] = f;
     const uint32_t v = visited[gw] | f;
     visited[gw] = v;
@@ -168,22 +184,24 @@ void BfsEngine::part_pack(uint32_t* send, cudaStream_t st) {
               part_rank_);
 }
 
-void BfsEngine::part_merge(const uint32_t* recv, uint32_t* fsend, unsigned long long* red, cudaStream_t st) {
+void BfsEngine::part_merge(const uint32_t* recv, uint32_t* fsend, cudaStream_t st) {
   part_st_ = st;
   const int64_t L = part_L_;
   if (nparts_ > 1)
     LBFS_LAUNCH(k_part_merge, grid_for(nwl_ * 32, sm_count_), 256, 0, st, recv, nwl_, part_log_, part_rank_,
                 visited_, fglob_, row_ptr_, col_idx_, new2old_, pred_int_, resolve_cnt_);
   compact_level(part_cur_, L, fsend, st);
-  LBFS_LAUNCH(k_part_counts, 1, 1, 0, st, &cnt_[(L + 1) % kCounterRing], red);
+  LBFS_LAUNCH(k_part_counts, 1, 1, 0, st, &cnt_[(L + 1) % kCounterRing], fsend + nwl_);
 }
 
 void BfsEngine::part_sync(const uint32_t* fgath, cudaStream_t st) {
   part_st_ = st;
+  if (!red_dev_) red_dev_ = dev_alloc<unsigned long long>(2);
   // (one partition: visited and prev are already complete after k_compact)
   if (nparts_ > 1)
-    LBFS_LAUNCH(k_part_sync, grid_for(nwords_, sm_count_), 256, 0, st, fgath, fglob_, visited_, prev_, nwords_, nwl_,
-                part_log_);
+    LBFS_LAUNCH(k_part_sync, grid_for(nwords_, sm_count_), 256, 0, st, fgath, fglob_, visited_, prev_, nwords_,
+                nwl_ + 4, part_log_);
+  LBFS_LAUNCH(k_part_sum, 1, 1, 0, st, fgath, nparts_, nwl_ + 4, nwl_, red_dev_);
 }
 
 void BfsEngine::part_level_done(const unsigned long long* red_global, lbfs_layer* layer, int* done) {
@@ -191,6 +209,10 @@ void BfsEngine::part_level_done(const unsigned long long* red_global, lbfs_layer
   const int64_t L = part_L_;
   const int slot = (int)((L + 1) % kCounterRing);
   if (L >= 0) LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[slot], &cnt_[slot], sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  if (!red_global) {  // a level: the counts part_sync summed from the gathered slices
+    if (L < 0) throw_inval("part_level_done: the start needs the summed root counts");
+    red_global = red_dev_;
+  }
   LBFS_CUDA(cudaMemcpyAsync(h_red_, red_global, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   LBFS_CUDA(cudaStreamSynchronize(st));
   const unsigned long long disc = h_red_[0], edges = h_red_[1];

@@ -4,14 +4,15 @@ B200s of one box, and each level exchanges the frontier bitmap").
 
 The partition and the per-level kernels live in liblbfs (csrc/partition.cu,
 C ABI ``lbfs_part_*`` in include/lbfs.h); this module is the level loop,
-which interleaves them with three collectives per level:
+which interleaves them with the collectives between the steps:
 
     expand -> pack -> all_to_all(marks by owner) -> merge (+ compaction)
-           -> all_gather(owned words of F_{L+1}) + all_reduce(counts)
-           -> sync -> level_done (layer, termination)
+           -> all_gather(owned words of F_{L+1} + the rank's counts)
+           -> sync (counts summed on the device) -> level_done
 
 This is the reference's level-synchronous loop (traversal.py:90, 152, 366)
-with the frontier exchanged between levels. Collectives go through an
+with the frontier exchanged between levels (two collectives per level; one
+all-reduce at the start for the root's degree). Collectives go through an
 *exchange* object:
 
 * ``TorchExchange`` — torch.distributed (NCCL between GPUs; gloo on CPU for
@@ -97,7 +98,7 @@ class PartitionedGraph:
         W, P = self.words_per_peer, self.nparts
         i32 = dict(dtype=torch.int32, device=self.device)
         return {"send": torch.empty(P * W, **i32), "recv": torch.empty(P * W, **i32),
-                "fsend": torch.empty(W, **i32), "fgath": torch.empty(P * W, **i32),
+                "fsend": torch.empty(W + 4, **i32), "fgath": torch.empty(P * (W + 4), **i32),
                 "red": torch.zeros(2, dtype=torch.int64, device=self.device)}
 
     def new_outputs(self):
@@ -118,16 +119,17 @@ class PartitionedGraph:
     def pack(self, send) -> None:
         _lib.check(_lib.load().lbfs_part_pack(self._h, send.data_ptr(), _stream_ptr(send)))
 
-    def merge(self, recv, fsend, red) -> None:
-        _lib.check(_lib.load().lbfs_part_merge(self._h, recv.data_ptr(), fsend.data_ptr(), red.data_ptr(),
-                                                _stream_ptr(red)))
+    def merge(self, recv, fsend) -> None:
+        _lib.check(_lib.load().lbfs_part_merge(self._h, recv.data_ptr(), fsend.data_ptr(), _stream_ptr(fsend)))
 
     def sync(self, fgath) -> None:
         _lib.check(_lib.load().lbfs_part_sync(self._h, fgath.data_ptr(), _stream_ptr(fgath)))
 
-    def level_done(self, red) -> tuple[LayerStats | None, bool]:
+    def level_done(self, red=None) -> tuple[LayerStats | None, bool]:
+        """red: the summed start counts (after start); None after a level."""
         ly, done = _lib.Layer(), ctypes.c_int()
-        _lib.check(_lib.load().lbfs_part_level_done(self._h, red.data_ptr(), ctypes.byref(ly), ctypes.byref(done)))
+        _lib.check(_lib.load().lbfs_part_level_done(self._h, red.data_ptr() if red is not None else None,
+                                                     ctypes.byref(ly), ctypes.byref(done)))
         return LayerStats(int(ly.input), int(ly.edges), int(ly.discovered)), bool(done.value)
 
     def finish(self, pred, level) -> None:
@@ -143,7 +145,7 @@ class PartitionedGraph:
 
 # ------------------------------------------------------------------ exchanges
 class TorchExchange:
-    """The three collectives over torch.distributed: NCCL for CUDA tensors
+    """The collectives over torch.distributed: NCCL for CUDA tensors
     (one partition per process), gloo for CPU tensors. Lists hold this
     process's single partition's buffers."""
 
@@ -239,12 +241,11 @@ def bfs_partitioned(parts: list, root: int, exchange, bufs: list | None = None, 
             p.pack(b["send"])
         exchange.all_to_all([b["send"] for b in bufs], [b["recv"] for b in bufs])
         for p, b in zip(parts, bufs):
-            p.merge(b["recv"], b["fsend"], b["red"])
+            p.merge(b["recv"], b["fsend"])
         exchange.all_gather([b["fsend"] for b in bufs], [b["fgath"] for b in bufs])
-        exchange.all_reduce_sum(reds)
         for p, b in zip(parts, bufs):
             p.sync(b["fgath"])
-        outs = [p.level_done(b["red"]) for p, b in zip(parts, bufs)]
+        outs = [p.level_done() for p in parts]
         layer, done = outs[0]
         assert all(o == outs[0] for o in outs), "partitions disagree on the layer"
         layers.append(layer)
