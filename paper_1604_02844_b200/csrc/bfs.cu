@@ -52,7 +52,11 @@ namespace lbfs {
 constexpr unsigned kFull = 0xFFFFFFFFu;
 // kQueueDirect: queue mode without the visited pre-probe (k_levels: small
 // frontiers, where the probe's round trip costs more than extra atomics)
-enum Mode : int { kBitmapOut = 0, kQueueOut = 1, kQueueDirect = 2 };
+// kHeavy: bitmap mode for the heavy levels (most of the graph's edges in one
+// level): targets in the hot prefix are OR'ed blindly into the CTA's zeroed
+// shared copy (no probe, no parent; k_merge_hot folds the copies into the
+// visited bitmap and k_compact resolves their parents), the rest as kBitmapOut.
+enum Mode : int { kBitmapOut = 0, kQueueOut = 1, kQueueDirect = 2, kHeavy = 3 };
 
 // ---------------------------------------------------------------- memory ops
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
@@ -282,6 +286,38 @@ __device__ __forceinline__ uint32_t probe_mask(const LevelArgs& a, const Hot& h,
                                                uint32_t okmask) {
   if constexpr (M == kQueueDirect) return okmask;
   uint32_t cmask = 0;
+  if constexpr (M == kHeavy) {
+    // hot: one red.shared.or, nothing waits on it; cold: the probe of kBitmapOut
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t bit = 1u << (nb[k] & 31);
+      const uint32_t sa = h.base + 4u * (uint32_t)(nb[k] >> 5);
+      const bool ok = (okmask >> k) & 1u;
+      if constexpr (W == kAllHot) {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(sa),
+                     "r"(bit), "r"((uint32_t)ok)
+                     : "memory");
+      } else if constexpr (W == kAllCold) {
+        const uint32_t w = __ldcg(a.visited + (nb[k] >> 5));
+        cmask |= ((~w >> (nb[k] & 31)) & 1u) << k;
+      } else {
+        uint32_t w;
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.lt.s32 p, %1, %2;\n\t"
+            "setp.ne.u32 q, %6, 0;\n\t"
+            "and.pred q, q, p;\n\t"
+            "mov.u32 %0, 0xFFFFFFFF;\n\t"
+            "@q red.shared.or.b32 [%3], %5;\n\t"
+            "@!p ld.global.cg.u32 %0, [%4];\n\t}"
+            : "=r"(w)
+            : "r"(nb[k] >> 5), "r"(h.words), "r"(sa), "l"(a.visited + (nb[k] >> 5)), "r"(bit), "r"((uint32_t)ok)
+            : "memory");
+        cmask |= ((~w >> (nb[k] & 31)) & 1u) << k;
+      }
+    }
+    return cmask & okmask;
+  }
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     uint32_t w;
@@ -304,7 +340,7 @@ __device__ __forceinline__ uint32_t probe_mask(const LevelArgs& a, const Hot& h,
 template <int M, int K, typename ParFn>
 __device__ __forceinline__ void settle(const LevelArgs& a, const Hot& h, const int32_t (&nb)[K], uint32_t cmask,
                                        ParFn par, int lane, Acc& acc) {
-  if constexpr (M == kBitmapOut) {
+  if constexpr (M == kBitmapOut || M == kHeavy) {
     if (cmask) settle_bitmap<K>(a, h, nb, cmask, par);
   } else {
     settle_queue<K>(a, nb, cmask, par, lane, acc);
@@ -319,7 +355,7 @@ __device__ __forceinline__ void probe_batch(const LevelArgs& a, const Hot& h, co
 
 template <int M>
 __device__ __forceinline__ void flush_acc(const LevelArgs& a, Acc& acc) {
-  if constexpr (M != kBitmapOut) {
+  if constexpr (M == kQueueOut || M == kQueueDirect) {
     unsigned long long d = acc.disc, e = acc.edges;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -633,7 +669,7 @@ __device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier
   WarpScratch& ws = s.ws[wib];
   const int32_t* s_T = s.T;
   const int64_t* s_B = s.B;
-  const int refresh_every = h.words > 0 ? a.refresh_chunks : 0;
+  const int refresh_every = (h.words > 0 && M != kHeavy) ? a.refresh_chunks : 0;
   auto& s_bar = s.bar;
   auto& s_meta = s.meta;
 
@@ -878,12 +914,52 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
   __shared__ ExpandSmem s;
   expand_init(s, a);
   const Hot h{reinterpret_cast<uint32_t*>(s_dyn + kRingBytes), smem_u32(s_dyn + kRingBytes), hot_words};
-  hot_load(s, h, a.visited);
+  uint4* h4 = reinterpret_cast<uint4*>(h.s);
+  const int hw4 = hot_words >> 2;  // hot_words is a multiple of 4
+  if constexpr (M == kHeavy) {
+    for (int i = threadIdx.x; i < hw4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+  } else {
+    hot_load(s, h, a.visited);
+  }
   uint32_t par_bits = 0;
   Acc acc;
   expand_phases<M, kPhases>(a, f, s, s_dyn, h, par_bits, acc);
   flush_acc<M>(a, acc);
   hot_drain(s);
+  if constexpr (M == kHeavy) {  // this CTA's blind ORs -> its stage row
+    uint4* row = reinterpret_cast<uint4*>(a.stage) + (size_t)blockIdx.x * hw4;
+    for (int i = threadIdx.x; i < hw4; i += blockDim.x) {
+      uint4 x = h4[i];
+      if (!a.stage_first) {
+        const uint4 y = __ldcg(row + i);
+        x.x |= y.x, x.y |= y.y, x.z |= y.z, x.w |= y.w;
+      }
+      __stcg(row + i, x);
+    }
+  }
+}
+
+// Heavy levels: visited |= OR of the CTAs' stage rows over the hot prefix.
+// grid (ceil(hw4 / 256), ceil(rows / kMergeRows)): a thread ORs kMergeRows
+// rows of one 16-byte column and folds the result in with red.or.
+constexpr int kMergeRows = 16;
+__global__ void __launch_bounds__(256) k_merge_hot(const uint4* __restrict__ stage, int rows, int hw4,
+                                                   uint32_t* __restrict__ visited) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= hw4) return;
+  const int r0 = blockIdx.y * kMergeRows, r1 = min(rows, r0 + kMergeRows);
+  uint4 x = make_uint4(0, 0, 0, 0);
+#pragma unroll 8
+  for (int r = r0; r < r1; ++r) {
+    const uint4 y = __ldcg(stage + (size_t)r * hw4 + i);
+    x.x |= y.x, x.y |= y.y, x.z |= y.z, x.w |= y.w;
+  }
+  uint32_t* w = visited + 4 * (size_t)i;
+  if (x.x) red_or(w + 0, x.x);
+  if (x.y) red_or(w + 1, x.y);
+  if (x.z) red_or(w + 2, x.z);
+  if (x.w) red_or(w + 3, x.w);
 }
 
 // ---------------------------------------------------------------- K5 on the device
@@ -1156,6 +1232,48 @@ __device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk,
         s_deg[r] = deg;
       }
       if (v < c.t_cta) atomicAdd(&s_hitems[wl], (deg + kChunk - 1) / kChunk);
+    }
+  }
+  if (c.resolve_verts > v0) {
+    // heavy level: the new hot vertices were discovered by blind ORs with no
+    // parent; take the first neighbour one level up (rows are sorted by
+    // internal id, i.e. by descending degree: the first entry is usually it).
+    // Any such neighbour is a valid parent (traversal.py:145-147).
+#pragma unroll 1
+    for (int j0 = 0; j0 < kCompactSteps; j0 += 8) {
+      int32_t u[8], lv[8];
+      bool need[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {  // first neighbour (precomputed per row: coalesced)
+        const int wl = (t >> 5) + (j0 + q) * (kCompactThreads / 32);
+        const int64_t v = v0 + t + (j0 + q) * kCompactThreads;
+        need[q] = v < c.resolve_verts && ((s_new[wl] >> b) & 1u);
+        u[q] = need[q] ? __ldg(c.first_nbr + v) : 0;
+      }
+#pragma unroll
+      // through L1: most first neighbours are a few hubs (an L2 hot spot otherwise);
+      // frontier entries (level cur_level) were written by an earlier launch, and a
+      // stale copy of an entry written now reads -1, never cur_level
+      for (int q = 0; q < 8; ++q) lv[q] = need[q] ? __ldg(c.level_int + u[q]) : -1;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (!need[q]) continue;
+        const int64_t v = v0 + t + (j0 + q) * kCompactThreads;
+        int32_t par = kSentinel;
+        if (lv[q] == c.cur_level) {
+          par = __ldg(c.new2old + u[q]);
+        } else {  // rare: scan the rest of the row
+          const int64_t p = __ldg(c.row_ptr + v), e = __ldg(c.row_ptr + v + 1);
+          for (int64_t k = p + 1; k < e; ++k) {
+            const int32_t x = __ldg(c.col_idx + k);
+            if (__ldg(c.level_int + x) == c.cur_level) {
+              par = __ldg(c.new2old + x);
+              break;
+            }
+          }
+        }
+        c.pred_int[v] = par;
+      }
     }
   }
   gsync(bar);
@@ -1671,7 +1789,11 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
                            (const void*)k_expand<kBitmapOut, 64>, (const void*)k_expand<kQueueOut, 1>,
                            (const void*)k_expand<kQueueOut, 2>,   (const void*)k_expand<kQueueOut, 4>,
                            (const void*)k_expand<kQueueOut, 8>,   (const void*)k_expand<kQueueOut, 16>,
-                           (const void*)k_expand<kQueueOut, 32>,  (const void*)k_expand<kQueueOut, 64>};
+                           (const void*)k_expand<kQueueOut, 32>,  (const void*)k_expand<kQueueOut, 64>,
+                           (const void*)k_expand<kHeavy, 1>,      (const void*)k_expand<kHeavy, 2>,
+                           (const void*)k_expand<kHeavy, 4>,      (const void*)k_expand<kHeavy, 8>,
+                           (const void*)k_expand<kHeavy, 16>,     (const void*)k_expand<kHeavy, 32>,
+                           (const void*)k_expand<kHeavy, 64>};
   size_t max_static = 0;
   for (auto fn : kernels) {
     cudaFuncAttributes fa{};
@@ -1686,6 +1808,11 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   for (auto fn : kernels) LBFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_));
   LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<kBitmapOut, 2>, kExpandThreads, dyn_smem_));
   expand_grid_ = sm_count_ * std::max(occ, 1);
+  if (nparts_ == 1 && hot_words_ >= 4) {
+    stage_ = dev_alloc<uint32_t>((size_t)expand_grid_ * hot_words_);
+    LBFS_CUDA(cudaFuncSetAttribute((const void*)k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSweepRingBytes + hot_words_ * 4));
+  }
   // device-side level loop: one co-resident CTA per SM (cooperative launch)
   int coop = 0, locc = 0;
   LBFS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device_));
@@ -1720,6 +1847,10 @@ BfsEngine::~BfsEngine() {
   cudaStreamSynchronize(stream_);
   dev_free(visited_);
   dev_free(prev_);
+  dev_free(stage_);
+  dev_free(side_);
+  dev_free(first_nbr_);
+  dev_free(win_info_);
   dev_free(pred_int_);
   dev_free(level_int_);
   dev_free(front_);
@@ -1788,9 +1919,11 @@ static void launch_expand_m(int pi, unsigned grid, int smem, const LevelArgs& a,
   }
 }
 
-void BfsEngine::launch_expand(bool bitmap, int pi, unsigned grid, const LevelArgs& a, const Frontier& f,
+void BfsEngine::launch_expand(int mode, int pi, unsigned grid, const LevelArgs& a, const Frontier& f,
                               cudaStream_t st) {
-  if (bitmap)
+  if (mode == kHeavy)
+    launch_expand_m<kHeavy>(pi, grid, dyn_smem_, a, f, hot_words_, hub_ldg_, st);
+  else if (mode == kBitmapOut)
     launch_expand_m<kBitmapOut>(pi, grid, dyn_smem_, a, f, hot_words_, hub_ldg_, st);
   else
     launch_expand_m<kQueueOut>(pi, grid, kRingBytes, a, f, 0, hub_ldg_, st);
@@ -1822,8 +1955,11 @@ LevelArgs BfsEngine::level_args() const {
   return a;
 }
 
-unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, bool bitmap, bool prev_bitmap, int cur, int64_t L,
+unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool prev_bitmap, int cur, int64_t L,
                                  cudaStream_t st) {
+  const bool bitmap = mode != kQueueOut;
+  a.stage = stage_;
+  a.stage_first = 1;
   a.next_level = (int32_t)(L + 1);
   a.next_cnt = &cnt_[(L + 1) % kCounterRing];
   a.next_small = q_small_[cur ^ 1];
@@ -1867,6 +2003,21 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, bool bitmap, b
                                   (f.n_warp + (f.n_small + 31) / 32 + kExpandWarps - 1) / kExpandWarps,
                                   (int64_t)1});
   const unsigned grid = bitmap ? (unsigned)expand_grid_ : clamp_grid(need, expand_grid_);
+  // heavy level after a bitmap level: the big-row region is swept whole (sweep.cu)
+  const bool sweep = mode == kHeavy && prev_bitmap && side_ && !sweep_off_;
+  sweep_used_ = sweep;
+  if (sweep) {
+    if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[0], st));
+    LBFS_LAUNCH(k_sweep_plan, clamp_grid((n_side_win_ + 255) / 256, (int64_t)sm_count_ * 16), 256, 0, st, side_, front_,
+                n_side_win_, win_info_);
+    SweepArgs sa{col_idx_, side_, n_side_win_, e_big_, front_, win_info_, visited_, pred_int_, new2old_loc_,
+                 stage_, 1, hot_words_, getenv("LBFS_SWEEP_DBG") ? atoi(getenv("LBFS_SWEEP_DBG")) : 0};
+    LBFS_LAUNCH(k_sweep, (unsigned)expand_grid_, kSweepThreads, kSweepRingBytes + hot_words_ * 4, st, sa);
+    a.stage_first = 0;
+    f.n_cta = 0;
+    f.n_wslice = 0;
+    f.dense_warp = false;
+  }
   const bool any = f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice + f.n_dense > 0 || f.dense_warp;
   if (any) {
     // one launch per non-empty bin: each phase kernel gets its own register
@@ -1874,32 +2025,48 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, bool bitmap, b
     const bool has[6] = {f.n_cta > 0, f.n_items > 0, f.n_warp + f.n_small > 0, f.n_wslice > 0, f.n_dense > 0,
                          f.dense_warp};
     for (int pi = 0; pi < 6; ++pi) {
-      if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[pi], st));
+      if (split_ && !(sweep && pi == 0)) LBFS_CUDA(cudaEventRecord(ev_split_[pi], st));
       if (!has[pi]) continue;
-      launch_expand(bitmap, pi, grid, a, f, st);
+      launch_expand(mode, pi, grid, a, f, st);
+      a.stage_first = 0;
     }
     if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[6], st));
   }
-  split_any_ = any;
+  split_any_ = any || sweep;
   return grid;
 }
 
-void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st) {
+void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st, bool heavy) {
   CompactArgs ca{row_ptr_, new2old_loc_, visited_, prev_, nwl_, level_int_, (int32_t)(L + 1),
                  t_cta_, t_warp_, t_nz_, &cnt_[(L + 1) % kCounterRing], q_small_[cur ^ 1], q_cta_[cur ^ 1],
-                 q_items_[cur ^ 1], q_wslice_[cur ^ 1], front_, part_log_, part_rank_, fsend};
+                 q_items_[cur ^ 1], q_wslice_[cur ^ 1], front_, part_log_, part_rank_, fsend,
+                 col_idx_, first_nbr_, pred_int_,
+                 // heavy: blind hot ORs leave no parent; after a sweep no new vertex has one
+                 heavy ? (int32_t)(sweep_used_ ? n_loc_ : std::min<int64_t>((int64_t)hot_words_ * 32, n_loc_)) : 0,
+                 (int32_t)L};
   LBFS_LAUNCH(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
+}
+
+void BfsEngine::merge_hot(cudaStream_t st) {
+  const int hw4 = hot_words_ / 4;
+  const dim3 grid((unsigned)((hw4 + 255) / 256), (unsigned)((expand_grid_ + kMergeRows - 1) / kMergeRows));
+  LBFS_LAUNCH(k_merge_hot, grid, 256, 0, st, reinterpret_cast<const uint4*>(stage_), expand_grid_, hw4, visited_);
 }
 
 void BfsEngine::read_env() {
   trace_ = env_flag("LBFS_TRACE");  // per-level table on stderr
   count_ = env_flag("LBFS_COUNT");  // candidate-write counters (slow)
+  {  // heavy levels: bitmap levels with edges >= nnz / LBFS_HEAVY_DIV (0: off)
+    const char* hd = getenv("LBFS_HEAVY_DIV");
+    heavy_div_ = hd ? atoi(hd) : 8;
+  }
   split_ = env_flag("LBFS_SPLIT");  // one launch per bin
   dense_off_ = env_flag("LBFS_NO_DENSE");  // experiment: always use the small-bin list
   dense_warp_ = env_flag("LBFS_DENSE_WARP");  // experiment: dense warp-bin region
   hub_ldg_ = env_flag("LBFS_HUB_LDG");  // experiment: hub bin without TMA staging
   loop_off_ = env_flag("LBFS_NO_LOOP");  // experiment: host-driven queue-mode levels
   loop_prof_ = env_flag("LBFS_LOOP_PROF");
+  sweep_off_ = env_flag("LBFS_NO_SWEEP");
   // LBFS_MEGA=1: whole BFS in one persistent launch (k_bfs). Measured on
   // S24 it is ~12% slower than the host-driven loop (its phases run as
   // calls inside one kernel: 10-15% slower per level than one launch per
@@ -2114,10 +2281,12 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       continue;
     }
     const bool bitmap = c.edges >= bitmap_min_edges;
+    const bool heavy = bitmap && stage_ && heavy_div_ > 0 && c.edges * (unsigned long long)heavy_div_ >= (unsigned long long)nnz_;
     LBFS_CUDA(cudaEventRecord(ev_[2], st));
-    const unsigned grid = expand_level(a, c, bitmap, prev_bitmap, cur, L, st);
+    const unsigned grid = expand_level(a, c, heavy ? kHeavy : bitmap ? kBitmapOut : kQueueOut, prev_bitmap, cur, L, st);
+    if (heavy) merge_hot(st);
     LBFS_CUDA(cudaEventRecord(ev_[3], st));
-    if (bitmap) compact_level(cur, L, nullptr, st);
+    if (bitmap) compact_level(cur, L, nullptr, st, heavy);
     LBFS_CUDA(cudaEventRecord(ev_[5], st));
     publish_and_wait(slot, (int)((L + 2) % kCounterRing), st);
     LBFS_CUDA(cudaEventSynchronize(ev_[5]));
@@ -2144,7 +2313,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       fprintf(stderr,
               "[lbfs] L%-3lld %s in=%-9llu edges=%-10llu bins(s|list/w/c/items)=%llu/%llu/%llu/%llu grid=%u "
               "expand=%.3fms compact=%.3fms disc=%llu\n",
-              (long long)L, bitmap ? "bitmap" : "queue ", c.discovered, c.edges, c.bin[0], c.bin[1], c.bin[2], c.bin[3],
+              (long long)L, heavy ? "heavy " : bitmap ? "bitmap" : "queue ", c.discovered, c.edges, c.bin[0], c.bin[1], c.bin[2], c.bin[3],
               grid, ms, bitmap ? cms : 0.f, nx.discovered);
     layers_.push_back(lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, (int64_t)nx.discovered});
     cur ^= 1;

@@ -119,6 +119,12 @@ struct LevelArgs {
   int32_t* next_small;
   int32_t* next_warp;
   CtaItem* next_cta;
+  // heavy bitmap levels (k_expand<kHeavy>): each CTA ORs hot targets blindly
+  // into its zeroed shared copy of the hot prefix and leaves it in row
+  // blockIdx.x of stage (hot_words words per row); stage_first: the first
+  // launch of the level stores the row, later launches OR into it
+  uint32_t* stage;
+  int32_t stage_first;
 };
 
 struct CompactArgs {
@@ -138,6 +144,14 @@ struct CompactArgs {
   uint32_t* front;
   int32_t part_log, part_rank;
   uint32_t* fsend;          // partitioned: owned words of the next frontier (all-gather input)
+  // heavy levels: parents of the new vertices with internal id < resolve_verts
+  // (the hot prefix, discovered by blind ORs) are resolved here: the first
+  // neighbour whose level is cur_level (0 = off)
+  const int32_t* col_idx;
+  const int32_t* first_nbr;  // first (highest-degree) neighbour of each row
+  int32_t* pred_int;
+  int32_t resolve_verts;
+  int32_t cur_level;
 };
 
 // Owner / local id of a global internal id (word-cyclic partition).
@@ -205,6 +219,32 @@ struct LoopArgs {
   unsigned long long* prof;  // LBFS_LOOP_PROF: {expand ns, barrier ns, levels, scratch}
 };
 
+// Heavy-level sweep of the big-row region (sweep.cu).
+constexpr int kSweepWindow = 128;   // col_idx elements per window / side entry
+constexpr int kSweepConsumers = 16;  // consumer warps; one CTA per SM
+constexpr int kSweepProducers = 4;   // producer warps (each a latency-bound side -> frontier -> copy chain)
+constexpr int kSweepThreads = 32 * (kSweepConsumers + kSweepProducers);
+constexpr int kSweepStages = 5;      // ring depth (16 KB chunks)
+constexpr int kSweepRingBytes = kSweepStages * 32 * kSweepWindow * 4;
+struct SweepArgs {
+  const int32_t* col_idx;
+  const uint2* side;        // per window: {row of its first element, offsets of rows starting inside}
+  int64_t nwin;             // windows of [0, e_big)
+  int64_t e_big;            // end of the rows of degree >= 32 (ids [0, t_warp))
+  const uint32_t* front;    // frontier bitmap of the level (internal ids)
+  const uint32_t* info;     // per window: k_sweep_plan's frontier bits | code << 8
+  uint32_t* visited;
+  int32_t* pred_int;
+  const int32_t* new2old;
+  uint32_t* stage;          // per-CTA rows of the hot prefix (see LevelArgs::stage)
+  int32_t stage_first;
+  int32_t hot_words;
+  int32_t dbg_flags;        // LBFS_SWEEP_DBG (experiments; wrong results): 1 no hot ORs, 2 no cold probes
+};
+__global__ void k_side_table(const int64_t* rp, int32_t nrows, int64_t nwin, uint2* side);
+__global__ void k_sweep(const __grid_constant__ SweepArgs s);
+__global__ void k_sweep_plan(const uint2* side, const uint32_t* front, int64_t nwin, uint32_t* info);
+
 bool env_flag(const char* name);
 __global__ void k_init(uint4* vis4, uint4* prev4, int64_t nwords4, int4* lvl4, int64_t n4);
 __global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int32_t root_orig, Counters* cnt0,
@@ -256,12 +296,14 @@ class BfsEngine {
 
  private:
   void build_layout(const Csr& csr);
-  void launch_expand(bool bitmap, int pi, unsigned grid, const LevelArgs& a, const Frontier& f, cudaStream_t st);
+  void launch_expand(int mode, int pi, unsigned grid, const LevelArgs& a, const Frontier& f, cudaStream_t st);
   LevelArgs level_args() const;
   // frontier of level L (queue slot cur, counters c) -> launches; returns the grid
-  unsigned expand_level(LevelArgs& a, const Counters& c, bool bitmap, bool prev_bitmap, int cur, int64_t L,
+  // mode: 0 bitmap, 1 queue, 3 heavy bitmap (blind hot ORs, see LevelArgs::stage)
+  unsigned expand_level(LevelArgs& a, const Counters& c, int mode, bool prev_bitmap, int cur, int64_t L,
                         cudaStream_t st);
-  void compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st);
+  void compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st, bool heavy = false);
+  void merge_hot(cudaStream_t st);
   void read_env();
   bool split_any_ = false;
 
@@ -328,6 +370,14 @@ class BfsEngine {
   LoopState* loop_ = nullptr;
   LoopState* h_loop_ = nullptr;     // pinned
   int32_t hot_words_ = 0;  // visited words mirrored in shared memory
+  uint32_t* stage_ = nullptr;    // heavy levels: expand_grid_ rows of hot_words_ words
+  uint2* side_ = nullptr;        // sweep side entries (nparts 1)
+  int32_t* first_nbr_ = nullptr; // first neighbour of each row (heavy-level parent resolution)
+  uint32_t* win_info_ = nullptr; // sweep: per-level window codes (k_sweep_plan)
+  int64_t n_side_win_ = 0, e_big_ = 0;
+  bool sweep_off_ = false;       // LBFS_NO_SWEEP=1: heavy levels use the slice lists
+  bool sweep_used_ = false;      // the last expand_level swept the big-row region
+  int heavy_div_ = 8;            // heavy when a bitmap level's edges >= nnz / heavy_div_ (0: off)
   int dyn_smem_ = 0;
   bool trace_ = false;  // LBFS_TRACE=1: per-level table on stderr
   bool count_ = false;

@@ -87,6 +87,12 @@ static unsigned grid_of(int64_t work, int threads = 256) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + threads - 1) / threads, cap));
 }
 
+__global__ void k_first_nbr(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t n,
+                            int32_t* __restrict__ out) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    out[v] = rp[v] < rp[v + 1] ? ci[rp[v]] : 0;
+}
+
 void BfsEngine::build_layout(const Csr& csr) {
   cudaStream_t st = stream_;
   const int64_t n = csr.n;
@@ -199,6 +205,21 @@ void BfsEngine::build_layout(const Csr& csr) {
   dense_tasks_ = dev_alloc<DenseTask>(std::max<size_t>(tasks.size(), 1));
   if (!tasks.empty())
     LBFS_CUDA(cudaMemcpyAsync(dense_tasks_, tasks.data(), sizeof(DenseTask) * tasks.size(), cudaMemcpyHostToDevice, st));
+  // 7. heavy levels: first neighbour of each row (the parent candidate of a
+  // vertex found by a blind OR) and the side entries of the big-row windows
+  if (nparts_ == 1) {
+    first_nbr_ = dev_alloc<int32_t>((size_t)std::max<int64_t>(nl, 1));
+    LBFS_LAUNCH(k_first_nbr, clamp_grid((nl + 255) / 256, 148 * 16), 256, 0, st, row_ptr_, col_idx_, nl, first_nbr_);
+  }
+  // 7. heavy-level sweep: side entries of the big-row region's windows
+  e_big_ = h_rp[(size_t)t_warp_];
+  n_side_win_ = t_warp_ > 0 ? (e_big_ + kSweepWindow - 1) / kSweepWindow : 0;
+  if (nparts_ == 1 && n_side_win_ > 0) {
+    side_ = dev_alloc<uint2>((size_t)n_side_win_);
+    win_info_ = dev_alloc<uint32_t>((size_t)n_side_win_);
+    LBFS_LAUNCH(k_side_table, clamp_grid((n_side_win_ + 255) / 256, 148 * 16), 256, 0, st, row_ptr_, t_warp_,
+                n_side_win_, side_);
+  }
   LBFS_CUDA(cudaStreamSynchronize(st));
 }
 

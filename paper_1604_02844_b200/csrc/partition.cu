@@ -175,7 +175,7 @@ void BfsEngine::part_expand(cudaStream_t st) {
   LevelArgs a = level_args();
   // always bitmap mode: the exchange works on bitmaps, and queue-mode
   // settling would elect winners for vertices this rank does not own
-  expand_level(a, c, true, part_prev_bitmap_, part_cur_, L, st);
+  expand_level(a, c, /*mode=bitmap*/ 0, part_prev_bitmap_, part_cur_, L, st);
 }
 
 void BfsEngine::part_pack(uint32_t* send, cudaStream_t st) {

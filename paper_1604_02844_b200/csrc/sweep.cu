@@ -1,0 +1,317 @@
+// Heavy-level sweep of the big-row region (K1 + K2 for the levels that carry
+// most of the graph's edges; the reference's _frontier_neighbors + Listing-1
+// gather + the bitmap test-and-set, traversal.py:107-119, 175-193, 297-332).
+//
+// Rows of degree >= 32 (internal ids [0, t_warp): hubs and warp-bin rows)
+// occupy one contiguous col_idx range [0, e_big). At a heavy level most of
+// those rows are in the frontier, so instead of per-row slice lists the
+// region is streamed whole, in 128-element windows, with 128-bit loads. A
+// per-window side entry (built once with the layout) names the row holding
+// the window's first element and the offsets of the <= 4 rows starting
+// inside it, so a lane finds the row of its elements without row_ptr: the
+// frontier bits of those <= 5 consecutive rows decide whether the window is
+// skipped (no load), taken whole, or masked per element.
+//
+// Per element (heavy semantics, see kHeavy in bfs.cu): a target in the hot
+// prefix is OR'ed blindly into the CTA's shared copy (flushed to its stage
+// row; k_merge_hot folds the rows into visited and k_compact resolves those
+// parents), a cold target is probed in L2 and, when clear, settled with
+// red.or + its parent.
+//
+// Warp-specialised pipeline per CTA (one per SM): a producer warp reads the
+// side entries and frontier words of a 32-window chunk, writes the window
+// metadata and bulk-copies (TMA) the windows that hold frontier rows into a
+// kSweepStages-deep shared ring; 16 consumer warps take two windows each,
+// OR the hot targets, issue the cold probes, and test those probes one chunk
+// later (the stage is released only then), so no warp waits on L2 per chunk.
+#include <algorithm>
+
+#include "bfs_engine.cuh"
+
+namespace lbfs {
+
+namespace {
+
+constexpr unsigned kAll = 0xFFFFFFFFu;
+constexpr int kWin = kSweepWindow;  // elements per window
+
+__device__ __forceinline__ int4 ld_stream4(const int32_t* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void red_or_g(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Window info for lanes 0..3 (window 4g + lane): 5 frontier bits of the rows
+// first .. first+4 masked to the rows present, and a code (0 skip, 1 whole,
+// 2 masked) in bits 8..9.
+__device__ __forceinline__ uint32_t window_info(uint2 sd, uint2 fw, bool valid) {
+  if (!valid) return 0u;
+  int ns = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) ns += ((sd.y >> (8 * k)) & 0xFFu) != 0xFFu;
+  const uint32_t sh = sd.x & 31u;
+  const uint64_t f64 = ((uint64_t)fw.y << 32) | fw.x;
+  const uint32_t mask = (2u << ns) - 1u;
+  const uint32_t fb = (uint32_t)(f64 >> sh) & mask;
+  const uint32_t code = fb == 0 ? 0u : (fb == mask ? 1u : 2u);
+  return fb | (code << 8);
+}
+
+}  // namespace
+
+__global__ void k_side_table(const int64_t* __restrict__ rp, int32_t nrows, int64_t nwin, uint2* __restrict__ side) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t P = w * kWin;
+    int32_t lo = 0, hi = nrows - 1;  // last row with rp[row] <= P (rp[0] = 0)
+    while (lo < hi) {
+      const int32_t mid = (lo + hi + 1) >> 1;
+      if (rp[mid] <= P) lo = mid;
+      else hi = mid - 1;
+    }
+    uint32_t starts = kAll;
+    int k = 0;
+    for (int32_t r = lo + 1; r < nrows && k < 4; ++r, ++k) {
+      const int64_t s = rp[r];
+      if (s >= P + kWin) break;
+      starts = (starts & ~(0xFFu << (8 * k))) | ((uint32_t)(s - P) << (8 * k));
+    }
+    side[w] = make_uint2((uint32_t)lo, starts);
+  }
+}
+
+// Per heavy level, before k_sweep: window_info of every window (frontier
+// bits of its rows + skip / whole / masked code).
+__global__ void k_sweep_plan(const uint2* __restrict__ side, const uint32_t* __restrict__ front, int64_t nwin,
+                             uint32_t* __restrict__ info) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
+    const uint2 sd = __ldg(side + w);
+    const uint2 fw = make_uint2(__ldg(front + (sd.x >> 5)), __ldg(front + (sd.x >> 5) + 1));
+    info[w] = window_info(sd, fw, true);
+  }
+}
+
+namespace {
+
+// CTA layout: kSweepConsumers consumer warps + 1 producer warp. The CTA
+// walks chunks blockIdx.x, blockIdx.x + gridDim.x, ... of kChunkWins
+// windows; chunk i goes through ring stage i % kStages.
+constexpr int kChunkWins = 32;                       // windows per chunk (16 KB)
+constexpr int kConsumers = kSweepConsumers;          // consumer warps
+constexpr int kWinPerWarp = kChunkWins / kConsumers;  // windows per consumer warp per chunk
+constexpr int kEl = 4 * kWinPerWarp;                 // elements per consumer lane per chunk
+constexpr int kStages = kSweepStages;
+
+struct WinMeta {
+  int32_t first;    // row of the window's first element
+  uint32_t starts;  // offsets of rows starting inside (0xFF = none)
+  uint32_t info;    // window_info: frontier bits | code << 8
+  uint32_t pad;
+};
+
+struct SweepSmem {
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  WinMeta meta[kStages][kChunkWins];
+  uint32_t dummy[32];
+};
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "SWEEP_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra SWEEP_WAIT;\n"
+      "}\n" ::"r"(saddr(b)),
+      "r"(parity)
+      : "memory");
+}
+// (producers) poll with a short sleep between attempts: the consumers need the issue slots
+__device__ __forceinline__ void bar_wait_backoff(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(saddr(b)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(100);
+  }
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   saddr(dst)),
+               "l"(src), "r"(bytes), "r"(saddr(b))
+               : "memory");
+}
+
+// row of offset o inside a window (relative to its first row)
+__device__ __forceinline__ int row_rel(uint32_t starts, int o) {
+  int r = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) r += (int)((starts >> (8 * t)) & 0xFFu) <= o;
+  return r;
+}
+
+}  // namespace
+
+// dynamic shared memory: [ring: kStages x kChunkWins x kWin int32][hot prefix: hot_words]
+__global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constant__ SweepArgs s) {
+  extern __shared__ __align__(128) uint8_t s_dyn[];
+  __shared__ SweepSmem sm;
+  int32_t* ring = reinterpret_cast<int32_t*>(s_dyn);
+  uint32_t* s_hot = reinterpret_cast<uint32_t*>(s_dyn + kSweepRingBytes);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int hw4 = s.hot_words >> 2;
+  uint4* h4 = reinterpret_cast<uint4*>(s_hot);
+  for (int i = tid; i < hw4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+  if (tid == 0) {
+    for (int b = 0; b < kStages; ++b) {
+      bar_init(&sm.full[b], 1);
+      bar_init(&sm.empty[b], kConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t nchunks = (s.nwin + kChunkWins - 1) / kChunkWins;
+  const int64_t my_chunks = nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  if (warp >= kConsumers) {
+    // ---------------- producers: producer warp p takes the CTA's chunks
+    // p, p + kProducers, ...; lane j owns window j of a chunk. Per chunk two
+    // independent loads (side entry, window info from k_sweep_plan) and one
+    // wait: kSweepProducers chains in flight cover the latency.
+    const int64_t i0 = warp - kConsumers;
+    int st = (int)(i0 % kStages);
+    uint32_t ph = (uint32_t)((i0 / kStages) & 1);
+    for (int64_t i = i0; i < my_chunks; i += kSweepProducers) {
+      const int64_t w0 = (blockIdx.x + i * gridDim.x) * kChunkWins;
+      const int64_t w = w0 + lane < s.nwin ? w0 + lane : -1;
+      const uint2 sd = w >= 0 ? __ldg(s.side + w) : make_uint2(0u, kAll);
+      const uint32_t info = w >= 0 ? __ldcg(s.info + w) : 0u;
+      bar_wait_backoff(&sm.empty[st], ph ^ 1u);  // consumers released the stage
+      sm.meta[st][lane] = WinMeta{(int32_t)sd.x, sd.y, info, 0u};
+      // one bulk copy per chunk, spanning its first to last window with frontier
+      // rows (a bulk copy costs ~0.25 us of TMA issue per SM: few large ones)
+      const uint32_t wbytes = w >= 0 ? (uint32_t)((std::min<int64_t>(kWin, s.e_big - w * kWin) * 4 + 15) & ~15) : 0u;
+      const uint32_t need = __ballot_sync(kAll, (info >> 8) != 0);
+      uint32_t incl = wbytes;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kAll, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int lo = need ? __ffs(need) - 1 : 0, hi = need ? 31 - __clz(need) : 0;
+      const uint32_t span = __shfl_sync(kAll, incl, hi) - __shfl_sync(kAll, incl, lo) + __shfl_sync(kAll, wbytes, lo);
+      __syncwarp();                                                  // every lane's meta store ...
+      if (lane == 0) bar_arrive_tx(&sm.full[st], need ? span : 0u);  // ... before the releasing arrive
+      if (need && lane == lo)
+        bulk_copy(ring + ((size_t)st * kChunkWins + lane) * kWin, s.col_idx + w * kWin, span, &sm.full[st]);
+      st += kSweepProducers;  // (kSweepProducers < kStages)
+      if (st >= kStages) {
+        st -= kStages;
+        ph ^= 1u;
+      }
+    }
+  } else {
+    // ---------------- consumers: warp c takes windows c*kWinPerWarp .. of each chunk.
+    // Nothing is probed: a hot target is OR'ed into the CTA copy, a cold one
+    // into the visited bitmap in L2 (red.or, fire and forget); the parents of
+    // all the level's new vertices are resolved by k_compact. So no warp ever
+    // waits on memory except for its next stage.
+    const uint32_t dummy = saddr(&sm.dummy[lane]);  // per-lane sink for masked-off ORs
+    const uint32_t hoff = saddr(s_hot);
+    const int32_t hv = s.hot_words * 32;            // hot vertices: internal ids < hv
+    const int wb = warp * kWinPerWarp;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int64_t i = 0; i < my_chunks; ++i) {
+      bar_wait(&sm.full[st], ph);
+      if (!(s.dbg_flags & 4)) {
+        const int32_t* buf = ring + (size_t)st * kChunkWins * kWin;
+        const int64_t wfirst = (blockIdx.x + i * gridDim.x) * kChunkWins + wb;
+#pragma unroll
+        for (int j = 0; j < kWinPerWarp; ++j) {
+          const WinMeta m = sm.meta[st][wb + j];
+          const uint32_t code = m.info >> 8;
+          if (code == 0) continue;  // (warp-uniform)
+          const int4 x = reinterpret_cast<const int4*>(buf + (wb + j) * kWin)[lane];
+          const int32_t e4[4] = {x.x, x.y, x.z, x.w};
+          const int64_t p = (wfirst + j) * kWin + 4 * lane;
+          uint32_t vm = 0xFu;
+          if (code == 2) {  // rows partly in the frontier: per element
+            vm = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) vm |= ((m.info >> row_rel(m.starts, 4 * lane + q)) & 1u) << q;
+          }
+          if (p + 3 >= s.e_big) vm &= p < s.e_big ? (1u << (uint32_t)(s.e_big - p)) - 1u : 0u;
+          const int32_t mx = max(max(e4[0], e4[1]), max(e4[2], e4[3]));
+          if (__all_sync(kAll, vm == 0xFu && mx < hv)) {
+            // whole window valid and hot: one shared OR per element
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t bit;
+              asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(e4[q]));
+              asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(hoff + (((uint32_t)e4[q] >> 3) & ~3u)), "r"(bit)
+                           : "memory");
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int32_t v = e4[q];
+              uint32_t bit;
+              asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(v));
+              const bool ok = (vm >> q) & 1u;
+              const bool hot = v < hv;
+              const uint32_t sa = (ok && hot) ? hoff + (((uint32_t)v >> 3) & ~3u) : dummy;
+              asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sa), "r"(bit) : "memory");
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\t"
+                  "setp.ne.u32 p, %2, 0;\n\t"
+                  "@p red.relaxed.gpu.global.or.b32 [%0], %1;\n\t}" ::"l"(s.visited + (v >> 5)),
+                  "r"(bit), "r"((uint32_t)(ok && !hot))
+                  : "memory");
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) bar_arrive(&sm.empty[st]);
+      if (++st == kStages) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+  }
+
+  __syncthreads();
+  uint4* row = reinterpret_cast<uint4*>(s.stage) + (size_t)blockIdx.x * hw4;
+  for (int i = tid; i < hw4; i += blockDim.x) {
+    uint4 x = h4[i];
+    if (!s.stage_first) {
+      const uint4 y = __ldcg(row + i);
+      x.x |= y.x, x.y |= y.y, x.z |= y.z, x.w |= y.w;
+    }
+    __stcg(row + i, x);
+  }
+}
+
+}  // namespace lbfs
