@@ -1040,6 +1040,8 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_levels(LevelArgs a, LoopArg
   unsigned gen = tid == 0 ? ld_acquire(&p.state->bar_gen) : 0u;
   Counters c = ld_counters(&p.ring[L % kCounterRing]);
   for (;;) {
+    // the frontier of level L: empty, large (bitmap mode, host-driven) or the cap -> stop
+    if (c.discovered == 0 || c.edges >= p.bitmap_min_edges || L - p.L0 >= p.max_levels) break;
     if (p.prof && blockIdx.x == 0 && tid == 0) t0 = gtimer();
     const int cur = (int)(L & 1);
     if (blockIdx.x == 0 && tid < (int)(sizeof(Counters) / 8))
@@ -1074,10 +1076,21 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_levels(LevelArgs a, LoopArg
     if (blockIdx.x == 0 && tid == 0)
       p.layers[L - p.L0] = lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, (int64_t)nx.discovered};
     ++L;
-    if (nx.discovered == 0 || nx.edges >= p.bitmap_min_edges || L - p.L0 >= p.max_levels) break;
     c = nx;
   }
-  if (blockIdx.x == 0 && tid == 0) p.state->L_end = L;
+  if (blockIdx.x == 0 && tid == 0) {
+    p.state->L_end = L;
+    if (p.mail) {
+      Counters m = c;
+      m.pad[0] = (unsigned long long)L;
+      volatile unsigned long long* dst = reinterpret_cast<volatile unsigned long long*>(p.mail);
+      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&m);
+#pragma unroll
+      for (int i = 0; i < (int)(sizeof(Counters) / 8); ++i) dst[i] = src[i];
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned long long*>(p.seq) = p.seq_value;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- K3 compaction
@@ -1712,6 +1725,11 @@ __global__ void k_publish(Counters* ring, int slot, int zero_slot, Counters* mai
 void BfsEngine::publish_and_wait(int slot, int zero_slot, cudaStream_t st) {
   const unsigned long long want = ++seq_;
   LBFS_LAUNCH(k_publish, 1, 32, 0, st, cnt_, slot, zero_slot, h_mail_, h_seq_, want);
+  wait_mail(want, st);
+  h_cnt_[slot] = *const_cast<const Counters*>(h_mail_);
+}
+
+void BfsEngine::wait_mail(unsigned long long want, cudaStream_t st) {
   // spin: a blocking stream sync costs tens of microseconds of wake-up per level
   volatile unsigned long long* p = h_seq_;
   const auto t0 = std::chrono::steady_clock::now();
@@ -1724,7 +1742,6 @@ void BfsEngine::publish_and_wait(int slot, int zero_slot, cudaStream_t st) {
         throw Failure(LBFS_ECUDA, "level did not complete within 120 s");
     }
   }
-  h_cnt_[slot] = *const_cast<const Counters*>(h_mail_);
 }
 
 // ---------------------------------------------------------------- engine
@@ -1780,6 +1797,8 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   }
   for (auto& e : ev_) LBFS_CUDA(cudaEventCreate(&e));
   for (auto& e : ev_split_) LBFS_CUDA(cudaEventCreate(&e));
+  LBFS_CUDA(cudaEventCreate(&ev_gap_));
+  for (auto& e : ev_loop_) LBFS_CUDA(cudaEventCreate(&e));
   int occ = 0;
   // shared memory: the TMA ring plus as much of the visited bitmap as fits
   // (static shared memory differs per phase kernel: take the largest)
@@ -1840,6 +1859,8 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   loop_ = dev_alloc<LoopState>(1);
   LBFS_CUDA(cudaMemset(loop_, 0, sizeof(LoopState)));
   LBFS_CUDA(cudaMallocHost(&h_layers_, sizeof(lbfs_layer) * kLoopCap));
+  LBFS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_loop_layers_), sizeof(lbfs_layer) * kLoopCap,
+                          cudaHostAllocMapped));
   LBFS_CUDA(cudaMallocHost(&h_loop_, sizeof(LoopState)));
 }
 
@@ -1871,11 +1892,14 @@ BfsEngine::~BfsEngine() {
   dev_free(d_layers_);
   dev_free(loop_);
   if (h_layers_) cudaFreeHost(h_layers_);
+  if (h_loop_layers_) cudaFreeHost(h_loop_layers_);
   if (h_loop_) cudaFreeHost(h_loop_);
   dev_free(own_pred_);
   dev_free(own_level_);
   for (auto& e : ev_) cudaEventDestroy(e);
   for (auto& e : ev_split_) cudaEventDestroy(e);
+  cudaEventDestroy(ev_gap_);
+  for (auto& e : ev_loop_) cudaEventDestroy(e);
   dev_free(row_ptr_);
   dev_free(col_idx_);
   if (new2old_loc_ != new2old_) dev_free(new2old_loc_);
@@ -2198,6 +2222,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   }
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = stream_;
+  n_loop_ev_ = 0;
   LBFS_CUDA(cudaEventRecord(ev_[0], st));
   {  // K4: bitmaps + internal levels (outputs are written once, by k_finalize)
     const unsigned grid = clamp_grid((n_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
@@ -2212,20 +2237,26 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   // ring invariant: at the start of level L, slot (L+1)%3 is zero
   LBFS_CUDA(cudaMemsetAsync(cnt_, 0, sizeof(Counters) * kCounterRing, st));
   LBFS_LAUNCH(k_seed, 1, 1, 0, st, a, prev_, old2new_, (int32_t)root, &cnt_[0], nullptr, nullptr);
-  LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[0], &cnt_[0], sizeof(Counters), cudaMemcpyDeviceToHost, st));
   LBFS_CUDA(cudaEventRecord(ev_[1], st));
-  LBFS_CUDA(cudaStreamSynchronize(st));
+  const bool dev_loop = loop_grid_ > 0 && !loop_off_ && !split_ && !count_;
+  // with the device loop the first launch is k_levels (it runs no level when
+  // the root's degree needs bitmap mode) and the host learns the counters
+  // from its mailbox; otherwise read them here
+  bool known = !dev_loop;
+  if (!dev_loop) {
+    LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[0], &cnt_[0], sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    LBFS_CUDA(cudaStreamSynchronize(st));
+  }
 
   layers_.clear();
   double expand_ms = 0.0;
   bool prev_bitmap = false;
   const unsigned long long bitmap_min_edges = (unsigned long long)std::max<int64_t>(1 << 16, n_ / 64);
   int64_t L = 0;
-  const bool dev_loop = loop_grid_ > 0 && !loop_off_ && !split_ && !count_;
   for (;;) {
     const Counters c = h_cnt_[L % kCounterRing];
     const int slot = (int)((L + 1) % kCounterRing);
-    if (dev_loop && !prev_bitmap && c.edges < bitmap_min_edges) {
+    if (dev_loop && !prev_bitmap && (!known || c.edges < bitmap_min_edges)) {
       // a run of queue-mode levels on the device (k_levels), one launch
       LoopArgs p{};
       for (int b = 0; b < 2; ++b) {
@@ -2245,26 +2276,33 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       }
       // queue slot parity must match the level parity the kernel assumes
       if (cur != (int)(L & 1)) throw Failure(LBFS_EINVAL, "internal: queue parity");
-      LBFS_CUDA(cudaEventRecord(ev_[2], st));
+      // layers straight into mapped host memory, completion through the mailbox
+      p.layers = h_loop_layers_;
+      p.mail = h_mail_;  // (mapped: valid on the device under unified addressing)
+      p.seq = h_seq_;
+      p.seq_value = ++seq_;
+      const int le = n_loop_ev_ < kLoopEvents ? n_loop_ev_++ : -1;  // segment timing, read after the BFS
+      if (le >= 0) LBFS_CUDA(cudaEventRecord(ev_loop_[2 * le], st));
       void* args[] = {(void*)&a, (void*)&p};
       LBFS_CUDA(cudaLaunchCooperativeKernel((const void*)k_levels, dim3(loop_grid_), dim3(kLoopThreads), args, 0, st));
       g_launches.fetch_add(1);
-      LBFS_CUDA(cudaEventRecord(ev_[3], st));
-      LBFS_CUDA(cudaMemcpyAsync(h_cnt_, cnt_, sizeof(Counters) * kCounterRing, cudaMemcpyDeviceToHost, st));
-      LBFS_CUDA(cudaMemcpyAsync(h_loop_, loop_, sizeof(LoopState), cudaMemcpyDeviceToHost, st));
-      LBFS_CUDA(cudaMemcpyAsync(h_layers_, d_layers_, sizeof(lbfs_layer) * 64, cudaMemcpyDeviceToHost, st));
-      LBFS_CUDA(cudaStreamSynchronize(st));
-      const int64_t L_end = h_loop_->L_end, k = L_end - L;
-      if (k < 1 || k > kLoopCap) throw Failure(LBFS_ECUDA, "internal: device level loop state");
-      if (k > 64) {
-        LBFS_CUDA(cudaMemcpyAsync(h_layers_ + 64, d_layers_ + 64, sizeof(lbfs_layer) * (k - 64),
-                                  cudaMemcpyDeviceToHost, st));
-        LBFS_CUDA(cudaStreamSynchronize(st));
+      if (le >= 0) LBFS_CUDA(cudaEventRecord(ev_loop_[2 * le + 1], st));
+      if (trace_) LBFS_CUDA(cudaEventRecord(ev_gap_, st));
+      wait_mail(p.seq_value, st);
+      const Counters m = *const_cast<const Counters*>(h_mail_);
+      const int64_t L_end = (int64_t)m.pad[0], k = L_end - L;
+      if (k < 0 || k > kLoopCap) throw Failure(LBFS_ECUDA, "internal: device level loop state");
+      h_cnt_[L_end % kCounterRing] = m;
+      known = true;
+      if (k == 0) {  // the first frontier already needs bitmap mode
+        continue;
       }
       float ms = 0.f;
-      LBFS_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
-      expand_ms += ms;
-      for (int64_t i = 0; i < k; ++i) layers_.push_back(h_layers_[i]);
+      if (trace_ && le >= 0) {
+        LBFS_CUDA(cudaEventSynchronize(ev_loop_[2 * le + 1]));
+        LBFS_CUDA(cudaEventElapsedTime(&ms, ev_loop_[2 * le], ev_loop_[2 * le + 1]));
+      }
+      for (int64_t i = 0; i < k; ++i) layers_.push_back(h_loop_layers_[i]);
       if (loop_prof_) {
         unsigned long long pr[4];
         LBFS_CUDA(cudaMemcpy(pr, dbg_, sizeof(pr), cudaMemcpyDeviceToHost));
@@ -2273,16 +2311,17 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       }
       if (trace_)
         fprintf(stderr, "[lbfs] L%-3lld..L%-3lld device loop (%lld levels) %.3fms, last disc=%lld\n", (long long)L,
-                (long long)(L_end - 1), (long long)k, ms, (long long)h_layers_[k - 1].discovered);
+                (long long)(L_end - 1), (long long)k, ms, (long long)h_loop_layers_[k - 1].discovered);
       cur ^= (int)(k & 1);
       L = L_end;
       prev_bitmap = false;
-      if (h_layers_[k - 1].discovered == 0) break;
+      if (m.discovered == 0) break;
       continue;
     }
     const bool bitmap = c.edges >= bitmap_min_edges;
     const bool heavy = bitmap && stage_ && heavy_div_ > 0 && c.edges * (unsigned long long)heavy_div_ >= (unsigned long long)nnz_;
     LBFS_CUDA(cudaEventRecord(ev_[2], st));
+    float gap_ms = -1.f;
     const unsigned grid = expand_level(a, c, heavy ? kHeavy : bitmap ? kBitmapOut : kQueueOut, prev_bitmap, cur, L, st);
     if (heavy) merge_hot(st);
     LBFS_CUDA(cudaEventRecord(ev_[3], st));
@@ -2290,6 +2329,11 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     LBFS_CUDA(cudaEventRecord(ev_[5], st));
     publish_and_wait(slot, (int)((L + 2) % kCounterRing), st);
     LBFS_CUDA(cudaEventSynchronize(ev_[5]));
+    if (trace_) {
+      LBFS_CUDA(cudaEventSynchronize(ev_[2]));
+      if (L > 0) LBFS_CUDA(cudaEventElapsedTime(&gap_ms, ev_gap_, ev_[2]));
+      LBFS_CUDA(cudaEventRecord(ev_gap_, st));  // end of this level (after k_publish)
+    }
     float ms = 0.f, cms = 0.f;
     LBFS_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
     LBFS_CUDA(cudaEventElapsedTime(&cms, ev_[3], ev_[5]));
@@ -2312,15 +2356,16 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     if (trace_)
       fprintf(stderr,
               "[lbfs] L%-3lld %s in=%-9llu edges=%-10llu bins(s|list/w/c/items)=%llu/%llu/%llu/%llu grid=%u "
-              "expand=%.3fms compact=%.3fms disc=%llu\n",
+              "expand=%.3fms compact=%.3fms disc=%llu gap_before=%.3fms\n",
               (long long)L, heavy ? "heavy " : bitmap ? "bitmap" : "queue ", c.discovered, c.edges, c.bin[0], c.bin[1], c.bin[2], c.bin[3],
-              grid, ms, bitmap ? cms : 0.f, nx.discovered);
+              grid, ms, bitmap ? cms : 0.f, nx.discovered, gap_ms);
     layers_.push_back(lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, (int64_t)nx.discovered});
     cur ^= 1;
     ++L;
     prev_bitmap = bitmap;
     if (nx.discovered == 0) break;
   }
+  if (trace_) LBFS_CUDA(cudaEventRecord(ev_gap_, st));
   {  // outputs in original ids
     const unsigned grid = clamp_grid((npad_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
     const bool aligned = ((uintptr_t)d_pred % 16 == 0) && ((uintptr_t)d_level % 16 == 0);
@@ -2332,6 +2377,18 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   }
   LBFS_CUDA(cudaEventRecord(ev_[4], st));
   LBFS_CUDA(cudaEventSynchronize(ev_[4]));
+  for (int i = 0; i < n_loop_ev_; ++i) {  // device-loop segments
+    float ms = 0.f;
+    LBFS_CUDA(cudaEventElapsedTime(&ms, ev_loop_[2 * i], ev_loop_[2 * i + 1]));
+    expand_ms += ms;
+  }
+  n_loop_ev_ = 0;
+  if (trace_) {
+    float fin = 0.f, tot = 0.f;
+    LBFS_CUDA(cudaEventElapsedTime(&fin, ev_gap_, ev_[4]));
+    LBFS_CUDA(cudaEventElapsedTime(&tot, ev_[0], ev_[4]));
+    fprintf(stderr, "[lbfs] finalize %.3fms total %.3fms\n", fin, tot);
+  }
   if (t) {
     float total = 0.f, init = 0.f;
     LBFS_CUDA(cudaEventElapsedTime(&total, ev_[0], ev_[4]));

@@ -217,6 +217,11 @@ struct LoopArgs {
   int64_t L0, max_levels;
   unsigned long long bitmap_min_edges;
   unsigned long long* prof;  // LBFS_LOOP_PROF: {expand ns, barrier ns, levels, scratch}
+  // completion mailbox in mapped host memory (host-driven runs): the counters
+  // of the first level not run (pad[0] = that level) and then the sequence word
+  Counters* mail;
+  unsigned long long* seq;
+  unsigned long long seq_value;
 };
 
 // Heavy-level sweep of the big-row region (sweep.cu).
@@ -352,10 +357,16 @@ class BfsEngine {
   unsigned long long* h_seq_ = nullptr;
   unsigned long long seq_ = 0;
   void publish_and_wait(int slot, int zero_slot, cudaStream_t st);
+  void wait_mail(unsigned long long want, cudaStream_t st);
+  lbfs_layer* h_loop_layers_ = nullptr;  // mapped: k_levels' per-level layers of the current run
   int32_t* own_pred_ = nullptr;
   int32_t* own_level_ = nullptr;
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev_[6] = {};
+  cudaEvent_t ev_gap_ = nullptr;  // LBFS_TRACE: end of the previous level (gap to the next one)
+  static constexpr int kLoopEvents = 16;
+  cudaEvent_t ev_loop_[2 * kLoopEvents] = {};  // device-loop segments of one BFS (timing)
+  int n_loop_ev_ = 0;
   std::vector<lbfs_layer> layers_;
   int expand_grid_ = 0;
   int loop_grid_ = 0;             // k_levels CTAs (0: device loop unavailable)
