@@ -287,36 +287,22 @@ __device__ __forceinline__ uint32_t probe_mask(const LevelArgs& a, const Hot& h,
   if constexpr (M == kQueueDirect) return okmask;
   uint32_t cmask = 0;
   if constexpr (M == kHeavy) {
-    // hot: one red.shared.or, nothing waits on it; cold: the probe of kBitmapOut
+    // hot: one red.shared.or into the CTA copy, cold: one red.or into visited
+    // in L2; nothing waits on memory and no parent is recorded (k_compact
+    // resolves the parents of every new vertex of a heavy level)
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const uint32_t bit = 1u << (nb[k] & 31);
-      const uint32_t sa = h.base + 4u * (uint32_t)(nb[k] >> 5);
+      uint32_t bit;
+      asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(nb[k]));
       const bool ok = (okmask >> k) & 1u;
-      if constexpr (W == kAllHot) {
-        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}" ::"r"(sa),
-                     "r"(bit), "r"((uint32_t)ok)
-                     : "memory");
-      } else if constexpr (W == kAllCold) {
-        const uint32_t w = __ldcg(a.visited + (nb[k] >> 5));
-        cmask |= ((~w >> (nb[k] & 31)) & 1u) << k;
-      } else {
-        uint32_t w;
-        asm volatile(
-            "{\n\t.reg .pred p, q;\n\t"
-            "setp.lt.s32 p, %1, %2;\n\t"
-            "setp.ne.u32 q, %6, 0;\n\t"
-            "and.pred q, q, p;\n\t"
-            "mov.u32 %0, 0xFFFFFFFF;\n\t"
-            "@q red.shared.or.b32 [%3], %5;\n\t"
-            "@!p ld.global.cg.u32 %0, [%4];\n\t}"
-            : "=r"(w)
-            : "r"(nb[k] >> 5), "r"(h.words), "r"(sa), "l"(a.visited + (nb[k] >> 5)), "r"(bit), "r"((uint32_t)ok)
-            : "memory");
-        cmask |= ((~w >> (nb[k] & 31)) & 1u) << k;
+      const bool hot = W == kAllHot || (W != kAllCold && (nb[k] >> 5) < h.words);
+      if (ok && hot) {
+        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(h.base + 4u * (uint32_t)(nb[k] >> 5)), "r"(bit) : "memory");
+      } else if (ok) {
+        red_or(a.visited + (nb[k] >> 5), bit);
       }
     }
-    return cmask & okmask;
+    return 0u;
   }
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -825,7 +811,10 @@ __device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier
           const uint32_t rel = (uint32_t)(pq - base);
           own[q] = lo + (d == 1 ? (int32_t)rel : (int32_t)__umulhi(rel, rcp));
           const bool in_task = pq >= dt.p0 && pq < a1;
-          const bool in_front = in_task && ((__ldcg(f.front + (own[q] >> 5)) >> (own[q] & 31)) & 1u);
+          // (the frontier bitmap is read-only during a k_expand launch: through L1;
+        // k_bfs rewrites it within its launch: through L2)
+        const uint32_t fw = !in_task ? 0u : (f.front_nc ? __ldg(f.front + (own[q] >> 5)) : __ldcg(f.front + (own[q] >> 5)));
+        const bool in_front = in_task && ((fw >> (own[q] & 31)) & 1u);
           okm |= (uint32_t)in_front << q;
           nb[q] = in_front ? nb[q] : 0;
         }
@@ -1821,7 +1810,12 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   }
   int optin = 0;
   LBFS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device_));
-  const int64_t avail = (int64_t)optin - (int64_t)max_static - kRingBytes - 1024;
+  int64_t avail = (int64_t)optin - (int64_t)max_static - kRingBytes - 1024;
+  if (nparts_ == 1) {  // the sweep kernel's ring + static part must fit next to the same hot prefix
+    cudaFuncAttributes fs{};
+    LBFS_CUDA(cudaFuncGetAttributes(&fs, (const void*)k_sweep));
+    avail = std::min<int64_t>(avail, (int64_t)optin - (int64_t)fs.sharedSizeBytes - kSweepRingBytes);
+  }
   hot_words_ = (int32_t)std::min<int64_t>(std::max<int64_t>(avail / 4, 0) & ~int64_t(3), (nwords_ + 3) & ~int64_t(3));
   dyn_smem_ = kRingBytes + hot_words_ * 4;
   for (auto fn : kernels) LBFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_));
@@ -1829,8 +1823,12 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   expand_grid_ = sm_count_ * std::max(occ, 1);
   if (nparts_ == 1 && hot_words_ >= 4) {
     stage_ = dev_alloc<uint32_t>((size_t)expand_grid_ * hot_words_);
-    LBFS_CUDA(cudaFuncSetAttribute((const void*)k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kSweepRingBytes + hot_words_ * 4));
+    cudaFuncAttributes fs{};
+    LBFS_CUDA(cudaFuncGetAttributes(&fs, (const void*)k_sweep));
+    sweep_fits_ = (int64_t)fs.sharedSizeBytes + kSweepRingBytes + (int64_t)hot_words_ * 4 <= optin;
+    if (sweep_fits_)
+      LBFS_CUDA(cudaFuncSetAttribute((const void*)k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kSweepRingBytes + hot_words_ * 4));
   }
   // device-side level loop: one co-resident CTA per SM (cooperative launch)
   int coop = 0, locc = 0;
@@ -1872,6 +1870,8 @@ BfsEngine::~BfsEngine() {
   dev_free(side_);
   dev_free(first_nbr_);
   dev_free(win_info_);
+  dev_free(svmask_);
+  dev_free(sdesc_);
   dev_free(pred_int_);
   dev_free(level_int_);
   dev_free(front_);
@@ -2003,6 +2003,7 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
     if (small_region > 0 && (int64_t)c.bin[kBinSmall] * kDenseDenom > small_region * kDenseNum && !dense_off_) {
       f.n_items = 0;
       f.front = front_;
+      f.front_nc = true;
       f.dense = dense_tasks_;
       f.n_dense = n_dense_tasks_;
     }
@@ -2028,19 +2029,34 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
                                   (int64_t)1});
   const unsigned grid = bitmap ? (unsigned)expand_grid_ : clamp_grid(need, expand_grid_);
   // heavy level after a bitmap level: the big-row region is swept whole (sweep.cu)
-  const bool sweep = mode == kHeavy && prev_bitmap && side_ && !sweep_off_;
+  const bool sweep = mode == kHeavy && prev_bitmap && side_ && sweep_fits_ && !sweep_off_;
   sweep_used_ = sweep;
   if (sweep) {
     if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[0], st));
     LBFS_LAUNCH(k_sweep_plan, clamp_grid((n_side_win_ + 255) / 256, (int64_t)sm_count_ * 16), 256, 0, st, side_, front_,
                 n_side_win_, win_info_);
-    SweepArgs sa{col_idx_, side_, n_side_win_, e_big_, front_, win_info_, visited_, pred_int_, new2old_loc_,
-                 stage_, 1, hot_words_, getenv("LBFS_SWEEP_DBG") ? atoi(getenv("LBFS_SWEEP_DBG")) : 0};
+    // the small region joins the sweep when most of it is in the frontier
+    // (else its frontier rows go through the group items below)
+    const bool sweep_small = svmask_ && f.n_dense > 0 && sweep_small_;
+    if (sweep_small) {
+      const int64_t nsw = n_win_all_ - w_small0_;
+      LBFS_LAUNCH(k_sweep_plan_small, (unsigned)((nsw + 63) / 64), 256, 0, st, classes_, sdesc_, front_, e_nz_,
+                  w_small0_, nsw, svmask_);
+    }
+    SweepArgs sa{col_idx_, side_, n_side_win_, e_big_, sweep_small ? n_win_all_ : n_side_win_,
+                 sweep_small ? e_nz_ : e_big_, sweep_small ? w_small0_ : n_win_all_ + 1, svmask_, front_, win_info_,
+                 visited_, pred_int_, new2old_loc_,
+                 stage_, 1, hot_words_, getenv("LBFS_SWEEP_PF") ? atoi(getenv("LBFS_SWEEP_PF")) : kSweepPrefetch,
+                 getenv("LBFS_SWEEP_DBG") ? atoi(getenv("LBFS_SWEEP_DBG")) : 0};
     LBFS_LAUNCH(k_sweep, (unsigned)expand_grid_, kSweepThreads, kSweepRingBytes + hot_words_ * 4, st, sa);
     a.stage_first = 0;
     f.n_cta = 0;
     f.n_wslice = 0;
     f.dense_warp = false;
+    if (sweep_small) {  // the small region is swept too
+      f.n_items = 0;
+      f.n_dense = 0;
+    }
   }
   const bool any = f.n_cta + f.n_warp + f.n_small + f.n_items + f.n_wslice + f.n_dense > 0 || f.dense_warp;
   if (any) {
@@ -2065,8 +2081,8 @@ void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t 
                  t_cta_, t_warp_, t_nz_, &cnt_[(L + 1) % kCounterRing], q_small_[cur ^ 1], q_cta_[cur ^ 1],
                  q_items_[cur ^ 1], q_wslice_[cur ^ 1], front_, part_log_, part_rank_, fsend,
                  col_idx_, first_nbr_, pred_int_,
-                 // heavy: blind hot ORs leave no parent; after a sweep no new vertex has one
-                 heavy ? (int32_t)(sweep_used_ ? n_loc_ : std::min<int64_t>((int64_t)hot_words_ * 32, n_loc_)) : 0,
+                 // heavy: blind ORs leave no parent for any new vertex
+                 heavy ? (int32_t)n_loc_ : 0,
                  (int32_t)L};
   LBFS_LAUNCH(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
 }
@@ -2091,6 +2107,7 @@ void BfsEngine::read_env() {
   loop_off_ = env_flag("LBFS_NO_LOOP");  // experiment: host-driven queue-mode levels
   loop_prof_ = env_flag("LBFS_LOOP_PROF");
   sweep_off_ = env_flag("LBFS_NO_SWEEP");
+  sweep_small_ = env_flag("LBFS_SWEEP_SMALL");  // experiment: the small region in the sweep too
   // LBFS_MEGA=1: whole BFS in one persistent launch (k_bfs). Measured on
   // S24 it is ~12% slower than the host-driven loop (its phases run as
   // calls inside one kernel: 10-15% slower per level than one launch per

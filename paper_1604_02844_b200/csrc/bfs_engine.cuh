@@ -87,6 +87,7 @@ struct Frontier {
   const DenseTask* dense;
   int64_t n_dense;
   bool dense_warp;         // stream the warp-bin region from the frontier bitmap
+  bool front_nc;           // front is read-only for the launch (non-coherent loads)
 };
 
 // Degree classes of the small region: internal ids with degree d form the
@@ -229,13 +230,21 @@ constexpr int kSweepWindow = 128;   // col_idx elements per window / side entry
 constexpr int kSweepConsumers = 16;  // consumer warps; one CTA per SM
 constexpr int kSweepProducers = 4;   // producer warps (each a latency-bound side -> frontier -> copy chain)
 constexpr int kSweepThreads = 32 * (kSweepConsumers + kSweepProducers);
-constexpr int kSweepStages = 5;      // ring depth (16 KB chunks)
+#ifndef LBFS_SWEEP_STAGES
+#define LBFS_SWEEP_STAGES 4
+#endif
+constexpr int kSweepStages = LBFS_SWEEP_STAGES;  // ring depth (16 KB chunks)
+constexpr int kSweepPrefetch = 0;    // L2 prefetch distance (chunks of a CTA)
 constexpr int kSweepRingBytes = kSweepStages * 32 * kSweepWindow * 4;
 struct SweepArgs {
   const int32_t* col_idx;
   const uint2* side;        // per window: {row of its first element, offsets of rows starting inside}
-  int64_t nwin;             // windows of [0, e_big)
+  int64_t nwin;             // windows of [0, e_big) (side entries)
   int64_t e_big;            // end of the rows of degree >= 32 (ids [0, t_warp))
+  int64_t nwin_all;         // windows of [0, e_end): the whole sweep
+  int64_t e_end;            // end of the small region (rows of degree 1..31)
+  int64_t w_small0;         // first window holding small-region elements (e_big / 128)
+  const uint4* svmask;      // valid masks of windows [w_small0, nwin_all) (k_sweep_plan_small)
   const uint32_t* front;    // frontier bitmap of the level (internal ids)
   const uint32_t* info;     // per window: k_sweep_plan's frontier bits | code << 8
   uint32_t* visited;
@@ -244,11 +253,16 @@ struct SweepArgs {
   uint32_t* stage;          // per-CTA rows of the hot prefix (see LevelArgs::stage)
   int32_t stage_first;
   int32_t hot_words;
+  int32_t prefetch;         // L2 prefetch distance in chunks of a CTA (0: off)
   int32_t dbg_flags;        // LBFS_SWEEP_DBG (experiments; wrong results): 1 no hot ORs, 2 no cold probes
 };
 __global__ void k_side_table(const int64_t* rp, int32_t nrows, int64_t nwin, uint2* side);
 __global__ void k_sweep(const __grid_constant__ SweepArgs s);
 __global__ void k_sweep_plan(const uint2* side, const uint32_t* front, int64_t nwin, uint32_t* info);
+__global__ void k_small_desc(const ClassTable* classes, int64_t e_big, int64_t e_end, int64_t w0, int64_t nw,
+                             uint2* desc);
+__global__ void k_sweep_plan_small(const ClassTable* classes, const uint2* desc, const uint32_t* front, int64_t e_end,
+                                   int64_t w0, int64_t nw, uint4* svmask);
 
 bool env_flag(const char* name);
 __global__ void k_init(uint4* vis4, uint4* prev4, int64_t nwords4, int4* lvl4, int64_t n4);
@@ -385,9 +399,14 @@ class BfsEngine {
   uint2* side_ = nullptr;        // sweep side entries (nparts 1)
   int32_t* first_nbr_ = nullptr; // first neighbour of each row (heavy-level parent resolution)
   uint32_t* win_info_ = nullptr; // sweep: per-level window codes (k_sweep_plan)
+  uint4* svmask_ = nullptr;      // sweep: per-level valid masks of the small-region windows
+  uint2* sdesc_ = nullptr;       // sweep: small-region window descriptors (k_small_desc)
+  int64_t e_nz_ = 0, n_win_all_ = 0, w_small0_ = 0;
   int64_t n_side_win_ = 0, e_big_ = 0;
   bool sweep_off_ = false;       // LBFS_NO_SWEEP=1: heavy levels use the slice lists
   bool sweep_used_ = false;      // the last expand_level swept the big-row region
+  bool sweep_fits_ = false;      // k_sweep's ring + hot prefix fit in shared memory
+  bool sweep_small_ = false;     // LBFS_SWEEP_SMALL=1: sweep the small region as well (slower today)
   int heavy_div_ = 8;            // heavy when a bitmap level's edges >= nnz / heavy_div_ (0: off)
   int dyn_smem_ = 0;
   bool trace_ = false;  // LBFS_TRACE=1: per-level table on stderr

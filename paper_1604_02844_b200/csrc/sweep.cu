@@ -95,6 +95,106 @@ __global__ void k_sweep_plan(const uint2* __restrict__ side, const uint32_t* __r
   }
 }
 
+// Small-region window descriptors (built once with the layout): for window
+// w >= w0, the first small element P0 = max(128 w, e_big), its degree class
+// d, row o0 = T[d+1] + (P0 - base[d]) / d and offset r0 = (P0 - base[d]) % d
+// in that row; x = o0, y = d | r0 << 8 | s0 << 16 | (window crosses a class
+// boundary) << 31, s0 = P0 - 128 w.
+__device__ __forceinline__ int small_class(const int64_t* B, int64_t p) {
+  int d = kSmallMax - 1;  // smallest d with base[d] <= p (base is non-increasing in d)
+#pragma unroll
+  for (int step = 16; step; step >>= 1)
+    if (d - step >= 1 && B[d - step] <= p) d -= step;
+  return d;
+}
+__global__ void k_small_desc(const ClassTable* __restrict__ classes, int64_t e_big, int64_t e_end, int64_t w0,
+                             int64_t nw, uint2* __restrict__ desc) {
+  __shared__ int32_t T[kSmallMax + 2];
+  __shared__ int64_t B[kSmallMax + 1];
+  if (threadIdx.x < kSmallMax + 2) T[threadIdx.x] = classes->T[threadIdx.x];
+  if (threadIdx.x < kSmallMax + 1) B[threadIdx.x] = classes->base[threadIdx.x];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t P = (w0 + i) * kWin, P0 = P > e_big ? P : e_big;
+    const int d = small_class(B, P0);
+    const int64_t rel = P0 - B[d];
+    const int64_t class_end = B[d] + (int64_t)(T[d] - T[d + 1]) * d;
+    const uint32_t cross = (P + kWin > class_end && class_end < e_end) ? 1u : 0u;
+    desc[i] = make_uint2((uint32_t)(T[d + 1] + rel / d),
+                         (uint32_t)d | (uint32_t)(rel % d) << 8 | (uint32_t)(P0 - P) << 16 | cross << 31);
+  }
+}
+
+// Per heavy level: valid-element masks of the small-region windows [w0,
+// w0 + nw), one warp per window (a lane's 4 elements: rows in closed form
+// from the window descriptor, their frontier bits through L1).
+__global__ void k_sweep_plan_small(const ClassTable* __restrict__ classes, const uint2* __restrict__ desc,
+                                   const uint32_t* __restrict__ front, int64_t e_end, int64_t w0, int64_t nw,
+                                   uint4* __restrict__ svmask) {
+  __shared__ int32_t T[kSmallMax + 2];
+  __shared__ int64_t B[kSmallMax + 1];
+  __shared__ uint32_t magic[kSmallMax + 1];
+  if (threadIdx.x < kSmallMax + 2) T[threadIdx.x] = classes->T[threadIdx.x];
+  if (threadIdx.x < kSmallMax + 1) {
+    B[threadIdx.x] = classes->base[threadIdx.x];
+    magic[threadIdx.x] = threadIdx.x ? (uint32_t)(0xFFFFFFFFull / threadIdx.x + 1ull) : 0u;  // x / d = umulhi(x, magic)
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // kPW windows per warp step, their loads batched (the kernel is latency-bound)
+  constexpr int kPW = 8;
+  for (int64_t i0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kPW; i0 < nw; i0 += nwarps * kPW) {
+    uint2 dc[kPW];
+#pragma unroll
+    for (int k = 0; k < kPW; ++k) dc[k] = i0 + k < nw ? __ldg(desc + i0 + k) : make_uint2(0u, 0u);
+    int32_t own[kPW][4];
+    uint32_t ok = 0;
+#pragma unroll
+    for (int k = 0; k < kPW; ++k) {
+      const int d = (int)(dc[k].y & 0xFFu), r0 = (int)((dc[k].y >> 8) & 0xFFu), s0 = (int)((dc[k].y >> 16) & 0xFFu);
+      const bool cross = dc[k].y >> 31;
+      const int64_t P = (w0 + i0 + k) * kWin;
+      const int lim = i0 + k < nw ? (int)min((int64_t)kWin, e_end - P) : 0;  // valid offsets [s0, lim)
+      // row and column of this lane's first element, then step through the other three
+      const int x0 = r0 + 4 * lane - s0;
+      const uint32_t q0 = d == 1 ? (uint32_t)max(x0, 0) : __umulhi((uint32_t)max(x0, 0), magic[d]);
+      int32_t row = (int32_t)dc[k].x + (int32_t)q0;
+      int col = max(x0, 0) - (int)q0 * d;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int off = 4 * lane + q;
+        own[k][q] = row;
+        if (cross && off >= s0 && off < lim) {  // (rare) the window crosses a class boundary
+          const int64_t p = P + off;
+          const int dd = small_class(B, p);
+          own[k][q] = T[dd + 1] + (int32_t)((p - B[dd]) / dd);
+        }
+        ok |= (uint32_t)(off >= s0 && off < lim) << (4 * k + q);
+        if (off >= s0 && ++col == d) {
+          col = 0;
+          ++row;
+        }
+      }
+    }
+    uint32_t fw[kPW][4];
+#pragma unroll
+    for (int k = 0; k < kPW; ++k)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) fw[k][q] = ((ok >> (4 * k + q)) & 1u) ? __ldg(front + (own[k][q] >> 5)) : 0u;
+#pragma unroll
+    for (int k = 0; k < kPW; ++k) {
+      uint32_t nib = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) nib |= ((fw[k][q] >> (own[k][q] & 31)) & 1u) << q;
+      uint32_t wk[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) wk[j] = __reduce_or_sync(kAll, (lane >> 3) == j ? nib << (4 * (lane & 7)) : 0u);
+      if (lane == 0 && i0 + k < nw) svmask[i0 + k] = make_uint4(wk[0], wk[1], wk[2], wk[3]);
+    }
+  }
+}
+
 namespace {
 
 // CTA layout: kSweepConsumers consumer warps + 1 producer warp. The CTA
@@ -107,11 +207,18 @@ constexpr int kEl = 4 * kWinPerWarp;                 // elements per consumer la
 constexpr int kStages = kSweepStages;
 
 struct WinMeta {
-  int32_t first;    // row of the window's first element
-  uint32_t starts;  // offsets of rows starting inside (0xFF = none)
-  uint32_t info;    // window_info: frontier bits | code << 8
-  uint32_t pad;
+  uint32_t vmask[4];  // valid elements of the window (rows in the frontier, below e_big): bit o of word o/32
+  uint32_t info;      // window_info: frontier bits | code << 8
+  uint32_t pad[3];
 };
+
+// bits [lo, hi) of word k of a 128-bit mask
+__device__ __forceinline__ uint32_t range_word(int lo, int hi, int k) {
+  const int a = max(lo - 32 * k, 0), b = min(hi - 32 * k, 32);
+  if (a >= b) return 0u;
+  const uint32_t hm = b >= 32 ? kAll : (1u << b) - 1u;
+  return hm & ~((1u << a) - 1u);
+}
 
 struct SweepSmem {
   uint64_t full[kStages];
@@ -191,7 +298,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int64_t nchunks = (s.nwin + kChunkWins - 1) / kChunkWins;
+  const int64_t nchunks = (s.nwin_all + kChunkWins - 1) / kChunkWins;
   const int64_t my_chunks = nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
   if (warp >= kConsumers) {
@@ -204,14 +311,58 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
     uint32_t ph = (uint32_t)((i0 / kStages) & 1);
     for (int64_t i = i0; i < my_chunks; i += kSweepProducers) {
       const int64_t w0 = (blockIdx.x + i * gridDim.x) * kChunkWins;
-      const int64_t w = w0 + lane < s.nwin ? w0 + lane : -1;
-      const uint2 sd = w >= 0 ? __ldg(s.side + w) : make_uint2(0u, kAll);
-      const uint32_t info = w >= 0 ? __ldcg(s.info + w) : 0u;
+      const int64_t w = w0 + lane < s.nwin_all ? w0 + lane : -1;
+      const bool big = w >= 0 && w < s.nwin, small = w >= s.w_small0;
+      const uint2 sd = big ? __ldg(s.side + w) : make_uint2(0u, kAll);
+      uint32_t info = big ? __ldcg(s.info + w) : 0u;
+      const uint4 sv = small ? __ldcg(s.svmask + (w - s.w_small0)) : make_uint4(0u, 0u, 0u, 0u);
+      if (s.prefetch > 0 && lane == 0 && i + s.prefetch < my_chunks) {
+        // warm L2 with the chunk s.prefetch ahead (whole chunk: its windows'
+        // codes are not known yet), so the bulk copy later is an L2 hit
+        const int64_t pw = (blockIdx.x + (i + s.prefetch) * gridDim.x) * kChunkWins;
+        const int64_t pb = std::min<int64_t>((int64_t)kChunkWins * kWin, s.e_end - pw * kWin) * 4;
+        if (pb > 0)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s.col_idx + pw * kWin),
+                       "r"((uint32_t)((pb + 15) & ~15))
+                       : "memory");
+      }
       bar_wait_backoff(&sm.empty[st], ph ^ 1u);  // consumers released the stage
-      sm.meta[st][lane] = WinMeta{(int32_t)sd.x, sd.y, info, 0u};
+      {  // valid-element mask: the ranges of the rows in the frontier, clipped at e_big
+        uint32_t vmask[4] = {0u, 0u, 0u, 0u};
+        const uint32_t code = info >> 8;
+        const int lim = w >= 0 ? (int)std::min<int64_t>(kWin, s.e_big - w * kWin) : 0;
+        if (code == 1) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) vmask[k] = range_word(0, lim, k);
+        } else if (code == 2) {
+          int lo = 0;
+#pragma unroll
+          for (int r = 0; r < 5; ++r) {
+            const int hi = r < 4 ? (int)((sd.y >> (8 * r)) & 0xFFu) : 255;  // next row start (0xFF: none)
+            const int e = min(min(hi, kWin), lim);
+            if ((info >> r) & 1u) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) vmask[k] |= range_word(lo, e, k);
+            }
+            lo = max(lo, min(hi, kWin));
+          }
+        }
+        vmask[0] |= sv.x;  // small-region elements (k_sweep_plan_small)
+        vmask[1] |= sv.y;
+        vmask[2] |= sv.z;
+        vmask[3] |= sv.w;
+        const uint32_t any = vmask[0] | vmask[1] | vmask[2] | vmask[3];
+        info = (info & 0xFFu) | (any ? 2u << 8 : 0u);
+        WinMeta m;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) m.vmask[k] = vmask[k];
+        m.info = info;
+        m.pad[0] = m.pad[1] = m.pad[2] = 0u;
+        sm.meta[st][lane] = m;
+      }
       // one bulk copy per chunk, spanning its first to last window with frontier
       // rows (a bulk copy costs ~0.25 us of TMA issue per SM: few large ones)
-      const uint32_t wbytes = w >= 0 ? (uint32_t)((std::min<int64_t>(kWin, s.e_big - w * kWin) * 4 + 15) & ~15) : 0u;
+      const uint32_t wbytes = w >= 0 ? (uint32_t)((std::min<int64_t>(kWin, s.e_end - w * kWin) * 4 + 15) & ~15) : 0u;
       const uint32_t need = __ballot_sync(kAll, (info >> 8) != 0);
       uint32_t incl = wbytes;
 #pragma unroll
@@ -247,22 +398,13 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
       bar_wait(&sm.full[st], ph);
       if (!(s.dbg_flags & 4)) {
         const int32_t* buf = ring + (size_t)st * kChunkWins * kWin;
-        const int64_t wfirst = (blockIdx.x + i * gridDim.x) * kChunkWins + wb;
 #pragma unroll
         for (int j = 0; j < kWinPerWarp; ++j) {
-          const WinMeta m = sm.meta[st][wb + j];
-          const uint32_t code = m.info >> 8;
-          if (code == 0) continue;  // (warp-uniform)
+          const uint32_t info = sm.meta[st][wb + j].info;
+          if ((info >> 8) == 0) continue;  // (warp-uniform) no row of the window in the frontier
           const int4 x = reinterpret_cast<const int4*>(buf + (wb + j) * kWin)[lane];
           const int32_t e4[4] = {x.x, x.y, x.z, x.w};
-          const int64_t p = (wfirst + j) * kWin + 4 * lane;
-          uint32_t vm = 0xFu;
-          if (code == 2) {  // rows partly in the frontier: per element
-            vm = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) vm |= ((m.info >> row_rel(m.starts, 4 * lane + q)) & 1u) << q;
-          }
-          if (p + 3 >= s.e_big) vm &= p < s.e_big ? (1u << (uint32_t)(s.e_big - p)) - 1u : 0u;
+          const uint32_t vm = (sm.meta[st][wb + j].vmask[lane >> 3] >> (4 * (lane & 7))) & 0xFu;
           const int32_t mx = max(max(e4[0], e4[1]), max(e4[2], e4[3]));
           if (__all_sync(kAll, vm == 0xFu && mx < hv)) {
             // whole window valid and hot: one shared OR per element

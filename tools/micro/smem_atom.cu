@@ -22,6 +22,9 @@ __global__ void __launch_bounds__(1024,1) k(uint32_t* out, uint32_t* gbm, int it
       else if(MODE==3){ uint32_t o=s[w]; if(((o>>(v&31))&1u)==0 && (x&7)==0) atomicOr(s+w,b); acc^=o; }
       else if(MODE==4){ asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;"::"l"(gbm+(v&((1u<<19)-1))),"r"(b):"memory"); }
       else if(MODE==5){ acc ^= __ldcg(gbm+(x&((1u<<19)-1))); }
+      else if(MODE==7){ asm volatile("st.global.u8 [%0], %1;"::"l"((unsigned char*)gbm+(v&((1u<<24)-1))),"r"(1u):"memory"); }
+      else if(MODE==8){ asm volatile("st.global.u32 [%0], %1;"::"l"(gbm+(v&((1u<<22)-1))),"r"(b):"memory"); }
+      else if(MODE==9){ asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;"::"l"(gbm+(v&((1u<<22)-1))),"r"(b):"memory"); }
       else if(MODE==6){ uint32_t r; asm volatile("atom.relaxed.gpu.global.or.b32 %0, [%1], %2;":"=r"(r):"l"(gbm+(v&((1u<<19)-1))),"r"(b):"memory"); acc^=r; }
     }
   }
@@ -31,7 +34,7 @@ __global__ void __launch_bounds__(1024,1) k(uint32_t* out, uint32_t* gbm, int it
 }
 int main(){
   int sms=148, words=36*1024, iters=200;
-  uint32_t *out,*gbm; cudaMalloc(&out,4096*4); cudaMalloc(&gbm,(1<<19)*4); cudaMemset(gbm,0,(1<<19)*4);
+  uint32_t *out,*gbm; cudaMalloc(&out,4096*4); cudaMalloc(&gbm,(1<<22)*4); cudaMemset(gbm,0,(1<<22)*4);
   int smem=words*4;
   auto run=[&](auto kern,const char* name){
     cudaFuncSetAttribute(kern,cudaFuncAttributeMaxDynamicSharedMemorySize,smem);
@@ -49,5 +52,8 @@ int main(){
   run(k<4>,"red.global.or 2MiB random");
   run(k<5>,"ld.cg 2MiB random");
   run(k<6>,"atom.global.or ret 2MiB random");
+  run(k<7>,"st.u8 16MiB random");
+  run(k<8>,"st.u32 16MiB random");
+  run(k<9>,"red.or 16MiB random");
   return 0;
 }
