@@ -1091,6 +1091,9 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_levels(LevelArgs a, LoopArg
 // items. One atomic per output per block reserves space. Pass 2 (one vertex
 // per thread per step, so new2old/row_ptr/pred_int reads coalesce) writes
 // levels and parents in original ids and folds the K6 stats.
+#ifndef LBFS_COMPACT_MINB
+#define LBFS_COMPACT_MINB 1
+#endif
 constexpr int kCompactThreads = 256;
 constexpr int kCompactVerts = 4096;
 constexpr int kCompactWords = kCompactVerts / 32;
@@ -1349,7 +1352,7 @@ __device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk,
   }
 }
 
-__global__ void __launch_bounds__(kCompactThreads) k_compact(CompactArgs c) {
+__global__ void __launch_bounds__(kCompactThreads, LBFS_COMPACT_MINB) k_compact(CompactArgs c) {
   __shared__ CompactSmem sm;
   compact_block(c, blockIdx.x, sm, threadIdx.x, 1);
 }
@@ -1750,6 +1753,9 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   n_loc_ = nparts_ == 1 ? n_ : nwl_ * 32;
   npad_ = pad32(n_);
   LBFS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  LBFS_CUDA(cudaStreamCreateWithFlags(&res_st_, cudaStreamNonBlocking));
+  LBFS_CUDA(cudaEventCreateWithFlags(&ev_resolve_, cudaEventDisableTiming));
+  LBFS_CUDA(cudaEventCreateWithFlags(&ev_side_done_, cudaEventDisableTiming));
   build_layout(csr);
   visited_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
   prev_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
@@ -1909,6 +1915,10 @@ BfsEngine::~BfsEngine() {
   dev_free(red_dev_);
   dev_free(resolve_cnt_);
   dev_free(old2new_);
+  cudaStreamSynchronize(res_st_);
+  cudaStreamDestroy(res_st_);
+  cudaEventDestroy(ev_resolve_);
+  cudaEventDestroy(ev_side_done_);
   cudaStreamDestroy(stream_);
 }
 
@@ -2081,10 +2091,66 @@ void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t 
                  t_cta_, t_warp_, t_nz_, &cnt_[(L + 1) % kCounterRing], q_small_[cur ^ 1], q_cta_[cur ^ 1],
                  q_items_[cur ^ 1], q_wslice_[cur ^ 1], front_, part_log_, part_rank_, fsend,
                  col_idx_, first_nbr_, pred_int_,
-                 // heavy: blind ORs leave no parent for any new vertex
-                 heavy ? (int32_t)n_loc_ : 0,
+                 // heavy: blind ORs leave no parent for any new vertex; resolved here
+                 // only when LBFS_RESOLVE_INLINE=1, else by k_resolve off the critical path
+                 heavy && resolve_inline_ ? (int32_t)n_loc_ : 0,
                  (int32_t)L};
   LBFS_LAUNCH(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
+  if (heavy && !resolve_inline_) {
+    // the parents of level L+1's vertices are read by k_finalize only: resolve
+    // them on the side stream while the next levels run (joined before k_finalize)
+    LBFS_CUDA(cudaEventRecord(ev_resolve_, st));
+    LBFS_CUDA(cudaStreamWaitEvent(res_st_, ev_resolve_, 0));
+    const int64_t n4 = (n_loc_ + 3) / 4;
+    LBFS_LAUNCH(k_resolve, clamp_grid((n4 + 255) / 256, (int64_t)sm_count_ * 16), 256, 0, res_st_, level_int_,
+                first_nbr_, row_ptr_, col_idx_, new2old_loc_, pred_int_, n_loc_, (int32_t)(L + 1));
+    side_pending_ = true;
+  }
+}
+
+// Parents of the vertices at level lvl (found by blind ORs at a heavy level):
+// the first neighbour one level up; rows are sorted by internal id, i.e. by
+// descending degree, and the first entry is almost always it (else scan on).
+// Any such neighbour is a valid parent (traversal.py:145-147).
+__global__ void __launch_bounds__(256) k_resolve(const int32_t* __restrict__ level_int,
+                                                 const int32_t* __restrict__ first_nbr,
+                                                 const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                                                 const int32_t* __restrict__ new2old, int32_t* __restrict__ pred_int,
+                                                 int64_t n, int32_t lvl) {
+  const int64_t n4 = (n + 3) / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 l4 = __ldg(reinterpret_cast<const int4*>(level_int) + i);  // (level_int is padded to 4)
+    const int32_t lv4[4] = {l4.x, l4.y, l4.z, l4.w};
+    bool need[4];
+    int32_t u[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      need[q] = lv4[q] == lvl && 4 * i + q < n;
+      u[q] = need[q] ? __ldg(first_nbr + 4 * i + q) : 0;
+    }
+    int32_t lu[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) lu[q] = need[q] ? __ldg(level_int + u[q]) : 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (!need[q]) continue;
+      const int64_t v = 4 * i + q;
+      int32_t par = kSentinel;
+      if (lu[q] == lvl - 1) {
+        par = __ldg(new2old + u[q]);
+      } else {
+        const int64_t e = __ldg(row_ptr + v + 1);
+        for (int64_t k = __ldg(row_ptr + v) + 1; k < e; ++k) {
+          const int32_t x = __ldg(col_idx + k);
+          if (__ldg(level_int + x) == lvl - 1) {
+            par = __ldg(new2old + x);
+            break;
+          }
+        }
+      }
+      pred_int[v] = par;
+    }
+  }
 }
 
 void BfsEngine::merge_hot(cudaStream_t st) {
@@ -2108,6 +2174,7 @@ void BfsEngine::read_env() {
   loop_prof_ = env_flag("LBFS_LOOP_PROF");
   sweep_off_ = env_flag("LBFS_NO_SWEEP");
   sweep_small_ = env_flag("LBFS_SWEEP_SMALL");  // experiment: the small region in the sweep too
+  resolve_inline_ = env_flag("LBFS_RESOLVE_INLINE");  // experiment: heavy-level parents inside k_compact
   // LBFS_MEGA=1: whole BFS in one persistent launch (k_bfs). Measured on
   // S24 it is ~12% slower than the host-driven loop (its phases run as
   // calls inside one kernel: 10-15% slower per level than one launch per
@@ -2383,6 +2450,11 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     if (nx.discovered == 0) break;
   }
   if (trace_) LBFS_CUDA(cudaEventRecord(ev_gap_, st));
+  if (side_pending_) {  // parents resolved on the side stream
+    LBFS_CUDA(cudaEventRecord(ev_side_done_, res_st_));
+    LBFS_CUDA(cudaStreamWaitEvent(st, ev_side_done_, 0));
+    side_pending_ = false;
+  }
   {  // outputs in original ids
     const unsigned grid = clamp_grid((npad_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
     const bool aligned = ((uintptr_t)d_pred % 16 == 0) && ((uintptr_t)d_level % 16 == 0);

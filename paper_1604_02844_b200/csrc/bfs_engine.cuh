@@ -259,6 +259,8 @@ struct SweepArgs {
 __global__ void k_side_table(const int64_t* rp, int32_t nrows, int64_t nwin, uint2* side);
 __global__ void k_sweep(const __grid_constant__ SweepArgs s);
 __global__ void k_sweep_plan(const uint2* side, const uint32_t* front, int64_t nwin, uint32_t* info);
+__global__ void k_resolve(const int32_t* level_int, const int32_t* first_nbr, const int64_t* row_ptr,
+                          const int32_t* col_idx, const int32_t* new2old, int32_t* pred_int, int64_t n, int32_t lvl);
 __global__ void k_small_desc(const ClassTable* classes, int64_t e_big, int64_t e_end, int64_t w0, int64_t nw,
                              uint2* desc);
 __global__ void k_sweep_plan_small(const ClassTable* classes, const uint2* desc, const uint32_t* front, int64_t e_end,
@@ -406,6 +408,10 @@ class BfsEngine {
   bool sweep_off_ = false;       // LBFS_NO_SWEEP=1: heavy levels use the slice lists
   bool sweep_used_ = false;      // the last expand_level swept the big-row region
   bool sweep_fits_ = false;      // k_sweep's ring + hot prefix fit in shared memory
+  bool resolve_inline_ = false;  // LBFS_RESOLVE_INLINE=1: heavy-level parents in k_compact (critical path)
+  cudaStream_t res_st_ = nullptr;  // heavy-level parent resolution (k_resolve), joined before k_finalize
+  cudaEvent_t ev_resolve_ = nullptr, ev_side_done_ = nullptr;
+  bool side_pending_ = false;
   bool sweep_small_ = false;     // LBFS_SWEEP_SMALL=1: sweep the small region as well (slower today)
   int heavy_div_ = 8;            // heavy when a bitmap level's edges >= nnz / heavy_div_ (0: off)
   int dyn_smem_ = 0;
