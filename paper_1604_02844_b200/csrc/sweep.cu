@@ -412,8 +412,9 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
             for (int q = 0; q < 4; ++q) {
               uint32_t bit;
               asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(e4[q]));
-              asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(hoff + (((uint32_t)e4[q] >> 3) & ~3u)), "r"(bit)
-                           : "memory");
+              if (!(s.dbg_flags & 1))
+                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(hoff + (((uint32_t)e4[q] >> 3) & ~3u)), "r"(bit)
+                             : "memory");
             }
           } else {
 #pragma unroll
@@ -424,12 +425,12 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
               const bool ok = (vm >> q) & 1u;
               const bool hot = v < hv;
               const uint32_t sa = (ok && hot) ? hoff + (((uint32_t)v >> 3) & ~3u) : dummy;
-              asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sa), "r"(bit) : "memory");
+              if (!(s.dbg_flags & 1)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sa), "r"(bit) : "memory");
               asm volatile(
                   "{\n\t.reg .pred p;\n\t"
                   "setp.ne.u32 p, %2, 0;\n\t"
                   "@p red.relaxed.gpu.global.or.b32 [%0], %1;\n\t}" ::"l"(s.visited + (v >> 5)),
-                  "r"(bit), "r"((uint32_t)(ok && !hot))
+                  "r"(bit), "r"((uint32_t)(ok && !hot && !(s.dbg_flags & 2)))
                   : "memory");
             }
           }

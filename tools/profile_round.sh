@@ -12,6 +12,7 @@ timeout -k 10 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 
     --log-file gpurun_out/${R}_launches.csv $CMD > gpurun_out/${R}_launches.log 2>&1
 WARM_S=0 timeout -k 10 120 python tools/quick_bfs_time.py 24 1 > gpurun_out/${R}_one.log 2>&1
 WARM_S=0 timeout -k 10 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_expand|k_compact" -c 24 -o gpurun_out/${R}_full python tools/quick_bfs_time.py 24 1 \
+    -k regex:"k_expand|k_compact|k_sweep|k_merge|k_levels|k_resolve|k_finalize|k_init" -c 40 \
+    -o gpurun_out/${R}_full python tools/quick_bfs_time.py 24 1 \
     > gpurun_out/${R}_full.log 2>&1
 echo done
