@@ -191,7 +191,7 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, const int32_t (
   for (int k = 0; k < K; ++k) {
     const bool w = ((win >> k) & 1u) && nb[k] < a.t_cta;
     if (!__any_sync(kFull, w)) continue;
-    const int items = w ? (deg[k] + kChunk - 1) / kChunk : 0;
+    const int items = w ? (deg[k] + a.qchunk - 1) / a.qchunk : 0;
     const int32_t vo = w ? __ldg(a.new2old + nb[k]) : 0;
     int inc = items;
 #pragma unroll
@@ -205,7 +205,7 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, const int32_t (
     base = __shfl_sync(kFull, base, 31);
     const int off = inc - items;
     for (int j = 0; j < items; ++j)
-      a.next_cta[base + off + j] = CtaItem{st[k] + (int64_t)j * kChunk, min(kChunk, deg[k] - j * kChunk), vo};
+      a.next_cta[base + off + j] = CtaItem{st[k] + (int64_t)j * a.qchunk, min(a.qchunk, deg[k] - j * a.qchunk), vo};
   }
 }
 
@@ -1453,9 +1453,9 @@ __device__ __forceinline__ void seed_root(const LevelArgs& a, uint32_t* prev, co
     c.discovered = 1;
     c.edges = (unsigned long long)deg;
     if (l < a.t_cta) {
-      const int items = (deg + kChunk - 1) / kChunk;
+      const int items = (deg + a.qchunk - 1) / a.qchunk;
       for (int k = 0; k < items; ++k)
-        a.next_cta[k] = CtaItem{st + (int64_t)k * kChunk, min(kChunk, deg - k * kChunk), root_orig};
+        a.next_cta[k] = CtaItem{st + (int64_t)k * a.qchunk, min(a.qchunk, deg - k * a.qchunk), root_orig};
       c.bin[kBinCta] = (unsigned long long)items;
     } else if (l < a.t_warp) {
       a.next_warp[0] = l;
@@ -1771,7 +1771,7 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   }
   // Bins, double-buffered: a vertex enters a bin once per BFS, so n entries
   // bound the small/warp bins; CTA items <= nnz/kChunk + #(deg >= kCtaMin).
-  cap_cta_ = nnz_loc_ / kChunk + t_cta_ + 2;
+  cap_cta_ = nnz_loc_ / kQChunkMin + t_cta_ + 2;
   // group items: one per started kItemElems of each 32-entry group, per block
   cap_items_ = nnz_loc_ / kItemElems + n_loc_ / 32 + 2 * ((n_loc_ + kCompactVerts - 1) / kCompactVerts) + 16;
   for (int b = 0; b < 2; ++b) {
@@ -1986,6 +1986,10 @@ LevelArgs BfsEngine::level_args() const {
   a.t_nz = t_nz_;
   a.part_log = part_log_;
   a.part_rank = part_rank_;
+  // queue-mode hub items: small enough that a hub's row spreads over many
+  // warps (a queue level is latency-bound per slice, not bandwidth-bound)
+  const char* qc = getenv("LBFS_QCHUNK");
+  a.qchunk = std::min(kChunk, std::max(kQChunkMin, qc ? atoi(qc) : kQChunkDefault)) & ~3;
   return a;
 }
 
@@ -2159,8 +2163,18 @@ void BfsEngine::merge_hot(cudaStream_t st) {
   LBFS_LAUNCH(k_merge_hot, grid, 256, 0, st, reinterpret_cast<const uint4*>(stage_), expand_grid_, hw4, visited_);
 }
 
+void BfsEngine::gap_mark(cudaStream_t st) {
+  if (!gaps_) return;
+  if (gap_ev_.empty()) {
+    gap_ev_.resize(256);
+    for (auto& e : gap_ev_) LBFS_CUDA(cudaEventCreate(&e));
+  }
+  if (n_gap_ < (int)gap_ev_.size()) LBFS_CUDA(cudaEventRecord(gap_ev_[n_gap_++], st));
+}
+
 void BfsEngine::read_env() {
   trace_ = env_flag("LBFS_TRACE");  // per-level table on stderr
+  gaps_ = env_flag("LBFS_GAPS");
   count_ = env_flag("LBFS_COUNT");  // candidate-write counters (slow)
   {  // heavy levels: bitmap levels with edges >= nnz / LBFS_HEAVY_DIV (0: off)
     const char* hd = getenv("LBFS_HEAVY_DIV");
@@ -2307,6 +2321,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   const int64_t launches0 = g_launches.load();
   cudaStream_t st = stream_;
   n_loop_ev_ = 0;
+  n_gap_ = 0;
   LBFS_CUDA(cudaEventRecord(ev_[0], st));
   {  // K4: bitmaps + internal levels (outputs are written once, by k_finalize)
     const unsigned grid = clamp_grid((n_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
@@ -2367,9 +2382,11 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       p.seq_value = ++seq_;
       const int le = n_loop_ev_ < kLoopEvents ? n_loop_ev_++ : -1;  // segment timing, read after the BFS
       if (le >= 0) LBFS_CUDA(cudaEventRecord(ev_loop_[2 * le], st));
+      gap_mark(st);
       void* args[] = {(void*)&a, (void*)&p};
       LBFS_CUDA(cudaLaunchCooperativeKernel((const void*)k_levels, dim3(loop_grid_), dim3(kLoopThreads), args, 0, st));
       g_launches.fetch_add(1);
+      gap_mark(st);
       if (le >= 0) LBFS_CUDA(cudaEventRecord(ev_loop_[2 * le + 1], st));
       if (trace_) LBFS_CUDA(cudaEventRecord(ev_gap_, st));
       wait_mail(p.seq_value, st);
@@ -2405,6 +2422,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     const bool bitmap = c.edges >= bitmap_min_edges;
     const bool heavy = bitmap && stage_ && heavy_div_ > 0 && c.edges * (unsigned long long)heavy_div_ >= (unsigned long long)nnz_;
     LBFS_CUDA(cudaEventRecord(ev_[2], st));
+    gap_mark(st);
     float gap_ms = -1.f;
     const unsigned grid = expand_level(a, c, heavy ? kHeavy : bitmap ? kBitmapOut : kQueueOut, prev_bitmap, cur, L, st);
     if (heavy) merge_hot(st);
@@ -2412,6 +2430,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     if (bitmap) compact_level(cur, L, nullptr, st, heavy);
     LBFS_CUDA(cudaEventRecord(ev_[5], st));
     publish_and_wait(slot, (int)((L + 2) % kCounterRing), st);
+    gap_mark(st);
     LBFS_CUDA(cudaEventSynchronize(ev_[5]));
     if (trace_) {
       LBFS_CUDA(cudaEventSynchronize(ev_[2]));
@@ -2466,6 +2485,28 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   }
   LBFS_CUDA(cudaEventRecord(ev_[4], st));
   LBFS_CUDA(cudaEventSynchronize(ev_[4]));
+  if (gaps_ && n_gap_ > 0) {  // segments: [start, end) per level or device-loop run; gaps between them
+    std::string line = "[lbfs] gaps:";
+    float first = 0.f, tot = 0.f, busy = 0.f;
+    LBFS_CUDA(cudaEventElapsedTime(&first, ev_[0], gap_ev_[0]));
+    char buf[96];
+    snprintf(buf, sizeof(buf), " init->L0 %.1fus |", first * 1e3f);
+    line += buf;
+    for (int i = 0; i + 1 < n_gap_; i += 2) {
+      float span = 0.f, gap = 0.f;
+      LBFS_CUDA(cudaEventElapsedTime(&span, gap_ev_[i], gap_ev_[i + 1]));
+      if (i + 2 < n_gap_) LBFS_CUDA(cudaEventElapsedTime(&gap, gap_ev_[i + 1], gap_ev_[i + 2]));
+      else LBFS_CUDA(cudaEventElapsedTime(&gap, gap_ev_[i + 1], ev_[4]));
+      snprintf(buf, sizeof(buf), " %.1f+%.1f", span * 1e3f, gap * 1e3f);
+      line += buf;
+      busy += span;
+      tot += gap;
+    }
+    snprintf(buf, sizeof(buf), " | busy %.1fus gaps %.1fus (us: span+gap after)", busy * 1e3f, tot * 1e3f);
+    line += buf;
+    fprintf(stderr, "%s\n", line.c_str());
+    n_gap_ = 0;
+  }
   for (int i = 0; i < n_loop_ev_; ++i) {  // device-loop segments
     float ms = 0.f;
     LBFS_CUDA(cudaEventElapsedTime(&ms, ev_loop_[2 * i], ev_loop_[2 * i + 1]));

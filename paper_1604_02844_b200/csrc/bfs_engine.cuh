@@ -16,6 +16,11 @@ namespace lbfs {
 constexpr int32_t kSentinel = LBFS_SENTINEL;  // traversal.py:22
 constexpr int kSmallMax = 32;                 // deg < 32: warp-cooperative small bin
 constexpr int kCtaMin = 1024;                 // deg >= 1024: CTA bin (TMA-staged chunks)
+constexpr int kQChunkMin = 128;              // smallest queue-mode hub item (sizes the item buffers)
+#ifndef LBFS_QCHUNK_DEFAULT
+#define LBFS_QCHUNK_DEFAULT 512
+#endif
+constexpr int kQChunkDefault = LBFS_QCHUNK_DEFAULT;  // default queue-mode hub item (LBFS_QCHUNK overrides)
 constexpr int kChunk = 3960;                  // edges per CTA-bin item (<= 992 staged int4 slots)
 constexpr int kBinSmall = 0, kBinWarp = 1, kBinCta = 2, kBinItems = 3, kBinWSlice = 4;
 constexpr int kItemElems = 512;               // elements per group item (load balance unit)
@@ -120,6 +125,7 @@ struct LevelArgs {
   int32_t* next_small;
   int32_t* next_warp;
   CtaItem* next_cta;
+  int32_t qchunk;           // edges per hub item appended by a queue-mode winner (<= kChunk)
   // heavy bitmap levels (k_expand<kHeavy>): each CTA ORs hot targets blindly
   // into its zeroed shared copy of the hot prefix and leaves it in row
   // blockIdx.x of stage (hot_words words per row); stage_first: the first
@@ -416,6 +422,10 @@ class BfsEngine {
   int heavy_div_ = 8;            // heavy when a bitmap level's edges >= nnz / heavy_div_ (0: off)
   int dyn_smem_ = 0;
   bool trace_ = false;  // LBFS_TRACE=1: per-level table on stderr
+  bool gaps_ = false;   // LBFS_GAPS=1: per-level busy span / host gap line on stderr (no syncs added)
+  std::vector<cudaEvent_t> gap_ev_;  // LBFS_GAPS: [2i] segment start, [2i+1] segment end
+  int n_gap_ = 0;
+  void gap_mark(cudaStream_t st);
   bool count_ = false;
   bool split_ = false;
   bool hub_ldg_ = false;  // LBFS_SPLIT=1: one launch per bin, timed separately
