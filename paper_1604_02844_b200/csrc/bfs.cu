@@ -1138,7 +1138,7 @@ __device__ __forceinline__ int scan128(int t, int bar, int val, int* s_w, int* t
 
 struct CompactSmem {
   unsigned long long base[4];
-  unsigned long long red[2][kCompactThreads / 32];
+  unsigned long long red[3][kCompactThreads / 32];
   uint32_t new_[kCompactWords];
   uint32_t lmask[kCompactWords];
   int32_t lpre[kCompactWords];
@@ -1202,7 +1202,7 @@ __device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk,
   gsync(bar);
   // pass 2: thread t owns vertices v0 + t + 256 j (bit t&31 of word t/32 + 8 j);
   // four vertices' loads are issued before any of their stores
-  unsigned long long edges = 0;
+  unsigned long long edges = 0, big = 0;
   const int b = t & 31;
 #pragma unroll
   for (int j0 = 0; j0 < kCompactSteps; j0 += 4) {
@@ -1226,6 +1226,7 @@ __device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk,
       c.level_int[v] = c.next_level;  // coalesced; outputs are written by k_finalize
       const int32_t deg = (int32_t)(en[q] - st[q]);
       edges += (unsigned long long)deg;
+      if (v < c.t_warp) big += (unsigned long long)deg;
       const uint32_t wm = s_wmask[wl];
       if ((wm >> b) & 1u)  // warp-bin row: one slice, parent = the row's vertex
         c.next_wslice[s_base[3] + s_wpre[wl] + __popc(wm & ((1u << b) - 1u))] =
@@ -1330,25 +1331,29 @@ __device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk,
     gi.pad = 0;
     c.next_items[s_base[2] + gpre + k] = gi;
   }
-  unsigned long long e = edges, d = (unsigned long long)__popc(nb);
+  unsigned long long e = edges, d = (unsigned long long)__popc(nb), bg = big;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     e += __shfl_xor_sync(kFull, e, o);
     d += __shfl_xor_sync(kFull, d, o);
+    bg += __shfl_xor_sync(kFull, bg, o);
   }
   if (lane == 0) {
     sm.red[0][warp] = e;
     sm.red[1][warp] = d;
+    sm.red[2][warp] = bg;
   }
   gsync(bar);
   if (t == 0) {
-    unsigned long long e_tot = 0, d_tot = 0;
+    unsigned long long e_tot = 0, d_tot = 0, b_tot = 0;
     for (int k = 0; k < kCompactThreads / 32; ++k) {
       e_tot += sm.red[0][k];
       d_tot += sm.red[1][k];
+      b_tot += sm.red[2][k];
     }
     if (e_tot) atomicAdd(&c.next_cnt->edges, e_tot);
     if (d_tot) atomicAdd(&c.next_cnt->discovered, d_tot);
+    if (b_tot) atomicAdd(&c.next_cnt->big_edges, b_tot);
   }
 }
 
@@ -2043,7 +2048,10 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
                                   (int64_t)1});
   const unsigned grid = bitmap ? (unsigned)expand_grid_ : clamp_grid(need, expand_grid_);
   // heavy level after a bitmap level: the big-row region is swept whole (sweep.cu)
-  const bool sweep = mode == kHeavy && prev_bitmap && side_ && sweep_fits_ && !sweep_off_;
+  // (only when the frontier's big rows hold enough of the region's edges:
+  // below that the sweep streams mostly rows outside the frontier)
+  const bool sweep = mode == kHeavy && prev_bitmap && side_ && sweep_fits_ && !sweep_off_ &&
+                     c.big_edges * 100ull >= (unsigned long long)e_big_ * (unsigned long long)sweep_min_pct_;
   sweep_used_ = sweep;
   if (sweep) {
     if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[0], st));
@@ -2175,10 +2183,18 @@ void BfsEngine::gap_mark(cudaStream_t st) {
 void BfsEngine::read_env() {
   trace_ = env_flag("LBFS_TRACE");  // per-level table on stderr
   gaps_ = env_flag("LBFS_GAPS");
+  {
+    const char* bd = getenv("LBFS_BITMAP_DIV");  // bitmap mode when a frontier has >= n / this many edges
+    bitmap_div_ = std::max(1, bd ? atoi(bd) : kBitmapDiv);
+  }
+  {
+    const char* sm = getenv("LBFS_SWEEP_MIN");  // sweep when big-row frontier edges >= this % of the region
+    sweep_min_pct_ = sm ? atoi(sm) : kSweepMinPct;
+  }
   count_ = env_flag("LBFS_COUNT");  // candidate-write counters (slow)
   {  // heavy levels: bitmap levels with edges >= nnz / LBFS_HEAVY_DIV (0: off)
     const char* hd = getenv("LBFS_HEAVY_DIV");
-    heavy_div_ = hd ? atoi(hd) : 8;
+    heavy_div_ = hd ? atoi(hd) : kHeavyDiv;
   }
   split_ = env_flag("LBFS_SPLIT");  // one launch per bin
   dense_off_ = env_flag("LBFS_NO_DENSE");  // experiment: always use the small-bin list
@@ -2216,7 +2232,7 @@ void BfsEngine::run_mega(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_t
   p.state = loop_;
   p.max_levels = kLoopCap;
   if (const char* ml = getenv("LBFS_MEGA_LEVELS")) p.max_levels = std::max(1, atoi(ml));  // debug: levels per launch
-  p.bitmap_min_edges = (unsigned long long)std::max<int64_t>(1 << 16, n_ / 64);
+  p.bitmap_min_edges = (unsigned long long)std::max<int64_t>(1 << 16, n_ / bitmap_div_);
   p.small_region = (int64_t)t_nz_ - t_warp_;
   p.dense_off = dense_off_ ? 1 : 0;
   p.hot_words = env_flag("LBFS_MEGA_NOHOT") ? 0 : hot_words_;  // debug
@@ -2350,7 +2366,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   layers_.clear();
   double expand_ms = 0.0;
   bool prev_bitmap = false;
-  const unsigned long long bitmap_min_edges = (unsigned long long)std::max<int64_t>(1 << 16, n_ / 64);
+  const unsigned long long bitmap_min_edges = (unsigned long long)std::max<int64_t>(1 << 16, n_ / bitmap_div_);
   int64_t L = 0;
   for (;;) {
     const Counters c = h_cnt_[L % kCounterRing];
@@ -2458,9 +2474,10 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     }
     if (trace_)
       fprintf(stderr,
-              "[lbfs] L%-3lld %s in=%-9llu edges=%-10llu bins(s|list/w/c/items)=%llu/%llu/%llu/%llu grid=%u "
+              "[lbfs] L%-3lld %s in=%-9llu edges=%-10llu big=%-10llu bins(s|list/w/c/items/ws)=%llu/%llu/%llu/%llu/%llu grid=%u "
               "expand=%.3fms compact=%.3fms disc=%llu gap_before=%.3fms\n",
-              (long long)L, heavy ? "heavy " : bitmap ? "bitmap" : "queue ", c.discovered, c.edges, c.bin[0], c.bin[1], c.bin[2], c.bin[3],
+              (long long)L, heavy ? (sweep_used_ ? "sweep " : "heavy ") : bitmap ? "bitmap" : "queue ", c.discovered, c.edges,
+              c.big_edges, c.bin[0], c.bin[1], c.bin[2], c.bin[3], c.bin[4],
               grid, ms, bitmap ? cms : 0.f, nx.discovered, gap_ms);
     layers_.push_back(lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, (int64_t)nx.discovered});
     cur ^= 1;

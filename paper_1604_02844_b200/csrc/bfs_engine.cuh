@@ -52,7 +52,8 @@ struct alignas(64) Counters {
   unsigned long long bin[5];  // small queue | small list, warp queue, hub slices, group items, warp slices
   unsigned long long discovered;
   unsigned long long edges;
-  unsigned long long pad[1];
+  unsigned long long pad[1];       // (mailbox copy of k_levels: the level it stopped at)
+  unsigned long long big_edges;    // bitmap-mode frontier: edges of its rows with degree >= 32 (the sweep region)
 };
 
 // A balanced unit of non-hub work: up to 32 consecutive entries of the
@@ -240,6 +241,15 @@ constexpr int kSweepThreads = 32 * (kSweepConsumers + kSweepProducers);
 #define LBFS_SWEEP_STAGES 4
 #endif
 constexpr int kSweepStages = LBFS_SWEEP_STAGES;  // ring depth (16 KB chunks)
+#ifndef LBFS_SWEEP_MIN_PCT
+#define LBFS_SWEEP_MIN_PCT 30
+#endif
+#ifndef LBFS_BITMAP_DIV
+#define LBFS_BITMAP_DIV 16
+#endif
+constexpr int kBitmapDiv = LBFS_BITMAP_DIV;  // bitmap-mode output when a frontier's edges >= max(2^16, n / this)
+constexpr int kHeavyDiv = 32;  // heavy (blind-OR) semantics when a bitmap level's edges >= nnz / this
+constexpr int kSweepMinPct = LBFS_SWEEP_MIN_PCT;  // sweep a heavy level when its big-row edges >= this % of e_big
 constexpr int kSweepPrefetch = 0;    // L2 prefetch distance (chunks of a CTA)
 constexpr int kSweepRingBytes = kSweepStages * 32 * kSweepWindow * 4;
 struct SweepArgs {
@@ -419,9 +429,11 @@ class BfsEngine {
   cudaEvent_t ev_resolve_ = nullptr, ev_side_done_ = nullptr;
   bool side_pending_ = false;
   bool sweep_small_ = false;     // LBFS_SWEEP_SMALL=1: sweep the small region as well (slower today)
-  int heavy_div_ = 8;            // heavy when a bitmap level's edges >= nnz / heavy_div_ (0: off)
+  int heavy_div_ = kHeavyDiv;    // heavy when a bitmap level's edges >= nnz / heavy_div_ (0: off)
   int dyn_smem_ = 0;
   bool trace_ = false;  // LBFS_TRACE=1: per-level table on stderr
+  int sweep_min_pct_ = kSweepMinPct;
+  int bitmap_div_ = kBitmapDiv;
   bool gaps_ = false;   // LBFS_GAPS=1: per-level busy span / host gap line on stderr (no syncs added)
   std::vector<cudaEvent_t> gap_ev_;  // LBFS_GAPS: [2i] segment start, [2i+1] segment end
   int n_gap_ = 0;

@@ -396,44 +396,20 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
     uint32_t ph = 0;
     for (int64_t i = 0; i < my_chunks; ++i) {
       bar_wait(&sm.full[st], ph);
-      if (!(s.dbg_flags & 4)) {
-        const int32_t* buf = ring + (size_t)st * kChunkWins * kWin;
+      // copy this warp's windows (elements + valid nibble) into registers and
+      // release the stage at once: the TMA refill of the stage overlaps the
+      // ORs below instead of waiting for them
+      int4 x[kWinPerWarp];
+      uint32_t vm[kWinPerWarp];
+      const int32_t* buf = ring + (size_t)st * kChunkWins * kWin;
 #pragma unroll
-        for (int j = 0; j < kWinPerWarp; ++j) {
-          const uint32_t info = sm.meta[st][wb + j].info;
-          if ((info >> 8) == 0) continue;  // (warp-uniform) no row of the window in the frontier
-          const int4 x = reinterpret_cast<const int4*>(buf + (wb + j) * kWin)[lane];
-          const int32_t e4[4] = {x.x, x.y, x.z, x.w};
-          const uint32_t vm = (sm.meta[st][wb + j].vmask[lane >> 3] >> (4 * (lane & 7))) & 0xFu;
-          const int32_t mx = max(max(e4[0], e4[1]), max(e4[2], e4[3]));
-          if (__all_sync(kAll, vm == 0xFu && mx < hv)) {
-            // whole window valid and hot: one shared OR per element
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t bit;
-              asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(e4[q]));
-              if (!(s.dbg_flags & 1))
-                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(hoff + (((uint32_t)e4[q] >> 3) & ~3u)), "r"(bit)
-                             : "memory");
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int32_t v = e4[q];
-              uint32_t bit;
-              asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(v));
-              const bool ok = (vm >> q) & 1u;
-              const bool hot = v < hv;
-              const uint32_t sa = (ok && hot) ? hoff + (((uint32_t)v >> 3) & ~3u) : dummy;
-              if (!(s.dbg_flags & 1)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sa), "r"(bit) : "memory");
-              asm volatile(
-                  "{\n\t.reg .pred p;\n\t"
-                  "setp.ne.u32 p, %2, 0;\n\t"
-                  "@p red.relaxed.gpu.global.or.b32 [%0], %1;\n\t}" ::"l"(s.visited + (v >> 5)),
-                  "r"(bit), "r"((uint32_t)(ok && !hot && !(s.dbg_flags & 2)))
-                  : "memory");
-            }
-          }
+      for (int j = 0; j < kWinPerWarp; ++j) {
+        const uint32_t info = sm.meta[st][wb + j].info;
+        vm[j] = 0u;
+        x[j] = make_int4(0, 0, 0, 0);
+        if ((info >> 8) != 0 && !(s.dbg_flags & 4)) {  // (warp-uniform) some row of the window is in the frontier
+          x[j] = reinterpret_cast<const int4*>(buf + (wb + j) * kWin)[lane];
+          vm[j] = (sm.meta[st][wb + j].vmask[lane >> 3] >> (4 * (lane & 7))) & 0xFu;
         }
       }
       __syncwarp();
@@ -441,6 +417,40 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
       if (++st == kStages) {
         st = 0;
         ph ^= 1u;
+      }
+#pragma unroll
+      for (int j = 0; j < kWinPerWarp; ++j) {
+        if (!__any_sync(kAll, vm[j] != 0u)) continue;
+        const int32_t e4[4] = {x[j].x, x[j].y, x[j].z, x[j].w};
+        const int32_t mx = max(max(e4[0], e4[1]), max(e4[2], e4[3]));
+        if (__all_sync(kAll, vm[j] == 0xFu && mx < hv)) {
+          // whole window valid and hot: one shared OR per element
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t bit;
+            asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(e4[q]));
+            if (!(s.dbg_flags & 1))
+              asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(hoff + (((uint32_t)e4[q] >> 3) & ~3u)), "r"(bit)
+                           : "memory");
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int32_t v = e4[q];
+            uint32_t bit;
+            asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(v));
+            const bool ok = (vm[j] >> q) & 1u;
+            const bool hot = v < hv;
+            const uint32_t sa = (ok && hot) ? hoff + (((uint32_t)v >> 3) & ~3u) : dummy;
+            if (!(s.dbg_flags & 1)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sa), "r"(bit) : "memory");
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.u32 p, %2, 0;\n\t"
+                "@p red.relaxed.gpu.global.or.b32 [%0], %1;\n\t}" ::"l"(s.visited + (v >> 5)),
+                "r"(bit), "r"((uint32_t)(ok && !hot && !(s.dbg_flags & 2)))
+                : "memory");
+          }
+        }
       }
     }
   }
