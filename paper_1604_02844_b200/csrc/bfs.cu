@@ -917,7 +917,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
   flush_acc<M>(a, acc);
   hot_drain(s);
   if constexpr (M == kHeavy) {  // this CTA's blind ORs -> its stage row
-    uint4* row = reinterpret_cast<uint4*>(a.stage) + (size_t)blockIdx.x * hw4;
+    uint4* row = reinterpret_cast<uint4*>(a.stage) + (size_t)blockIdx.x * (a.stage_words >> 2);
     for (int i = threadIdx.x; i < hw4; i += blockDim.x) {
       uint4 x = h4[i];
       if (!a.stage_first) {
@@ -933,7 +933,7 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
 // grid (ceil(hw4 / 256), ceil(rows / kMergeRows)): a thread ORs kMergeRows
 // rows of one 16-byte column and folds the result in with red.or.
 constexpr int kMergeRows = 16;
-__global__ void __launch_bounds__(256) k_merge_hot(const uint4* __restrict__ stage, int rows, int hw4,
+__global__ void __launch_bounds__(256) k_merge_hot(const uint4* __restrict__ stage, int rows, int hw4, int stride4,
                                                    uint32_t* __restrict__ visited) {
   const int i = blockIdx.x * 256 + threadIdx.x;
   if (i >= hw4) return;
@@ -941,7 +941,7 @@ __global__ void __launch_bounds__(256) k_merge_hot(const uint4* __restrict__ sta
   uint4 x = make_uint4(0, 0, 0, 0);
 #pragma unroll 8
   for (int r = r0; r < r1; ++r) {
-    const uint4 y = __ldcg(stage + (size_t)r * hw4 + i);
+    const uint4 y = __ldcg(stage + (size_t)r * stride4 + i);
     x.x |= y.x, x.y |= y.y, x.z |= y.z, x.w |= y.w;
   }
   uint32_t* w = visited + 4 * (size_t)i;
@@ -1833,13 +1833,18 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<kBitmapOut, 2>, kExpandThreads, dyn_smem_));
   expand_grid_ = sm_count_ * std::max(occ, 1);
   if (nparts_ == 1 && hot_words_ >= 4) {
-    stage_ = dev_alloc<uint32_t>((size_t)expand_grid_ * hot_words_);
+    // the sweep has no per-warp rings: its hot prefix takes what its own ring leaves
     cudaFuncAttributes fs{};
     LBFS_CUDA(cudaFuncGetAttributes(&fs, (const void*)k_sweep));
-    sweep_fits_ = (int64_t)fs.sharedSizeBytes + kSweepRingBytes + (int64_t)hot_words_ * 4 <= optin;
+    const int64_t sw_avail = (int64_t)optin - (int64_t)fs.sharedSizeBytes - kSweepRingBytes;
+    sweep_hot_words_ = (int32_t)std::max<int64_t>(
+        hot_words_, std::min<int64_t>((sw_avail / 4) & ~int64_t(3), (nwords_ + 3) & ~int64_t(3)));
+    if (getenv("LBFS_SWEEP_HOT_SAME")) sweep_hot_words_ = hot_words_;  // (experiment)
+    stage_ = dev_alloc<uint32_t>((size_t)expand_grid_ * sweep_hot_words_);
+    sweep_fits_ = (int64_t)fs.sharedSizeBytes + kSweepRingBytes + (int64_t)sweep_hot_words_ * 4 <= optin;
     if (sweep_fits_)
       LBFS_CUDA(cudaFuncSetAttribute((const void*)k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kSweepRingBytes + hot_words_ * 4));
+                                     kSweepRingBytes + sweep_hot_words_ * 4));
   }
   // device-side level loop: one co-resident CTA per SM (cooperative launch)
   int coop = 0, locc = 0;
@@ -2003,6 +2008,7 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
   const bool bitmap = mode != kQueueOut;
   a.stage = stage_;
   a.stage_first = 1;
+  a.stage_words = sweep_hot_words_;
   a.next_level = (int32_t)(L + 1);
   a.next_cnt = &cnt_[(L + 1) % kCounterRing];
   a.next_small = q_small_[cur ^ 1];
@@ -2053,6 +2059,7 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
   const bool sweep = mode == kHeavy && prev_bitmap && side_ && sweep_fits_ && !sweep_off_ &&
                      c.big_edges * 100ull >= (unsigned long long)e_big_ * (unsigned long long)sweep_min_pct_;
   sweep_used_ = sweep;
+  merge_wide_ = sweep;
   if (sweep) {
     if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[0], st));
     LBFS_LAUNCH(k_sweep_plan, clamp_grid((n_side_win_ + 255) / 256, (int64_t)sm_count_ * 16), 256, 0, st, side_, front_,
@@ -2068,9 +2075,9 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
     SweepArgs sa{col_idx_, side_, n_side_win_, e_big_, sweep_small ? n_win_all_ : n_side_win_,
                  sweep_small ? e_nz_ : e_big_, sweep_small ? w_small0_ : n_win_all_ + 1, svmask_, front_, win_info_,
                  visited_, pred_int_, new2old_loc_,
-                 stage_, 1, hot_words_, getenv("LBFS_SWEEP_PF") ? atoi(getenv("LBFS_SWEEP_PF")) : kSweepPrefetch,
+                 stage_, 1, sweep_hot_words_, getenv("LBFS_SWEEP_PF") ? atoi(getenv("LBFS_SWEEP_PF")) : kSweepPrefetch,
                  getenv("LBFS_SWEEP_DBG") ? atoi(getenv("LBFS_SWEEP_DBG")) : 0};
-    LBFS_LAUNCH(k_sweep, (unsigned)expand_grid_, kSweepThreads, kSweepRingBytes + hot_words_ * 4, st, sa);
+    LBFS_LAUNCH(k_sweep, (unsigned)expand_grid_, kSweepThreads, kSweepRingBytes + sweep_hot_words_ * 4, st, sa);
     a.stage_first = 0;
     f.n_cta = 0;
     f.n_wslice = 0;
@@ -2166,9 +2173,11 @@ __global__ void __launch_bounds__(256) k_resolve(const int32_t* __restrict__ lev
 }
 
 void BfsEngine::merge_hot(cudaStream_t st) {
-  const int hw4 = hot_words_ / 4;
+  // (the sweep stores whole rows first in its level; expand kernels alone write only their prefix)
+  const int hw4 = (merge_wide_ ? sweep_hot_words_ : hot_words_) / 4;
   const dim3 grid((unsigned)((hw4 + 255) / 256), (unsigned)((expand_grid_ + kMergeRows - 1) / kMergeRows));
-  LBFS_LAUNCH(k_merge_hot, grid, 256, 0, st, reinterpret_cast<const uint4*>(stage_), expand_grid_, hw4, visited_);
+  LBFS_LAUNCH(k_merge_hot, grid, 256, 0, st, reinterpret_cast<const uint4*>(stage_), expand_grid_, hw4,
+              sweep_hot_words_ / 4, visited_);
 }
 
 void BfsEngine::gap_mark(cudaStream_t st) {

@@ -133,6 +133,7 @@ struct LevelArgs {
   // launch of the level stores the row, later launches OR into it
   uint32_t* stage;
   int32_t stage_first;
+  int32_t stage_words;      // row stride of stage (>= the kernel's hot words: the sweep's prefix can be longer)
 };
 
 struct CompactArgs {
@@ -413,6 +414,8 @@ class BfsEngine {
   LoopState* loop_ = nullptr;
   LoopState* h_loop_ = nullptr;     // pinned
   int32_t hot_words_ = 0;  // visited words mirrored in shared memory
+  int32_t sweep_hot_words_ = 0;  // the sweep's (longer) hot prefix; also the stage row stride
+  bool merge_wide_ = false;      // this level's stage rows hold the sweep's prefix
   uint32_t* stage_ = nullptr;    // heavy levels: expand_grid_ rows of hot_words_ words
   uint2* side_ = nullptr;        // sweep side entries (nparts 1)
   int32_t* first_nbr_ = nullptr; // first neighbour of each row (heavy-level parent resolution)

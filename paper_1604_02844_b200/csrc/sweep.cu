@@ -28,12 +28,20 @@
 
 #include "bfs_engine.cuh"
 
+#ifndef LBFS_SWEEP_DBG
+#define LBFS_SWEEP_DBG 0  // experiments (wrong results): 1 no hot ORs, 2 no cold ORs, 4 consumers skip the data
+#endif
+
 namespace lbfs {
 
 namespace {
 
 constexpr unsigned kAll = 0xFFFFFFFFu;
 constexpr int kWin = kSweepWindow;  // elements per window
+constexpr int kSweepDbg = LBFS_SWEEP_DBG;
+#ifndef LBFS_SWEEP_HOTCHK
+#define LBFS_SWEEP_HOTCHK 0
+#endif
 
 __device__ __forceinline__ int4 ld_stream4(const int32_t* p) {
   int4 v;
@@ -309,13 +317,28 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
     const int64_t i0 = warp - kConsumers;
     int st = (int)(i0 % kStages);
     uint32_t ph = (uint32_t)((i0 / kStages) & 1);
-    for (int64_t i = i0; i < my_chunks; i += kSweepProducers) {
+    // the side entry / window info / small mask of a chunk are loaded one
+    // iteration ahead, so their latency overlaps the wait for a free stage
+    auto win_of = [&](int64_t i) {
       const int64_t w0 = (blockIdx.x + i * gridDim.x) * kChunkWins;
-      const int64_t w = w0 + lane < s.nwin_all ? w0 + lane : -1;
+      return w0 + lane < s.nwin_all ? w0 + lane : (int64_t)-1;
+    };
+    uint2 n_sd = make_uint2(0u, kAll);
+    uint32_t n_info = 0u;
+    uint4 n_sv = make_uint4(0u, 0u, 0u, 0u);
+    auto load_win = [&](int64_t w) {
       const bool big = w >= 0 && w < s.nwin, small = w >= s.w_small0;
-      const uint2 sd = big ? __ldg(s.side + w) : make_uint2(0u, kAll);
-      uint32_t info = big ? __ldcg(s.info + w) : 0u;
-      const uint4 sv = small ? __ldcg(s.svmask + (w - s.w_small0)) : make_uint4(0u, 0u, 0u, 0u);
+      n_sd = big ? __ldg(s.side + w) : make_uint2(0u, kAll);
+      n_info = big ? __ldcg(s.info + w) : 0u;
+      n_sv = small ? __ldcg(s.svmask + (w - s.w_small0)) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    if (i0 < my_chunks) load_win(win_of(i0));
+    for (int64_t i = i0; i < my_chunks; i += kSweepProducers) {
+      const int64_t w = win_of(i);
+      const uint2 sd = n_sd;
+      uint32_t info = n_info;
+      const uint4 sv = n_sv;
+      if (i + kSweepProducers < my_chunks) load_win(win_of(i + kSweepProducers));
       if (s.prefetch > 0 && lane == 0 && i + s.prefetch < my_chunks) {
         // warm L2 with the chunk s.prefetch ahead (whole chunk: its windows'
         // codes are not known yet), so the bulk copy later is an L2 hit
@@ -407,7 +430,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
         const uint32_t info = sm.meta[st][wb + j].info;
         vm[j] = 0u;
         x[j] = make_int4(0, 0, 0, 0);
-        if ((info >> 8) != 0 && !(s.dbg_flags & 4)) {  // (warp-uniform) some row of the window is in the frontier
+        if ((info >> 8) != 0 && !(kSweepDbg & 4)) {  // (warp-uniform) some row of the window is in the frontier
           x[j] = reinterpret_cast<const int4*>(buf + (wb + j) * kWin)[lane];
           vm[j] = (sm.meta[st][wb + j].vmask[lane >> 3] >> (4 * (lane & 7))) & 0xFu;
         }
@@ -425,15 +448,42 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
         const int32_t mx = max(max(e4[0], e4[1]), max(e4[2], e4[3]));
         if (__all_sync(kAll, vm[j] == 0xFu && mx < hv)) {
           // whole window valid and hot: one shared OR per element
+#if LBFS_SWEEP_HOTCHK
+          // skip the OR when the CTA copy already has the bit: the hottest
+          // words (the first entries of every hub row) stop taking atomics,
+          // which serialise on a shared address
+          uint32_t sa[4], bit[4], cw[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit[q]) : "r"(e4[q]));
+            sa[q] = hoff + (((uint32_t)e4[q] >> 3) & ~3u);
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw[q]) : "r"(sa[q]));
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t a = (cw[q] & bit[q]) ? dummy : sa[q];
+            if (!(kSweepDbg & 1)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(bit[q]) : "memory");
+          }
+#else
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint32_t bit;
             asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(e4[q]));
-            if (!(s.dbg_flags & 1))
+            if (!(kSweepDbg & 1))
               asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(hoff + (((uint32_t)e4[q] >> 3) & ~3u)), "r"(bit)
                            : "memory");
           }
+#endif
         } else {
+#if LBFS_SWEEP_HOTCHK
+          uint32_t sa[4], cw[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool ok = (vm[j] >> q) & 1u;
+            sa[q] = (ok && e4[q] < hv) ? hoff + (((uint32_t)e4[q] >> 3) & ~3u) : dummy;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw[q]) : "r"(sa[q]));
+          }
+#endif
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int32_t v = e4[q];
@@ -441,13 +491,17 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
             asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(v));
             const bool ok = (vm[j] >> q) & 1u;
             const bool hot = v < hv;
-            const uint32_t sa = (ok && hot) ? hoff + (((uint32_t)v >> 3) & ~3u) : dummy;
-            if (!(s.dbg_flags & 1)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sa), "r"(bit) : "memory");
+#if LBFS_SWEEP_HOTCHK
+            const uint32_t sa1 = (cw[q] & bit) ? dummy : sa[q];
+#else
+            const uint32_t sa1 = (ok && hot) ? hoff + (((uint32_t)v >> 3) & ~3u) : dummy;
+#endif
+            if (!(kSweepDbg & 1)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sa1), "r"(bit) : "memory");
             asm volatile(
                 "{\n\t.reg .pred p;\n\t"
                 "setp.ne.u32 p, %2, 0;\n\t"
                 "@p red.relaxed.gpu.global.or.b32 [%0], %1;\n\t}" ::"l"(s.visited + (v >> 5)),
-                "r"(bit), "r"((uint32_t)(ok && !hot && !(s.dbg_flags & 2)))
+                "r"(bit), "r"((uint32_t)(ok && !hot && !(kSweepDbg & 2)))
                 : "memory");
           }
         }
