@@ -2062,8 +2062,7 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
   merge_wide_ = sweep;
   if (sweep) {
     if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[0], st));
-    LBFS_LAUNCH(k_sweep_plan, clamp_grid((n_side_win_ + 255) / 256, (int64_t)sm_count_ * 16), 256, 0, st, side_, front_,
-                n_side_win_, win_info_);
+    // (window infos are computed by the sweep's producers from the side entries and front_)
     // the small region joins the sweep when most of it is in the frontier
     // (else its frontier rows go through the group items below)
     const bool sweep_small = svmask_ && f.n_dense > 0 && sweep_small_;

@@ -317,28 +317,40 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
     const int64_t i0 = warp - kConsumers;
     int st = (int)(i0 % kStages);
     uint32_t ph = (uint32_t)((i0 / kStages) & 1);
-    // the side entry / window info / small mask of a chunk are loaded one
-    // iteration ahead, so their latency overlaps the wait for a free stage
+    // per window: side entry -> frontier words of its rows -> window_info.
+    // The side entry is loaded two iterations ahead and the frontier words
+    // (which depend on it) one ahead, so neither latency meets the wait for
+    // a free stage; the small-region mask is loaded one ahead
     auto win_of = [&](int64_t i) {
       const int64_t w0 = (blockIdx.x + i * gridDim.x) * kChunkWins;
       return w0 + lane < s.nwin_all ? w0 + lane : (int64_t)-1;
     };
-    uint2 n_sd = make_uint2(0u, kAll);
-    uint32_t n_info = 0u;
-    uint4 n_sv = make_uint4(0u, 0u, 0u, 0u);
-    auto load_win = [&](int64_t w) {
-      const bool big = w >= 0 && w < s.nwin, small = w >= s.w_small0;
-      n_sd = big ? __ldg(s.side + w) : make_uint2(0u, kAll);
-      n_info = big ? __ldcg(s.info + w) : 0u;
-      n_sv = small ? __ldcg(s.svmask + (w - s.w_small0)) : make_uint4(0u, 0u, 0u, 0u);
+    auto is_big = [&](int64_t w) { return w >= 0 && w < s.nwin; };
+    auto ld_side = [&](int64_t i) {
+      const int64_t w = i < my_chunks ? win_of(i) : -1;
+      return is_big(w) ? __ldg(s.side + w) : make_uint2(0u, kAll);
     };
-    if (i0 < my_chunks) load_win(win_of(i0));
+    auto ld_front = [&](int64_t i, uint2 sd) {
+      const int64_t w = i < my_chunks ? win_of(i) : -1;
+      return is_big(w) ? make_uint2(__ldcg(s.front + (sd.x >> 5)), __ldcg(s.front + (sd.x >> 5) + 1))
+                       : make_uint2(0u, 0u);
+    };
+    auto ld_small = [&](int64_t i) {
+      const int64_t w = i < my_chunks ? win_of(i) : -1;
+      return w >= 0 && w >= s.w_small0 ? __ldcg(s.svmask + (w - s.w_small0)) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    uint2 sd1 = ld_side(i0), sd2 = ld_side(i0 + kSweepProducers);
+    uint2 fw1 = ld_front(i0, sd1);
+    uint4 sv1 = ld_small(i0);
     for (int64_t i = i0; i < my_chunks; i += kSweepProducers) {
       const int64_t w = win_of(i);
-      const uint2 sd = n_sd;
-      uint32_t info = n_info;
-      const uint4 sv = n_sv;
-      if (i + kSweepProducers < my_chunks) load_win(win_of(i + kSweepProducers));
+      const uint2 sd = sd1;
+      uint32_t info = window_info(sd, fw1, is_big(w));
+      const uint4 sv = sv1;
+      sd1 = sd2;
+      fw1 = ld_front(i + kSweepProducers, sd1);
+      sv1 = ld_small(i + kSweepProducers);
+      sd2 = ld_side(i + 2 * kSweepProducers);
       if (s.prefetch > 0 && lane == 0 && i + s.prefetch < my_chunks) {
         // warm L2 with the chunk s.prefetch ahead (whole chunk: its windows'
         // codes are not known yet), so the bulk copy later is an L2 hit
