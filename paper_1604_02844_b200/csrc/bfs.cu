@@ -1850,7 +1850,13 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   int coop = 0, locc = 0;
   LBFS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device_));
   LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&locc, k_levels, kLoopThreads, 0));
-  loop_grid_ = (coop && locc > 0) ? sm_count_ : 0;
+  // fewer CTAs than SMs: queue-mode levels are latency-bound and the grid
+  // barrier / same-line counter traffic grows with the CTA count (measured on
+  // the 4096^2 lattice: 148 CTAs 1.07 GTEPS, 32 CTAs 1.34; S20/S24 unchanged)
+  {
+    const char* lg = getenv("LBFS_LOOP_GRID");
+    loop_grid_ = (coop && locc > 0) ? std::max(1, std::min(lg ? atoi(lg) : kLoopGrid, sm_count_ * locc)) : 0;
+  }
   // whole-BFS kernel: the dynamic part must also hold four compaction groups
   {
     cudaFuncAttributes fa{};

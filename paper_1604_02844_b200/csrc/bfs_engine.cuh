@@ -176,6 +176,7 @@ __host__ __device__ __forceinline__ int64_t part_global(int64_t l, int32_t part_
 
 // Device-side level loop (k_levels): cooperative launch, one CTA per SM.
 constexpr int kLoopThreads = 512;
+constexpr int kLoopGrid = 32;  // CTAs of the device level loop (k_levels)
 constexpr int64_t kLoopCap = 1 << 16;  // layers per k_levels launch
 
 struct LoopState {
