@@ -118,13 +118,16 @@ def hm(values):
     return harmonic_mean_teps(values)[0]
 
 
-def traffic_from_profiles():
+def traffic_from_profiles(scale: int):
+    """ncu DRAM bytes per BFS expansion (profiles/roofline_traffic.json), only
+    for the workload it was captured on (an S24 root unless it says otherwise)."""
     p = ROOT / "profiles" / "roofline_traffic.json"
     if p.exists():
         try:
-            return json.loads(p.read_text())
+            t = json.loads(p.read_text())
         except Exception:
             return None
+        return t if int(t.get("scale", 24)) == scale else None
     return None
 
 
@@ -413,7 +416,7 @@ def run_ours(args, rank, world, local):
         cpu = {"value": hm(vals), "unit": "GTEPS", "cores": thr, "kind": "port",
                "sample": f"{len(vals)} of the {args.roots} roots on the same graph, oracle bfs_parallel "
                          f"(OpenMP restatement of bfs_parallel_naive), {secs:.1f}s"}
-    traffic = traffic_from_profiles()
+    traffic = traffic_from_profiles(args.scale)
     achieved = exp_bytes / (exp_ms * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
@@ -426,13 +429,13 @@ def run_ours(args, rank, world, local):
                    "l2": "inputs larger than L2 (CSR %.2f GB vs 126 MB L2); no flush" % ((8 * n + 4 * nnz) / 1e9),
                    "graph_build_s": round(build_s, 2), "validated": ok},
         # dominant work = the level expansion: per BFS, every expansion launch
-        # (k_sweep + its plan kernels, k_expand_* bins, k_merge_hot, k_levels),
+        # (k_sweep, k_expand_* bins, k_merge_hot, k_levels),
         # timed with CUDA events on the BFS stream around each level's launches
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
                      "frac": achieved / hbm_gbs, "peak_kind": peak_kind,
                      "traffic": traffic.get("dram_bytes_per_bfs_expansion") if traffic else None,
                      "traffic_alg": traffic.get("alg_bytes_per_bfs_expansion") if traffic else None,
-                     "kernel": "level expansion per BFS (k_sweep, k_sweep_plan, k_expand_*, k_merge_hot, k_levels)",
+                     "kernel": "level expansion per BFS (k_sweep, k_expand_*, k_merge_hot, k_levels)",
                      "alg_bytes_per_bfs_expansion": exp_bytes / len(runs),
                      "expansion_ms_per_bfs": exp_ms / len(runs),
                      "whole_bfs": {"alg_bytes": alg_bytes / len(runs), "ms": bfs_ms / len(runs),

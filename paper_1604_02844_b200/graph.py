@@ -165,13 +165,20 @@ class CsrGraph:
             csr_box[0] = None
 
     # -- host views ---------------------------------------------------------
-    def _download(self):
+    def _download(self, rows: bool = True):
+        """Host copies of the device CSR, fetched on first use: row_ptr alone
+        for degree queries (pick_roots, degrees), col_idx only when the rows
+        themselves are read (an S27 col_idx is 17 GB)."""
         n = self.num_vertices
-        cs = np.empty(n + 1, dtype=np.int64)
-        rows = _aligned_i32(self._nnz)
-        _lib.check(_lib.load().lbfs_csr_download(self._handles[0][0], _lib.ptr(cs),
-                                                 _lib.ptr(rows) if self._nnz else None))
-        self._colstarts, self._rows = cs, rows
+        if self._colstarts is None:
+            cs = np.empty(n + 1, dtype=np.int64)
+            _lib.check(_lib.load().lbfs_csr_download(self._handles[0][0], _lib.ptr(cs), None))
+            self._colstarts = cs
+        if rows and self._rows is None:
+            r = _aligned_i32(self._nnz)
+            if self._nnz:
+                _lib.check(_lib.load().lbfs_csr_download(self._handles[0][0], None, _lib.ptr(r)))
+            self._rows = r
 
     @property
     def rows(self) -> np.ndarray:
@@ -182,7 +189,7 @@ class CsrGraph:
     @property
     def colstarts(self) -> np.ndarray:
         if self._colstarts is None:
-            self._download()
+            self._download(rows=False)
         return self._colstarts
 
     @property

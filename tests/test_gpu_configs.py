@@ -130,3 +130,35 @@ def test_whole_bfs_kernel_s20_and_lattice(golden, whole_bfs_kernel):
         res = bfs(g, int(r))
         assert layers_of(res) == want["layers"]
         assert sha(res.levels, "<i4") == want["levels_sha"]
+
+
+def test_config_s27_one_gpu_and_eight_partitions():
+    """configs[4] (SCALE 27, ~4.2e9 CSR entries; the reference cannot build it,
+    SURVEY G5) on ONE B200: device construction, BFS from seeded roots
+    certified on the host (root, parent one level up and adjacent, every
+    edge spans <= 1 level: levels are exact BFS distances), the device
+    validator, and the 8-way 1D partition of the multi-GPU config driven in
+    lockstep on this GPU, bit-exact with the single-GPU levels and layers."""
+    from paper_1604_02844_b200.distributed import LocalExchange, PartitionedGraph, bfs_partitioned
+    from paper_1604_02844_b200.validate import validate_tree_device
+
+    g = build_rmat_graph(RmatParams(scale=27, seed=1))
+    n = g.num_vertices
+    assert n == 1 << 27 and g.num_edges > (1 << 31)  # past int32 offsets
+    roots = pick_roots(g, 64, 1, filter_unconnected=True).tolist()[:2]
+    rp, ci = g.colstarts, g.rows
+    singles = {}
+    for r in roots:
+        res = bfs(g, r)
+        assert res.traversed_edge_count == sum(l.edges for l in res.layers)
+        code, where = oracle.check_bfs(rp, ci, r, res.predecessors.p, res.levels)
+        assert code == 0, (r, oracle.CHECK_CODES[code], where)
+        assert validate_tree_device(g, r, res.predecessors).passed
+        singles[r] = res
+    parts = [PartitionedGraph(g, k, 8) for k in range(8)]
+    r = roots[0]
+    pr = bfs_partitioned(parts, r, LocalExchange())
+    assert layers_of(pr) == layers_of(singles[r])
+    assert np.array_equal(pr.level[0].cpu().numpy()[:n], singles[r].levels)
+    code, where = oracle.check_bfs(rp, ci, r, pr.pred[0].cpu().numpy()[:n], pr.level[0].cpu().numpy()[:n])
+    assert code == 0, (oracle.CHECK_CODES[code], where)

@@ -15,7 +15,7 @@ dram = sum(d["dram_rd"] + d["dram_wr"] for d in exp)
 ms = sum(d["ms"] for d in exp)
 out = {"dram_bytes_per_bfs_expansion": dram, "alg_bytes_per_bfs_expansion": 8 * E + 40 * V,
        "expansion_kernel_ms_serialised": ms, "launches": len(exp), "root": root, "E": E, "V": V,
-       "kernels": sorted({d["kernel"] for d in exp}),
+       "kernels": sorted({d["kernel"] for d in exp}), "scale": 24,
        "source": f"{rep} (ncu --set full --clock-control none, one S24 BFS; dram__bytes_read.sum + "
                  "dram__bytes_write.sum summed over the expansion launches)", "commit": commit}
 Path("profiles/roofline_traffic.json").write_text(json.dumps(out, indent=1) + "\n")
