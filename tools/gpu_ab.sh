@@ -1,3 +1,5 @@
 mkdir -p gpurun_out
-timeout -k 10 900 python -m pytest tests/test_gpu_configs.py -m gpu -x -q -k s27 > gpurun_out/s27_test.log 2>&1; echo "rc=$?" >> gpurun_out/s27_test.log
-timeout -k 10 900 python bench.py --scale 27 --steps 1 --warmup 3 > gpurun_out/s27_bench.json 2> gpurun_out/s27_bench.err; echo "rc=$?" >> gpurun_out/s27_bench.err
+timeout 200 python tools/quick_bfs_time.py 24 64 2>&1 | tail -1 > gpurun_out/ab_fq.log
+timeout 200 python tools/quick_bfs_time.py 20 64 2>&1 | tail -1 >> gpurun_out/ab_fq.log
+WARM_S=0.3 LBFS_GAPS=1 timeout 200 python tools/quick_bfs_time.py 24 8 2>&1 | tail -9 | cut -c1-150 >> gpurun_out/ab_fq.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/ab_fq_pytest.log 2>&1
