@@ -1098,6 +1098,7 @@ constexpr int kCompactThreads = 256;
 constexpr int kCompactVerts = 4096;
 constexpr int kCompactWords = kCompactVerts / 32;
 constexpr int kCompactSteps = kCompactVerts / kCompactThreads;
+constexpr int kCompactSparseDiv = 8;  // pass 2 walks only the new ids when fewer than 1/8 of the block's ids are new
 
 // A compaction group is 256 threads synchronised on named barrier `bar`
 // (a whole CTA in k_compact; a quarter of a k_bfs CTA).
@@ -1142,6 +1143,7 @@ struct CompactSmem {
   uint32_t new_[kCompactWords];
   uint32_t lmask[kCompactWords];
   int32_t lpre[kCompactWords];
+  int32_t npre[kCompactWords];  // exclusive prefix of new vertices per word
   uint32_t wmask[kCompactWords];
   int32_t wpre[kCompactWords];
   int32_t gsum[kCompactWords];
@@ -1190,56 +1192,103 @@ __device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk,
     s_lmask[t] = mlist;
     s_wmask[t] = mwarp;
   }
-  int n_list = 0, n_wsl = 0;
-  const int lpre = scan128(t, bar, __popc(mlist), s_w, &n_list);
-  if (t < kCompactWords) s_lpre[t] = lpre;
-  const int wpre = scan128(t, bar, __popc(mwarp), s_w, &n_wsl);
-  if (t < kCompactWords) s_wpre[t] = wpre;
+  // one scan for the list and warp-slice ranks (packed 16 | 16: a block has
+  // <= 4096 ids), one for the rank of every new vertex (pass 2 walks only those)
+  int n_list = 0, n_wsl = 0, n_new = 0, packed_tot = 0;
+  const int ppre = scan128(t, bar, __popc(mlist) | (__popc(mwarp) << 16), s_w, &packed_tot);
+  n_list = packed_tot & 0xFFFF;
+  n_wsl = packed_tot >> 16;
+  if (t < kCompactWords) {
+    s_lpre[t] = ppre & 0xFFFF;
+    s_wpre[t] = ppre >> 16;
+  }
+  const int npre = scan128(t, bar, __popc(nb), s_w, &n_new);
+  if (t < kCompactWords) sm.npre[t] = npre;
   if (t == 0) {
     s_base[0] = n_list ? atomicAdd(&c.next_cnt->bin[kBinSmall], (unsigned long long)n_list) : 0;
     s_base[3] = n_wsl ? atomicAdd(&c.next_cnt->bin[kBinWSlice], (unsigned long long)n_wsl) : 0;
   }
   gsync(bar);
-  // pass 2: thread t owns vertices v0 + t + 256 j (bit t&31 of word t/32 + 8 j);
-  // four vertices' loads are issued before any of their stores
+  // pass 2. Dense blocks (most ids new): thread t owns vertices v0 + t + 256 j
+  // (bit t&31 of word t/32 + 8 j). Sparse blocks: the block's new vertices in
+  // ascending order, new vertex i to thread i % 256 (word by binary search over
+  // the new-vertex ranks, bit by select), so no step waits on loads for ids
+  // that are not new. Four vertices' loads are issued before any of their stores.
   unsigned long long edges = 0, big = 0;
-  const int b = t & 31;
-#pragma unroll
-  for (int j0 = 0; j0 < kCompactSteps; j0 += 4) {
-    int64_t st[4], en[4];
-    int32_t vo[4];
-    bool nw[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int wl = (t >> 5) + (j0 + q) * (kCompactThreads / 32);
-      const int64_t v = v0 + t + (j0 + q) * kCompactThreads;
-      nw[q] = (s_new[wl] >> b) & 1u;
-      vo[q] = nw[q] && v >= c.t_cta && v < c.t_warp ? __ldg(c.new2old + v) : 0;  // warp-slice parent
-      st[q] = nw[q] ? __ldg(c.row_ptr + v) : 0;
-      en[q] = nw[q] ? __ldg(c.row_ptr + v + 1) : 0;
+  auto settle_new = [&](int wl, int b, int64_t st, int64_t en, int32_t vo) {
+    const int64_t v = v0 + wl * 32 + b;
+    c.level_int[v] = c.next_level;  // outputs are written by k_finalize
+    const int32_t deg = (int32_t)(en - st);
+    edges += (unsigned long long)deg;
+    if (v < c.t_warp) big += (unsigned long long)deg;
+    const uint32_t wm = s_wmask[wl];
+    if ((wm >> b) & 1u)  // warp-bin row: one slice, parent = the row's vertex
+      c.next_wslice[s_base[3] + s_wpre[wl] + __popc(wm & ((1u << b) - 1u))] = CtaItem{st, deg, vo};
+    const uint32_t lm = s_lmask[wl];
+    if ((lm >> b) & 1u) {
+      const int r = s_lpre[wl] + __popc(lm & ((1u << b) - 1u));
+      c.next_list[s_base[0] + r] = (int32_t)v;
+      s_deg[r] = deg;
     }
+    if (v < c.t_cta) atomicAdd(&s_hitems[wl], (deg + kChunk - 1) / kChunk);
+  };
+  if (n_new * kCompactSparseDiv > kCompactVerts) {
+#pragma unroll 1
+    for (int j0 = 0; j0 < kCompactSteps; j0 += 4) {
+      int64_t st[4], en[4];
+      int32_t vo[4];
+      bool nw[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int wl = (t >> 5) + (j0 + q) * (kCompactThreads / 32);
-      const int64_t v = v0 + t + (j0 + q) * kCompactThreads;
-      if (!nw[q]) continue;
-      c.level_int[v] = c.next_level;  // coalesced; outputs are written by k_finalize
-      const int32_t deg = (int32_t)(en[q] - st[q]);
-      edges += (unsigned long long)deg;
-      if (v < c.t_warp) big += (unsigned long long)deg;
-      const uint32_t wm = s_wmask[wl];
-      if ((wm >> b) & 1u)  // warp-bin row: one slice, parent = the row's vertex
-        c.next_wslice[s_base[3] + s_wpre[wl] + __popc(wm & ((1u << b) - 1u))] =
-            CtaItem{st[q], deg, vo[q]};
-      const uint32_t lm = s_lmask[wl];
-      if ((lm >> b) & 1u) {
-        const int r = s_lpre[wl] + __popc(lm & ((1u << b) - 1u));
-        c.next_list[s_base[0] + r] = (int32_t)v;
-        s_deg[r] = deg;
+      for (int q = 0; q < 4; ++q) {
+        const int wl = (t >> 5) + (j0 + q) * (kCompactThreads / 32);
+        const int64_t v = v0 + t + (j0 + q) * kCompactThreads;
+        nw[q] = (s_new[wl] >> (t & 31)) & 1u;
+        vo[q] = nw[q] && v >= c.t_cta && v < c.t_warp ? __ldg(c.new2old + v) : 0;
+        st[q] = nw[q] ? __ldg(c.row_ptr + v) : 0;
+        en[q] = nw[q] ? __ldg(c.row_ptr + v + 1) : 0;
       }
-      if (v < c.t_cta) atomicAdd(&s_hitems[wl], (deg + kChunk - 1) / kChunk);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (nw[q]) settle_new((t >> 5) + (j0 + q) * (kCompactThreads / 32), t & 31, st[q], en[q], vo[q]);
+    }
+  } else {
+#pragma unroll 1
+    for (int i0 = 0; i0 < n_new; i0 += 4 * kCompactThreads) {
+      int64_t st[4], en[4];
+      int32_t vo[4];
+      int wlq[4], bq[4];
+      bool nw[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = i0 + q * kCompactThreads + t;
+        nw[q] = i < n_new;
+        int wl = 0;
+#pragma unroll
+        for (int step = kCompactWords / 2; step; step >>= 1)  // largest wl with npre[wl] <= i
+          if (sm.npre[wl + step] <= i) wl += step;
+        uint32_t m = s_new[wl];
+        int k = i - sm.npre[wl], pos = 0;
+#pragma unroll
+        for (int half = 16; half; half >>= 1) {  // position of the k-th set bit of m
+          const int cnt = __popc(m & ((1u << half) - 1u));
+          const bool up = k >= cnt;
+          k -= up ? cnt : 0;
+          m = up ? m >> half : m;
+          pos += up ? half : 0;
+        }
+        wlq[q] = wl;
+        bq[q] = pos;
+        const int64_t v = v0 + wl * 32 + pos;
+        vo[q] = nw[q] && v >= c.t_cta && v < c.t_warp ? __ldg(c.new2old + v) : 0;
+        st[q] = nw[q] ? __ldg(c.row_ptr + v) : 0;
+        en[q] = nw[q] ? __ldg(c.row_ptr + v + 1) : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (nw[q]) settle_new(wlq[q], bq[q], st[q], en[q], vo[q]);
     }
   }
+  const int b = t & 31;
   if (c.resolve_verts > v0) {
     // heavy level: the new hot vertices were discovered by blind ORs with no
     // parent; take the first neighbour one level up (rows are sorted by
