@@ -236,7 +236,10 @@ struct LoopArgs {
 
 // Heavy-level sweep of the big-row region (sweep.cu).
 constexpr int kSweepWindow = 128;   // col_idx elements per window / side entry
-constexpr int kSweepConsumers = 16;  // consumer warps; one CTA per SM
+#ifndef LBFS_SWEEP_CONSUMERS
+#define LBFS_SWEEP_CONSUMERS 16
+#endif
+constexpr int kSweepConsumers = LBFS_SWEEP_CONSUMERS;  // consumer warps; one CTA per SM
 constexpr int kSweepProducers = 4;   // producer warps (each a latency-bound side -> frontier -> copy chain)
 constexpr int kSweepThreads = 32 * (kSweepConsumers + kSweepProducers);
 #ifndef LBFS_SWEEP_STAGES
