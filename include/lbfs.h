@@ -141,6 +141,15 @@ int lbfs_bfs_device(lbfs_graph* g, int64_t root, int32_t* d_pred, int32_t* d_lev
                     lbfs_timing* t_out);
 /* Layers of the most recent BFS on this handle. */
 int lbfs_graph_last_layers(const lbfs_graph* g, lbfs_layer* out, int64_t cap, int64_t* n_layers);
+/* Traversal direction of later lbfs_bfs / lbfs_bfs_device calls on this
+ * handle: LBFS_DIR_TOP_DOWN (default; the paper's algorithm, the benchmarked
+ * path) or LBFS_DIR_OPTIMIZING (bottom-up levels while the frontier is large,
+ * Beamer's alpha = 14 / beta = 24 rule). Levels, visited
+ * set and layers are identical in both; parents may differ (any neighbour one
+ * level up). No reference counterpart: the reference is top-down only. */
+#define LBFS_DIR_TOP_DOWN 0
+#define LBFS_DIR_OPTIMIZING 1
+int lbfs_graph_set_direction(lbfs_graph* g, int direction);
 
 /* ---- tree validation (replaces validate_tree, validate.py:50-155) ------
  * The reference's five checks on a parent array in original ids (n int32;

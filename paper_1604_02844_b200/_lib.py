@@ -73,6 +73,7 @@ SIGNATURES = {
     "lbfs_bfs_device": (ctypes.c_int, [_p, _i64, _p, _p, ctypes.POINTER(Layer), _i64,
                                        ctypes.POINTER(_i64), ctypes.POINTER(Timing)]),
     "lbfs_graph_last_layers": (ctypes.c_int, [_p, ctypes.POINTER(Layer), _i64, ctypes.POINTER(_i64)]),
+    "lbfs_graph_set_direction": (ctypes.c_int, [_p, ctypes.c_int]),
     "lbfs_set_device": (ctypes.c_int, [ctypes.c_int]),
     "lbfs_validate_tree": (ctypes.c_int, [_p, _i64, _p, _p]),
     "lbfs_validate_tree_device": (ctypes.c_int, [_p, _i64, _p, _p]),

@@ -328,6 +328,15 @@ int lbfs_graph_info(const lbfs_graph* g, int64_t* n, int64_t* nnz) {
   });
 }
 
+int lbfs_graph_set_direction(lbfs_graph* g, int direction) {
+  return guarded([&] {
+    if (!g) throw_inval("graph is NULL");
+    if (direction != LBFS_DIR_TOP_DOWN && direction != LBFS_DIR_OPTIMIZING) throw_inval("unknown direction");
+    std::lock_guard<std::mutex> lk(g->eng->mu);
+    g->eng->set_direction(direction);
+  });
+}
+
 static void copy_layers(const BfsEngine& e, lbfs_layer* out, int64_t cap, int64_t* n_layers) {
   const auto& L = e.layers();
   if (n_layers) *n_layers = (int64_t)L.size();

@@ -2058,6 +2058,24 @@ LevelArgs BfsEngine::level_args() const {
   return a;
 }
 
+// A bottom-up level (bottomup.cu): the frontier bitmap (from k_compact after
+// a bitmap level, else rebuilt from the queues), then one warp per visited
+// word of the rows with degree >= 1. k_compact follows as for any bitmap level.
+unsigned BfsEngine::bottom_up_level(const Counters& c, bool prev_bitmap, int cur, cudaStream_t st) {
+  if (!prev_bitmap) {
+    LBFS_CUDA(cudaMemsetAsync(front_, 0, sizeof(uint32_t) * (size_t)nwords_, st));
+    const int64_t ns = (int64_t)c.bin[kBinSmall], nw = (int64_t)c.bin[kBinWarp], nc = (int64_t)c.bin[kBinCta];
+    LBFS_LAUNCH(k_front_from_queues, clamp_grid((ns + nw + nc + 255) / 256, (int64_t)sm_count_ * 8), 256, 0, st,
+                front_, q_small_[cur], ns, q_warp_[cur], nw, q_cta_[cur], nc, old2new_);
+  }
+  const int64_t nw_nz = ((int64_t)t_nz_ + 31) / 32;
+  BottomUpArgs b{row_ptr_, col_idx_, new2old_loc_, front_, visited_, pred_int_, nw_nz, (int64_t)t_nz_};
+  const unsigned grid = clamp_grid((nw_nz * 32 + 255) / 256, (int64_t)sm_count_ * 16);
+  LBFS_LAUNCH(k_bottom_up, grid, 256, 0, st, b);
+  split_any_ = false;
+  return grid;
+}
+
 unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool prev_bitmap, int cur, int64_t L,
                                  cudaStream_t st) {
   const bool bitmap = mode != kQueueOut;
@@ -2247,8 +2265,18 @@ void BfsEngine::read_env() {
   trace_ = env_flag("LBFS_TRACE");  // per-level table on stderr
   gaps_ = env_flag("LBFS_GAPS");
   {
+    const char* dm = getenv("LBFS_DIRECTION");  // (also lbfs_graph_set_direction) 1: direction-optimising
+    if (dm) direction_ = atoi(dm);
+    const char* al = getenv("LBFS_BU_ALPHA");
+    const char* be = getenv("LBFS_BU_BETA");
+    if (al) bu_alpha_ = std::max(1, atoi(al));
+    if (be) bu_beta_ = std::max(1, atoi(be));
+  }
+  {
     const char* bd = getenv("LBFS_BITMAP_DIV");  // bitmap mode when a frontier has >= n / this many edges
     bitmap_div_ = std::max(1, bd ? atoi(bd) : kBitmapDiv);
+    const char* bm = getenv("LBFS_BITMAP_MIN");  // (tests) floor of the bitmap-mode threshold
+    bitmap_floor_ = std::max<int64_t>(1, bm ? atoll(bm) : (int64_t)1 << 16);
   }
   {
     const char* sm = getenv("LBFS_SWEEP_MIN");  // sweep when big-row frontier edges >= this % of the region
@@ -2295,7 +2323,7 @@ void BfsEngine::run_mega(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_t
   p.state = loop_;
   p.max_levels = kLoopCap;
   if (const char* ml = getenv("LBFS_MEGA_LEVELS")) p.max_levels = std::max(1, atoi(ml));  // debug: levels per launch
-  p.bitmap_min_edges = (unsigned long long)std::max<int64_t>(1 << 16, n_ / bitmap_div_);
+  p.bitmap_min_edges = (unsigned long long)std::max<int64_t>(bitmap_floor_, n_ / bitmap_div_);
   p.small_region = (int64_t)t_nz_ - t_warp_;
   p.dense_off = dense_off_ ? 1 : 0;
   p.hot_words = env_flag("LBFS_MEGA_NOHOT") ? 0 : hot_words_;  // debug
@@ -2428,8 +2456,8 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
 
   layers_.clear();
   double expand_ms = 0.0;
-  bool prev_bitmap = false;
-  const unsigned long long bitmap_min_edges = (unsigned long long)std::max<int64_t>(1 << 16, n_ / bitmap_div_);
+  bool prev_bitmap = false, prev_bu = false;
+  const unsigned long long bitmap_min_edges = (unsigned long long)std::max<int64_t>(bitmap_floor_, n_ / bitmap_div_);
   int64_t L = 0;
   for (;;) {
     const Counters c = h_cnt_[L % kCounterRing];
@@ -2499,11 +2527,25 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       continue;
     }
     const bool bitmap = c.edges >= bitmap_min_edges;
-    const bool heavy = bitmap && stage_ && heavy_div_ > 0 && c.edges * (unsigned long long)heavy_div_ >= (unsigned long long)nnz_;
+    // direction-optimising (opt-in): bottom-up while the frontier's edges
+    // outweigh the unvisited vertices' edges / alpha, back to top-down when
+    // the frontier drops below n / beta (Beamer et al.'s rule)
+    bool bottom_up = false;
+    if (direction_ && bitmap && nparts_ == 1) {
+      unsigned long long seen = c.edges;  // degrees of every vertex visited so far (each was one frontier)
+      for (const auto& l : layers_) seen += (unsigned long long)l.edges;
+      const unsigned long long m_u = (unsigned long long)nnz_ > seen ? (unsigned long long)nnz_ - seen : 0ull;
+      bottom_up = prev_bu ? c.discovered * (unsigned long long)bu_beta_ >= (unsigned long long)n_
+                          : c.edges * (unsigned long long)bu_alpha_ > m_u;
+    }
+    const bool heavy = !bottom_up && bitmap && stage_ && heavy_div_ > 0 &&
+                       c.edges * (unsigned long long)heavy_div_ >= (unsigned long long)nnz_;
     LBFS_CUDA(cudaEventRecord(ev_[2], st));
     gap_mark(st);
     float gap_ms = -1.f;
-    const unsigned grid = expand_level(a, c, heavy ? kHeavy : bitmap ? kBitmapOut : kQueueOut, prev_bitmap, cur, L, st);
+    const unsigned grid = bottom_up ? bottom_up_level(c, prev_bitmap, cur, st)
+                                    : expand_level(a, c, heavy ? kHeavy : bitmap ? kBitmapOut : kQueueOut, prev_bitmap,
+                                                   cur, L, st);
     if (heavy) merge_hot(st);
     LBFS_CUDA(cudaEventRecord(ev_[3], st));
     if (bitmap) compact_level(cur, L, nullptr, st, heavy);
@@ -2539,13 +2581,15 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       fprintf(stderr,
               "[lbfs] L%-3lld %s in=%-9llu edges=%-10llu big=%-10llu bins(s|list/w/c/items/ws)=%llu/%llu/%llu/%llu/%llu grid=%u "
               "expand=%.3fms compact=%.3fms disc=%llu gap_before=%.3fms\n",
-              (long long)L, heavy ? (sweep_used_ ? "sweep " : "heavy ") : bitmap ? "bitmap" : "queue ", c.discovered, c.edges,
+              (long long)L, bottom_up ? "bottom" : heavy ? (sweep_used_ ? "sweep " : "heavy ") : bitmap ? "bitmap" : "queue ",
+              c.discovered, c.edges,
               c.big_edges, c.bin[0], c.bin[1], c.bin[2], c.bin[3], c.bin[4],
               grid, ms, bitmap ? cms : 0.f, nx.discovered, gap_ms);
     layers_.push_back(lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, (int64_t)nx.discovered});
     cur ^= 1;
     ++L;
     prev_bitmap = bitmap;
+    prev_bu = bottom_up;
     if (nx.discovered == 0) break;
   }
   if (trace_) LBFS_CUDA(cudaEventRecord(ev_gap_, st));

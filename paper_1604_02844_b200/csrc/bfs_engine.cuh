@@ -277,6 +277,19 @@ struct SweepArgs {
   int32_t prefetch;         // L2 prefetch distance in chunks of a CTA (0: off)
   int32_t dbg_flags;        // LBFS_SWEEP_DBG (experiments; wrong results): 1 no hot ORs, 2 no cold probes
 };
+struct BottomUpArgs {
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  const int32_t* new2old;
+  const uint32_t* front;   // frontier bitmap of the level
+  uint32_t* visited;
+  int32_t* pred_int;
+  int64_t nwords;          // visited words covering [0, t_nz)
+  int64_t t_nz;            // rows of degree >= 1 are [0, t_nz)
+};
+__global__ void k_bottom_up(const BottomUpArgs b);
+__global__ void k_front_from_queues(uint32_t* front, const int32_t* qs, int64_t ns, const int32_t* qw, int64_t nw,
+                                    const CtaItem* qc, int64_t nc, const int32_t* old2new);
 __global__ void k_side_table(const int64_t* rp, int32_t nrows, int64_t nwin, uint2* side);
 __global__ void k_sweep(const __grid_constant__ SweepArgs s);
 __global__ void k_sweep_plan(const uint2* side, const uint32_t* front, int64_t nwin, uint32_t* info);
@@ -321,6 +334,7 @@ class BfsEngine {
   int64_t nwords() const { return nwords_; }
   int64_t n_local() const { return n_loc_; }
   int64_t nnz_local() const { return nnz_loc_; }
+  void set_direction(int d) { direction_ = d; }
   unsigned long long resolve_scanned() const;
   // validate_tree (validate.py:50-155) on a device parent array in original
   // ids: out[0..4] passed flags, out[5..9] details (-1 when passed)
@@ -342,6 +356,7 @@ class BfsEngine {
   LevelArgs level_args() const;
   // frontier of level L (queue slot cur, counters c) -> launches; returns the grid
   // mode: 0 bitmap, 1 queue, 3 heavy bitmap (blind hot ORs, see LevelArgs::stage)
+  unsigned bottom_up_level(const Counters& c, bool prev_bitmap, int cur, cudaStream_t st);
   unsigned expand_level(LevelArgs& a, const Counters& c, int mode, bool prev_bitmap, int cur, int64_t L,
                         cudaStream_t st);
   void compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st, bool heavy = false);
@@ -440,7 +455,10 @@ class BfsEngine {
   int dyn_smem_ = 0;
   bool trace_ = false;  // LBFS_TRACE=1: per-level table on stderr
   int sweep_min_pct_ = kSweepMinPct;
+  int direction_ = 0;              // 0 top-down (the paper's algorithm), 1 direction-optimising (bottom-up levels)
+  int bu_alpha_ = 14, bu_beta_ = 24;
   int bitmap_div_ = kBitmapDiv;
+  int64_t bitmap_floor_ = (int64_t)1 << 16;
   bool gaps_ = false;   // LBFS_GAPS=1: per-level busy span / host gap line on stderr (no syncs added)
   std::vector<cudaEvent_t> gap_ev_;  // LBFS_GAPS: [2i] segment start, [2i+1] segment end
   int n_gap_ = 0;

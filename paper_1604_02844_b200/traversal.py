@@ -132,12 +132,26 @@ def _layers_from(buf, k: int, h: int) -> list[LayerStats]:
 _LAYER_CAP = 256
 
 
-def bfs(g, s: int) -> BfsResult:
+DIRECTIONS = {"top_down": 0, "optimizing": 1}
+
+
+def _set_direction(h, direction: str) -> None:
+    """Traversal direction of this call: "top_down" (the paper's algorithm;
+    the default and the benchmarked path) or "optimizing" (bottom-up levels
+    while the frontier is large). Levels, visited set
+    and layers are the same either way; parents may differ (any neighbour one
+    level up, as the reference's own parallel variants allow)."""
+    assert direction in DIRECTIONS, f"direction must be one of {sorted(DIRECTIONS)}"
+    _lib.check(_lib.load().lbfs_graph_set_direction(h, DIRECTIONS[direction]))
+
+
+def bfs(g, s: int, direction: str = "top_down") -> BfsResult:
     """Top-down BFS from s on the device; host outputs (one D2H copy of the
     predecessor and level arrays inside the call)."""
     n = g.num_vertices
     assert 0 <= s < n
     h = _handle(g)
+    _set_direction(h, direction)
     padded = (n + BITS_PER_WORD - 1) // BITS_PER_WORD * BITS_PER_WORD
     # outputs land in page-locked memory (pooled), so the D2H copy inside the
     # call runs at full link rate
@@ -152,7 +166,7 @@ def bfs(g, s: int) -> BfsResult:
     return BfsResult(pred, layers, int(t.edges), levels, t.as_dict())
 
 
-def bfs_device(g, s: int, pred_out, level_out) -> BfsResult:
+def bfs_device(g, s: int, pred_out, level_out, direction: str = "top_down") -> BfsResult:
     """BFS into device buffers (anything with ``data_ptr()``, e.g. torch CUDA
     int32 tensors of pad32(n) and n entries). No host copy of the outputs;
     ``predecessors`` of the result is None."""
@@ -161,6 +175,7 @@ def bfs_device(g, s: int, pred_out, level_out) -> BfsResult:
     padded = (n + BITS_PER_WORD - 1) // BITS_PER_WORD * BITS_PER_WORD
     assert pred_out.numel() >= padded and level_out.numel() >= n
     h = _handle(g)
+    _set_direction(h, direction)
     buf = (_lib.Layer * _LAYER_CAP)()
     k = ctypes.c_int64()
     t = _lib.Timing()

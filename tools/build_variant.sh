@@ -10,7 +10,7 @@ OUT=$ROOT/paper_1604_02844_b200/_native/variants
 OBJ=$OUT/obj_$NAME
 mkdir -p $OBJ
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include --expt-relaxed-constexpr $*"
-for f in api bfs construct layout partition sweep validate; do
+for f in api bfs bottomup construct layout partition sweep validate; do
   $NV -c $SRC/$f.cu -o $OBJ/$f.o -Xptxas -v 2> $OBJ/$f.ptxas.log &
 done
 wait

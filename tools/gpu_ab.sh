@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
-for V in default c8 c32 default c8; do
-  if [ "$V" = default ]; then L=""; else L=paper_1604_02844_b200/_native/variants/$V.so; fi
-  echo "VARIANT=$V $(LBFS_LIB=$L timeout 200 python tools/quick_bfs_time.py 24 64 2>&1 | tail -1)" >> gpurun_out/ab_cons.log
-  LBFS_LIB=$L WARM_S=0.3 LBFS_TRACE=1 LBFS_SPLIT=1 timeout 200 python tools/quick_bfs_time.py 24 2 2>&1 | grep -B1 "sweep " | grep split | cut -c1-40 >> gpurun_out/ab_cons.log
-done
+timeout 900 python -m pytest tests/test_gpu_direction.py -x -q > gpurun_out/do_pytest.log 2>&1
+LBFS_DIRECTION=1 timeout 200 python tools/quick_bfs_time.py 24 64 2>&1 | tail -1 > gpurun_out/do.log
+LBFS_DIRECTION=1 timeout 200 python tools/quick_bfs_time.py 20 64 2>&1 | tail -1 >> gpurun_out/do.log
+LBFS_DIRECTION=1 WARM_S=0.3 LBFS_TRACE=1 timeout 200 python tools/quick_bfs_time.py 24 2 2>&1 | grep "L[0-9]\|root" | cut -c1-200 >> gpurun_out/do.log
+LBFS_DIRECTION=1 timeout 300 python tools/quick_lattice_time.py 4096 2 2>&1 | tail -1 >> gpurun_out/do.log
