@@ -380,6 +380,16 @@ def run_ours(args, rank, world, local):
     alg_bytes = sum(8 * r.traversed_edge_count + 40 * r.timing["reached"] + 8 * n + n // 8 for r in runs)
     bfs_ms = sum(r.timing["bfs_ms"] for r in runs)
 
+    # direction-optimising BFS (opt-in; not the headline: the north star is
+    # top-down): one untimed pass, then one pass over the same roots, device
+    # outputs, same E per root and the same CUDA-event timing
+    for r in roots[:3]:
+        bfs_device(g, r, pred, lvl, direction="optimizing")
+    do_runs = [bfs_device(g, r, pred, lvl, direction="optimizing") for r in roots]
+    do_value = hm([x.traversed_edge_count / (x.timing["bfs_ms"] * 1e-3) / 1e9 if x.traversed_edge_count else 0.0
+                   for x in do_runs])
+    do_ok = all(x.layers == y.layers for x, y in zip(do_runs, runs[:len(do_runs)]))
+
     # e2e through the public API with host outputs (D2H inside the call);
     # untimed warm-up calls first (they fill the page-locked output pool)
     # (each call runs while the previous result is alive, as in the timed loop,
@@ -444,6 +454,10 @@ def run_ours(args, rank, world, local):
         "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 8,
                 "d2h_bytes_per_step": d2h_bytes, "step": "one bfs(g, root) call (harmonic mean over roots)",
                 "api": "paper_1604_02844_b200.bfs(g, root), host outputs", "roots_timed": len(e2e_vals)},
+        "direction_optimizing": {"value": do_value, "unit": "GTEPS", "roots": len(do_runs),
+                                 "layers_equal_top_down": do_ok,
+                                 "note": "opt-in bottom-up levels (bfs(..., direction='optimizing')); same E, "
+                                         "levels and layers as the top-down headline; not the north-star path"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "wall_s_timed": wall,
