@@ -11,6 +11,17 @@
 namespace lbfs {
 
 std::atomic<int64_t> g_launches{0};
+bool g_sync_each = [] {
+  const char* v = getenv("LBFS_SYNC_EACH");
+  return v && *v && *v != '0';
+}();
+void sync_check(cudaStream_t st, const char* kernel, const char* file, int line) {
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[lbfs] LBFS_SYNC_EACH: %s failed: %s (%s:%d)\n", kernel, cudaGetErrorString(e), file, line);
+    throw_cuda(e, kernel, file, line);
+  }
+}
 static thread_local std::string t_err;
 
 void set_error(const std::string& m) { t_err = m; }

@@ -459,8 +459,8 @@ class BfsEngine {
   int bu_alpha_ = 14, bu_beta_ = 24;
   int bitmap_div_ = kBitmapDiv;
   int64_t bitmap_floor_ = (int64_t)1 << 16;
-  bool fuse_hq_ = true;   // hub + queue bins of a bitmap/heavy level in one launch (LBFS_FUSE_HQ=0: two)
-  bool fuse_all_ = true;  // every bin of a bitmap/heavy level in one launch (LBFS_FUSE_ALL=0: per bin)
+  bool fuse_hq_ = false;   // (LBFS_FUSE_HQ=1) hub + queue bins of a bitmap/heavy level in one launch
+  bool fuse_all_ = false;  // (LBFS_FUSE_ALL=1) every bin of a bitmap/heavy level in one launch
   bool gaps_ = false;   // LBFS_GAPS=1: per-level busy span / host gap line on stderr (no syncs added)
   std::vector<cudaEvent_t> gap_ev_;  // LBFS_GAPS: [2i] segment start, [2i+1] segment end
   int n_gap_ = 0;

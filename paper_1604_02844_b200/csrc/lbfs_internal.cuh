@@ -33,11 +33,14 @@ struct Failure : std::runtime_error {
 // Counted launch: every kernel the library issues goes through this macro
 // so bench.py can report gpu_launches.
 extern std::atomic<int64_t> g_launches;
+extern bool g_sync_each;  // LBFS_SYNC_EACH=1 (debug): synchronise after every launch, name the failing kernel
+void sync_check(cudaStream_t st, const char* kernel, const char* file, int line);
 #define LBFS_LAUNCH(kernel, grid, block, smem, stream, ...)               \
   do {                                                                     \
     kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
     ::lbfs::g_launches.fetch_add(1, std::memory_order_relaxed);            \
     LBFS_CUDA(cudaGetLastError());                                         \
+    if (::lbfs::g_sync_each) ::lbfs::sync_check((stream), #kernel, __FILE__, __LINE__); \
   } while (0)
 
 void set_error(const std::string& m);
