@@ -211,6 +211,12 @@ def run_partitioned(args, rank, world, local):
     from paper_1604_02844_b200.distributed import PartitionedGraph, TorchExchange, bfs_partitioned
 
     torch.cuda.set_device(local)
+    if "RANK" not in os.environ:  # --partitioned without torchrun: a world of one
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t0 = time.perf_counter()
     g = build_rmat_graph(RmatParams(scale=args.scale, seed=1))

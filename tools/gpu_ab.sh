@@ -1,5 +1,2 @@
 mkdir -p gpurun_out
-rm -f gpurun_out/ab_stab.log
-for i in $(seq 1 30); do
-  echo "nofuse run$i $(timeout 200 python tools/quick_bfs_time.py 24 64 2>&1 | tail -1)" >> gpurun_out/ab_stab.log
-done
+timeout -k 10 900 python bench.py --partitioned --steps 1 --warmup 1 > gpurun_out/part_bench.json 2> gpurun_out/part_bench.err; echo "rc=$?" >> gpurun_out/part_bench.err
