@@ -56,7 +56,7 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 // level): targets in the hot prefix are OR'ed blindly into the CTA's zeroed
 // shared copy (no probe, no parent; k_merge_hot folds the copies into the
 // visited bitmap and k_compact resolves their parents), the rest as kBitmapOut.
-enum Mode : int { kBitmapOut = 0, kQueueOut = 1, kQueueDirect = 2, kHeavy = 3 };
+// (enum Mode: bfs_engine.cuh)
 
 // ---------------------------------------------------------------- memory ops
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
@@ -1886,6 +1886,10 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   for (auto fn : kernels) LBFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_));
   LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<kBitmapOut, 2>, kExpandThreads, dyn_smem_));
   expand_grid_ = sm_count_ * std::max(occ, 1);
+  if (nparts_ > 1 && hot_words_ >= 4) {  // partitions: heavy levels without the sweep
+    sweep_hot_words_ = hot_words_;
+    stage_ = dev_alloc<uint32_t>((size_t)expand_grid_ * hot_words_);
+  }
   if (nparts_ == 1 && hot_words_ >= 4) {
     // the sweep has no per-warp rings: its hot prefix takes what its own ring leaves
     cudaFuncAttributes fs{};
@@ -2140,7 +2144,7 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
   // heavy level after a bitmap level: the big-row region is swept whole (sweep.cu)
   // (only when the frontier's big rows hold enough of the region's edges:
   // below that the sweep streams mostly rows outside the frontier)
-  const bool sweep = mode == kHeavy && prev_bitmap && side_ && sweep_fits_ && !sweep_off_ &&
+  const bool sweep = mode == kHeavy && nparts_ == 1 && prev_bitmap && side_ && sweep_fits_ && !sweep_off_ &&
                      c.big_edges * 100ull >= (unsigned long long)e_big_ * (unsigned long long)sweep_min_pct_;
   sweep_used_ = sweep;
   merge_wide_ = sweep;
@@ -2287,6 +2291,10 @@ void BfsEngine::gap_mark(cudaStream_t st) {
 void BfsEngine::read_env() {
   trace_ = env_flag("LBFS_TRACE");  // per-level table on stderr
   gaps_ = env_flag("LBFS_GAPS");
+  {
+    const char* ph = getenv("LBFS_PART_HEAVY");
+    part_heavy_off_ = ph && atoi(ph) == 0;
+  }
   {
     const char* fh = getenv("LBFS_FUSE_HQ");
     fuse_hq_ = fh ? atoi(fh) != 0 : false;  // default off: see DESIGN (intermittent fault under investigation)

@@ -48,6 +48,10 @@ constexpr int kRingBytes = kExpandWarps * kWarpStages * kWarpChunk * 4;  // per-
 // Per-level counters (K6). Slot L holds the frontier of level L:
 // discovered = |frontier| (layers[L].input), edges = sum of its degrees
 // (layers[L].edges); bin[] are the bin sizes (entries / items).
+// Expansion modes (bfs.cu): bitmap-mode output, queue-mode output, queue mode
+// inside the device loop, heavy (blind-OR) bitmap levels.
+enum Mode : int { kBitmapOut = 0, kQueueOut = 1, kQueueDirect = 2, kHeavy = 3 };
+
 struct alignas(64) Counters {
   unsigned long long bin[5];  // small queue | small list, warp queue, hub slices, group items, warp slices
   unsigned long long discovered;
@@ -459,6 +463,8 @@ class BfsEngine {
   int bu_alpha_ = 14, bu_beta_ = 24;
   int bitmap_div_ = kBitmapDiv;
   int64_t bitmap_floor_ = (int64_t)1 << 16;
+  bool part_heavy_ = false;      // this partition level runs with heavy (blind-OR) semantics
+  bool part_heavy_off_ = false;  // LBFS_PART_HEAVY=0
   bool fuse_hq_ = false;   // (LBFS_FUSE_HQ=1) hub + queue bins of a bitmap/heavy level in one launch
   bool fuse_all_ = false;  // (LBFS_FUSE_ALL=1) every bin of a bitmap/heavy level in one launch
   bool gaps_ = false;   // LBFS_GAPS=1: per-level busy span / host gap line on stderr (no syncs added)

@@ -44,8 +44,11 @@ __global__ void k_part_pack(const uint32_t* __restrict__ visited, const uint32_t
 
 // Warp per owned word (lane = bit): remote discoveries of this level and
 // their parents. recv[p*nwl + j] is peer p's marks for owned word j.
+// With prev (a heavy level: blind ORs wrote no parent), every new owned
+// vertex, local or remote discovery, gets its parent here.
 __global__ void k_part_merge(const uint32_t* __restrict__ recv, int64_t nwl, int part_log, int rank,
-                             uint32_t* __restrict__ visited, const uint32_t* __restrict__ fglob,
+                             uint32_t* __restrict__ visited, const uint32_t* __restrict__ prev,
+                             const uint32_t* __restrict__ fglob,
                              const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                              const int32_t* __restrict__ new2old, int32_t* __restrict__ pred_int,
                              unsigned long long* __restrict__ scanned) {
@@ -56,12 +59,12 @@ __global__ void k_part_merge(const uint32_t* __restrict__ recv, int64_t nwl, int
     uint32_t inc = 0;
     for (int p = 0; p < (1 << part_log); ++p)
       if (p != rank) inc |= __ldg(recv + (int64_t)p * nwl + j);
-    if (!inc) continue;  // warp-uniform
     const int64_t gw = (j << part_log) | rank;
+    if (!inc && !prev) continue;  // warp-uniform
     const uint32_t vis = visited[gw];
-    const uint32_t nb = inc & ~vis;
+    const uint32_t nb = prev ? (vis | inc) & ~prev[gw] : inc & ~vis;
     __syncwarp();
-    if (lane == 0 && nb) visited[gw] = vis | nb;
+    if (lane == 0 && (inc & ~vis)) visited[gw] = vis | inc;
     if ((nb >> lane) & 1u) {
       const int64_t l = j * 32 + lane;
       const int64_t e0 = row_ptr[l], e1 = row_ptr[l + 1];
@@ -79,7 +82,7 @@ __global__ void k_part_merge(const uint32_t* __restrict__ recv, int64_t nwl, int
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
-  if (lane == 0 && cnt) atomicAdd(scanned, cnt);
+  if (lane == 0 && cnt && scanned) atomicAdd(scanned, cnt);
 }
 
 // local counts of the next frontier -> the 4 words after the frontier words
@@ -173,9 +176,16 @@ void BfsEngine::part_expand(cudaStream_t st) {
   const Counters c = h_cnt_[L % kCounterRing];
   LBFS_CUDA(cudaMemsetAsync(&cnt_[(L + 1) % kCounterRing], 0, sizeof(Counters), st));
   LevelArgs a = level_args();
-  // always bitmap mode: the exchange works on bitmaps, and queue-mode
-  // settling would elect winners for vertices this rank does not own
-  expand_level(a, c, /*mode=bitmap*/ 0, part_prev_bitmap_, part_cur_, L, st);
+  // bitmap mode (the exchange works on bitmaps, and queue-mode settling
+  // would elect winners for vertices this rank does not own); heavy levels
+  // (the level's global frontier edges >= nnz / heavy_div) use the blind-OR
+  // semantics: no parent is written during the expansion, part_merge resolves
+  // the parents of every new owned vertex
+  read_env();
+  part_heavy_ = stage_ && heavy_div_ > 0 && part_edges_ * (unsigned long long)heavy_div_ >= (unsigned long long)nnz_ &&
+                !part_heavy_off_;
+  expand_level(a, c, part_heavy_ ? kHeavy : kBitmapOut, part_prev_bitmap_, part_cur_, L, st);
+  if (part_heavy_) merge_hot(st);
 }
 
 void BfsEngine::part_pack(uint32_t* send, cudaStream_t st) {
@@ -187,9 +197,10 @@ void BfsEngine::part_pack(uint32_t* send, cudaStream_t st) {
 void BfsEngine::part_merge(const uint32_t* recv, uint32_t* fsend, cudaStream_t st) {
   part_st_ = st;
   const int64_t L = part_L_;
-  if (nparts_ > 1)
+  if (nparts_ > 1 || part_heavy_)
     LBFS_LAUNCH(k_part_merge, grid_for(nwl_ * 32, sm_count_), 256, 0, st, recv, nwl_, part_log_, part_rank_,
-                visited_, fglob_, row_ptr_, col_idx_, new2old_, pred_int_, resolve_cnt_);
+                visited_, part_heavy_ ? prev_ : nullptr, nparts_ > 1 ? fglob_ : front_ /* F_L */, row_ptr_,
+                col_idx_, new2old_, pred_int_, resolve_cnt_);
   compact_level(part_cur_, L, fsend, st);
   LBFS_LAUNCH(k_part_counts, 1, 1, 0, st, &cnt_[(L + 1) % kCounterRing], fsend + nwl_);
 }
