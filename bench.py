@@ -217,6 +217,15 @@ def run_partitioned(args, rank, world, local):
             sk.bind(("127.0.0.1", 0))
             port = sk.getsockname()[1]
         os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # NCCL writes its version banner / debug log to stdout (with NCCL_DEBUG
+    # set, even at WARN): send it to stderr so rank 0's stdout is the JSON line
+    # (at VERSION it prints the banner to stdout regardless of NCCL_DEBUG_FILE:
+    # report the version on stderr ourselves and keep NCCL quiet)
+    if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+        os.environ.pop("NCCL_DEBUG")
+        print(f"[bench] NCCL version {'.'.join(map(str, torch.cuda.nccl.version()))}", file=sys.stderr)
+    if os.environ.get("NCCL_DEBUG"):
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     t0 = time.perf_counter()
     g = build_rmat_graph(RmatParams(scale=args.scale, seed=1))
