@@ -37,7 +37,10 @@ def rows(path):
 
 if __name__ == "__main__":
     res = rows(sys.argv[1])
-    print("%-22s " % "kernel" + " ".join("%9s" % s for s in SHORT))
+    # dramGB/s = (dram_rd + dram_wr) / ms: achieved DRAM bandwidth of the launch
+    # (cold caches, --clock-control none); thr/inst = warp execution efficiency
+    print("%-22s " % "kernel" + " ".join("%9s" % s for s in SHORT) + " %9s" % "dramGB/s")
     for d in res:
+        gbs = (d["dram_rd"] + d["dram_wr"]) / (d["ms"] * 1e-3) / 1e9 if d["ms"] > 0 else float("nan")
         print("%-22s " % d["kernel"][:22] + " ".join(
-            ("%9.3f" % d[s]) if s == "ms" else ("%9.3g" % d[s]) for s in SHORT))
+            ("%9.3f" % d[s]) if s == "ms" else ("%9.3g" % d[s]) for s in SHORT) + " %9.0f" % gbs)
