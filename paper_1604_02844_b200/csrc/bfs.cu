@@ -57,6 +57,9 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 // shared copy (no probe, no parent; k_merge_hot folds the copies into the
 // visited bitmap and k_compact resolves their parents), the rest as kBitmapOut.
 // (enum Mode: bfs_engine.cuh)
+#ifndef LBFS_QUEUE_ROWS_STREAMED
+#define LBFS_QUEUE_ROWS_STREAMED 0  // warp-bin queue rows through stream_slices (experiment)
+#endif
 
 // ---------------------------------------------------------------- memory ops
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
@@ -529,15 +532,15 @@ __device__ __forceinline__ CtaItem ld_item(const CtaItem* p) {
 // A warp walks row slices (grid-stride over items) in 128-element chunks of
 // one 128-bit load per lane; the loads of chunk i+1 are issued before chunk
 // i is probed.
-template <int M>
-__device__ __forceinline__ void stream_slices(const LevelArgs& a, const Hot& h, const CtaItem* items, int64_t n,
-                                              int64_t gwarp, int64_t nwarps, int lane, Acc& acc) {
+template <int M, typename Fetch>
+__device__ __forceinline__ void stream_slices_f(const LevelArgs& a, const Hot& h, Fetch fetch, int64_t n,
+                                                int64_t gwarp, int64_t nwarps, int lane, Acc& acc) {
   if (gwarp >= n) return;
   int64_t it = gwarp;
-  CtaItem cur = ld_item(items + it);
+  CtaItem cur = fetch(it);
   // the descriptor after cur is loaded one row ahead, so a row switch never
   // waits on it before issuing the row's first col_idx load
-  CtaItem nxt = it + nwarps < n ? ld_item(items + it + nwarps) : CtaItem{0, 0, 0};
+  CtaItem nxt = it + nwarps < n ? fetch(it + nwarps) : CtaItem{0, 0, 0};
   int64_t pos = cur.start & ~int64_t(3);
   int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
   auto load = [&](int64_t p0, int64_t e0) {
@@ -554,7 +557,7 @@ __device__ __forceinline__ void stream_slices(const LevelArgs& a, const Hot& h, 
       it += nwarps;
       if (it < n) {
         cur = nxt;
-        if (it + nwarps < n) nxt = ld_item(items + it + nwarps);
+        if (it + nwarps < n) nxt = fetch(it + nwarps);
         pos = cur.start & ~int64_t(3);
         end = (cur.start + cur.len + 3) & ~int64_t(3);
       } else {
@@ -580,6 +583,29 @@ __device__ __forceinline__ void stream_slices(const LevelArgs& a, const Hot& h, 
     if (!more) break;
     x = nx;
   }
+}
+
+template <int M>
+__device__ __forceinline__ void stream_slices(const LevelArgs& a, const Hot& h, const CtaItem* items, int64_t n,
+                                              int64_t gwarp, int64_t nwarps, int lane, Acc& acc) {
+  stream_slices_f<M>(a, h, [&](int64_t i) { return ld_item(items + i); }, n, gwarp, nwarps, lane, acc);
+}
+
+// Warp-bin rows of a queue-mode frontier (raw vertex ids) streamed like
+// slices: the row of queue entry i is [row_ptr[v], row_ptr[v+1]) with parent
+// new2old[v], fetched one row ahead (pipelined, unlike one expand_range call
+// per row).
+template <int M>
+__device__ __forceinline__ void stream_queue_rows(const LevelArgs& a, const Hot& h, const int32_t* q, int64_t n,
+                                                  int64_t gwarp, int64_t nwarps, int lane, Acc& acc) {
+  stream_slices_f<M>(
+      a, h,
+      [&](int64_t i) {
+        const int32_t v = __ldcg(q + i);
+        const int64_t st = __ldg(a.row_ptr + v);
+        return CtaItem{st, (int32_t)(__ldg(a.row_ptr + v + 1) - st), __ldg(a.new2old + v)};
+      },
+      n, gwarp, nwarps, lane, acc);
 }
 
 struct ChunkMeta {
@@ -888,6 +914,16 @@ __device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier
   // ---- phase 3: raw warp/small queues (after a queue-mode level): a warp
   // takes one warp-bin vertex or 32 small-bin vertices ---------------------
   if (phases & 4) {
+#if LBFS_QUEUE_ROWS_STREAMED
+    stream_queue_rows<M>(a, h, f.warp, f.n_warp, gwarp, nwarps, lane, acc);
+    const int64_t ng = (f.n_small + 31) / 32;
+    for (int64_t g = gwarp; g < ng; g += nwarps) {
+      const int64_t base = g * 32;
+      const int n = (int)std::min<int64_t>(32, f.n_small - base);
+      const int32_t v = lane < n ? __ldcg(f.small + base + lane) : 0;
+      expand_range<M>(a, h, n, v, 0, 1 << 30, s_T, s_B, lane, ws, acc);
+    }
+#else
     const int64_t ng = f.n_warp + (f.n_small + 31) / 32;
     for (int64_t g = gwarp; g < ng; g += nwarps) {
       const bool wb = g < f.n_warp;
@@ -896,6 +932,7 @@ __device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier
       const int32_t v = lane < n ? __ldcg((wb ? f.warp : f.small) + base + lane) : 0;
       expand_range<M>(a, h, n, v, 0, 1 << 30, s_T, s_B, lane, ws, acc);
     }
+#endif
   }
 }
 
@@ -1045,7 +1082,12 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_levels(LevelArgs a, LoopArg
     a.next_cta = p.q_cta[cur ^ 1];
     Acc acc;
     stream_slices<kQueueDirect>(a, h, p.q_cta[cur], (int64_t)c.bin[kBinCta], gwarp, nwarps, lane, acc);
+#if LBFS_QUEUE_ROWS_STREAMED
+    stream_queue_rows<kQueueDirect>(a, h, p.q_warp[cur], (int64_t)c.bin[kBinWarp], gwarp, nwarps, lane, acc);
+    const int64_t n_warp = 0, n_small = (int64_t)c.bin[kBinSmall];
+#else
     const int64_t n_warp = (int64_t)c.bin[kBinWarp], n_small = (int64_t)c.bin[kBinSmall];
+#endif
     const int32_t* qw = p.q_warp[cur];
     const int32_t* qs = p.q_small[cur];
     const int64_t ng = n_warp + (n_small + 31) / 32;

@@ -1,4 +1,7 @@
 mkdir -p gpurun_out
-echo "NCCL_DEBUG=$NCCL_DEBUG" > gpurun_out/ph_env.txt
-timeout -k 10 600 python bench.py --partitioned --steps 1 --warmup 1 --e2e-roots 2 --no-cpu-baseline > gpurun_out/ph_b2.json 2> gpurun_out/ph_b2.err; echo "rc=$?" >> gpurun_out/ph_b2.err
-NCCL_DEBUG=INFO timeout -k 10 600 python bench.py --partitioned --steps 1 --warmup 1 --e2e-roots 2 --no-cpu-baseline > gpurun_out/ph_b3.json 2> gpurun_out/ph_b3.err; echo "rc=$?" >> gpurun_out/ph_b3.err
+rm -f gpurun_out/ab_qrs.log
+V=paper_1604_02844_b200/_native/variants/qrs.so
+LBFS_LIB=$V timeout 900 python -m pytest tests/test_gpu_traversal.py tests/test_gpu_configs.py tests/test_gpu_direction.py -m gpu -x -q > gpurun_out/ab_qrs_pytest.log 2>&1
+for L in "" $V "" $V; do
+echo "LIB=$L S24 $(LBFS_LIB=$L timeout 200 python tools/quick_bfs_time.py 24 64 2>&1 | tail -1) S20 $(LBFS_LIB=$L timeout 200 python tools/quick_bfs_time.py 20 64 2>&1 | tail -1) LAT $(LBFS_LIB=$L timeout 200 python tools/quick_lattice_time.py 4096 1 2>&1 | tail -1)" >> gpurun_out/ab_qrs.log
+done
