@@ -57,6 +57,23 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 // shared copy (no probe, no parent; k_merge_hot folds the copies into the
 // visited bitmap and k_compact resolves their parents), the rest as kBitmapOut.
 // (enum Mode: bfs_engine.cuh)
+#ifndef LBFS_CHECKS
+#define LBFS_CHECKS 0  // debug builds: bounds checks that trap with a location
+#endif
+#if LBFS_CHECKS
+#define LBFS_DCHECK(cond, what)                                                                   \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("[lbfs check] %s failed at %s:%d (block %d thread %d)\n", what, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                                \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define LBFS_DCHECK(cond, what) \
+  do {                          \
+  } while (0)
+#endif
 #ifndef LBFS_QUEUE_ROWS_STREAMED
 #define LBFS_QUEUE_ROWS_STREAMED 0  // warp-bin queue rows through stream_slices (experiment)
 #endif
@@ -253,6 +270,7 @@ __device__ __forceinline__ void settle_bitmap(const LevelArgs& a, const Hot& h, 
     if (!((cmask >> k) & 1u)) continue;
     const int32_t v = nb[k];
     const int32_t wi = v >> 5;
+    LBFS_DCHECK(v >= 0 && (int64_t)v < a.chk_n, "settle_bitmap target id");
     if (wi != run_w) {
       if (run_bits) {
         red_or(a.visited + run_w, run_bits);
@@ -299,6 +317,8 @@ __device__ __forceinline__ uint32_t probe_mask(const LevelArgs& a, const Hot& h,
       asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(nb[k]));
       const bool ok = (okmask >> k) & 1u;
       const bool hot = W == kAllHot || (W != kAllCold && (nb[k] >> 5) < h.words);
+      LBFS_DCHECK(!ok || (nb[k] >= 0 && (int64_t)nb[k] < a.chk_n), "heavy probe target id");
+      LBFS_DCHECK(!(ok && hot) || (nb[k] >> 5) < h.words, "heavy hot word");
       if (ok && hot) {
         asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(h.base + 4u * (uint32_t)(nb[k] >> 5)), "r"(bit) : "memory");
       } else if (ok) {
@@ -426,6 +446,7 @@ __device__ __forceinline__ void expand_group(const LevelArgs& a, const Hot& h, i
       int lo = 0;
       for (int step = top; step; step >>= 1)
         if (ws.off[lo + step] <= e) lo += step;
+      LBFS_DCHECK(!ok || (ws.start[lo] + e >= 0 && ws.start[lo] + e < a.chk_nnz), "expand_group element");
       nb[k] = ok ? ld_stream(a.col_idx + ws.start[lo] + e) : 0;
       par[k] = ws.vert[lo];
     }
@@ -545,6 +566,7 @@ __device__ __forceinline__ void stream_slices_f(const LevelArgs& a, const Hot& h
   int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
   auto load = [&](int64_t p0, int64_t e0) {
     const int64_t i1 = p0 + lane * 4;
+    LBFS_DCHECK(!(i1 < e0) || (i1 >= 0 && i1 + 4 <= a.chk_nnz + 8), "slice load");
     return i1 < e0 ? ld_stream4(a.col_idx + i1) : make_int4(0, 0, 0, 0);
   };
   int4 x = load(pos, end);
@@ -710,6 +732,7 @@ __device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier
         end = (cur.start + cur.len + 3) & ~int64_t(3);
       }
       const int64_t cnt = std::min<int64_t>(kWarpChunk, end - pos);
+      LBFS_DCHECK(pos >= 0 && cnt > 0 && pos + cnt <= a.chk_nnz + 8 && cur.len >= 0, "hub chunk range");
       s_meta[wib][b] = ChunkMeta{pos, cur.start, cur.start + cur.len, cur.u};
       mbar_expect_tx(&s_bar[wib][b], (uint32_t)(cnt * 4));
       bulk_g2s(wbuf + b * kWarpChunk, a.col_idx + pos, (uint32_t)(cnt * 4), &s_bar[wib][b]);
@@ -930,6 +953,7 @@ __device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier
       const int64_t base = wb ? g : (g - f.n_warp) * 32;
       const int n = wb ? 1 : (int)std::min<int64_t>(32, f.n_small - base);
       const int32_t v = lane < n ? __ldcg((wb ? f.warp : f.small) + base + lane) : 0;
+      LBFS_DCHECK(!(lane < n) || (v >= 0 && (int64_t)v < a.chk_n), "queue entry");
       expand_range<M>(a, h, n, v, 0, 1 << 30, s_T, s_B, lane, ws, acc);
     }
 #endif
@@ -2108,6 +2132,8 @@ LevelArgs BfsEngine::level_args() const {
   a.t_nz = t_nz_;
   a.part_log = part_log_;
   a.part_rank = part_rank_;
+  a.chk_n = n_;
+  a.chk_nnz = nnz_loc_;
   // queue-mode hub items: small enough that a hub's row spreads over many
   // warps (a queue level is latency-bound per slice, not bandwidth-bound)
   const char* qc = getenv("LBFS_QCHUNK");

@@ -138,6 +138,7 @@ struct LevelArgs {
   uint32_t* stage;
   int32_t stage_first;
   int32_t stage_words;      // row stride of stage (>= the kernel's hot words: the sweep's prefix can be longer)
+  int64_t chk_n, chk_nnz;   // sizes for the LBFS_CHECKS debug build's bounds checks
 };
 
 struct CompactArgs {
