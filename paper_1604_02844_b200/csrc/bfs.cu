@@ -2015,7 +2015,6 @@ BfsEngine::~BfsEngine() {
   dev_free(stage_);
   dev_free(side_);
   dev_free(first_nbr_);
-  dev_free(win_info_);
   dev_free(svmask_);
   dev_free(sdesc_);
   dev_free(pred_int_);
@@ -2228,7 +2227,7 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
                   w_small0_, nsw, svmask_);
     }
     SweepArgs sa{col_idx_, side_, n_side_win_, e_big_, sweep_small ? n_win_all_ : n_side_win_,
-                 sweep_small ? e_nz_ : e_big_, sweep_small ? w_small0_ : n_win_all_ + 1, svmask_, front_, win_info_,
+                 sweep_small ? e_nz_ : e_big_, sweep_small ? w_small0_ : n_win_all_ + 1, svmask_, front_,
                  visited_, pred_int_, new2old_loc_,
                  stage_, 1, sweep_hot_words_, getenv("LBFS_SWEEP_PF") ? atoi(getenv("LBFS_SWEEP_PF")) : kSweepPrefetch,
                  getenv("LBFS_SWEEP_DBG") ? atoi(getenv("LBFS_SWEEP_DBG")) : 0};

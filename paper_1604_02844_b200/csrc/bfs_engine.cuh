@@ -272,7 +272,6 @@ struct SweepArgs {
   int64_t w_small0;         // first window holding small-region elements (e_big / 128)
   const uint4* svmask;      // valid masks of windows [w_small0, nwin_all) (k_sweep_plan_small)
   const uint32_t* front;    // frontier bitmap of the level (internal ids)
-  const uint32_t* info;     // per window: k_sweep_plan's frontier bits | code << 8
   uint32_t* visited;
   int32_t* pred_int;
   const int32_t* new2old;
@@ -297,7 +296,6 @@ __global__ void k_front_from_queues(uint32_t* front, const int32_t* qs, int64_t 
                                     const CtaItem* qc, int64_t nc, const int32_t* old2new);
 __global__ void k_side_table(const int64_t* rp, int32_t nrows, int64_t nwin, uint2* side);
 __global__ void k_sweep(const __grid_constant__ SweepArgs s);
-__global__ void k_sweep_plan(const uint2* side, const uint32_t* front, int64_t nwin, uint32_t* info);
 __global__ void k_resolve(const int32_t* level_int, const int32_t* first_nbr, const int64_t* row_ptr,
                           const int32_t* col_idx, const int32_t* new2old, int32_t* pred_int, int64_t n, int32_t lvl);
 __global__ void k_small_desc(const ClassTable* classes, int64_t e_big, int64_t e_end, int64_t w0, int64_t nw,
@@ -443,7 +441,6 @@ class BfsEngine {
   uint32_t* stage_ = nullptr;    // heavy levels: expand_grid_ rows of hot_words_ words
   uint2* side_ = nullptr;        // sweep side entries (nparts 1)
   int32_t* first_nbr_ = nullptr; // first neighbour of each row (heavy-level parent resolution)
-  uint32_t* win_info_ = nullptr; // sweep: per-level window codes (k_sweep_plan)
   uint4* svmask_ = nullptr;      // sweep: per-level valid masks of the small-region windows
   uint2* sdesc_ = nullptr;       // sweep: small-region window descriptors (k_small_desc)
   int64_t e_nz_ = 0, n_win_all_ = 0, w_small0_ = 0;

@@ -224,7 +224,6 @@ void BfsEngine::build_layout(const Csr& csr) {
   n_side_win_ = t_warp_ > 0 ? (e_big_ + kSweepWindow - 1) / kSweepWindow : 0;
   if (nparts_ == 1 && n_side_win_ > 0) {
     side_ = dev_alloc<uint2>((size_t)n_side_win_);
-    win_info_ = dev_alloc<uint32_t>((size_t)n_side_win_);
     LBFS_LAUNCH(k_side_table, clamp_grid((n_side_win_ + 255) / 256, 148 * 16), 256, 0, st, row_ptr_, t_warp_,
                 n_side_win_, side_);
   }

@@ -14,16 +14,16 @@
 //
 // Per element (heavy semantics, see kHeavy in bfs.cu): a target in the hot
 // prefix is OR'ed blindly into the CTA's shared copy (flushed to its stage
-// row; k_merge_hot folds the rows into visited and k_compact resolves those
-// parents), a cold target is probed in L2 and, when clear, settled with
-// red.or + its parent.
+// row; k_merge_hot folds the rows into visited), a cold target blindly into
+// visited in L2 with a fire-and-forget red.or. No parent is written: k_resolve
+// gives every vertex of the level its first neighbour one level up.
 //
-// Warp-specialised pipeline per CTA (one per SM): a producer warp reads the
-// side entries and frontier words of a 32-window chunk, writes the window
-// metadata and bulk-copies (TMA) the windows that hold frontier rows into a
-// kSweepStages-deep shared ring; 16 consumer warps take two windows each,
-// OR the hot targets, issue the cold probes, and test those probes one chunk
-// later (the stage is released only then), so no warp waits on L2 per chunk.
+// Warp-specialised pipeline per CTA (one per SM): producer warps read the
+// side entries and frontier words of a 32-window chunk (two chunks ahead),
+// write the window metadata and bulk-copy (TMA) the span of windows that hold
+// frontier rows into a kSweepStages-deep shared ring; 16 consumer warps copy
+// two windows each into registers, release the stage, then OR the targets,
+// so no warp waits on L2 per element.
 #include <algorithm>
 
 #include "bfs_engine.cuh"
@@ -89,17 +89,6 @@ __global__ void k_side_table(const int64_t* __restrict__ rp, int32_t nrows, int6
       starts = (starts & ~(0xFFu << (8 * k))) | ((uint32_t)(s - P) << (8 * k));
     }
     side[w] = make_uint2((uint32_t)lo, starts);
-  }
-}
-
-// Per heavy level, before k_sweep: window_info of every window (frontier
-// bits of its rows + skip / whole / masked code).
-__global__ void k_sweep_plan(const uint2* __restrict__ side, const uint32_t* __restrict__ front, int64_t nwin,
-                             uint32_t* __restrict__ info) {
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwin; w += (int64_t)gridDim.x * blockDim.x) {
-    const uint2 sd = __ldg(side + w);
-    const uint2 fw = make_uint2(__ldg(front + (sd.x >> 5)), __ldg(front + (sd.x >> 5) + 1));
-    info[w] = window_info(sd, fw, true);
   }
 }
 
@@ -311,9 +300,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
 
   if (warp >= kConsumers) {
     // ---------------- producers: producer warp p takes the CTA's chunks
-    // p, p + kProducers, ...; lane j owns window j of a chunk. Per chunk two
-    // independent loads (side entry, window info from k_sweep_plan) and one
-    // wait: kSweepProducers chains in flight cover the latency.
+    // p, p + kProducers, ...; lane j owns window j of a chunk and derives its
+    // window info from the side entry and the frontier bitmap.
     const int64_t i0 = warp - kConsumers;
     int st = (int)(i0 % kStages);
     uint32_t ph = (uint32_t)((i0 / kStages) & 1);
