@@ -84,6 +84,7 @@ struct alignas(16) DenseTask {
 };
 constexpr int kDenseTask = 4096;  // elements per dense task
 constexpr int kDenseNum = 1, kDenseDenom = 2;  // dense when list > region/2
+constexpr int64_t kDenseMinElems = (int64_t)1 << 22;  // ... and the small region holds >= 4 M elements
 
 struct Frontier {
   const int32_t* small;    // after a queue-mode level: small/warp-bin queues ...
@@ -397,6 +398,8 @@ class BfsEngine {
   DenseTask* dense_tasks_ = nullptr;
   int64_t n_dense_tasks_ = 0;
   bool dense_off_ = false;
+  int dense_pct_ = 100 * kDenseNum / kDenseDenom;
+  int64_t dense_min_elems_ = kDenseMinElems;
   bool dense_warp_ = false;
   int32_t* q_small_[2] = {nullptr, nullptr};
   int32_t* q_warp_[2] = {nullptr, nullptr};
