@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-rm -f gpurun_out/ab_dense3.log
-for M in 2097152 4194304 8388608; do
-echo "MIN=$M S20 $(LBFS_DENSE_MIN=$M timeout 200 python tools/quick_bfs_time.py 20 64 2>&1 | tail -1) S22 $(LBFS_DENSE_MIN=$M timeout 200 python tools/quick_bfs_time.py 22 64 2>&1 | tail -1)" >> gpurun_out/ab_dense3.log
-done
+WARM_S=0.5 LBFS_GAPS=1 timeout 200 python tools/quick_bfs_time.py 20 6 2>&1 | tail -13 > gpurun_out/s20_gaps.log
+WARM_S=0.5 LBFS_TRACE=1 LBFS_SPLIT=1 timeout 200 python tools/quick_bfs_time.py 20 2 2>&1 | grep -v "^\[lbfs\]      split" | tail -20 >> gpurun_out/s20_gaps.log
