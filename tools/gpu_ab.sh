@@ -1,3 +1,6 @@
 mkdir -p gpurun_out
-WARM_S=0.5 LBFS_GAPS=1 timeout 200 python tools/quick_bfs_time.py 20 6 2>&1 | tail -13 > gpurun_out/s20_gaps.log
-WARM_S=0.5 LBFS_TRACE=1 LBFS_SPLIT=1 timeout 200 python tools/quick_bfs_time.py 20 2 2>&1 | grep -v "^\[lbfs\]      split" | tail -20 >> gpurun_out/s20_gaps.log
+rm -f gpurun_out/ab_fold.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/ab_fold_pytest.log 2>&1
+for F in 1 0 1 0; do
+echo "FOLD=$F S24 $(LBFS_FOLD_PUBLISH=$F timeout 200 python tools/quick_bfs_time.py 24 64 2>&1 | tail -1) S20 $(LBFS_FOLD_PUBLISH=$F timeout 200 python tools/quick_bfs_time.py 20 64 2>&1 | tail -1)" >> gpurun_out/ab_fold.log
+done
