@@ -1491,9 +1491,12 @@ __device__ __forceinline__ void init_range(uint4* __restrict__ vis4, uint4* __re
   for (int64_t i = t; i < n4; i += stride) lvl4[i] = m4;
 }
 __global__ void k_init(uint4* __restrict__ vis4, uint4* __restrict__ prev4, int64_t nwords4,
-                       int4* __restrict__ lvl4, int64_t n4) {
+                       int4* __restrict__ lvl4, int64_t n4, Counters* __restrict__ ring) {
   init_range(vis4, prev4, nwords4, lvl4, n4, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
              (int64_t)gridDim.x * blockDim.x);
+  // (host-driven BFS) the counter ring cleared here instead of by a memset
+  if (ring && blockIdx.x == 0 && threadIdx.x < (int)(kCounterRing * sizeof(Counters) / 8))
+    reinterpret_cast<unsigned long long*>(ring)[threadIdx.x] = 0ull;
 }
 
 // Outputs in original ids, once per BFS: sequential (128-bit) writes of
@@ -2548,7 +2551,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   {  // K4: bitmaps + internal levels (outputs are written once, by k_finalize)
     const unsigned grid = clamp_grid((n_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
     LBFS_LAUNCH(k_init, grid, 256, 0, st, (uint4*)visited_, (uint4*)prev_, (nwords_ + 3) / 4, (int4*)level_int_,
-                (n_ + 3) / 4);
+                (n_ + 3) / 4, cnt_);
   }
   LevelArgs a = level_args();
   int cur = 0;
@@ -2556,7 +2559,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   a.next_warp = q_warp_[cur];
   a.next_cta = q_cta_[cur];
   // ring invariant: at the start of level L, slot (L+1)%3 is zero
-  LBFS_CUDA(cudaMemsetAsync(cnt_, 0, sizeof(Counters) * kCounterRing, st));
+  // (the counter ring was cleared by k_init)
   LBFS_LAUNCH(k_seed, 1, 1, 0, st, a, prev_, old2new_, (int32_t)root, &cnt_[0], nullptr, nullptr);
   LBFS_CUDA(cudaEventRecord(ev_[1], st));
   const bool dev_loop = loop_grid_ > 0 && !loop_off_ && !split_ && !count_;

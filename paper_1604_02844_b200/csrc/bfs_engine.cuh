@@ -305,7 +305,8 @@ __global__ void k_sweep_plan_small(const ClassTable* classes, const uint2* desc,
                                    int64_t w0, int64_t nw, uint4* svmask);
 
 bool env_flag(const char* name);
-__global__ void k_init(uint4* vis4, uint4* prev4, int64_t nwords4, int4* lvl4, int64_t n4);
+__global__ void k_init(uint4* vis4, uint4* prev4, int64_t nwords4, int4* lvl4, int64_t n4,
+                       Counters* ring = nullptr);
 __global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int32_t root_orig, Counters* cnt0,
                        uint32_t* fglob, unsigned long long* red);
 unsigned clamp_grid(int64_t blocks, int64_t cap);
