@@ -1,6 +1,6 @@
+set -x
 mkdir -p gpurun_out
-rm -f gpurun_out/ab_init.log
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/ab_init_pytest.log 2>&1
-for i in 1 2 3; do
-echo "S24 $(timeout 200 python tools/quick_bfs_time.py 24 64 2>&1 | tail -1) S20 $(timeout 200 python tools/quick_bfs_time.py 20 64 2>&1 | tail -1)" >> gpurun_out/ab_init.log
-done
+timeout -k 10 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r1k_smoke.log 2>&1; echo "smoke rc=$?"
+timeout -k 10 600 python bench.py > gpurun_out/r1k_bench.json 2> gpurun_out/r1k_bench.err; echo "bench rc=$?"
+timeout -k 10 600 python bench.py --impl reference > gpurun_out/r1k_reference.json 2> gpurun_out/r1k_reference.err; echo "ref rc=$?"
+bash tools/profile_round.sh r1k; echo "prof rc=$?"
