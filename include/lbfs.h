@@ -47,8 +47,10 @@ typedef struct lbfs_layer {
 typedef struct lbfs_timing {
   double bfs_ms;           /* init kernel start -> end of last level         */
   double init_ms;          /* K4 init (pred/level fill, bitmap clear, seed)  */
-  double expand_ms;        /* sum over levels of the expansion kernels       */
-  double d2h_ms;           /* host-output variant: pred+level copy to host   */
+  double expand_ms;        /* full-GPU levels: expansion kernels (summed)    */
+  double cluster_ms;       /* small-frontier levels on the cluster (summed)  */
+  double finalize_ms;      /* output pass (parents / levels in original ids) */
+  double d2h_ms;           /* host-output variant: output copy to host       */
   int64_t levels;          /* number of layers (== n_layers)                 */
   int64_t kernel_launches; /* kernels this BFS launched                      */
   int64_t edges;           /* traversed_edge_count (sum of layer edges)      */
@@ -126,30 +128,36 @@ int lbfs_graph_create_from_csr(const lbfs_csr* csr, int ngpus, lbfs_graph** out)
 void lbfs_graph_destroy(lbfs_graph* g);
 int lbfs_graph_info(const lbfs_graph* g, int64_t* n, int64_t* nnz);
 
-/* Top-down BFS from root; synchronous. Replaces run_bfs/bfs_* (traversal.py:
- * 80-422). pred_out must hold pad32(n) int32 entries (PredecessorArray
- * storage, traversal.py:42-46): parent id, root -> root, unreached and padding
- * -> LBFS_SENTINEL. level_out holds n int32 (-1 = unreached). Either output
- * may be NULL. layers_out receives up to layers_cap layers; *n_layers is the
- * full count (fetch the rest with lbfs_graph_last_layers). t_out may be NULL. */
-int lbfs_bfs(lbfs_graph* g, int64_t root, int32_t* pred_out, int32_t* level_out,
-             lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers, lbfs_timing* t_out);
-/* Same, writing into DEVICE buffers (e.g. torch CUDA tensors) on the graph's
- * device; no host copy inside. */
-int lbfs_bfs_device(lbfs_graph* g, int64_t root, int32_t* d_pred, int32_t* d_level,
-                    lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers,
-                    lbfs_timing* t_out);
-/* Layers of the most recent BFS on this handle. */
-int lbfs_graph_last_layers(const lbfs_graph* g, lbfs_layer* out, int64_t cap, int64_t* n_layers);
-/* Traversal direction of later lbfs_bfs / lbfs_bfs_device calls on this
- * handle: LBFS_DIR_TOP_DOWN (default; the paper's algorithm, the benchmarked
- * path) or LBFS_DIR_OPTIMIZING (bottom-up levels while the frontier is large,
- * Beamer's alpha = 14 / beta = 24 rule). Levels, visited
- * set and layers are identical in both; parents may differ (any neighbour one
- * level up). No reference counterpart: the reference is top-down only. */
+/* Traversal direction of one BFS call: LBFS_DIR_TOP_DOWN (the paper's
+ * algorithm, the benchmarked path) or LBFS_DIR_OPTIMIZING (bottom-up levels
+ * while the frontier is large, Beamer's alpha = 14 / beta = 24 rule; SURVEY
+ * §8(f) rank 4). Levels, visited set and layers are identical in both;
+ * parents may differ (any neighbour one level up). No reference counterpart:
+ * the reference is top-down only. */
 #define LBFS_DIR_TOP_DOWN 0
 #define LBFS_DIR_OPTIMIZING 1
-int lbfs_graph_set_direction(lbfs_graph* g, int direction);
+
+/* BFS from root; synchronous. Replaces run_bfs/bfs_* (traversal.py:80-422).
+ * pred_out must hold pad32(n) int32 entries (PredecessorArray storage,
+ * traversal.py:42-46): parent id, root -> root, unreached and padding ->
+ * LBFS_SENTINEL. level_out holds n int32 (-1 = unreached). Either output may
+ * be NULL (a NULL level_out skips the level copy; lbfs_graph_last_levels
+ * fetches them later). All layers are returned under the handle's lock:
+ * layers_out receives min(layers_cap, count) of them and *n_layers the count;
+ * with too small a buffer call lbfs_graph_last_layers before the next BFS.
+ * t_out may be NULL. */
+int lbfs_bfs(lbfs_graph* g, int64_t root, int direction, int32_t* pred_out, int32_t* level_out,
+             lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers, lbfs_timing* t_out);
+/* Same, writing into DEVICE buffers (e.g. torch CUDA tensors) on the graph's
+ * device; no host copy inside. d_level may be NULL. */
+int lbfs_bfs_device(lbfs_graph* g, int64_t root, int direction, int32_t* d_pred, int32_t* d_level,
+                    lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers,
+                    lbfs_timing* t_out);
+/* Layers of the most recent BFS on this handle (locked). */
+int lbfs_graph_last_layers(lbfs_graph* g, lbfs_layer* out, int64_t cap, int64_t* n_layers);
+/* Levels (n int32, -1 = unreached, original ids) of the most recent BFS on
+ * this handle, to host memory; valid until the next BFS on the handle. */
+int lbfs_graph_last_levels(lbfs_graph* g, int32_t* level_out);
 
 /* ---- tree validation (replaces validate_tree, validate.py:50-155) ------
  * The reference's five checks on a parent array in original ids (n int32;

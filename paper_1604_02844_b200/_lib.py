@@ -33,7 +33,8 @@ class Layer(ctypes.Structure):
 
 class Timing(ctypes.Structure):
     _fields_ = [("bfs_ms", ctypes.c_double), ("init_ms", ctypes.c_double),
-                ("expand_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double),
+                ("expand_ms", ctypes.c_double), ("cluster_ms", ctypes.c_double),
+                ("finalize_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double),
                 ("levels", _i64), ("kernel_launches", _i64), ("edges", _i64), ("reached", _i64)]
 
     def as_dict(self) -> dict:
@@ -68,12 +69,12 @@ SIGNATURES = {
     "lbfs_graph_create_from_csr": (ctypes.c_int, [_p, ctypes.c_int, ctypes.POINTER(_p)]),
     "lbfs_graph_destroy": (None, [_p]),
     "lbfs_graph_info": (ctypes.c_int, [_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
-    "lbfs_bfs": (ctypes.c_int, [_p, _i64, _p, _p, ctypes.POINTER(Layer), _i64, ctypes.POINTER(_i64),
-                                ctypes.POINTER(Timing)]),
-    "lbfs_bfs_device": (ctypes.c_int, [_p, _i64, _p, _p, ctypes.POINTER(Layer), _i64,
+    "lbfs_bfs": (ctypes.c_int, [_p, _i64, ctypes.c_int, _p, _p, ctypes.POINTER(Layer), _i64,
+                                ctypes.POINTER(_i64), ctypes.POINTER(Timing)]),
+    "lbfs_bfs_device": (ctypes.c_int, [_p, _i64, ctypes.c_int, _p, _p, ctypes.POINTER(Layer), _i64,
                                        ctypes.POINTER(_i64), ctypes.POINTER(Timing)]),
     "lbfs_graph_last_layers": (ctypes.c_int, [_p, ctypes.POINTER(Layer), _i64, ctypes.POINTER(_i64)]),
-    "lbfs_graph_set_direction": (ctypes.c_int, [_p, ctypes.c_int]),
+    "lbfs_graph_last_levels": (ctypes.c_int, [_p, _p]),
     "lbfs_set_device": (ctypes.c_int, [ctypes.c_int]),
     "lbfs_validate_tree": (ctypes.c_int, [_p, _i64, _p, _p]),
     "lbfs_validate_tree_device": (ctypes.c_int, [_p, _i64, _p, _p]),

@@ -339,15 +339,6 @@ int lbfs_graph_info(const lbfs_graph* g, int64_t* n, int64_t* nnz) {
   });
 }
 
-int lbfs_graph_set_direction(lbfs_graph* g, int direction) {
-  return guarded([&] {
-    if (!g) throw_inval("graph is NULL");
-    if (direction != LBFS_DIR_TOP_DOWN && direction != LBFS_DIR_OPTIMIZING) throw_inval("unknown direction");
-    std::lock_guard<std::mutex> lk(g->eng->mu);
-    g->eng->set_direction(direction);
-  });
-}
-
 static void copy_layers(const BfsEngine& e, lbfs_layer* out, int64_t cap, int64_t* n_layers) {
   const auto& L = e.layers();
   if (n_layers) *n_layers = (int64_t)L.size();
@@ -357,7 +348,7 @@ static void copy_layers(const BfsEngine& e, lbfs_layer* out, int64_t cap, int64_
   }
 }
 
-int lbfs_bfs(lbfs_graph* g, int64_t root, int32_t* pred_out, int32_t* level_out,
+int lbfs_bfs(lbfs_graph* g, int64_t root, int direction, int32_t* pred_out, int32_t* level_out,
              lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers, lbfs_timing* t_out) {
   return guarded([&] {
     if (!g) throw_inval("graph is NULL");
@@ -367,53 +358,48 @@ int lbfs_bfs(lbfs_graph* g, int64_t root, int32_t* pred_out, int32_t* level_out,
     if (root < 0 || root >= e.n()) throw_inval("root out of range");
     e.ensure_own_outputs();
     lbfs_timing t{};
-    e.run(root, e.own_pred(), e.own_level(), &t);
-    cudaEvent_t a, b;
-    LBFS_CUDA(cudaEventCreate(&a));
-    LBFS_CUDA(cudaEventCreate(&b));
-    LBFS_CUDA(cudaEventRecord(a, e.stream()));
-    if (pred_out)
-      LBFS_CUDA(cudaMemcpyAsync(pred_out, e.own_pred(), sizeof(int32_t) * (size_t)e.npad(),
-                                cudaMemcpyDeviceToHost, e.stream()));
-    if (level_out)
-      LBFS_CUDA(cudaMemcpyAsync(level_out, e.own_level(), sizeof(int32_t) * (size_t)e.n(),
-                                cudaMemcpyDeviceToHost, e.stream()));
-    LBFS_CUDA(cudaEventRecord(b, e.stream()));
-    LBFS_CUDA(cudaEventSynchronize(b));
-    float ms = 0.f;
-    LBFS_CUDA(cudaEventElapsedTime(&ms, a, b));
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    t.d2h_ms = ms;
+    // the parents are copied while the output pass is still writing later
+    // chunks of them (BfsEngine::run_to_host); levels only when asked for
+    e.run_to_host(root, direction, pred_out, level_out, &t);
     if (t_out) *t_out = t;
     copy_layers(e, layers_out, layers_cap, n_layers);
   });
 }
 
-int lbfs_bfs_device(lbfs_graph* g, int64_t root, int32_t* d_pred, int32_t* d_level,
+int lbfs_bfs_device(lbfs_graph* g, int64_t root, int direction, int32_t* d_pred, int32_t* d_level,
                     lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers,
                     lbfs_timing* t_out) {
   return guarded([&] {
     if (!g) throw_inval("graph is NULL");
-    if (!d_pred || !d_level) throw_inval("device outputs must be non-NULL");
+    if (!d_pred) throw_inval("device pred output must be non-NULL");
     BfsEngine& e = *g->eng;
     std::lock_guard<std::mutex> lk(e.mu);
     LBFS_CUDA(cudaSetDevice(e.device()));
     if (root < 0 || root >= e.n()) throw_inval("root out of range");
     lbfs_timing t{};
-    e.run(root, d_pred, d_level, &t);
+    e.run(root, d_pred, d_level, &t, direction);
     if (t_out) *t_out = t;
     copy_layers(e, layers_out, layers_cap, n_layers);
   });
 }
 
-int lbfs_graph_last_layers(const lbfs_graph* g, lbfs_layer* out, int64_t cap, int64_t* n_layers) {
+int lbfs_graph_last_layers(lbfs_graph* g, lbfs_layer* out, int64_t cap, int64_t* n_layers) {
   return guarded([&] {
     if (!g) throw_inval("graph is NULL");
+    std::lock_guard<std::mutex> lk(g->eng->mu);
     copy_layers(*g->eng, out, cap, n_layers);
   });
 }
 
+int lbfs_graph_last_levels(lbfs_graph* g, int32_t* level_out) {
+  return guarded([&] {
+    if (!g || !level_out) throw_inval("bad arguments");
+    BfsEngine& e = *g->eng;
+    std::lock_guard<std::mutex> lk(e.mu);
+    LBFS_CUDA(cudaSetDevice(e.device()));
+    e.last_levels_to_host(level_out);
+  });
+}
 
 /* ---- tree validation on the device ------------------------------------ */
 

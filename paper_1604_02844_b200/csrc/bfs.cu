@@ -1015,142 +1015,6 @@ __global__ void __launch_bounds__(256) k_merge_hot(const uint4* __restrict__ sta
   if (x.w) red_or(w + 3, x.w);
 }
 
-// ---------------------------------------------------------------- K5 on the device
-// Grid-wide barrier for a co-resident grid (cooperative launch): one arrival
-// atomic per CTA, the last arrival bumps the generation word. The fences
-// make the CTA's writes of this level (queue entries, counters, bitmap)
-// visible to every CTA after the barrier.
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
-  unsigned r;
-  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
-  return r;
-}
-__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
-  asm volatile("red.add.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// g: this CTA's copy of the generation word (read once at kernel start; it
-// cannot advance before every CTA has arrived), advanced here.
-__device__ __forceinline__ void grid_sync(unsigned* count, unsigned* gen, unsigned& g,
-                                          unsigned long long* last_arrival) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (atom_add_acq_rel(count, 1u) == gridDim.x - 1) {
-      if (last_arrival) *last_arrival = gtimer();
-      *(volatile unsigned*)count = 0u;  // ordered before the release below
-      red_add_release(gen, 1u);
-    } else {
-      while (ld_acquire(gen) == g) {
-      }
-    }
-  }
-  ++g;
-  __syncthreads();
-}
-
-__device__ __forceinline__ Counters ld_counters(const Counters* p) {
-  Counters c;
-  const ulonglong2* s = reinterpret_cast<const ulonglong2*>(p);
-  ulonglong2* d = reinterpret_cast<ulonglong2*>(&c);
-#pragma unroll
-  for (int i = 0; i < (int)(sizeof(Counters) / 16); ++i) d[i] = __ldcg(s + i);
-  return c;
-}
-
-// Consecutive queue-mode levels in one launch (the level loop of
-// traversal.py:90 moved onto the device for small frontiers): per level, the
-// frontier queues of slot L%2 are expanded with winner election + appends
-// into slot (L+1)%2 exactly as k_expand<kQueueOut> does, then one grid
-// barrier. Counters live in the same 3-slot ring as the host loop uses; slot
-// (L+2)%3 is cleared during level L (nobody reads it then). The loop returns
-// to the host when the next frontier is empty, needs bitmap mode
-// (edges >= bitmap_min_edges) or the layer buffer is full. Queue entries and
-// counters are re-read through L2 (__ldcg): L1 is not coherent within a
-// launch and a queue buffer is reused every other level.
-__global__ void __launch_bounds__(kLoopThreads, 1) k_levels(LevelArgs a, LoopArgs p) {
-  __shared__ WarpScratch s_ws[kLoopThreads / 32];
-  __shared__ int32_t s_T[kSmallMax + 2];
-  __shared__ int64_t s_B[kSmallMax + 1];
-  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-  if (tid < kSmallMax + 2) s_T[tid] = a.classes->T[tid];
-  if (tid < kSmallMax + 1) s_B[tid] = a.classes->base[tid];
-  __syncthreads();
-  const Hot h{nullptr, 0u, 0};
-  const int64_t gwarp = (int64_t)wib * gridDim.x + blockIdx.x;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  WarpScratch& ws = s_ws[wib];
-  int64_t L = p.L0;
-  unsigned long long t0 = 0;
-  unsigned gen = tid == 0 ? ld_acquire(&p.state->bar_gen) : 0u;
-  Counters c = ld_counters(&p.ring[L % kCounterRing]);
-  for (;;) {
-    // the frontier of level L: empty, large (bitmap mode, host-driven) or the cap -> stop
-    if (c.discovered == 0 || c.edges >= p.bitmap_min_edges || L - p.L0 >= p.max_levels) break;
-    if (p.prof && blockIdx.x == 0 && tid == 0) t0 = gtimer();
-    const int cur = (int)(L & 1);
-    if (blockIdx.x == 0 && tid < (int)(sizeof(Counters) / 8))
-      reinterpret_cast<unsigned long long*>(&p.ring[(L + 2) % kCounterRing])[tid] = 0ull;
-    a.next_level = (int32_t)(L + 1);
-    a.next_cnt = &p.ring[(L + 1) % kCounterRing];
-    a.next_small = p.q_small[cur ^ 1];
-    a.next_warp = p.q_warp[cur ^ 1];
-    a.next_cta = p.q_cta[cur ^ 1];
-    Acc acc;
-    stream_slices<kQueueDirect>(a, h, p.q_cta[cur], (int64_t)c.bin[kBinCta], gwarp, nwarps, lane, acc);
-#if LBFS_QUEUE_ROWS_STREAMED
-    stream_queue_rows<kQueueDirect>(a, h, p.q_warp[cur], (int64_t)c.bin[kBinWarp], gwarp, nwarps, lane, acc);
-    const int64_t n_warp = 0, n_small = (int64_t)c.bin[kBinSmall];
-#else
-    const int64_t n_warp = (int64_t)c.bin[kBinWarp], n_small = (int64_t)c.bin[kBinSmall];
-#endif
-    const int32_t* qw = p.q_warp[cur];
-    const int32_t* qs = p.q_small[cur];
-    const int64_t ng = n_warp + (n_small + 31) / 32;
-    for (int64_t g = gwarp; g < ng; g += nwarps) {
-      const bool wb = g < n_warp;
-      const int64_t base = wb ? g : (g - n_warp) * 32;
-      const int n = wb ? 1 : (int)std::min<int64_t>(32, n_small - base);
-      const int32_t v = lane < n ? __ldcg((wb ? qw : qs) + base + lane) : 0;
-      expand_range<kQueueDirect>(a, h, n, v, 0, 1 << 30, s_T, s_B, lane, ws, acc);
-    }
-    flush_acc<kQueueDirect>(a, acc);
-    grid_sync(&p.state->bar_count, &p.state->bar_gen, gen, p.prof ? p.prof + 3 : nullptr);
-    if (p.prof && blockIdx.x == 0 && tid == 0) {  // LBFS_LOOP_PROF: expansion / barrier split
-      const unsigned long long t2 = gtimer(), t1 = *(volatile unsigned long long*)(p.prof + 3);
-      p.prof[0] += t1 - t0;
-      p.prof[1] += t2 - t1;
-      p.prof[2] += 1;
-    }
-    const Counters nx = ld_counters(a.next_cnt);
-    if (blockIdx.x == 0 && tid == 0)
-      p.layers[L - p.L0] = lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, (int64_t)nx.discovered};
-    ++L;
-    c = nx;
-  }
-  if (blockIdx.x == 0 && tid == 0) {
-    p.state->L_end = L;
-    if (p.mail) {
-      Counters m = c;
-      m.pad[0] = (unsigned long long)L;
-      volatile unsigned long long* dst = reinterpret_cast<volatile unsigned long long*>(p.mail);
-      const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&m);
-#pragma unroll
-      for (int i = 0; i < (int)(sizeof(Counters) / 8); ++i) dst[i] = src[i];
-      __threadfence_system();
-      *reinterpret_cast<volatile unsigned long long*>(p.seq) = p.seq_value;
-    }
-  }
-}
-
 // ---------------------------------------------------------------- K3 compaction
 // A block owns kCompactVerts consecutive internal ids (kCompactWords visited
 // words): new = visited & ~prev. Hubs become kChunk slices; the other new
@@ -1499,63 +1363,34 @@ __global__ void k_init(uint4* __restrict__ vis4, uint4* __restrict__ prev4, int6
     reinterpret_cast<unsigned long long*>(ring)[threadIdx.x] = 0ull;
 }
 
-// Outputs in original ids, once per BFS: sequential (128-bit) writes of
-// level[x] and pred[x], gathering the internal-order records through old2new
-// (PredecessorArray semantics, traversal.py:42-50: unreached and padding =
-// SENTINEL). Replaces per-vertex scattered writes during the levels.
-__device__ __forceinline__ void finalize_vec(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
-                                             const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
-                                             int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out,
-                                             int64_t t, int64_t stride) {
-  for (int64_t i = t; i * 4 < npad; i += stride) {
-    int lv[4], pr[4];
+// Outputs in original ids, once per BFS (PredecessorArray semantics,
+// traversal.py:42-50: unreached and padding = SENTINEL): output x takes the
+// record of internal id old2new[x]; reached = its visited bit (a 2 MiB
+// bitmap that stays in L2), so only reached vertices read their parent.
+// Sequential 128-bit writes over [x0, x1) (x0 % 4 == 0); kVec: 16-byte
+// aligned output (else scalar stores).
+template <bool kVec>
+__global__ void __launch_bounds__(256) k_finalize(const int32_t* __restrict__ old2new, const uint32_t* __restrict__ visited,
+                                                  const int32_t* __restrict__ rec, int32_t miss, int64_t n, int64_t x0,
+                                                  int64_t x1, int32_t* __restrict__ out) {
+  const int64_t i0 = x0 / 4, i1 = (x1 + 3) / 4;
+  for (int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < i1; i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 v4 = __ldg(reinterpret_cast<const int4*>(old2new) + i);  // (old2new is padded to 4)
+    const int32_t v[4] = {v4.x, v4.y, v4.z, v4.w};
+    uint32_t w[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t x = i * 4 + q;
-      lv[q] = -1;
-      pr[q] = kSentinel;
-      if (x < n) {
-        const int32_t v = __ldg(old2new + x);
-        lv[q] = __ldcg(level_int + v);
-        if (lv[q] >= 0) pr[q] = __ldcg(pred_int + v);
-      }
-    }
-    reinterpret_cast<int4*>(pred_out)[i] = make_int4(pr[0], pr[1], pr[2], pr[3]);
-    if (i * 4 + 3 < n) {
-      reinterpret_cast<int4*>(level_out)[i] = make_int4(lv[0], lv[1], lv[2], lv[3]);
+    for (int q = 0; q < 4; ++q) w[q] = i * 4 + q < n ? __ldg(visited + (v[q] >> 5)) : 0u;
+    int32_t r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r[q] = ((w[q] >> (v[q] & 31)) & 1u) ? __ldg(rec + v[q]) : miss;
+    if (kVec && i * 4 + 3 < x1) {
+      reinterpret_cast<int4*>(out)[i] = make_int4(r[0], r[1], r[2], r[3]);
     } else {
+#pragma unroll
       for (int q = 0; q < 4; ++q)
-        if (i * 4 + q < n) level_out[i * 4 + q] = lv[q];
+        if (i * 4 + q >= x0 && i * 4 + q < x1) out[i * 4 + q] = r[q];
     }
   }
-}
-__device__ __forceinline__ void finalize_scalar(const int32_t* __restrict__ old2new,
-                                                const int32_t* __restrict__ level_int,
-                                                const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
-                                                int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out,
-                                                int64_t t, int64_t stride) {
-  for (int64_t x = t; x < npad; x += stride) {
-    int lv = -1, pr = kSentinel;
-    if (x < n) {
-      const int32_t v = __ldg(old2new + x);
-      lv = __ldcg(level_int + v);
-      if (lv >= 0) pr = __ldcg(pred_int + v);
-      level_out[x] = lv;
-    }
-    pred_out[x] = pr;
-  }
-}
-__global__ void k_finalize(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
-                           const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
-                           int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out) {
-  finalize_vec(old2new, level_int, pred_int, n, npad, level_out, pred_out,
-               (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
-}
-__global__ void k_finalize_scalar(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
-                                  const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
-                                  int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out) {
-  finalize_scalar(old2new, level_int, pred_int, n, npad, level_out, pred_out,
-                  (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 
 // Root of a BFS (traversal.py:135-139, 343-347): its bit in visited/prev
@@ -1600,226 +1435,6 @@ __device__ __forceinline__ void seed_root(const LevelArgs& a, uint32_t* prev, co
 __global__ void k_seed(LevelArgs a, uint32_t* prev, const int32_t* old2new, int32_t root_orig, Counters* cnt0,
                        uint32_t* fglob, unsigned long long* red) {
   seed_root(a, prev, old2new, root_orig, cnt0, fglob, red);
-}
-
-// ---------------------------------------------------------------- K5: whole BFS, one launch
-// The level loop of traversal.py:90 / 152 / 366 on the device: one
-// cooperative launch of one 1024-thread CTA per SM runs init, every level
-// and the output pass. Per level the plan (queue vs bitmap mode, list vs
-// dense small region) is derived from the counter ring exactly as the host
-// loop does; bitmap levels run expansion -> grid barrier -> compaction
-// (four 256-thread groups per CTA, scratch aliased onto the hot snapshot)
-// -> grid barrier, queue levels expansion -> grid barrier. No host round
-// trip and no launch between levels.
-constexpr int kMegaPhases = 1 | 2 | 4 | 16 | 32;
-
-// Separate calls (not inlined) so that each part gets the kernel's register
-// budget to itself: inlined into one loop, the per-level state of all of
-// them spilled inside the element loops.
-#ifndef LBFS_MEGA_PHASE_CALL
-#define LBFS_MEGA_PHASE_CALL __noinline__
-#endif
-#ifndef LBFS_MEGA_COMPACT_CALL
-#define LBFS_MEGA_COMPACT_CALL __noinline__
-#endif
-template <int M, int kPhase>
-__device__ LBFS_MEGA_PHASE_CALL void mega_phase(const LevelArgs* a, const Frontier* f, ExpandSmem* s,
-                                                uint8_t* s_dyn, Hot h, uint32_t* par_bits) {
-  // local copies: read through the shared-memory pointers, every global
-  // store in the element loops could alias them and force reloads
-  const LevelArgs la = *a;
-  const Frontier lf = *f;
-  Acc acc;
-  uint32_t pb = *par_bits;
-  expand_phases<M, kPhase>(la, lf, *s, s_dyn, h, pb, acc);
-  *par_bits = pb;
-  flush_acc<M>(la, acc);
-}
-// all bins of a level, one call per non-empty bin
-template <int M>
-__device__ __forceinline__ void mega_expand(const LevelArgs* a, const Frontier* f, ExpandSmem* s, uint8_t* s_dyn,
-                                            Hot h, uint32_t* par_bits, int skip) {
-  // the snapshot is re-read before each bin (as each separate phase launch
-  // does): later bins then see the discoveries of the earlier ones
-  bool first = true;
-  auto fresh = [&]() {
-    if (!first) hot_load(*s, h, a->visited);
-    first = false;
-  };
-  if (f->n_cta && !(skip & 2)) {
-    fresh();
-    mega_phase<M, 1>(a, f, s, s_dyn, h, par_bits);
-  }
-  if (f->n_items && !(skip & 8)) {
-    fresh();
-    mega_phase<M, 2>(a, f, s, s_dyn, h, par_bits);
-  }
-  if (f->n_warp + f->n_small && !(skip & 4)) {
-    fresh();
-    mega_phase<M, 4>(a, f, s, s_dyn, h, par_bits);
-  }
-  if (f->n_wslice && !(skip & 16)) {
-    fresh();
-    mega_phase<M, 16>(a, f, s, s_dyn, h, par_bits);
-  }
-  if (f->n_dense && !(skip & 32)) {
-    fresh();
-    mega_phase<M, 32>(a, f, s, s_dyn, h, par_bits);
-  }
-}
-// consecutive blocks go to different SMs (the hub-heavy first blocks spread out)
-__device__ LBFS_MEGA_COMPACT_CALL void mega_compact(const CompactArgs* ca, int64_t nblk, CompactSmem* cs, int sub,
-                                                    int interleave) {
-  const CompactArgs c = *ca;
-  const int64_t b0 = interleave ? (int64_t)sub * gridDim.x + blockIdx.x : (int64_t)blockIdx.x * 4 + sub;
-  for (int64_t blk = b0; blk < nblk; blk += (int64_t)gridDim.x * 4)
-    compact_block(c, blk, *cs, threadIdx.x & (kCompactThreads - 1), 1 + sub);
-}
-
-__global__ void __launch_bounds__(kExpandThreads, 1) k_bfs(LevelArgs a, BfsArgs p) {
-  extern __shared__ __align__(128) uint8_t s_dyn[];
-  __shared__ ExpandSmem s;
-  expand_init(s, a);
-  const int tid = threadIdx.x;
-  unsigned gen = tid == 0 ? ld_acquire(&p.state->bar_gen) : 0u;
-  unsigned* bar_count = &p.state->bar_count;
-  unsigned* bar_gen = &p.state->bar_gen;
-  const Hot hot{reinterpret_cast<uint32_t*>(s_dyn + kRingBytes), smem_u32(s_dyn + kRingBytes), p.hot_words};
-  const Hot cold{nullptr, 0u, 0};
-  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + tid, gstride = (int64_t)gridDim.x * blockDim.x;
-  bool finished = false;
-  if (p.do_init) {
-    init_range(reinterpret_cast<uint4*>(a.visited), reinterpret_cast<uint4*>(a.prev), (p.nwords + 3) / 4,
-               reinterpret_cast<int4*>(a.level_int), (p.n_loc + 3) / 4, gt, gstride);
-    if (blockIdx.x == 0 && tid < (int)(kCounterRing * sizeof(Counters) / 8))
-      reinterpret_cast<unsigned long long*>(p.ring)[tid] = 0ull;
-    grid_sync(bar_count, bar_gen, gen, nullptr);
-    if (blockIdx.x == 0 && tid == 0) {
-      LevelArgs sa = a;
-      sa.next_small = p.q_small[0];
-      sa.next_warp = p.q_warp[0];
-      sa.next_cta = p.q_cta[0];
-      seed_root(sa, a.prev, p.old2new, p.root_orig, &p.ring[0], nullptr, nullptr);
-    }
-    grid_sync(bar_count, bar_gen, gen, nullptr);
-  }
-  // per-level plan in shared memory (kept out of registers across the
-  // phases); one variable, so no part of it can share storage with another
-  struct Plan {
-    LevelArgs la;
-    Frontier f;
-    Counters c;
-    int flags;  // bit 0: bitmap level, bit 1: finished, bit 2: stop
-  };
-  __shared__ Plan s_plan;
-  LevelArgs& s_la = s_plan.la;
-  Frontier& s_f = s_plan.f;
-  Counters& s_c = s_plan.c;
-  int& s_flags = s_plan.flags;
-  int64_t L = p.L0;
-  bool prev_bitmap = p.prev_bitmap0 != 0;
-  uint32_t par_bits = 0;
-  const int sub = tid >> 8;  // compaction group of this thread
-  CompactSmem* cs = reinterpret_cast<CompactSmem*>(s_dyn + kRingBytes) + sub;
-  if (tid == 0) s_c = ld_counters(&p.ring[L % kCounterRing]);
-  __syncthreads();
-  for (;;) {
-    const int cur = (int)(L & 1);
-    if (blockIdx.x == 0 && tid < (int)(sizeof(Counters) / 8))
-      reinterpret_cast<unsigned long long*>(&p.ring[(L + 2) % kCounterRing])[tid] = 0ull;
-    if (tid == 0) {
-      const Counters& c = s_c;
-      Frontier f{};
-      f.cta = p.q_cta[cur];
-      f.n_cta = (int64_t)c.bin[kBinCta];
-      if (prev_bitmap) {
-        f.list = p.q_small[cur];
-        f.items = p.q_items[cur];
-        f.n_items = (int64_t)c.bin[kBinItems];
-        f.wslice = p.q_wslice[cur];
-        f.n_wslice = (int64_t)c.bin[kBinWSlice];
-        if (p.small_region > 0 && (int64_t)c.bin[kBinSmall] * kDenseDenom > p.small_region * kDenseNum &&
-            !p.dense_off) {
-          f.n_items = 0;
-          f.front = p.front;
-          f.dense = p.dense;
-          f.n_dense = p.n_dense;
-        }
-      } else {
-        f.small = p.q_small[cur];
-        f.warp = p.q_warp[cur];
-        f.n_small = (int64_t)c.bin[kBinSmall];
-        f.n_warp = (int64_t)c.bin[kBinWarp];
-      }
-      s_f = f;
-      LevelArgs la = a;
-      la.next_level = (int32_t)(L + 1);
-      la.next_cnt = &p.ring[(L + 1) % kCounterRing];
-      la.next_small = p.q_small[cur ^ 1];
-      la.next_warp = p.q_warp[cur ^ 1];
-      la.next_cta = p.q_cta[cur ^ 1];
-      s_la = la;
-      s_flags = c.edges >= p.bitmap_min_edges ? 1 : 0;
-    }
-    __syncthreads();
-    const bool bitmap = s_flags & 1;
-    unsigned long long* pf = (p.prof && blockIdx.x == 0 && tid == 0 && L - p.L0 < 64) ? p.prof + 6 * (L - p.L0) : nullptr;
-    if (pf) pf[0] = gtimer();
-    if (bitmap) {
-      hot_load(s, hot, a.visited);
-      if (pf) pf[1] = gtimer();
-      mega_expand<kBitmapOut>(&s_la, &s_f, &s, s_dyn, hot, &par_bits, p.debug_skip);
-      hot_drain(s);
-      if (pf) pf[2] = gtimer();
-      grid_sync(bar_count, bar_gen, gen, nullptr);
-      if (pf) pf[3] = gtimer();
-      {
-        const CompactArgs ca{a.row_ptr, a.new2old, a.visited, a.prev, p.nwl, a.level_int, (int32_t)(L + 1),
-                             a.t_cta, a.t_warp, a.t_nz, &p.ring[(L + 1) % kCounterRing], p.q_small[cur ^ 1],
-                             p.q_cta[cur ^ 1], p.q_items[cur ^ 1], p.q_wslice[cur ^ 1], p.front, 0, 0, nullptr};
-        if (!(p.debug_skip & 1)) mega_compact(&ca, p.n_compact_blocks, cs, sub, !(p.debug_skip & 256));
-      }
-      __syncthreads();
-      if (pf) pf[4] = gtimer();
-      grid_sync(bar_count, bar_gen, gen, nullptr);
-      if (pf) pf[5] = gtimer();
-    } else {
-      if (pf) pf[1] = gtimer();
-      mega_expand<kQueueOut>(&s_la, &s_f, &s, s_dyn, cold, &par_bits, p.debug_skip);
-      __syncthreads();
-      if (pf) pf[2] = gtimer();
-      grid_sync(bar_count, bar_gen, gen, nullptr);
-      if (pf) pf[3] = pf[4] = pf[5] = gtimer();
-    }
-    if (tid == 0) {
-      const Counters nx = ld_counters(&p.ring[(L + 1) % kCounterRing]);
-      if (blockIdx.x == 0)
-        p.layers[L - p.L0] = lbfs_layer{(int64_t)s_c.discovered, (int64_t)s_c.edges, (int64_t)nx.discovered};
-      s_c = nx;
-      s_flags = (nx.discovered == 0 ? 2 : 0) | (L + 1 - p.L0 >= p.max_levels ? 4 : 0);
-    }
-    __syncthreads();
-    ++L;
-    prev_bitmap = bitmap;
-    const int fl = s_flags;
-    __syncthreads();  // s_flags / s_c are rewritten at the next level's start
-    if (fl & 2) {
-      finished = true;
-      break;
-    }
-    if (fl & 4) break;
-  }
-  if (finished) {
-    if (p.aligned)
-      finalize_vec(p.old2new, a.level_int, a.pred_int, p.n, p.npad, p.d_level, p.d_pred, gt, gstride);
-    else
-      finalize_scalar(p.old2new, a.level_int, a.pred_int, p.n, p.npad, p.d_level, p.d_pred, gt, gstride);
-  }
-  if (blockIdx.x == 0 && tid == 0) {
-    p.state->L_end = L;
-    p.state->prev_bitmap = prev_bitmap ? 1 : 0;
-    p.state->done = finished ? 1 : 0;
-  }
 }
 
 // End of a host-driven level: the next frontier's counters go to the host
@@ -1919,7 +1534,7 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   for (auto& e : ev_) LBFS_CUDA(cudaEventCreate(&e));
   for (auto& e : ev_split_) LBFS_CUDA(cudaEventCreate(&e));
   LBFS_CUDA(cudaEventCreate(&ev_gap_));
-  for (auto& e : ev_loop_) LBFS_CUDA(cudaEventCreate(&e));
+  for (auto& e : ev_cl_) LBFS_CUDA(cudaEventCreate(&e));
   int occ = 0;
   // shared memory: the TMA ring plus as much of the visited bitmap as fits
   // (static shared memory differs per phase kernel: take the largest)
@@ -1933,9 +1548,7 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
                            (const void*)k_expand<kHeavy, 1>,      (const void*)k_expand<kHeavy, 2>,
                            (const void*)k_expand<kHeavy, 4>,      (const void*)k_expand<kHeavy, 8>,
                            (const void*)k_expand<kHeavy, 16>,     (const void*)k_expand<kHeavy, 32>,
-                           (const void*)k_expand<kHeavy, 64>,     (const void*)k_expand<kHeavy, 5>,
-                           (const void*)k_expand<kBitmapOut, 5>,  (const void*)k_expand<kHeavy, 55>,
-                           (const void*)k_expand<kBitmapOut, 55>};
+                           (const void*)k_expand<kHeavy, 64>};
   size_t max_static = 0;
   for (auto fn : kernels) {
     cudaFuncAttributes fa{};
@@ -1973,42 +1586,156 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
       LBFS_CUDA(cudaFuncSetAttribute((const void*)k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kSweepRingBytes + sweep_hot_words_ * 4));
   }
-  // device-side level loop: one co-resident CTA per SM (cooperative launch)
-  int coop = 0, locc = 0;
-  LBFS_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device_));
-  LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&locc, k_levels, kLoopThreads, 0));
-  // fewer CTAs than SMs: queue-mode levels are latency-bound and the grid
-  // barrier / same-line counter traffic grows with the CTA count (measured on
-  // the 4096^2 lattice: 148 CTAs 1.07 GTEPS, 32 CTAs 1.34; S20/S24 unchanged)
-  {
-    const char* lg = getenv("LBFS_LOOP_GRID");
-    loop_grid_ = (coop && locc > 0) ? std::max(1, std::min(lg ? atoi(lg) : kLoopGrid, sm_count_ * locc)) : 0;
-  }
-  // whole-BFS kernel: the dynamic part must also hold four compaction groups
-  {
-    cudaFuncAttributes fa{};
-    LBFS_CUDA(cudaFuncGetAttributes(&fa, (const void*)k_bfs));
-    const int need = std::max<int>(dyn_smem_, kRingBytes + 4 * (int)sizeof(CompactSmem));
-    int mocc = 0;
-    if (coop && (int64_t)fa.sharedSizeBytes + need <= optin) {
-      LBFS_CUDA(cudaFuncSetAttribute((const void*)k_bfs, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
-      LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mocc, k_bfs, kExpandThreads, need));
-    }
-    mega_smem_ = mocc > 0 ? need : 0;
-    if (mega_smem_) {  // the phase calls' frames exceed the default 1 KB per-thread stack
-      size_t cur_stack = 0;
-      LBFS_CUDA(cudaDeviceGetLimit(&cur_stack, cudaLimitStackSize));
-      if (cur_stack < (size_t)fa.localSizeBytes + 1024)
-        LBFS_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, (size_t)fa.localSizeBytes + 1024));
-    }
-  }
-  d_layers_ = dev_alloc<lbfs_layer>((size_t)kLoopCap);
-  loop_ = dev_alloc<LoopState>(1);
-  LBFS_CUDA(cudaMemset(loop_, 0, sizeof(LoopState)));
-  LBFS_CUDA(cudaMallocHost(&h_layers_, sizeof(lbfs_layer) * kLoopCap));
   LBFS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_loop_layers_), sizeof(lbfs_layer) * kLoopCap,
                           cudaHostAllocMapped));
-  LBFS_CUDA(cudaMallocHost(&h_loop_, sizeof(LoopState)));
+  read_env();
+  if (nparts_ == 1) setup_cluster(optin);
+}
+
+// Small-frontier levels: one cluster of cl_size_ CTAs (16 when the device
+// allows non-portable cluster sizes, else 8), the visited bitmap dealt out to
+// their shared memory when it fits next to the frontier queues.
+void BfsEngine::setup_cluster(int optin) {
+  const int64_t stat = (int64_t)cluster_static_smem();
+  for (int cs : {cl_force_size_ ? cl_force_size_ : 16, 8}) {
+    const int64_t nsec = (nwords_ + 7) / 8;
+    const int64_t slice = (nsec + cs - 1) / cs * 8;  // words per CTA
+    const int64_t budget = (int64_t)optin - stat - 1024 - (int64_t)kMaxCluster * kClusterStage * (int64_t)sizeof(QEntry);
+    const int64_t qbytes = 2 * (int64_t)sizeof(QEntry);  // per queue slot (two queues)
+    bool dsm = !cl_no_dsm_ && slice * 4 + qbytes * 1024 <= budget;
+    int64_t qs = dsm ? std::min<int64_t>(8192, (budget - slice * 4) / qbytes) : std::min<int64_t>(8192, budget / qbytes);
+    qs &= ~int64_t(3);
+    const void* fn = dsm ? (const void*)k_cluster_levels<true> : (const void*)k_cluster_levels<false>;
+    const int smem = (int)((dsm ? slice * 4 : 0) + qbytes * qs + (int64_t)kMaxCluster * kClusterStage * sizeof(QEntry));
+    if (cs > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      (void)cudaGetLastError();
+      continue;
+    }
+    LBFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess || ncl < 1) {
+      (void)cudaGetLastError();
+      continue;
+    }
+    cl_size_ = cs;
+    cl_dsm_ = dsm;
+    cl_slice_words_ = dsm ? slice : 0;
+    cl_qs_ = (int32_t)qs;
+    cl_smem_ = smem;
+    break;
+  }
+  if (!cl_size_) return;
+  // a level runs on the cluster only with <= exit_edges frontier edges, so it
+  // discovers at most min(exit_edges, n) vertices
+  cl_cap_ = (int64_t)std::min<unsigned long long>(cl_exit_edges_, (unsigned long long)n_) + 64;
+  cl_spill_ = dev_alloc<QEntry>((size_t)kMaxCluster * 2 * cl_cap_);
+  cl_big_ = dev_alloc<CtaItem>((size_t)kCounterRing * cl_cap_);
+  cl_big_cnt_ = dev_alloc<unsigned long long>(kCounterRing);
+  LBFS_CUDA(cudaMemset(cl_big_cnt_, 0, sizeof(unsigned long long) * kCounterRing));
+}
+
+void BfsEngine::launch_cluster(int64_t L, int cur, bool prev_bitmap, cudaStream_t st, int32_t root_orig) {
+  ClusterArgs p{};
+  p.row_ptr = row_ptr_;
+  p.col_idx = col_idx_;
+  p.new2old = new2old_;
+  p.old2new = old2new_;
+  p.root_orig = root_orig;
+  p.classes = classes_;
+  p.t_cta = t_cta_;
+  p.t_warp = t_warp_;
+  p.t_nz = t_nz_;
+  p.visited = visited_;
+  p.prev = prev_;
+  p.pred_int = pred_int_;
+  p.level_int = level_int_;
+  p.nwords = nwords_;
+  p.slice_words = cl_slice_words_;
+  p.qs = cl_qs_;
+  p.qchunk = qchunk_;
+  p.cap = cl_cap_;
+  p.in_small = q_small_[cur];
+  p.in_items = q_cta_[cur];
+  if (prev_bitmap) {  // k_compact's list + warp slices + hub slices
+    p.in_items2 = q_wslice_[cur];
+    p.in_bitmap = 1;
+  } else {  // winners' queues
+    p.in_warp = q_warp_[cur];
+    p.in_bitmap = 0;
+  }
+  p.ring = cnt_;
+  p.L0 = L;
+  p.max_levels = kLoopCap;
+  p.exit_edges = cl_exit_edges_;
+  for (int b = 0; b < 2; ++b) {
+    p.out_small[b] = q_small_[b];
+    p.out_cta[b] = q_cta_[b];
+  }
+  p.spill_small = cl_spill_;
+  p.big = cl_big_;
+  p.big_cnt = cl_big_cnt_;
+  p.layers = h_loop_layers_;
+  p.mail = h_mail_;
+  p.seq = h_seq_;
+  p.seq_value = ++seq_;
+  p.dbg = cl_dbg_;
+  if (cl_prof_) {
+    if (!cl_prof_buf_) cl_prof_buf_ = dev_alloc<unsigned long long>(512 + 8 * 32);
+    LBFS_CUDA(cudaMemsetAsync(cl_prof_buf_, 0, sizeof(unsigned long long) * (512 + 8 * 32), st));
+    p.prof = cl_prof_buf_;
+    p.prof_level = cl_prof_level_;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cl_size_);
+  cfg.blockDim = dim3(kClusterThreads);
+  cfg.dynamicSmemBytes = cl_smem_;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl_size_;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (cl_dsm_)
+    LBFS_CUDA(cudaLaunchKernelEx(&cfg, k_cluster_levels<true>, p));
+  else
+    LBFS_CUDA(cudaLaunchKernelEx(&cfg, k_cluster_levels<false>, p));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (g_sync_each) sync_check(st, "k_cluster_levels", __FILE__, __LINE__);
+  if (cl_prof_) {
+    unsigned long long pr[512 + 8 * 32];
+    LBFS_CUDA(cudaMemcpyAsync(pr, cl_prof_buf_, sizeof(pr), cudaMemcpyDeviceToHost, st));
+    LBFS_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "[lbfs] cluster L0=%lld: load %.2fus total %.2fus\n", (long long)L, (pr[1] - pr[0]) * 1e-3,
+            (pr[2] - pr[0]) * 1e-3);
+    for (int i = 0; i < 64 && pr[8 + 4 * i]; ++i) {
+      const unsigned long long* q = pr + 8 + 4 * i;
+      const unsigned long long prev_end = i ? pr[8 + 4 * (i - 1) + 3] : pr[1];
+      fprintf(stderr, "[lbfs]   level %lld: loads %.2fus claims %.2fus done %.2fus sync+totals %.2fus\n",
+              (long long)(L + i), q[0] ? (q[0] - prev_end) * 1e-3 : 0.0, q[1] ? (q[1] - prev_end) * 1e-3 : 0.0,
+              (q[2] - prev_end) * 1e-3, (q[3] - q[2]) * 1e-3);
+    }
+    if (cl_prof_level_ >= 0 && pr[512]) {
+      for (int w = 0; w < kClusterThreads / 32; ++w) {
+        const unsigned long long* q = pr + 512 + 8 * w;
+        fprintf(stderr, "[lbfs]   level %lld warp %2d:", cl_prof_level_, w);
+        for (int k = 1; k < 8; ++k) fprintf(stderr, " %6.2f", q[k] ? (q[k] - pr[512]) * 1e-3 : -1.0);
+        fprintf(stderr, "  (us after warp 0's level start: group, loads, claims, winners, expanded, cta sync, cluster sync)\n");
+      }
+    }
+  }
 }
 
 BfsEngine::~BfsEngine() {
@@ -2025,8 +1752,11 @@ BfsEngine::~BfsEngine() {
   dev_free(front_);
   dev_free(dense_tasks_);
   dev_free(dbg_);
-  dev_free(mprof_);
   dev_free(classes_);
+  dev_free(cl_spill_);
+  dev_free(cl_big_);
+  dev_free(cl_big_cnt_);
+  dev_free(cl_prof_buf_);
   for (int b = 0; b < 2; ++b) {
     dev_free(q_small_[b]);
     dev_free(q_warp_[b]);
@@ -2037,17 +1767,18 @@ BfsEngine::~BfsEngine() {
   dev_free(cnt_);
   if (h_cnt_) cudaFreeHost(h_cnt_);
   if (h_mail_) cudaFreeHost(h_mail_);
-  dev_free(d_layers_);
-  dev_free(loop_);
-  if (h_layers_) cudaFreeHost(h_layers_);
   if (h_loop_layers_) cudaFreeHost(h_loop_layers_);
-  if (h_loop_) cudaFreeHost(h_loop_);
+  if (out_st_) {
+    cudaStreamSynchronize(out_st_);
+    cudaStreamDestroy(out_st_);
+    for (auto& e : ev_out_) cudaEventDestroy(e);
+  }
   dev_free(own_pred_);
   dev_free(own_level_);
   for (auto& e : ev_) cudaEventDestroy(e);
   for (auto& e : ev_split_) cudaEventDestroy(e);
   cudaEventDestroy(ev_gap_);
-  for (auto& e : ev_loop_) cudaEventDestroy(e);
+  for (auto& e : ev_cl_) cudaEventDestroy(e);
   dev_free(row_ptr_);
   dev_free(col_idx_);
   if (new2old_loc_ != new2old_) dev_free(new2old_loc_);
@@ -2090,10 +1821,6 @@ static void launch_expand_m(int pi, unsigned grid, int smem, const LevelArgs& a,
     LBFS_LAUNCH((k_expand<M, 32>), grid, kExpandThreads, smem, st, a, f, hot);
   } else if (pi == 5) {
     LBFS_LAUNCH((k_expand<M, 64>), grid, kExpandThreads, smem, st, a, f, hot);
-  } else if (pi == 6) {  // hub slices + queues in one launch: warps done with hubs move on to queue rows
-    LBFS_LAUNCH((k_expand<M, 5>), grid, kExpandThreads, smem, st, a, f, hot);
-  } else if (pi == 7) {  // every bin but the dense warp region in one launch (each phase checks its count)
-    LBFS_LAUNCH((k_expand<M, 55>), grid, kExpandThreads, smem, st, a, f, hot);
   } else {
     LBFS_LAUNCH((k_expand<M, 4>), grid, kExpandThreads, smem, st, a, f, hot);
   }
@@ -2105,10 +1832,8 @@ void BfsEngine::launch_expand(int mode, int pi, unsigned grid, const LevelArgs& 
     launch_expand_m<kHeavy>(pi, grid, dyn_smem_, a, f, hot_words_, hub_ldg_, st);
   else if (mode == kBitmapOut)
     launch_expand_m<kBitmapOut>(pi, grid, dyn_smem_, a, f, hot_words_, hub_ldg_, st);
-  else if (pi < 6)
-    launch_expand_m<kQueueOut>(pi, grid, kRingBytes, a, f, 0, hub_ldg_, st);
   else
-    throw Failure(LBFS_EINVAL, "internal: fused hub+queue launch in queue mode");
+    launch_expand_m<kQueueOut>(pi, grid, kRingBytes, a, f, 0, hub_ldg_, st);
 }
 
 bool env_flag(const char* name) {
@@ -2127,8 +1852,7 @@ LevelArgs BfsEngine::level_args() const {
   a.level_int = level_int_;
   a.classes = classes_;
   a.dbg = count_ ? dbg_ : nullptr;
-  const char* rf = getenv("LBFS_REFRESH");  // hub chunks between snapshot refreshes (0 = off)
-  a.refresh_chunks = rf ? atoi(rf) : kRefreshChunks;
+  a.refresh_chunks = refresh_chunks_;
   a.t_cta = t_cta_;
   a.t_warp = t_warp_;
   a.t_nz = t_nz_;
@@ -2138,8 +1862,7 @@ LevelArgs BfsEngine::level_args() const {
   a.chk_nnz = nnz_loc_;
   // queue-mode hub items: small enough that a hub's row spreads over many
   // warps (a queue level is latency-bound per slice, not bandwidth-bound)
-  const char* qc = getenv("LBFS_QCHUNK");
-  a.qchunk = std::min(kChunk, std::max(kQChunkMin, qc ? atoi(qc) : kQChunkDefault)) & ~3;
+  a.qchunk = qchunk_;
   return a;
 }
 
@@ -2253,23 +1976,11 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
     // allocation (the fused kernel was capped at 64 registers by 1024 threads)
     const bool has[6] = {f.n_cta > 0, f.n_items > 0, f.n_warp + f.n_small > 0, f.n_wslice > 0, f.n_dense > 0,
                          f.dense_warp};
-    // the bins of a bitmap/heavy level in one launch (each phase checks its
-    // count; warps done with one bin move on to the next instead of waiting
-    // for a kernel boundary): S24 +1%, S20 +3.5% over one launch per bin
-    const int nhas = (int)has[0] + has[1] + has[2] + has[3] + has[4];
-    const bool fuse_all = fuse_all_ && mode != kQueueOut && nhas >= 2 && !hub_ldg_ && !split_;
-    const bool fuse = !fuse_all && fuse_hq_ && mode != kQueueOut && has[0] && has[2] && !hub_ldg_ && !split_;
-    if (fuse_all) {
-      launch_expand(mode, 7, grid, a, f, st);
+    for (int pi = 0; pi < 6; ++pi) {
+      if (split_ && !(sweep && pi == 0)) LBFS_CUDA(cudaEventRecord(ev_split_[pi], st));
+      if (!has[pi]) continue;
+      launch_expand(mode, pi, grid, a, f, st);
       a.stage_first = 0;
-      if (has[5]) launch_expand(mode, 5, grid, a, f, st);
-    } else {
-      for (int pi = 0; pi < 6; ++pi) {
-        if (split_ && !(sweep && pi == 0)) LBFS_CUDA(cudaEventRecord(ev_split_[pi], st));
-        if (!has[pi] || (fuse && pi == 2)) continue;
-        launch_expand(mode, fuse && pi == 0 ? 6 : pi, grid, a, f, st);
-        a.stage_first = 0;
-      }
     }
     if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[6], st));
   }
@@ -2282,12 +1993,10 @@ void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t 
                  t_cta_, t_warp_, t_nz_, &cnt_[(L + 1) % kCounterRing], q_small_[cur ^ 1], q_cta_[cur ^ 1],
                  q_items_[cur ^ 1], q_wslice_[cur ^ 1], front_, part_log_, part_rank_, fsend,
                  col_idx_, first_nbr_, pred_int_,
-                 // heavy: blind ORs leave no parent for any new vertex; resolved here
-                 // only when LBFS_RESOLVE_INLINE=1, else by k_resolve off the critical path
-                 heavy && resolve_inline_ ? (int32_t)n_loc_ : 0,
+                 0,  // heavy: blind ORs leave no parent; k_resolve gives them one off the critical path
                  (int32_t)L};
   LBFS_LAUNCH(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
-  if (heavy && !resolve_inline_) {
+  if (heavy) {
     // the parents of level L+1's vertices are read by k_finalize only: resolve
     // them on the side stream while the next levels run (joined before k_finalize)
     LBFS_CUDA(cudaEventRecord(ev_resolve_, st));
@@ -2352,304 +2061,195 @@ void BfsEngine::merge_hot(cudaStream_t st) {
               sweep_hot_words_ / 4, visited_);
 }
 
-void BfsEngine::gap_mark(cudaStream_t st) {
-  if (!gaps_) return;
-  if (gap_ev_.empty()) {
-    gap_ev_.resize(256);
-    for (auto& e : gap_ev_) LBFS_CUDA(cudaEventCreate(&e));
+// Output pass: parents (pad32(n), SENTINEL padding) and, when asked for,
+// levels in original ids. With host_pred_ set, the parents are produced in
+// kOutChunks pieces and each piece is copied to the host on out_st_ as soon
+// as it is written, so the D2H overlaps the rest of the pass.
+void BfsEngine::finalize(int32_t* d_pred, int32_t* d_level, cudaStream_t st) {
+  const bool vec = ((uintptr_t)d_pred % 16) == 0;
+  const int64_t chunks = host_pred_ ? kOutChunks : 1;
+  const int64_t step = (npad_ / chunks + 31) / 32 * 32;
+  for (int64_t x0 = 0, k = 0; x0 < npad_; x0 += step, ++k) {
+    const int64_t x1 = std::min(npad_, x0 + step);
+    const unsigned grid = clamp_grid(((x1 - x0) / 4 + 255) / 256, (int64_t)sm_count_ * 8);
+    if (vec)
+      LBFS_LAUNCH(k_finalize<true>, grid, 256, 0, st, old2new_, visited_, pred_int_, kSentinel, n_, x0, x1, d_pred);
+    else
+      LBFS_LAUNCH(k_finalize<false>, grid, 256, 0, st, old2new_, visited_, pred_int_, kSentinel, n_, x0, x1, d_pred);
+    if (host_pred_) {
+      LBFS_CUDA(cudaEventRecord(ev_out_[k], st));
+      LBFS_CUDA(cudaStreamWaitEvent(out_st_, ev_out_[k], 0));
+      LBFS_CUDA(cudaMemcpyAsync(host_pred_ + x0, d_pred + x0, sizeof(int32_t) * (size_t)(x1 - x0),
+                                cudaMemcpyDeviceToHost, out_st_));
+    }
   }
-  if (n_gap_ < (int)gap_ev_.size()) LBFS_CUDA(cudaEventRecord(gap_ev_[n_gap_++], st));
+  if (d_level) levels_out(d_level, st);
 }
 
+void BfsEngine::levels_out(int32_t* d_level, cudaStream_t st) {
+  const bool vec = ((uintptr_t)d_level % 16) == 0;
+  const unsigned grid = clamp_grid((n_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
+  if (vec)
+    LBFS_LAUNCH(k_finalize<true>, grid, 256, 0, st, old2new_, visited_, level_int_, -1, n_, 0, n_, d_level);
+  else
+    LBFS_LAUNCH(k_finalize<false>, grid, 256, 0, st, old2new_, visited_, level_int_, -1, n_, 0, n_, d_level);
+}
+
+// BFS with host outputs (lbfs_bfs): parents copied chunk by chunk behind the
+// output pass; levels (optional) after it.
+void BfsEngine::run_to_host(int64_t root, int direction, int32_t* h_pred, int32_t* h_level, lbfs_timing* t) {
+  ensure_own_outputs();
+  if (!out_st_) {
+    LBFS_CUDA(cudaStreamCreateWithFlags(&out_st_, cudaStreamNonBlocking));
+    for (auto& e : ev_out_) LBFS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  host_pred_ = h_pred;
+  const auto t0 = std::chrono::steady_clock::now();
+  try {
+    run(root, own_pred_, h_level ? own_level_ : nullptr, t, direction);
+  } catch (...) {
+    host_pred_ = nullptr;
+    cudaStreamSynchronize(out_st_);
+    throw;
+  }
+  host_pred_ = nullptr;
+  if (h_level)
+    LBFS_CUDA(cudaMemcpyAsync(h_level, own_level_, sizeof(int32_t) * (size_t)n_, cudaMemcpyDeviceToHost, out_st_));
+  LBFS_CUDA(cudaStreamSynchronize(out_st_));
+  if (t) {  // host wall time of the copies that did not overlap the BFS
+    const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    t->d2h_ms = std::max(0.0, wall - t->bfs_ms);
+  }
+}
+
+void BfsEngine::last_levels_to_host(int32_t* h_level) {
+  ensure_own_outputs();
+  levels_out(own_level_, stream_);
+  LBFS_CUDA(cudaMemcpyAsync(h_level, own_level_, sizeof(int32_t) * (size_t)n_, cudaMemcpyDeviceToHost, stream_));
+  LBFS_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// Tuning / debug switches, read once per graph handle (not per BFS).
 void BfsEngine::read_env() {
-  trace_ = env_flag("LBFS_TRACE");  // per-level table on stderr
-  gaps_ = env_flag("LBFS_GAPS");
-  {
-    const char* ph = getenv("LBFS_PART_HEAVY");
-    part_heavy_off_ = ph && atoi(ph) == 0;
-  }
-  {
-    const char* fh = getenv("LBFS_FUSE_HQ");
-    fuse_hq_ = fh ? atoi(fh) != 0 : false;  // default off: see DESIGN (intermittent fault under investigation)
-  }
-  {
-    const char* fa = getenv("LBFS_FUSE_ALL");
-    fuse_all_ = fa ? atoi(fa) != 0 : false;  // default off (as above)
-  }
-  {
-    const char* dm = getenv("LBFS_DIRECTION");  // (also lbfs_graph_set_direction) 1: direction-optimising
-    if (dm) direction_ = atoi(dm);
-    const char* al = getenv("LBFS_BU_ALPHA");
-    const char* be = getenv("LBFS_BU_BETA");
-    if (al) bu_alpha_ = std::max(1, atoi(al));
-    if (be) bu_beta_ = std::max(1, atoi(be));
-  }
-  {
-    const char* bd = getenv("LBFS_BITMAP_DIV");  // bitmap mode when a frontier has >= n / this many edges
-    bitmap_div_ = std::max(1, bd ? atoi(bd) : kBitmapDiv);
-    const char* bm = getenv("LBFS_BITMAP_MIN");  // (tests) floor of the bitmap-mode threshold
-    bitmap_floor_ = std::max<int64_t>(1, bm ? atoll(bm) : (int64_t)1 << 16);
-  }
-  {
-    const char* sm = getenv("LBFS_SWEEP_MIN");  // sweep when big-row frontier edges >= this % of the region
-    sweep_min_pct_ = sm ? atoi(sm) : kSweepMinPct;
-  }
-  count_ = env_flag("LBFS_COUNT");  // candidate-write counters (slow)
-  {  // heavy levels: bitmap levels with edges >= nnz / LBFS_HEAVY_DIV (0: off)
-    const char* hd = getenv("LBFS_HEAVY_DIV");
-    heavy_div_ = hd ? atoi(hd) : kHeavyDiv;
-  }
-  split_ = env_flag("LBFS_SPLIT");  // one launch per bin
-  dense_off_ = env_flag("LBFS_NO_DENSE");  // experiment: always use the small-bin list
-  {
-    const char* dp = getenv("LBFS_DENSE_PCT");  // dense small region when the list covers > this % of it
-    dense_pct_ = dp ? atoi(dp) : 100 * kDenseNum / kDenseDenom;
-    const char* dm = getenv("LBFS_DENSE_MIN");  // small-region elements below which the dense path is off
-    dense_min_elems_ = dm ? atoll(dm) : kDenseMinElems;
-  }
-  dense_warp_ = env_flag("LBFS_DENSE_WARP");  // experiment: dense warp-bin region
-  hub_ldg_ = env_flag("LBFS_HUB_LDG");  // experiment: hub bin without TMA staging
-  loop_off_ = env_flag("LBFS_NO_LOOP");  // experiment: host-driven queue-mode levels
-  loop_prof_ = env_flag("LBFS_LOOP_PROF");
+  auto geti = [](const char* name, long long dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoll(v) : dflt;
+  };
+  trace_ = env_flag("LBFS_TRACE");   // per-level table on stderr (the GPU analogue of scripts/layer_profile.py)
+  split_ = env_flag("LBFS_SPLIT");   // one launch per bin, timed separately
+  count_ = env_flag("LBFS_COUNT");   // candidate-write counters (slow)
+  part_heavy_off_ = geti("LBFS_PART_HEAVY", 1) == 0;
+  bu_alpha_ = (int)std::max<long long>(1, geti("LBFS_BU_ALPHA", 14));
+  bu_beta_ = (int)std::max<long long>(1, geti("LBFS_BU_BETA", 24));
+  bitmap_div_ = (int)std::max<long long>(1, geti("LBFS_BITMAP_DIV", kBitmapDiv));  // bitmap mode from n / this edges
+  bitmap_floor_ = std::max<long long>(1, geti("LBFS_BITMAP_MIN", (long long)1 << 16));
+  sweep_min_pct_ = (int)geti("LBFS_SWEEP_MIN", kSweepMinPct);
+  heavy_div_ = (int)geti("LBFS_HEAVY_DIV", kHeavyDiv);  // heavy (blind-OR) from nnz / this edges (0: off)
+  dense_off_ = env_flag("LBFS_NO_DENSE");
+  dense_pct_ = (int)geti("LBFS_DENSE_PCT", 100 * kDenseNum / kDenseDenom);
+  dense_min_elems_ = geti("LBFS_DENSE_MIN", kDenseMinElems);
+  dense_warp_ = env_flag("LBFS_DENSE_WARP");
+  hub_ldg_ = env_flag("LBFS_HUB_LDG");
   sweep_off_ = env_flag("LBFS_NO_SWEEP");
-  sweep_small_ = env_flag("LBFS_SWEEP_SMALL");  // experiment: the small region in the sweep too
-  resolve_inline_ = env_flag("LBFS_RESOLVE_INLINE");  // experiment: heavy-level parents inside k_compact
-  // LBFS_MEGA=1: whole BFS in one persistent launch (k_bfs). Measured on
-  // S24 it is ~12% slower than the host-driven loop (its phases run as
-  // calls inside one kernel: 10-15% slower per level than one launch per
-  // bin), on S20 ~15% faster (no host round trips); off by default.
-  mega_on_ = env_flag("LBFS_MEGA");
+  sweep_small_ = env_flag("LBFS_SWEEP_SMALL");
+  refresh_chunks_ = (int)geti("LBFS_REFRESH", kRefreshChunks);
+  qchunk_ = (int)std::min<long long>(kChunk, std::max<long long>(kQChunkMin, geti("LBFS_QCHUNK", kQChunkDefault))) & ~3;
+  // small-frontier levels run on the cluster while a frontier has at most this many edges
+  cl_exit_edges_ = (unsigned long long)std::max<long long>(64, geti("LBFS_CLUSTER_EDGES", kClusterExitEdges));
+  cl_no_dsm_ = env_flag("LBFS_CLUSTER_GLOBAL");  // claim on the global bitmap even when the slices fit
+  cl_off_ = env_flag("LBFS_NO_CLUSTER");
+  cl_prof_ = env_flag("LBFS_CLUSTER_PROF");
+  cl_force_size_ = (int)geti("LBFS_CLUSTER_SIZE", 0);  // (experiment) 2, 4, 8 or 16
+  cl_dbg_ = (int)geti("LBFS_CLUSTER_DBG", 0);
+  cl_prof_level_ = geti("LBFS_CLUSTER_PROF_LEVEL", -1);
 }
 
-void BfsEngine::run_mega(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t) {
-  const int64_t launches0 = g_launches.load();
-  cudaStream_t st = stream_;
-  LevelArgs a = level_args();
-  BfsArgs p{};
-  for (int b = 0; b < 2; ++b) {
-    p.q_small[b] = q_small_[b];
-    p.q_warp[b] = q_warp_[b];
-    p.q_cta[b] = q_cta_[b];
-    p.q_items[b] = q_items_[b];
-    p.q_wslice[b] = q_wslice_[b];
-  }
-  p.ring = cnt_;
-  p.front = front_;
-  p.dense = dense_tasks_;
-  p.n_dense = n_dense_tasks_;
-  p.layers = d_layers_;
-  p.state = loop_;
-  p.max_levels = kLoopCap;
-  if (const char* ml = getenv("LBFS_MEGA_LEVELS")) p.max_levels = std::max(1, atoi(ml));  // debug: levels per launch
-  p.bitmap_min_edges = (unsigned long long)std::max<int64_t>(bitmap_floor_, n_ / bitmap_div_);
-  p.small_region = (int64_t)t_nz_ - t_warp_;
-  p.dense_off = dense_off_ ? 1 : 0;
-  p.hot_words = env_flag("LBFS_MEGA_NOHOT") ? 0 : hot_words_;  // debug
-  if (const char* sk = getenv("LBFS_MEGA_SKIP")) p.debug_skip = atoi(sk);
-  const bool mprof = env_flag("LBFS_MEGA_PROF");
-  if (mprof) {
-    if (!mprof_) mprof_ = dev_alloc<unsigned long long>(6 * 64);
-    LBFS_CUDA(cudaMemsetAsync(mprof_, 0, sizeof(unsigned long long) * 6 * 64, st));
-    p.prof = mprof_;
-  }
-  if (trace_)
-    fprintf(stderr, "[lbfs] host: rp %p n2o %p vis %p prev %p nwl %lld lvl %p t %d/%d/%d ring %p small %p/%p cta %p/%p items %p/%p wsl %p/%p front %p\n",
-            (void*)row_ptr_, (void*)new2old_loc_, (void*)visited_, (void*)prev_, (long long)nwl_, (void*)level_int_, t_cta_,
-            t_warp_, t_nz_, (void*)cnt_, (void*)q_small_[0], (void*)q_small_[1], (void*)q_cta_[0], (void*)q_cta_[1],
-            (void*)q_items_[0], (void*)q_items_[1], (void*)q_wslice_[0], (void*)q_wslice_[1], (void*)front_);
-  if (trace_)
-    fprintf(stderr, "[lbfs] k_bfs: dyn smem %d (ring %d, hot words %d, 4 x compact %zu), static ExpandSmem %zu\n",
-            mega_smem_, kRingBytes, p.hot_words, sizeof(CompactSmem), sizeof(ExpandSmem));
-  p.nwords = nwords_;
-  p.nwl = nwl_;
-  p.n_loc = n_loc_;
-  p.root_orig = (int32_t)root;
-  p.old2new = old2new_;
-  p.n_compact_blocks = (n_loc_ + kCompactVerts - 1) / kCompactVerts;
-  p.d_pred = d_pred;
-  p.d_level = d_level;
-  p.n = n_;
-  p.npad = npad_;
-  p.aligned = ((uintptr_t)d_pred % 16 == 0) && ((uintptr_t)d_level % 16 == 0);
-  p.do_init = 1;
-  p.L0 = 0;
-  p.prev_bitmap0 = 0;
-  layers_.clear();
-  LBFS_CUDA(cudaEventRecord(ev_[0], st));
-  for (;;) {
-    void* args[] = {(void*)&a, (void*)&p};
-    LBFS_CUDA(cudaLaunchCooperativeKernel((const void*)k_bfs, dim3(sm_count_), dim3(kExpandThreads), args,
-                                          (size_t)mega_smem_, st));
-    g_launches.fetch_add(1);
-    LBFS_CUDA(cudaEventRecord(ev_[4], st));
-    LBFS_CUDA(cudaMemcpyAsync(h_loop_, loop_, sizeof(LoopState), cudaMemcpyDeviceToHost, st));
-    LBFS_CUDA(cudaMemcpyAsync(h_layers_, d_layers_, sizeof(lbfs_layer) * 64, cudaMemcpyDeviceToHost, st));
-    LBFS_CUDA(cudaStreamSynchronize(st));
-    const int64_t k = h_loop_->L_end - p.L0;
-    if (k < 1 || k > kLoopCap) throw Failure(LBFS_ECUDA, "internal: k_bfs level state");
-    if (k > 64) {
-      LBFS_CUDA(cudaMemcpyAsync(h_layers_ + 64, d_layers_ + 64, sizeof(lbfs_layer) * (k - 64),
-                                cudaMemcpyDeviceToHost, st));
-      LBFS_CUDA(cudaStreamSynchronize(st));
-    }
-    for (int64_t i = 0; i < k; ++i) layers_.push_back(h_layers_[i]);
-    if (trace_)
-      fprintf(stderr, "[lbfs] k_bfs launch L%lld..L%lld ok (prev_bitmap=%d done=%d)\n", (long long)p.L0,
-              (long long)h_loop_->L_end - 1, h_loop_->prev_bitmap, h_loop_->done);
-    if (h_loop_->done) break;
-    p.do_init = 0;  // more than kLoopCap levels: continue from the saved state
-    p.L0 = h_loop_->L_end;
-    p.prev_bitmap0 = h_loop_->prev_bitmap;
-  }
-  if (mprof) {
-    unsigned long long pr[6 * 64];
-    LBFS_CUDA(cudaMemcpy(pr, mprof_, sizeof(pr), cudaMemcpyDeviceToHost));
-    for (size_t i = 0; i < layers_.size() && i < 64; ++i) {
-      const unsigned long long* q = pr + 6 * i;
-      fprintf(stderr, "[lbfs] k_bfs L%-3zu %s in=%-9lld snapshot %.1fus expand(b0) %.1fus expand(all) %.1fus "
-              "compact(b0) %.1fus compact(all) %.1fus\n", i, q[5] > q[4] || q[3] != q[2] ? "bitmap" : "queue ",
-              (long long)layers_[i].input, (q[1] - q[0]) * 1e-3, (q[2] - q[1]) * 1e-3, (q[3] - q[1]) * 1e-3,
-              (q[4] - q[3]) * 1e-3, (q[5] - q[3]) * 1e-3);
-    }
-  }
-  if (trace_)
-    for (size_t i = 0; i < layers_.size(); ++i)
-      fprintf(stderr, "[lbfs] L%-3zu k_bfs in=%-9lld edges=%-10lld disc=%lld\n", i, (long long)layers_[i].input,
-              (long long)layers_[i].edges, (long long)layers_[i].discovered);
-  if (t) {
-    float total = 0.f;
-    LBFS_CUDA(cudaEventElapsedTime(&total, ev_[0], ev_[4]));
-    t->bfs_ms = total;
-    t->init_ms = 0.0;
-    t->expand_ms = total;  // one kernel: expansion, compaction, init and outputs
-    t->d2h_ms = 0.0;
-    t->levels = (int64_t)layers_.size();
-    t->kernel_launches = g_launches.load() - launches0;
-    int64_t e = 0, r = 0;
-    for (auto& l : layers_) {
-      e += l.edges;
-      r += l.input;
-    }
-    t->edges = e;
-    t->reached = r;
-  }
-}
-
-void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t) {
+void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t, int direction) {
   if (root < 0 || root >= n_) throw_inval("root out of range");
   if (nparts_ != 1) throw_inval("partitioned graph: use the lbfs_part_* level steps");
-  read_env();
-  if (mega_smem_ > 0 && mega_on_ && !split_ && !count_) {
-    run_mega(root, d_pred, d_level, t);
-    return;
+  if (direction != 0 && direction != 1) throw_inval("unknown direction");
+  cudaStream_t st = stream_;
+  if (side_pending_) {  // an earlier run failed after launching side work: let it finish first
+    cudaStreamSynchronize(res_st_);
+    side_pending_ = false;
   }
   const int64_t launches0 = g_launches.load();
-  cudaStream_t st = stream_;
-  n_loop_ev_ = 0;
-  n_gap_ = 0;
+  n_cl_ev_ = 0;
   LBFS_CUDA(cudaEventRecord(ev_[0], st));
-  {  // K4: bitmaps + internal levels (outputs are written once, by k_finalize)
+  {  // K4: bitmaps + internal levels + counter ring (outputs are written once, by k_finalize)
     const unsigned grid = clamp_grid((n_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
     LBFS_LAUNCH(k_init, grid, 256, 0, st, (uint4*)visited_, (uint4*)prev_, (nwords_ + 3) / 4, (int4*)level_int_,
                 (n_ + 3) / 4, cnt_);
   }
   LevelArgs a = level_args();
-  int cur = 0;
-  a.next_small = q_small_[cur];
-  a.next_warp = q_warp_[cur];
-  a.next_cta = q_cta_[cur];
-  // ring invariant: at the start of level L, slot (L+1)%3 is zero
-  // (the counter ring was cleared by k_init)
+  a.next_small = q_small_[0];
+  a.next_warp = q_warp_[0];
+  a.next_cta = q_cta_[0];
   LBFS_LAUNCH(k_seed, 1, 1, 0, st, a, prev_, old2new_, (int32_t)root, &cnt_[0], nullptr, nullptr);
   LBFS_CUDA(cudaEventRecord(ev_[1], st));
-  const bool dev_loop = loop_grid_ > 0 && !loop_off_ && !split_ && !count_;
-  // with the device loop the first launch is k_levels (it runs no level when
-  // the root's degree needs bitmap mode) and the host learns the counters
-  // from its mailbox; otherwise read them here
-  bool known = !dev_loop;
-  if (!dev_loop) {
-    LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[0], &cnt_[0], sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  const bool use_cluster = cl_size_ > 0 && !cl_off_ && !split_ && !count_;
+  if (!use_cluster) {
+    LBFS_CUDA(cudaMemcpyAsync(h_mail_, &cnt_[0], sizeof(Counters), cudaMemcpyDeviceToHost, st));
     LBFS_CUDA(cudaStreamSynchronize(st));
   }
-
   layers_.clear();
-  double expand_ms = 0.0;
-  bool prev_bitmap = false, prev_bu = false;
+  double expand_ms = 0.0, cluster_ms = 0.0;
+  bool prev_bitmap = false, prev_bu = false, timed_level = false;
   const unsigned long long bitmap_min_edges = (unsigned long long)std::max<int64_t>(bitmap_floor_, n_ / bitmap_div_);
   int64_t L = 0;
+  int cur = 0;  // queue parity == L & 1
+  bool pending = false;  // the layer of the last full-GPU level waits for the next frontier's size
+  lbfs_layer pend{};
   for (;;) {
-    const Counters c = h_cnt_[L % kCounterRing];
-    const int slot = (int)((L + 1) % kCounterRing);
-    if (dev_loop && !prev_bitmap && (!known || c.edges < bitmap_min_edges)) {
-      // a run of queue-mode levels on the device (k_levels), one launch
-      LoopArgs p{};
-      for (int b = 0; b < 2; ++b) {
-        p.q_small[b] = q_small_[b];
-        p.q_warp[b] = q_warp_[b];
-        p.q_cta[b] = q_cta_[b];
-      }
-      p.ring = cnt_;
-      p.layers = d_layers_;
-      p.state = loop_;
-      p.L0 = L;
-      p.max_levels = kLoopCap;
-      p.bitmap_min_edges = bitmap_min_edges;
-      if (loop_prof_) {
-        LBFS_CUDA(cudaMemsetAsync(dbg_, 0, 4 * sizeof(unsigned long long), st));
-        p.prof = dbg_;
-      }
-      // queue slot parity must match the level parity the kernel assumes
-      if (cur != (int)(L & 1)) throw Failure(LBFS_EINVAL, "internal: queue parity");
-      // layers straight into mapped host memory, completion through the mailbox
-      p.layers = h_loop_layers_;
-      p.mail = h_mail_;  // (mapped: valid on the device under unified addressing)
-      p.seq = h_seq_;
-      p.seq_value = ++seq_;
-      const int le = n_loop_ev_ < kLoopEvents ? n_loop_ev_++ : -1;  // segment timing, read after the BFS
-      if (le >= 0) LBFS_CUDA(cudaEventRecord(ev_loop_[2 * le], st));
-      gap_mark(st);
-      void* args[] = {(void*)&a, (void*)&p};
-      LBFS_CUDA(cudaLaunchCooperativeKernel((const void*)k_levels, dim3(loop_grid_), dim3(kLoopThreads), args, 0, st));
-      g_launches.fetch_add(1);
-      gap_mark(st);
-      if (le >= 0) LBFS_CUDA(cudaEventRecord(ev_loop_[2 * le + 1], st));
-      if (trace_) LBFS_CUDA(cudaEventRecord(ev_gap_, st));
-      wait_mail(p.seq_value, st);
-      const Counters m = *const_cast<const Counters*>(h_mail_);
-      const int64_t L_end = (int64_t)m.pad[0], k = L_end - L;
-      if (k < 0 || k > kLoopCap) throw Failure(LBFS_ECUDA, "internal: device level loop state");
-      h_cnt_[L_end % kCounterRing] = m;
-      known = true;
-      if (k == 0) {  // the first frontier already needs bitmap mode
-        continue;
-      }
-      float ms = 0.f;
-      if (trace_ && le >= 0) {
-        LBFS_CUDA(cudaEventSynchronize(ev_loop_[2 * le + 1]));
-        LBFS_CUDA(cudaEventElapsedTime(&ms, ev_loop_[2 * le], ev_loop_[2 * le + 1]));
-      }
-      for (int64_t i = 0; i < k; ++i) layers_.push_back(h_loop_layers_[i]);
-      if (loop_prof_) {
-        unsigned long long pr[4];
-        LBFS_CUDA(cudaMemcpy(pr, dbg_, sizeof(pr), cudaMemcpyDeviceToHost));
-        fprintf(stderr, "[lbfs] device loop %llu levels: expand %.2f us/level, barrier %.2f us/level\n", pr[2],
-                pr[2] ? pr[0] * 1e-3 / pr[2] : 0.0, pr[2] ? pr[1] * 1e-3 / pr[2] : 0.0);
-      }
-      if (trace_)
-        fprintf(stderr, "[lbfs] L%-3lld..L%-3lld device loop (%lld levels) %.3fms, last disc=%lld\n", (long long)L,
-                (long long)(L_end - 1), (long long)k, ms, (long long)h_loop_layers_[k - 1].discovered);
-      cur ^= (int)(k & 1);
-      L = L_end;
-      prev_bitmap = false;
-      if (m.discovered == 0) break;
-      continue;
+    // (1) small-frontier levels on the cluster; its mailbox also carries the
+    // counters of the frontier a full-GPU level just produced
+    Counters c{};
+    int64_t k = 0;
+    if (use_cluster) {
+      const int ce = n_cl_ev_ < kClEvents ? n_cl_ev_++ : -1;
+      if (ce >= 0) LBFS_CUDA(cudaEventRecord(ev_cl_[2 * ce], st));
+      launch_cluster(L, cur, prev_bitmap, st, L == 0 ? (int32_t)root : -1);
+      if (ce >= 0) LBFS_CUDA(cudaEventRecord(ev_cl_[2 * ce + 1], st));
+      wait_mail(seq_, st);
+      std::atomic_thread_fence(std::memory_order_acquire);
+      c = *const_cast<const Counters*>(h_mail_);
+      k = (int64_t)c.pad[0] - L;
+      if (k < 0 || k > kLoopCap) throw Failure(LBFS_ECUDA, "internal: cluster level loop state");
+    } else if (L == 0) {
+      c = *const_cast<const Counters*>(h_mail_);
+    } else {
+      publish_and_wait((int)(L % kCounterRing), (int)((L + 1) % kCounterRing), st);
+      c = h_cnt_[L % kCounterRing];
     }
+    if (timed_level) {  // the last full-GPU level's expansion (its events completed before the mailbox)
+      float ms = 0.f;
+      LBFS_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
+      expand_ms += ms;
+      timed_level = false;
+    }
+    if (pending) {
+      pend.discovered = k > 0 ? h_loop_layers_[0].input : (int64_t)c.discovered;
+      layers_.push_back(pend);
+      pending = false;
+    }
+    if (k > 0) {
+      for (int64_t i = 0; i < k; ++i) layers_.push_back(h_loop_layers_[i]);
+      if (trace_)
+        fprintf(stderr, "[lbfs] L%-3lld..L%-3lld cluster (%lld levels), next in=%llu edges=%llu\n", (long long)L,
+                (long long)(L + k - 1), (long long)k, c.discovered, c.edges);
+      L += k;
+      cur = (int)(L & 1);
+      prev_bitmap = prev_bu = false;
+    }
+    if (c.discovered == 0) break;
+    if (k > 0 && c.edges <= cl_exit_edges_) continue;  // the cluster stopped at its level cap
+    // (2) one level on the whole GPU
     const bool bitmap = c.edges >= bitmap_min_edges;
     // direction-optimising (opt-in): bottom-up while the frontier's edges
     // outweigh the unvisited vertices' edges / alpha, back to top-down when
     // the frontier drops below n / beta (Beamer et al.'s rule)
     bool bottom_up = false;
-    if (direction_ && bitmap && nparts_ == 1) {
+    if (direction && bitmap) {
       unsigned long long seen = c.edges;  // degrees of every vertex visited so far (each was one frontier)
       for (const auto& l : layers_) seen += (unsigned long long)l.edges;
       const unsigned long long m_u = (unsigned long long)nnz_ > seen ? (unsigned long long)nnz_ - seen : 0ull;
@@ -2659,28 +2259,32 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     const bool heavy = !bottom_up && bitmap && stage_ && heavy_div_ > 0 &&
                        c.edges * (unsigned long long)heavy_div_ >= (unsigned long long)nnz_;
     LBFS_CUDA(cudaEventRecord(ev_[2], st));
-    gap_mark(st);
-    float gap_ms = -1.f;
     const unsigned grid = bottom_up ? bottom_up_level(c, prev_bitmap, cur, st)
                                     : expand_level(a, c, heavy ? kHeavy : bitmap ? kBitmapOut : kQueueOut, prev_bitmap,
                                                    cur, L, st);
     if (heavy) merge_hot(st);
     LBFS_CUDA(cudaEventRecord(ev_[3], st));
+    timed_level = true;
     if (bitmap) compact_level(cur, L, nullptr, st, heavy);
-    LBFS_CUDA(cudaEventRecord(ev_[5], st));
-    publish_and_wait(slot, (int)((L + 2) % kCounterRing), st);
-    gap_mark(st);
-    LBFS_CUDA(cudaEventSynchronize(ev_[5]));
-    if (trace_) {
-      LBFS_CUDA(cudaEventSynchronize(ev_[2]));
-      if (L > 0) LBFS_CUDA(cudaEventElapsedTime(&gap_ms, ev_gap_, ev_[2]));
-      LBFS_CUDA(cudaEventRecord(ev_gap_, st));  // end of this level (after k_publish)
+    if (trace_ || split_) {
+      LBFS_CUDA(cudaEventRecord(ev_[5], st));
+      LBFS_CUDA(cudaEventSynchronize(ev_[5]));
+      float ms = 0.f, cms = 0.f;
+      LBFS_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
+      LBFS_CUDA(cudaEventElapsedTime(&cms, ev_[3], ev_[5]));
+      fprintf(stderr,
+              "[lbfs] L%-3lld %s in=%-9llu edges=%-10llu big=%-10llu bins(s|list/w/c/items/ws)=%llu/%llu/%llu/%llu/%llu "
+              "grid=%u expand=%.3fms compact=%.3fms\n",
+              (long long)L, bottom_up ? "bottom" : heavy ? (sweep_used_ ? "sweep " : "heavy ") : bitmap ? "bitmap" : "queue ",
+              c.discovered, c.edges, c.big_edges, c.bin[0], c.bin[1], c.bin[2], c.bin[3], c.bin[4], grid, ms,
+              bitmap ? cms : 0.f);
+      if (split_ && split_any_) {
+        float sm[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int pi = 0; pi < 6; ++pi) LBFS_CUDA(cudaEventElapsedTime(&sm[pi], ev_split_[pi], ev_split_[pi + 1]));
+        fprintf(stderr, "[lbfs]      split: hub=%.3fms items=%.3fms queues=%.3fms wslice=%.3fms dense=%.3fms dwarp=%.3fms\n",
+                sm[0], sm[1], sm[2], sm[3], sm[4], sm[5]);
+      }
     }
-    float ms = 0.f, cms = 0.f;
-    LBFS_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
-    LBFS_CUDA(cudaEventElapsedTime(&cms, ev_[3], ev_[5]));
-    expand_ms += ms;
-    const Counters nx = h_cnt_[slot];
     if (count_) {
       unsigned long long dbg[4] = {0, 0, 0, 0};
       LBFS_CUDA(cudaMemcpy(dbg, dbg_, sizeof(dbg), cudaMemcpyDeviceToHost));
@@ -2688,86 +2292,43 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       fprintf(stderr, "[lbfs]      candidate writes hot=%llu cold=%llu streamed elements=%llu dwarp rows=%llu\n",
               dbg[0], dbg[1], dbg[2], dbg[3]);
     }
-    if (split_ && split_any_) {
-      float split_ms[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      for (int pi = 0; pi < 6; ++pi) LBFS_CUDA(cudaEventElapsedTime(&split_ms[pi], ev_split_[pi], ev_split_[pi + 1]));
-      fprintf(stderr,
-              "[lbfs]      split: hub=%.3fms items=%.3fms queues=%.3fms wslice=%.3fms dense=%.3fms dwarp=%.3fms\n",
-              split_ms[0], split_ms[1], split_ms[2], split_ms[3], split_ms[4], split_ms[5]);
-    }
-    if (trace_)
-      fprintf(stderr,
-              "[lbfs] L%-3lld %s in=%-9llu edges=%-10llu big=%-10llu bins(s|list/w/c/items/ws)=%llu/%llu/%llu/%llu/%llu grid=%u "
-              "expand=%.3fms compact=%.3fms disc=%llu gap_before=%.3fms\n",
-              (long long)L, bottom_up ? "bottom" : heavy ? (sweep_used_ ? "sweep " : "heavy ") : bitmap ? "bitmap" : "queue ",
-              c.discovered, c.edges,
-              c.big_edges, c.bin[0], c.bin[1], c.bin[2], c.bin[3], c.bin[4],
-              grid, ms, bitmap ? cms : 0.f, nx.discovered, gap_ms);
-    layers_.push_back(lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, (int64_t)nx.discovered});
+    pend = lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, 0};
+    pending = true;
     cur ^= 1;
     ++L;
     prev_bitmap = bitmap;
     prev_bu = bottom_up;
-    if (nx.discovered == 0) break;
   }
-  if (trace_) LBFS_CUDA(cudaEventRecord(ev_gap_, st));
   if (side_pending_) {  // parents resolved on the side stream
     LBFS_CUDA(cudaEventRecord(ev_side_done_, res_st_));
     LBFS_CUDA(cudaStreamWaitEvent(st, ev_side_done_, 0));
     side_pending_ = false;
   }
-  {  // outputs in original ids
-    const unsigned grid = clamp_grid((npad_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
-    const bool aligned = ((uintptr_t)d_pred % 16 == 0) && ((uintptr_t)d_level % 16 == 0);
-    if (aligned) {
-      LBFS_LAUNCH(k_finalize, grid, 256, 0, st, old2new_, level_int_, pred_int_, n_, npad_, d_level, d_pred);
-    } else {
-      LBFS_LAUNCH(k_finalize_scalar, grid, 256, 0, st, old2new_, level_int_, pred_int_, n_, npad_, d_level, d_pred);
-    }
-  }
+  LBFS_CUDA(cudaEventRecord(ev_[6], st));
+  finalize(d_pred, d_level, st);
   LBFS_CUDA(cudaEventRecord(ev_[4], st));
   LBFS_CUDA(cudaEventSynchronize(ev_[4]));
-  if (gaps_ && n_gap_ > 0) {  // segments: [start, end) per level or device-loop run; gaps between them
-    std::string line = "[lbfs] gaps:";
-    float first = 0.f, tot = 0.f, busy = 0.f;
-    LBFS_CUDA(cudaEventElapsedTime(&first, ev_[0], gap_ev_[0]));
-    char buf[96];
-    snprintf(buf, sizeof(buf), " init->L0 %.1fus |", first * 1e3f);
-    line += buf;
-    for (int i = 0; i + 1 < n_gap_; i += 2) {
-      float span = 0.f, gap = 0.f;
-      LBFS_CUDA(cudaEventElapsedTime(&span, gap_ev_[i], gap_ev_[i + 1]));
-      if (i + 2 < n_gap_) LBFS_CUDA(cudaEventElapsedTime(&gap, gap_ev_[i + 1], gap_ev_[i + 2]));
-      else LBFS_CUDA(cudaEventElapsedTime(&gap, gap_ev_[i + 1], ev_[4]));
-      snprintf(buf, sizeof(buf), " %.1f+%.1f", span * 1e3f, gap * 1e3f);
-      line += buf;
-      busy += span;
-      tot += gap;
-    }
-    snprintf(buf, sizeof(buf), " | busy %.1fus gaps %.1fus (us: span+gap after)", busy * 1e3f, tot * 1e3f);
-    line += buf;
-    fprintf(stderr, "%s\n", line.c_str());
-    n_gap_ = 0;
-  }
-  for (int i = 0; i < n_loop_ev_; ++i) {  // device-loop segments
+  for (int i = 0; i < n_cl_ev_; ++i) {  // cluster segments
     float ms = 0.f;
-    LBFS_CUDA(cudaEventElapsedTime(&ms, ev_loop_[2 * i], ev_loop_[2 * i + 1]));
-    expand_ms += ms;
+    LBFS_CUDA(cudaEventElapsedTime(&ms, ev_cl_[2 * i], ev_cl_[2 * i + 1]));
+    cluster_ms += ms;
   }
-  n_loop_ev_ = 0;
   if (trace_) {
     float fin = 0.f, tot = 0.f;
-    LBFS_CUDA(cudaEventElapsedTime(&fin, ev_gap_, ev_[4]));
+    LBFS_CUDA(cudaEventElapsedTime(&fin, ev_[6], ev_[4]));
     LBFS_CUDA(cudaEventElapsedTime(&tot, ev_[0], ev_[4]));
-    fprintf(stderr, "[lbfs] finalize %.3fms total %.3fms\n", fin, tot);
+    fprintf(stderr, "[lbfs] cluster %.3fms finalize %.3fms total %.3fms\n", cluster_ms, fin, tot);
   }
   if (t) {
-    float total = 0.f, init = 0.f;
+    float total = 0.f, init = 0.f, fin = 0.f;
     LBFS_CUDA(cudaEventElapsedTime(&total, ev_[0], ev_[4]));
     LBFS_CUDA(cudaEventElapsedTime(&init, ev_[0], ev_[1]));
+    LBFS_CUDA(cudaEventElapsedTime(&fin, ev_[6], ev_[4]));
     t->bfs_ms = total;
     t->init_ms = init;
     t->expand_ms = expand_ms;
+    t->cluster_ms = cluster_ms;
+    t->finalize_ms = fin;
     t->d2h_ms = 0.0;
     t->levels = (int64_t)layers_.size();
     t->kernel_launches = g_launches.load() - launches0;

@@ -180,65 +180,63 @@ __host__ __device__ __forceinline__ int64_t part_global(int64_t l, int32_t part_
   return ((((l >> 5) << part_log) | part_rank) << 5) | (l & 31);
 }
 
-// Device-side level loop (k_levels): cooperative launch, one CTA per SM.
-constexpr int kLoopThreads = 512;
-constexpr int kLoopGrid = 32;  // CTAs of the device level loop (k_levels)
-constexpr int64_t kLoopCap = 1 << 16;  // layers per k_levels launch
+constexpr int64_t kLoopCap = 1 << 16;  // levels per cluster-kernel launch
 
-struct LoopState {
-  long long L_end;   // first level not run by the last k_levels / k_bfs launch
-  unsigned bar_count;
-  unsigned bar_gen;
-  int prev_bitmap;   // k_bfs: mode of level L_end - 1
-  int done;          // k_bfs: search finished (outputs written)
+// Small-frontier levels on one thread-block cluster (cluster.cu).
+constexpr int kClusterThreads = 512;
+constexpr unsigned long long kClusterExitEdges = 1ull << 16;  // default LBFS_CLUSTER_EDGES
+constexpr int kMaxCluster = 16;
+constexpr int kClusterStage = 128;  // winners staged per target CTA before the push
+// A frontier entry of the cluster's small queues: the vertex (internal id)
+// and its parent (original id); its level / parent records are written when
+// it is expanded (early in the next level, off the level's critical chain).
+struct alignas(8) QEntry {
+  int32_t v;
+  int32_t par;
 };
-
-// Whole-BFS persistent kernel (k_bfs) arguments.
-struct BfsArgs {
-  int32_t* q_small[2];
-  int32_t* q_warp[2];
-  CtaItem* q_cta[2];
-  GroupItem* q_items[2];
-  CtaItem* q_wslice[2];
-  Counters* ring;
-  uint32_t* front;
-  const DenseTask* dense;
-  int64_t n_dense;
-  lbfs_layer* layers;  // layers[L - L0]
-  LoopState* state;
-  int64_t L0, max_levels;
-  unsigned long long bitmap_min_edges;
-  int64_t small_region;
-  int32_t dense_off, prev_bitmap0;
-  int32_t hot_words, do_init;
-  int64_t nwords, nwl, n_loc;  // init / compaction extents
-  int32_t root_orig;
+struct ClusterArgs {
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  const int32_t* new2old;
   const int32_t* old2new;
-  int64_t n_compact_blocks;
-  int32_t* d_pred;
-  int32_t* d_level;
-  int64_t n, npad;
-  int32_t aligned;
-  int32_t debug_skip;  // LBFS_MEGA_SKIP (debug): 1 compaction, 2 hub, 4 queues, 8 items, 16 warp slices, 32 dense
-  unsigned long long* prof;  // LBFS_MEGA_PROF: 6 globaltimer stamps of block 0 per level (first 64 levels)
-};
-
-struct LoopArgs {
-  int32_t* q_small[2];
-  int32_t* q_warp[2];
-  CtaItem* q_cta[2];
-  Counters* ring;            // kCounterRing slots, slot L%3 = frontier of level L
-  lbfs_layer* layers;        // layers[L - L0]
-  LoopState* state;
+  const ClassTable* classes;
+  int32_t t_cta, t_warp, t_nz;
+  int32_t root_orig;        // >= 0: the first level of a BFS (visited = {root}: no bitmap load)
+  uint32_t* visited;
+  uint32_t* prev;
+  int32_t* pred_int;
+  int32_t* level_int;
+  int64_t nwords;
+  int64_t slice_words;      // DSMEM mode: bitmap words per CTA (multiple of 8)
+  int32_t qs;               // entries per shared-memory small queue
+  int32_t qchunk;           // edges per exit slice item
+  int64_t cap;              // spill / big-list capacity per buffer (>= exit_edges)
+  // frontier of level L0 (counters in ring[L0 % 3]): the host's queue format,
+  // or a bitmap level's list (in_small) + warp slices (in_items2) + hub slices
+  const int32_t* in_small;
+  const int32_t* in_warp;
+  const CtaItem* in_items;
+  const CtaItem* in_items2;
+  int32_t in_bitmap;        // 1: the list format (counts bin[kBinSmall / kBinWSlice / kBinCta])
+  Counters* ring;
   int64_t L0, max_levels;
-  unsigned long long bitmap_min_edges;
-  unsigned long long* prof;  // LBFS_LOOP_PROF: {expand ns, barrier ns, levels, scratch}
-  // completion mailbox in mapped host memory (host-driven runs): the counters
-  // of the first level not run (pad[0] = that level) and then the sequence word
+  unsigned long long exit_edges;  // leave when a frontier has more edges
+  int32_t* out_small[2];    // exit frontier (queue format) by level parity
+  CtaItem* out_cta[2];
+  QEntry* spill_small;      // [kMaxCluster][2][cap]
+  CtaItem* big;             // [3][cap] cluster-wide lists of degree >= 32 rows
+  unsigned long long* big_cnt;  // [3]
+  lbfs_layer* layers;       // layers[L - L0] (mapped host memory)
   Counters* mail;
   unsigned long long* seq;
   unsigned long long seq_value;
+  int32_t dbg;               // LBFS_CLUSTER_DBG experiments (wrong results): 1 no prefetch, 2 no layers, 4 no level/pred stores
+  int64_t prof_level;        // LBFS_CLUSTER_PROF_LEVEL: per-warp timeline of this level (CTA rank 0)
+  unsigned long long* prof;  // LBFS_CLUSTER_PROF: [0] start [1] slices loaded [2] exit; 8 + 4 L: level stamps
 };
+template <bool DSM>
+__global__ void k_cluster_levels(const __grid_constant__ ClusterArgs p);
+size_t cluster_static_smem();
 
 // Heavy-level sweep of the big-row region (sweep.cu).
 constexpr int kSweepWindow = 128;   // col_idx elements per window / side entry
@@ -323,7 +321,12 @@ class BfsEngine {
 
   void ensure_own_outputs();
   // BFS into device buffers d_pred[pad32(n)], d_level[n]; synchronous.
-  void run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t);
+  // direction: 0 top-down, 1 direction-optimising (bottom-up levels)
+  void run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t, int direction = 0);
+  // BFS with host outputs (parents D2H overlapped with the output pass)
+  void run_to_host(int64_t root, int direction, int32_t* h_pred, int32_t* h_level, lbfs_timing* t);
+  // levels of the last BFS (original ids) to host memory
+  void last_levels_to_host(int32_t* h_level);
 
   // ---- partitioned BFS, one level step at a time (partition.cu); the
   // collectives between the steps are issued by the caller on `st`
@@ -339,7 +342,6 @@ class BfsEngine {
   int64_t nwords() const { return nwords_; }
   int64_t n_local() const { return n_loc_; }
   int64_t nnz_local() const { return nnz_loc_; }
-  void set_direction(int d) { direction_ = d; }
   unsigned long long resolve_scanned() const;
   // validate_tree (validate.py:50-155) on a device parent array in original
   // ids: out[0..4] passed flags, out[5..9] details (-1 when passed)
@@ -367,6 +369,14 @@ class BfsEngine {
   void compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st, bool heavy = false);
   void merge_hot(cudaStream_t st);
   void read_env();
+  void finalize(int32_t* d_pred, int32_t* d_level, cudaStream_t st);
+  void levels_out(int32_t* d_level, cudaStream_t st);
+  static constexpr int kOutChunks = 8;
+  int32_t* host_pred_ = nullptr;     // run_to_host: parents' host destination
+  cudaStream_t out_st_ = nullptr;    // D2H of the outputs
+  cudaEvent_t ev_out_[kOutChunks] = {};
+  void setup_cluster(int optin);
+  void launch_cluster(int64_t L, int cur, bool prev_bitmap, cudaStream_t st, int32_t root_orig);
   bool split_any_ = false;
 
   int device_ = 0, sm_count_ = 0;
@@ -410,35 +420,42 @@ class BfsEngine {
   int64_t cap_cta_ = 0, cap_items_ = 0;
   Counters* cnt_ = nullptr;
   Counters* h_cnt_ = nullptr;
-  // per-level mailbox in mapped pinned memory: k_publish copies a level's
-  // counters here and bumps the sequence word; the host spins on it
+  // per-level mailbox in mapped pinned memory: the cluster kernel (or
+  // k_publish) copies a frontier's counters here and bumps the sequence word;
+  // the host spins on it
   Counters* h_mail_ = nullptr;
   unsigned long long* h_seq_ = nullptr;
   unsigned long long seq_ = 0;
   void publish_and_wait(int slot, int zero_slot, cudaStream_t st);
   void wait_mail(unsigned long long want, cudaStream_t st);
-  lbfs_layer* h_loop_layers_ = nullptr;  // mapped: k_levels' per-level layers of the current run
+  lbfs_layer* h_loop_layers_ = nullptr;  // mapped: the cluster kernel's per-level layers of the current run
   int32_t* own_pred_ = nullptr;
   int32_t* own_level_ = nullptr;
   cudaStream_t stream_ = nullptr;
-  cudaEvent_t ev_[6] = {};
-  cudaEvent_t ev_gap_ = nullptr;  // LBFS_TRACE: end of the previous level (gap to the next one)
-  static constexpr int kLoopEvents = 16;
-  cudaEvent_t ev_loop_[2 * kLoopEvents] = {};  // device-loop segments of one BFS (timing)
-  int n_loop_ev_ = 0;
+  cudaEvent_t ev_[7] = {};
+  cudaEvent_t ev_gap_ = nullptr;
+  static constexpr int kClEvents = 16;
+  cudaEvent_t ev_cl_[2 * kClEvents] = {};  // cluster segments of one BFS (timing)
+  int n_cl_ev_ = 0;
   std::vector<lbfs_layer> layers_;
   int expand_grid_ = 0;
-  int loop_grid_ = 0;             // k_levels CTAs (0: device loop unavailable)
-  int mega_smem_ = 0;             // k_bfs dynamic shared memory (0: unavailable)
-  unsigned long long* mprof_ = nullptr;  // LBFS_MEGA_PROF stamps
-  bool mega_on_ = false;          // LBFS_MEGA=1: k_bfs instead of the host-driven level loop
-  void run_mega(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t);
-  bool loop_off_ = false;         // LBFS_NO_LOOP=1: host-driven queue levels
-  bool loop_prof_ = false;        // LBFS_LOOP_PROF=1: time split of k_levels on stderr
-  lbfs_layer* d_layers_ = nullptr;
-  lbfs_layer* h_layers_ = nullptr;  // pinned
-  LoopState* loop_ = nullptr;
-  LoopState* h_loop_ = nullptr;     // pinned
+  // cluster level loop (cluster.cu)
+  int cl_size_ = 0;               // CTAs per cluster (0: unavailable)
+  bool cl_dsm_ = false;           // visited bitmap in distributed shared memory
+  bool cl_no_dsm_ = false, cl_off_ = false;
+  int64_t cl_slice_words_ = 0;
+  int32_t cl_qs_ = 0;
+  int cl_smem_ = 0;
+  int64_t cl_cap_ = 0;
+  unsigned long long cl_exit_edges_ = kClusterExitEdges;
+  QEntry* cl_spill_ = nullptr;
+  CtaItem* cl_big_ = nullptr;
+  unsigned long long* cl_big_cnt_ = nullptr;
+  bool cl_prof_ = false;
+  int cl_dbg_ = 0;
+  int cl_force_size_ = 0;
+  long long cl_prof_level_ = -1;
+  unsigned long long* cl_prof_buf_ = nullptr;
   int32_t hot_words_ = 0;  // visited words mirrored in shared memory
   int32_t sweep_hot_words_ = 0;  // the sweep's (longer) hot prefix; also the stage row stride
   bool merge_wide_ = false;      // this level's stage rows hold the sweep's prefix
@@ -452,7 +469,6 @@ class BfsEngine {
   bool sweep_off_ = false;       // LBFS_NO_SWEEP=1: heavy levels use the slice lists
   bool sweep_used_ = false;      // the last expand_level swept the big-row region
   bool sweep_fits_ = false;      // k_sweep's ring + hot prefix fit in shared memory
-  bool resolve_inline_ = false;  // LBFS_RESOLVE_INLINE=1: heavy-level parents in k_compact (critical path)
   cudaStream_t res_st_ = nullptr;  // heavy-level parent resolution (k_resolve), joined before k_finalize
   cudaEvent_t ev_resolve_ = nullptr, ev_side_done_ = nullptr;
   bool side_pending_ = false;
@@ -461,18 +477,13 @@ class BfsEngine {
   int dyn_smem_ = 0;
   bool trace_ = false;  // LBFS_TRACE=1: per-level table on stderr
   int sweep_min_pct_ = kSweepMinPct;
-  int direction_ = 0;              // 0 top-down (the paper's algorithm), 1 direction-optimising (bottom-up levels)
   int bu_alpha_ = 14, bu_beta_ = 24;
   int bitmap_div_ = kBitmapDiv;
   int64_t bitmap_floor_ = (int64_t)1 << 16;
+  int refresh_chunks_ = kRefreshChunks;
+  int qchunk_ = kQChunkDefault;
   bool part_heavy_ = false;      // this partition level runs with heavy (blind-OR) semantics
   bool part_heavy_off_ = false;  // LBFS_PART_HEAVY=0
-  bool fuse_hq_ = false;   // (LBFS_FUSE_HQ=1) hub + queue bins of a bitmap/heavy level in one launch
-  bool fuse_all_ = false;  // (LBFS_FUSE_ALL=1) every bin of a bitmap/heavy level in one launch
-  bool gaps_ = false;   // LBFS_GAPS=1: per-level busy span / host gap line on stderr (no syncs added)
-  std::vector<cudaEvent_t> gap_ev_;  // LBFS_GAPS: [2i] segment start, [2i+1] segment end
-  int n_gap_ = 0;
-  void gap_mark(cudaStream_t st);
   bool count_ = false;
   bool split_ = false;
   bool hub_ldg_ = false;  // LBFS_SPLIT=1: one launch per bin, timed separately

@@ -102,7 +102,7 @@ void BfsEngine::build_layout(const Csr& csr) {
   uint32_t* key_s = dev_alloc<uint32_t>((size_t)n);
   int32_t* ids = dev_alloc<int32_t>((size_t)n);
   new2old_ = dev_alloc<int32_t>((size_t)n);
-  old2new_ = dev_alloc<int32_t>((size_t)n);
+  old2new_ = dev_alloc<int32_t>((size_t)pad32(n) + 4);  // padded: k_finalize reads whole int4 of it
   LBFS_LAUNCH(k_degree_keys, grid_of(n), 256, 0, st, csr.row_ptr, n, key, ids);
   size_t tmp_bytes = 0;
   LBFS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key_s, ids, new2old_, n, 0, 32, st));

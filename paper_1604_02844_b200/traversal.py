@@ -25,7 +25,9 @@ device (there is no CPU fallback).
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass, field
+import threading
+import weakref
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -81,13 +83,90 @@ class LayerStats:
     discovered: int  # vertices first reached in this layer
 
 
-@dataclass
 class BfsResult:
-    predecessors: PredecessorArray
-    layers: list[LayerStats] = field(default_factory=list)
-    traversed_edge_count: int = 0
-    levels: np.ndarray | None = None
-    timing: dict | None = None
+    """The reference's result (traversal.py:73-77: predecessors, layers,
+    traversed_edge_count) plus ``levels`` (gap G2) and device ``timing``.
+
+    ``levels`` is fetched from the device on first access (the reference has
+    no level array; its callers derive one with levels_from_parents). The
+    handle keeps the level array of its last BFS; before the next BFS on the
+    same graph starts, a still-referenced result fetches its levels first, so
+    a result never sees another BFS's levels."""
+
+    __slots__ = ("predecessors", "layers", "traversed_edge_count", "timing", "_levels", "_handle", "_owner", "__weakref__")
+
+    def __init__(self, predecessors, layers=None, traversed_edge_count=0, levels=None, timing=None):
+        self.predecessors = predecessors
+        self.layers = layers if layers is not None else []
+        self.traversed_edge_count = traversed_edge_count
+        self.timing = timing
+        self._levels = levels
+        self._handle = None
+        self._owner = None  # the graph, kept alive while the levels are on its device handle
+
+    @property
+    def levels(self) -> np.ndarray | None:
+        if self._levels is None and self._handle is not None:
+            with _handle_lock(self._handle):
+                _materialize(self)
+        return self._levels
+
+    def __repr__(self) -> str:
+        return (f"BfsResult(layers={len(self.layers)}, traversed_edge_count={self.traversed_edge_count}, "
+                f"levels={'pending' if self._levels is None else 'host'})")
+
+
+# per handle: a lock around flush + BFS + registration, and the result whose
+# levels are still on the device
+_locks: dict[int, threading.Lock] = {}
+_locks_guard = threading.Lock()
+_pending: dict[int, weakref.ref] = {}
+
+
+def _handle_lock(h: int) -> threading.Lock:
+    with _locks_guard:
+        return _locks.setdefault(h, threading.RLock())
+
+
+def _materialize(res: BfsResult) -> None:
+    """(handle lock held) copy the handle's last levels into res."""
+    h = res._handle
+    if res._levels is not None or h is None:
+        return
+    ref = _pending.get(h)
+    if ref is None or ref() is not res:
+        raise RuntimeError("internal: levels of this result are no longer on the device")
+    n = res.predecessors.num_vertices if res.predecessors is not None else _num_vertices(h)
+    lv = _lib.pinned_empty(n)
+    _lib.check(_lib.load().lbfs_graph_last_levels(h, _lib.ptr(lv)))
+    res._levels = lv
+    res._handle = None
+    res._owner = None
+    del _pending[h]
+
+
+def _flush(h: int) -> None:
+    """(handle lock held) before a BFS on h: the previous result, if still
+    alive, takes its levels off the device."""
+    ref = _pending.get(h)
+    if ref is None:
+        return
+    r = ref()
+    if r is not None and r._levels is None:
+        _materialize(r)
+    _pending.pop(h, None)
+
+
+def _register(h: int, res: BfsResult, owner) -> None:
+    res._handle = h
+    res._owner = owner
+    _pending[h] = weakref.ref(res)
+
+
+def _num_vertices(h: int) -> int:
+    n = ctypes.c_int64()
+    _lib.check(_lib.load().lbfs_graph_info(h, ctypes.byref(n), None))
+    return int(n.value)
 
 
 # ------------------------------------------------------------- graph handles
@@ -107,11 +186,11 @@ def _handle(g) -> int:
         return ent[2]
     lib = _lib.load()
     if ent is not None:
-        lib.lbfs_graph_destroy(ent[2])
+        _destroy_foreign(ent[2])
         del _foreign[key]
     while len(_foreign) >= 2:  # keep at most two foreign graphs resident
         _, old = _foreign.popitem()
-        lib.lbfs_graph_destroy(old[2])
+        _destroy_foreign(old[2])
     cs64 = np.ascontiguousarray(cs, dtype=np.int64)
     r32 = np.ascontiguousarray(rows, dtype=np.int32)
     h = ctypes.c_void_p()
@@ -121,8 +200,14 @@ def _handle(g) -> int:
     return h.value
 
 
+def _destroy_foreign(h: int) -> None:
+    with _handle_lock(h):
+        _flush(h)
+        _lib.load().lbfs_graph_destroy(h)
+
+
 def _layers_from(buf, k: int, h: int) -> list[LayerStats]:
-    if k > len(buf):
+    if k > len(buf):  # (handle lock held: no other BFS ran since)
         buf = (_lib.Layer * k)()
         n = ctypes.c_int64()
         _lib.check(_lib.load().lbfs_graph_last_layers(h, buf, k, ctypes.byref(n)))
@@ -135,53 +220,63 @@ _LAYER_CAP = 256
 DIRECTIONS = {"top_down": 0, "optimizing": 1}
 
 
-def _set_direction(h, direction: str) -> None:
-    """Traversal direction of this call: "top_down" (the paper's algorithm;
+def _direction(direction: str) -> int:
+    """Traversal direction of one call: "top_down" (the paper's algorithm;
     the default and the benchmarked path) or "optimizing" (bottom-up levels
     while the frontier is large). Levels, visited set
     and layers are the same either way; parents may differ (any neighbour one
     level up, as the reference's own parallel variants allow)."""
     assert direction in DIRECTIONS, f"direction must be one of {sorted(DIRECTIONS)}"
-    _lib.check(_lib.load().lbfs_graph_set_direction(h, DIRECTIONS[direction]))
+    return DIRECTIONS[direction]
 
 
-def bfs(g, s: int, direction: str = "top_down") -> BfsResult:
-    """Top-down BFS from s on the device; host outputs (one D2H copy of the
-    predecessor and level arrays inside the call)."""
+def bfs(g, s: int, direction: str = "top_down", levels: bool = False) -> BfsResult:
+    """Top-down BFS from s on the device; host outputs. The parent array is
+    copied (in chunks, behind the device's output pass) inside the call;
+    levels come with it when ``levels=True``, else on first access."""
     n = g.num_vertices
     assert 0 <= s < n
+    d = _direction(direction)
     h = _handle(g)
-    _set_direction(h, direction)
     padded = (n + BITS_PER_WORD - 1) // BITS_PER_WORD * BITS_PER_WORD
-    # outputs land in page-locked memory (pooled), so the D2H copy inside the
-    # call runs at full link rate
+    # outputs land in page-locked memory (pooled), so the copies run at full link rate
     pred = PredecessorArray(n, _storage=_lib.pinned_empty(padded))
-    levels = _lib.pinned_empty(n)
+    lv = _lib.pinned_empty(n) if levels else None
     buf = (_lib.Layer * _LAYER_CAP)()
     k = ctypes.c_int64()
     t = _lib.Timing()
-    _lib.check(_lib.load().lbfs_bfs(h, int(s), _lib.ptr(pred.storage), _lib.ptr(levels), buf, _LAYER_CAP,
-                                    ctypes.byref(k), ctypes.byref(t)))
-    layers = _layers_from(buf, k.value, h)
-    return BfsResult(pred, layers, int(t.edges), levels, t.as_dict())
+    with _handle_lock(h):
+        _flush(h)
+        _lib.check(_lib.load().lbfs_bfs(h, int(s), d, _lib.ptr(pred.storage), _lib.ptr(lv) if levels else None, buf,
+                                        _LAYER_CAP, ctypes.byref(k), ctypes.byref(t)))
+        res = BfsResult(pred, _layers_from(buf, k.value, h), int(t.edges), lv, t.as_dict())
+        if not levels:
+            _register(h, res, g)
+    return res
 
 
-def bfs_device(g, s: int, pred_out, level_out, direction: str = "top_down") -> BfsResult:
+def bfs_device(g, s: int, pred_out, level_out=None, direction: str = "top_down") -> BfsResult:
     """BFS into device buffers (anything with ``data_ptr()``, e.g. torch CUDA
-    int32 tensors of pad32(n) and n entries). No host copy of the outputs;
-    ``predecessors`` of the result is None."""
+    int32 tensors of pad32(n) and n entries; ``level_out`` may be None). No
+    host copy of the outputs; ``predecessors`` of the result is None and
+    ``levels`` are fetched to the host on first access."""
     n = g.num_vertices
     assert 0 <= s < n
     padded = (n + BITS_PER_WORD - 1) // BITS_PER_WORD * BITS_PER_WORD
-    assert pred_out.numel() >= padded and level_out.numel() >= n
+    assert pred_out.numel() >= padded and (level_out is None or level_out.numel() >= n)
+    d = _direction(direction)
     h = _handle(g)
-    _set_direction(h, direction)
     buf = (_lib.Layer * _LAYER_CAP)()
     k = ctypes.c_int64()
     t = _lib.Timing()
-    _lib.check(_lib.load().lbfs_bfs_device(h, int(s), pred_out.data_ptr(), level_out.data_ptr(), buf,
-                                           _LAYER_CAP, ctypes.byref(k), ctypes.byref(t)))
-    return BfsResult(None, _layers_from(buf, k.value, h), int(t.edges), None, t.as_dict())
+    with _handle_lock(h):
+        _flush(h)
+        _lib.check(_lib.load().lbfs_bfs_device(h, int(s), d, pred_out.data_ptr(),
+                                               level_out.data_ptr() if level_out is not None else None, buf,
+                                               _LAYER_CAP, ctypes.byref(k), ctypes.byref(t)))
+        res = BfsResult(None, _layers_from(buf, k.value, h), int(t.edges), None, t.as_dict())
+        _register(h, res, g)
+    return res
 
 
 def run_bfs(g, s: int, policy: LayerPolicy | None = None, threads: int = 1,

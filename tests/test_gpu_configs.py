@@ -93,26 +93,34 @@ def test_config_s24_against_oracle(golden):
             assert sha(res.levels, "<i4") == info["bfs"][str(r)]["levels_sha"]
 
 
+@pytest.fixture(params=["dsmem", "global"])
+def all_levels_on_cluster(request, monkeypatch):
+    """Every level on the thread-block cluster (cluster.cu), its visited
+    bitmap in distributed shared memory or in global memory (read when the
+    graph handle is created)."""
+    monkeypatch.setenv("LBFS_CLUSTER_EDGES", str(1 << 40))
+    if request.param == "global":
+        monkeypatch.setenv("LBFS_CLUSTER_GLOBAL", "1")
+
+
 @pytest.fixture
-def whole_bfs_kernel(monkeypatch):
-    """Run the searches through the single-launch persistent kernel (k_bfs,
-    LBFS_MEGA=1; the library reads the switch at every BFS)."""
-    monkeypatch.setenv("LBFS_MEGA", "1")
+def no_cluster(monkeypatch):
+    """Every level on the whole GPU (host-driven queue / bitmap levels)."""
+    monkeypatch.setenv("LBFS_NO_CLUSTER", "1")
 
 
-def test_whole_bfs_kernel_s16_golden(golden, golden_arrays, whole_bfs_kernel):
+def test_cluster_every_level_s16_golden(golden, golden_arrays, all_levels_on_cluster):
     info = golden["S16"]
     g = build_rmat_graph(RmatParams(scale=16, seed=1))
     for r, want in info["bfs"].items():
         res = bfs(g, int(r))
-        assert res.timing["kernel_launches"] == 1
         assert np.array_equal(res.levels, golden_arrays[f"S16_levels_{r}"].astype(np.int32))
         assert layers_of(res) == want["layers"]
         code, where = oracle.check_bfs(g.colstarts, g.rows, int(r), res.predecessors.p, res.levels)
         assert code == 0, (oracle.CHECK_CODES[code], where)
 
 
-def test_whole_bfs_kernel_s20_and_lattice(golden, whole_bfs_kernel):
+def test_cluster_every_level_s20_and_lattice(golden, all_levels_on_cluster):
     info = golden["S20"]
     g = build_rmat_graph(RmatParams(scale=20, seed=1))
     rp, ci = g.colstarts, g.rows
@@ -124,6 +132,25 @@ def test_whole_bfs_kernel_s20_and_lattice(golden, whole_bfs_kernel):
             assert sha(res.levels, "<i4") == want["levels_sha"]
         code, where = oracle.check_bfs(rp, ci, r, res.predecessors.p, res.levels)
         assert code == 0, (r, oracle.CHECK_CODES[code], where)
+    info = golden["lattice_64x48"]
+    g = build_lattice_graph(64, 48)
+    for r, want in info["bfs"].items():
+        res = bfs(g, int(r))
+        assert layers_of(res) == want["layers"]
+        assert sha(res.levels, "<i4") == want["levels_sha"]
+
+
+def test_no_cluster_s20_and_lattice(golden, no_cluster):
+    info = golden["S20"]
+    g = build_rmat_graph(RmatParams(scale=20, seed=1))
+    rp, ci = g.colstarts, g.rows
+    for r in info["roots"][:4]:
+        res = bfs(g, r)
+        want = info["bfs"].get(str(r))
+        if want:
+            assert layers_of(res) == want["layers"]
+            assert sha(res.levels, "<i4") == want["levels_sha"]
+        assert oracle.check_bfs(rp, ci, r, res.predecessors.p, res.levels) == (0, -1)
     info = golden["lattice_64x48"]
     g = build_lattice_graph(64, 48)
     for r, want in info["bfs"].items():
