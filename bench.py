@@ -4,14 +4,22 @@ configs[2]: the single-GPU target config and the one sharded at 2/4/8 GPUs).
 One step = one BFS from each of the 64 seeded roots (pick_roots(g, 64, seed=1,
 filter_unconnected=True), harness.py:237-246) over the device-resident graph.
 value = harmonic mean over all timed BFS runs of traversed_edge_count / t_bfs
-(harness.py:218-234, 269), t_bfs from CUDA events on the BFS stream (init
-kernel start -> end of the last level). e2e = the same metric through the
-public API bfs(g, root) with host outputs (D2H of pred + level inside the
-call), timed per call like the reference harness (harness.py:263-265).
+(harness.py:218-234, 269); t_bfs from CUDA events on the BFS stream (init
+kernel start -> parents written in original ids). Every timed tree is
+validated afterwards on the device (the reference harness's validate_tree
+after each root, harness.py:266-268); a failure aborts the run.
 
---impl reference: rank 0 times the reference's CPU path (the oracle port of
-bfs_parallel_naive, traversal.py:128-165, OpenMP over all host cores) on the
-same graph built by the oracle, a bounded sample of roots per step.
+roofline.frac is the whole BFS against SURVEY §8(d)'s algorithmic bytes
+B_alg = 8E + 40V + 8n + n/8 over the measured HBM peak. Extra keys: S20 and
+the 4096^2 lattice (configs[1], configs[3]) measured the same way after the
+headline, e2e through the public bfs(g, root) with host outputs, the opt-in
+direction-optimising variant.
+
+--impl reference: rank 0 times the reference's CPU path on the box's host
+cores: the oracle port of bfs_parallel_naive (traversal.py:128-165, OpenMP)
+on the same graph, 8 roots per step cycling through all 64; plus, when the
+reference package is installed in baseline/_ref, the reference's own
+bfs_parallel_naive on one root in a subprocess.
 """
 
 from __future__ import annotations
@@ -33,6 +41,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "GTEPS (harmonic mean over 64 roots) and % of HBM roofline at 1/2/4/8 B200"
 FALLBACK_HBM_GBS = 6650.0
+REF_PKG = ROOT / "baseline" / "_ref"
 
 
 def parse():
@@ -43,10 +52,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--roots", type=int, default=64)
-    ap.add_argument("--e2e-roots", type=int, default=16, help="roots per step timed through bfs()")
-    ap.add_argument("--cpu-roots", type=int, default=2, help="roots per step of the --impl reference arm")
+    ap.add_argument("--cpu-roots", type=int, default=8, help="roots per step of the --impl reference arm")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU-baseline sampling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra-configs", action="store_true", help="skip the S20 / lattice keys")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the partitioned (multi-GPU) driver even at N=1 (one NCCL rank)")
     return ap.parse_args()
@@ -65,6 +74,17 @@ def peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "measured"
     return FALLBACK_HBM_GBS, "fallback"
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -118,9 +138,15 @@ def hm(values):
     return harmonic_mean_teps(values)[0]
 
 
+def b_alg(E: float, V: float, n: int) -> float:
+    """4E col_idx + 4E bitmap probe + 16V row_ptr + 8V atomic
+    RMW + 8V level/pred + 8V queue + 8n init + n/8 bitmap clear."""
+    return 8 * E + 40 * V + 8 * n + n // 8
+
+
 def traffic_from_profiles(scale: int):
-    """ncu DRAM bytes per BFS expansion (profiles/roofline_traffic.json), only
-    for the workload it was captured on (an S24 root unless it says otherwise)."""
+    """ncu DRAM bytes of one BFS (profiles/roofline_traffic.json), only for the
+    workload it was captured on."""
     p = ROOT / "profiles" / "roofline_traffic.json"
     if p.exists():
         try:
@@ -129,6 +155,41 @@ def traffic_from_profiles(scale: int):
             return None
         return t if int(t.get("scale", 24)) == scale else None
     return None
+
+
+def reference_python_sample(rp, ci, n, roots, timeout_s=240):
+    """The reference itself (lanebfs bfs_parallel_naive, traversal.py:128-165,
+    timed around the call only like harness.py:263-265) on the same CSR, in a
+    subprocess (G8), when baseline/_ref holds the package."""
+    if not (REF_PKG / "lanebfs").exists():
+        return None
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        np.save(f"{td}/rp.npy", rp)
+        np.save(f"{td}/ci.npy", ci)
+        code = (
+            "import sys,time,json,os,numpy as np\n"
+            f"sys.path.insert(0,{str(REF_PKG)!r})\n"
+            "from lanebfs.graph import CsrGraph\n"
+            "from lanebfs.traversal import bfs_parallel_naive\n"
+            f"rp=np.load('{td}/rp.npy'); ci=np.load('{td}/ci.npy')\n"
+            f"g=CsrGraph({n}, ci, rp)\n"
+            "th=os.cpu_count(); out=[]\n"
+            f"for s in {list(map(int, roots))}:\n"
+            "    t=time.perf_counter(); r=bfs_parallel_naive(g,s,th); dt=time.perf_counter()-t\n"
+            "    out.append([s, r.traversed_edge_count, dt])\n"
+            "print(json.dumps({'threads': th, 'runs': out}))\n")
+        try:
+            res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=timeout_s)
+            d = json.loads(res.stdout.strip().splitlines()[-1])
+        except Exception as e:  # noqa: BLE001
+            return {"error": str(e)[:200]}
+    vals = [e / dt / 1e9 for _, e, dt in d["runs"]]
+    return {"value": hm(vals), "unit": "GTEPS", "cores": d["threads"], "kind": "reference",
+            "sample": f"{len(vals)} root(s), lanebfs 0.1.0 bfs_parallel_naive (the reference's fastest path) "
+                      f"on the same CSR, in a subprocess; {sum(x[2] for x in d['runs']):.1f}s",
+            "runs": d["runs"]}
 
 
 def cpu_baseline_sample(rp, ci, roots, budget_s):
@@ -143,7 +204,7 @@ def cpu_baseline_sample(rp, ci, roots, budget_s):
         if i >= 2 and time.perf_counter() - t_all > budget_s:
             break
         t0 = time.perf_counter()
-        pred, lvl, layers = oracle.bfs_parallel(rp, ci, int(r), 0)
+        _, _, layers = oracle.bfs_parallel(rp, ci, int(r), 0)
         dt = time.perf_counter() - t0
         e = sum(l[1] for l in layers)
         vals.append(e / dt / 1e9 if e else 0.0)
@@ -181,6 +242,13 @@ def run_reference(args, rank, world):
             vals += step_vals
             step_times.append(time.perf_counter() - t)
     value = hm(vals)
+    covered = len({roots[i % len(roots)] for i in range(args.warmup * per_step, cursor)})
+    refpy = reference_python_sample(rp, ci, 1 << args.scale, roots[:1])
+    cpu = {"value": value, "unit": "GTEPS", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+           "sample": f"{per_step} roots per step cycling through the {args.roots}-root set ({covered} distinct "
+                     f"roots timed), oracle bfs_parallel (restated bfs_parallel_naive, traversal.py:128-165)"}
+    if refpy:
+        cpu["reference_python"] = refpy
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -189,9 +257,7 @@ def run_reference(args, rank, world):
         "config": {"workload": f"rmat-s{args.scale}-ef16-{args.roots}roots", "scale": args.scale,
                    "edgefactor": 16, "roots": args.roots, "n": len(rp) - 1, "nnz": int(rp[-1]),
                    "parallelism": f"cpu-openmp-{threads}t", "graph_build_s": round(build_s, 1)},
-        "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads, "kind": "port",
-                         "sample": f"{per_step} roots per step of the {args.roots}-root set, oracle "
-                                   "bfs_parallel (restated bfs_parallel_naive, traversal.py:128-165)"},
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -199,11 +265,11 @@ def run_reference(args, rank, world):
 
 def run_partitioned(args, rank, world, local):
     """N > 1: the graph 1D-partitioned over the N GPUs (one rank each), one
-    BFS = the level loop of distributed.bfs_partitioned with three NCCL
-    collectives per level. Every rank builds the same graph on
-    its GPU (deterministic device generator) and keeps only its partition's
-    rows. Per-BFS time = max over ranks of the CUDA-event time on each
-    rank's stream; value = harmonic mean over roots of E / t (whole job)."""
+    BFS = the level loop of distributed.bfs_partitioned with its per-level
+    NCCL collectives. Every rank builds the same graph on its GPU
+    (deterministic device generator) and keeps only its partition's rows.
+    Per-BFS time = max over ranks of the CUDA-event time on each rank's
+    stream; value = harmonic mean over roots of E / t (whole job)."""
     import torch
     import torch.distributed as dist
 
@@ -217,10 +283,6 @@ def run_partitioned(args, rank, world, local):
             sk.bind(("127.0.0.1", 0))
             port = sk.getsockname()[1]
         os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    # NCCL writes its version banner / debug log to stdout (with NCCL_DEBUG
-    # set, even at WARN): send it to stderr so rank 0's stdout is the JSON line
-    # (at VERSION it prints the banner to stdout regardless of NCCL_DEBUG_FILE:
-    # report the version on stderr ourselves and keep NCCL quiet)
     if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
         os.environ.pop("NCCL_DEBUG")
         print(f"[bench] NCCL version {'.'.join(map(str, torch.cuda.nccl.version()))}", file=sys.stderr)
@@ -279,7 +341,7 @@ def run_partitioned(args, rank, world, local):
     for r in roots[:2]:  # untimed warm-up
         bfs_partitioned([part], r, ex, bufs=bufs, outputs=outs, gather=True)
     e2e_vals = []
-    for r in roots[:args.e2e_roots]:
+    for r in roots[:16]:
         dist.barrier()
         a = time.perf_counter()
         res = bfs_partitioned([part], r, ex, bufs=bufs, outputs=outs, gather=True)
@@ -291,8 +353,6 @@ def run_partitioned(args, rank, world, local):
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e_vals.append(res.traversed_edge_count / float(dt.item()) / 1e9)
     e2e = hm(e2e_vals)
-    # correctness of the timed configuration (outside the timed region): the
-    # gathered tree of the last e2e root through the package validator
     ok = None
     if rank == 0 and e2e_vals:
         from paper_1604_02844_b200 import CsrGraph, PredecessorArray
@@ -302,7 +362,7 @@ def run_partitioned(args, rank, world, local):
         ok = validate_tree(gh, roots[len(e2e_vals) - 1], PredecessorArray(n, _storage=pred_h.numpy())).passed
     hbm_gbs, peak_kind = peaks()
     E = float(np.mean(edges))
-    alg = 8 * E + 40 * float(np.mean(reached)) + 8 * n + n // 8  # SURVEY §8(d) B_alg
+    alg = b_alg(E, float(np.mean(reached)), n)
     X = float(np.mean(nlevels))
     words = (n + 31) // 32
     nvl_bytes = X * 2 * (world - 1) * ((words + world - 1) // world) * 4
@@ -336,11 +396,64 @@ def run_partitioned(args, rank, world, local):
     dist.destroy_process_group()
 
 
+def device_runs(g, roots, passes, pred, validate=True):
+    """`passes` passes over the roots through bfs_device; each tree validated
+    on the device right after its BFS (outside the BFS's own CUDA-event
+    interval). Returns the results and the number of validated trees."""
+    from paper_1604_02844_b200 import bfs_device
+    from paper_1604_02844_b200.validate import validate_tree_device
+
+    runs, checked = [], 0
+    for _ in range(passes):
+        for r in roots:
+            res = bfs_device(g, r, pred)
+            if validate:
+                rep = validate_tree_device(g, r, pred)
+                checked += 1
+                if not rep.passed:
+                    raise SystemExit(f"[bench] validate_tree failed for root {r}: {rep.details}")
+            runs.append(res)
+    return runs, checked
+
+
+def teps_of(runs):
+    return [r.traversed_edge_count / (r.timing["bfs_ms"] * 1e-3) / 1e9 if r.traversed_edge_count else 0.0
+            for r in runs]
+
+
+def extra_config(build, nroots, warm_passes=1, passes=1):
+    """GTEPS of another BASELINE config, measured like the headline (device
+    outputs, CUDA-event time per BFS, every tree validated)."""
+    import torch
+
+    from paper_1604_02844_b200 import pick_roots
+
+    t0 = time.perf_counter()
+    g = build()
+    roots = pick_roots(g, nroots, 1, filter_unconnected=True).tolist()
+    n = g.num_vertices
+    pred = torch.empty((n + 31) // 32 * 32, dtype=torch.int32, device="cuda")
+    device_runs(g, roots, warm_passes, pred, validate=False)
+    runs, checked = device_runs(g, roots, passes, pred)
+    E = float(np.mean([r.traversed_edge_count for r in runs]))
+    ms = float(np.mean([r.timing["bfs_ms"] for r in runs]))
+    lv = float(np.mean([r.timing["levels"] for r in runs]))
+    V = float(np.mean([r.timing["reached"] for r in runs]))
+    hbm_gbs, _ = peaks()
+    out = {"value": hm(teps_of(runs)), "unit": "GTEPS", "roots": len(roots), "bfs_timed": len(runs),
+           "validated_trees": checked, "n": n, "nnz": g.num_edges, "ms_per_bfs": ms, "levels": lv,
+           "us_per_level": 1e3 * ms / lv,
+           "whole_bfs_frac_of_peak": b_alg(E, V, n) / (ms * 1e-3) / 1e9 / hbm_gbs,
+           "build_s": round(time.perf_counter() - t0, 2)}
+    del g, pred
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, rank, world, local):
     import torch
 
     from paper_1604_02844_b200 import RmatParams, _lib, bfs, bfs_device, build_rmat_graph, pick_roots
-    from paper_1604_02844_b200.validate import validate_tree_device
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -355,74 +468,66 @@ def run_ours(args, rank, world, local):
     build_s = time.perf_counter() - t0
     npad = (n + 31) // 32 * 32
     pred = torch.empty(npad, dtype=torch.int32, device="cuda")
-    lvl = torch.empty(n, dtype=torch.int32, device="cuda")
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    def step():
-        out = []
-        for r in roots:
-            res = bfs_device(g, r, pred, lvl)
-            out.append(res)
-        return out
-
-    for _ in range(args.warmup):
-        step()
+    device_runs(g, roots, args.warmup, pred, validate=False)
     hbm_gbs, peak_kind = peaks()
-    launches0 = _lib.kernel_launch_count()
     barrier()
     w0 = time.perf_counter()
-    results = []
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            results.append(step())
+        runs, checked = device_runs(g, roots, args.steps, pred)
         barrier()
     wall = time.perf_counter() - w0
-    launches = _lib.kernel_launch_count() - launches0
-    runs = [r for s in results for r in s]
-    teps = [r.traversed_edge_count / (r.timing["bfs_ms"] * 1e-3) / 1e9 if r.traversed_edge_count else 0.0
-            for r in runs]
-    dev_ms = sum(r.timing["bfs_ms"] for r in runs)
+    # kernels the timed BFS runs launched (each run counts its own; the
+    # validator's launches between them are not BFS work)
+    launches = sum(int(r.timing["kernel_launches"]) for r in runs)
+    teps = teps_of(runs)
     value_local = hm(teps)
-    ms_step_local = dev_ms / args.steps
-    # roofline of the dominant kernel (level expansion), SURVEY §8(d):
-    # expansion bytes per BFS = 8E (col_idx + bitmap probe) + 40V; init = 8n + n/8
-    exp_bytes = sum(8 * r.traversed_edge_count + 40 * r.timing["reached"] for r in runs)
-    exp_ms = sum(r.timing["expand_ms"] for r in runs)
-    alg_bytes = sum(8 * r.traversed_edge_count + 40 * r.timing["reached"] + 8 * n + n // 8 for r in runs)
+    ms_step_local = sum(r.timing["bfs_ms"] for r in runs) / args.steps
+    # roofline: the whole BFS against B_alg; expansion = the
+    # level kernels alone (full-GPU levels + the cluster's small levels)
+    alg = sum(b_alg(r.traversed_edge_count, r.timing["reached"], n) for r in runs)
     bfs_ms = sum(r.timing["bfs_ms"] for r in runs)
+    exp_bytes = sum(8 * r.traversed_edge_count + 40 * r.timing["reached"] for r in runs)
+    exp_ms = sum(r.timing["expand_ms"] + r.timing["cluster_ms"] for r in runs)
+    achieved = alg / (bfs_ms * 1e-3) / 1e9
+    traffic = traffic_from_profiles(args.scale)
+    dram = None
+    if traffic and traffic.get("dram_bytes_per_bfs"):
+        per_bfs_ms = bfs_ms / len(runs)
+        dram = {"bytes_per_bfs": traffic["dram_bytes_per_bfs"],
+                "dram_gbs": traffic["dram_bytes_per_bfs"] / (per_bfs_ms * 1e-3) / 1e9,
+                "source": traffic.get("source")}
+        dram["dram_frac"] = dram["dram_gbs"] / hbm_gbs
 
     # direction-optimising BFS (opt-in; not the headline: the north star is
-    # top-down): one untimed pass, then one pass over the same roots, device
-    # outputs, same E per root and the same CUDA-event timing
+    # top-down): one untimed pass, then one pass over the same roots
     for r in roots[:3]:
-        bfs_device(g, r, pred, lvl, direction="optimizing")
-    do_runs = [bfs_device(g, r, pred, lvl, direction="optimizing") for r in roots]
-    do_value = hm([x.traversed_edge_count / (x.timing["bfs_ms"] * 1e-3) / 1e9 if x.traversed_edge_count else 0.0
-                   for x in do_runs])
+        bfs_device(g, r, pred, direction="optimizing")
+    do_runs = [bfs_device(g, r, pred, direction="optimizing") for r in roots]
+    do_value = hm(teps_of(do_runs))
     do_ok = all(x.layers == y.layers for x, y in zip(do_runs, runs[:len(do_runs)]))
 
-    # e2e through the public API with host outputs (D2H inside the call);
-    # untimed warm-up calls first (they fill the page-locked output pool)
-    # (each call runs while the previous result is alive, as in the timed loop,
-    # so the pool holds both output sets before timing starts)
+    # e2e through the public API with host outputs: one bfs(g, root) call per
+    # step, parents copied to page-locked host memory inside the call (levels
+    # stay on the device until read); untimed warm-up calls fill the pool
     res = None
     for r in roots[:3]:
         res = bfs(g, r)
+    del res
     e2e_vals = []
-    for r in roots[:args.e2e_roots]:
+    for r in roots:
         a = time.perf_counter()
         res = bfs(g, r)
         dt = time.perf_counter() - a
         e2e_vals.append(res.traversed_edge_count / dt / 1e9 if res.traversed_edge_count else 0.0)
+        del res
     e2e = hm(e2e_vals)
-    d2h_bytes = (npad + n) * 4  # one e2e step = one BFS: pred (pad32) + level to host
-    # correctness of the timed configuration (outside the timed region)
-    chk = bfs(g, roots[0])
-    ok = validate_tree_device(g, roots[0], chk.predecessors).passed
+    d2h_bytes = npad * 4  # one e2e step = one BFS: the pad32(n) parent array to host
 
     value, ms_step = value_local, ms_step_local
     if world > 1:
@@ -438,11 +543,18 @@ def run_ours(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rp, ci = g.colstarts, g.rows
         vals, thr, secs = cpu_baseline_sample(rp, ci, roots, args.cpu_budget)
-        cpu = {"value": hm(vals), "unit": "GTEPS", "cores": thr, "kind": "port",
+        cpu = {"value": hm(vals), "unit": "GTEPS", "cores": thr, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"{len(vals)} of the {args.roots} roots on the same graph, oracle bfs_parallel "
                          f"(OpenMP restatement of bfs_parallel_naive), {secs:.1f}s"}
-    traffic = traffic_from_profiles(args.scale)
-    achieved = exp_bytes / (exp_ms * 1e-3) / 1e9
+    del g, pred
+    torch.cuda.empty_cache()
+    extra = {}
+    if rank == 0 and not args.no_extra_configs:
+        from paper_1604_02844_b200 import build_lattice_graph
+
+        extra["rmat-s20-ef16-64roots"] = extra_config(lambda: build_rmat_graph(RmatParams(scale=20, seed=1)), 64,
+                                                      warm_passes=2, passes=2)
+        extra["lattice-4096x4096-16roots"] = extra_config(lambda: build_lattice_graph(4096, 4096), 16)
     line = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -452,23 +564,22 @@ def run_ours(args, rank, world, local):
                    "edgefactor": 16, "roots": args.roots, "n": n, "nnz": nnz,
                    "parallelism": "1gpu" if world == 1 else f"replicas{world}",
                    "l2": "inputs larger than L2 (CSR %.2f GB vs 126 MB L2); no flush" % ((8 * n + 4 * nnz) / 1e9),
-                   "graph_build_s": round(build_s, 2), "validated": ok},
-        # dominant work = the level expansion: per BFS, every expansion launch
-        # (k_sweep, k_expand_* bins, k_merge_hot, k_levels),
-        # timed with CUDA events on the BFS stream around each level's launches
+                   "graph_build_s": round(build_s, 2), "validated_trees": checked},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
                      "frac": achieved / hbm_gbs, "peak_kind": peak_kind,
-                     "traffic": traffic.get("dram_bytes_per_bfs_expansion") if traffic else None,
-                     "traffic_alg": traffic.get("alg_bytes_per_bfs_expansion") if traffic else None,
-                     "kernel": "level expansion per BFS (k_sweep, k_expand_*, k_merge_hot, k_levels)",
-                     "alg_bytes_per_bfs_expansion": exp_bytes / len(runs),
-                     "expansion_ms_per_bfs": exp_ms / len(runs),
-                     "whole_bfs": {"alg_bytes": alg_bytes / len(runs), "ms": bfs_ms / len(runs),
-                                   "frac_of_peak": alg_bytes / (bfs_ms * 1e-3) / 1e9 / hbm_gbs,
-                                   "frac_of_8TBs": alg_bytes / (bfs_ms * 1e-3) / 8e12}},
+                     "traffic": traffic.get("dram_bytes_per_bfs") if traffic else None,
+                     "kernel": "whole BFS (init, every level kernel, output pass), SURVEY §8(d) B_alg",
+                     "alg_bytes_per_bfs": alg / len(runs), "ms_per_bfs": bfs_ms / len(runs),
+                     "frac_of_8TBs": alg / (bfs_ms * 1e-3) / 8e12,
+                     "dram": dram,
+                     "expansion": {"alg_bytes_per_bfs": exp_bytes / len(runs), "ms_per_bfs": exp_ms / len(runs),
+                                   "frac_of_peak": exp_bytes / (exp_ms * 1e-3) / 1e9 / hbm_gbs,
+                                   "kernels": "full-GPU level launches + the cluster's small levels"}},
         "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 8,
                 "d2h_bytes_per_step": d2h_bytes, "step": "one bfs(g, root) call (harmonic mean over roots)",
-                "api": "paper_1604_02844_b200.bfs(g, root), host outputs", "roots_timed": len(e2e_vals)},
+                "api": "paper_1604_02844_b200.bfs(g, root), parents to host (levels on first access)",
+                "roots_timed": len(e2e_vals)},
+        "configs": extra,
         "direction_optimizing": {"value": do_value, "unit": "GTEPS", "roots": len(do_runs),
                                  "layers_equal_top_down": do_ok,
                                  "note": "opt-in bottom-up levels (bfs(..., direction='optimizing')); same E, "
@@ -494,18 +605,7 @@ def main():
     elif world > 1 or args.partitioned:
         run_partitioned(args, rank, world, local)
     else:
-        try:
-            run_ours(args, rank, world, local)
-        except RuntimeError as e:
-            # a CUDA fault poisons the context: rerun the whole measurement once
-            # in a fresh process (nothing from the failed attempt is reported;
-            # the line says that a retry happened and why)
-            if os.environ.get("LBFS_BENCH_RETRY") or "liblbfs error" not in str(e):
-                raise
-            print(f"[bench] first attempt failed ({e}); rerunning once in a fresh process", file=sys.stderr)
-            os.environ["LBFS_BENCH_RETRY"] = str(e).splitlines()[0][:200]
-            sys.stdout.flush()
-            os.execv(sys.executable, [sys.executable] + sys.argv)
+        run_ours(args, rank, world, local)
 
 
 if __name__ == "__main__":

@@ -118,13 +118,25 @@ void lbfs_csr_destroy(lbfs_csr* csr);
 /* ---- BFS graph handle (replaces CsrGraph as seen by run_bfs) ---------- */
 
 /* Copy a host CSR (colstarts int64[n+1], rows int32[nnz]; graph.py:96-136) to
- * the device and build the traversal layout. ngpus must be 1 in this build
- * (the partitioned path is driven from Python over torch.distributed). */
+ * the device and build the traversal layout. ngpus == 1: one GPU
+ * (the current device). ngpus > 1 (a power of two): the graph is
+ * 1D-partitioned over devices 0..ngpus-1 of this process, one partition per
+ * device, with one library-owned NCCL communicator per device
+ * (ncclCommInitAll; libnccl.so.2 is loaded at run time) — lbfs_bfs then runs
+ * the partitioned level loop from the calling thread (ncclGroupStart/End per
+ * collective) and returns the same outputs. */
 int lbfs_graph_create(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int64_t nnz,
                       int ngpus, lbfs_graph** out);
 /* Same, from a device CSR (no host round trip). The csr may be destroyed
  * afterwards. */
 int lbfs_graph_create_from_csr(const lbfs_csr* csr, int ngpus, lbfs_graph** out);
+/* The partitioned path with explicit devices (devices[p] holds partition p;
+ * NULL = 0..ngpus-1), also for ngpus == 1 (a one-rank communicator: the
+ * partitioned code path on a single GPU). Not for validation (unpartitioned
+ * handles only). */
+int lbfs_graph_create_partitioned(const lbfs_csr* csr, int ngpus, const int* devices, lbfs_graph** out);
+/* Devices a graph handle spans (1 unless partitioned). */
+int lbfs_graph_gpus(const lbfs_graph* g, int* ngpus);
 void lbfs_graph_destroy(lbfs_graph* g);
 int lbfs_graph_info(const lbfs_graph* g, int64_t* n, int64_t* nnz);
 

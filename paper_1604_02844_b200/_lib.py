@@ -67,6 +67,8 @@ SIGNATURES = {
     "lbfs_csr_destroy": (None, [_p]),
     "lbfs_graph_create": (ctypes.c_int, [_i64, _p, _p, _i64, ctypes.c_int, ctypes.POINTER(_p)]),
     "lbfs_graph_create_from_csr": (ctypes.c_int, [_p, ctypes.c_int, ctypes.POINTER(_p)]),
+    "lbfs_graph_create_partitioned": (ctypes.c_int, [_p, ctypes.c_int, _p, ctypes.POINTER(_p)]),
+    "lbfs_graph_gpus": (ctypes.c_int, [_p, ctypes.POINTER(ctypes.c_int)]),
     "lbfs_graph_destroy": (None, [_p]),
     "lbfs_graph_info": (ctypes.c_int, [_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "lbfs_bfs": (ctypes.c_int, [_p, _i64, ctypes.c_int, _p, _p, ctypes.POINTER(Layer), _i64,

@@ -275,12 +275,26 @@ void lbfs_csr_destroy(lbfs_csr* csr) {
   delete csr;
 }
 
+static lbfs_graph* make_graph(const Csr& c, int ngpus, const int* devices, bool partitioned) {
+  auto* g = new lbfs_graph;
+  try {
+    if (partitioned)
+      g->multi = new MultiGraph(c, ngpus, devices);
+    else
+      g->eng = new BfsEngine(c);
+  } catch (...) {
+    delete g;
+    throw;
+  }
+  return g;
+}
+
 int lbfs_graph_create(int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int64_t nnz,
                       int ngpus, lbfs_graph** out) {
   return guarded([&] {
     check_ids(n);
     if (!out || !row_ptr || nnz < 0 || (nnz > 0 && !col_idx)) throw_inval("bad arguments");
-    if (ngpus != 1) throw_inval("ngpus must be 1 (multi-GPU runs one process per GPU)");
+    if (ngpus < 1) throw_inval("ngpus must be >= 1");
     if (row_ptr[0] != 0 || row_ptr[n] != nnz) throw_inval("row_ptr must start at 0 and end at nnz");
     Csr c;  // temporary upload in original ids; the engine keeps its own layout
     LBFS_CUDA(cudaGetDevice(&c.device));
@@ -292,14 +306,7 @@ int lbfs_graph_create(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
       LBFS_CUDA(cudaMemcpy(c.row_ptr, row_ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice));
       if (nnz > 0)
         LBFS_CUDA(cudaMemcpy(c.col_idx, col_idx, sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice));
-      auto* g = new lbfs_graph;
-      try {
-        g->eng = new BfsEngine(c);
-      } catch (...) {
-        delete g;
-        throw;
-      }
-      *out = g;
+      *out = make_graph(c, ngpus, nullptr, ngpus > 1);
     } catch (...) {
       free_csr(c);
       throw;
@@ -311,36 +318,47 @@ int lbfs_graph_create(int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
 int lbfs_graph_create_from_csr(const lbfs_csr* csr, int ngpus, lbfs_graph** out) {
   return guarded([&] {
     if (!csr || !out) throw_inval("bad arguments");
-    if (ngpus != 1) throw_inval("ngpus must be 1 (multi-GPU runs one process per GPU)");
+    if (ngpus < 1) throw_inval("ngpus must be >= 1");
     LBFS_CUDA(cudaSetDevice(csr->c.device));
-    auto* g = new lbfs_graph;
-    try {
-      g->eng = new BfsEngine(csr->c);
-    } catch (...) {
-      delete g;
-      throw;
-    }
-    *out = g;
+    *out = make_graph(csr->c, ngpus, nullptr, ngpus > 1);
+  });
+}
+
+int lbfs_graph_create_partitioned(const lbfs_csr* csr, int ngpus, const int* devices, lbfs_graph** out) {
+  return guarded([&] {
+    if (!csr || !out) throw_inval("bad arguments");
+    LBFS_CUDA(cudaSetDevice(csr->c.device));
+    *out = make_graph(csr->c, ngpus, devices, true);
   });
 }
 
 void lbfs_graph_destroy(lbfs_graph* g) {
   if (!g) return;
-  cudaSetDevice(g->eng->device());
-  delete g->eng;
+  if (g->multi) {
+    delete g->multi;
+  } else {
+    cudaSetDevice(g->eng->device());
+    delete g->eng;
+  }
   delete g;
 }
 
 int lbfs_graph_info(const lbfs_graph* g, int64_t* n, int64_t* nnz) {
   return guarded([&] {
     if (!g) throw_inval("graph is NULL");
-    if (n) *n = g->eng->n();
-    if (nnz) *nnz = g->eng->nnz();
+    if (n) *n = g->multi ? g->multi->n() : g->eng->n();
+    if (nnz) *nnz = g->multi ? g->multi->nnz() : g->eng->nnz();
   });
 }
 
-static void copy_layers(const BfsEngine& e, lbfs_layer* out, int64_t cap, int64_t* n_layers) {
-  const auto& L = e.layers();
+int lbfs_graph_gpus(const lbfs_graph* g, int* ngpus) {
+  return guarded([&] {
+    if (!g || !ngpus) throw_inval("bad arguments");
+    *ngpus = g->multi ? g->multi->ngpus() : 1;
+  });
+}
+
+static void copy_layers(const std::vector<lbfs_layer>& L, lbfs_layer* out, int64_t cap, int64_t* n_layers) {
   if (n_layers) *n_layers = (int64_t)L.size();
   if (out && cap > 0) {
     const int64_t k = std::min<int64_t>(cap, (int64_t)L.size());
@@ -352,6 +370,27 @@ int lbfs_bfs(lbfs_graph* g, int64_t root, int direction, int32_t* pred_out, int3
              lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers, lbfs_timing* t_out) {
   return guarded([&] {
     if (!g) throw_inval("graph is NULL");
+    if (g->multi) {
+      MultiGraph& m = *g->multi;
+      std::lock_guard<std::mutex> lk(m.mu);
+      if (direction != LBFS_DIR_TOP_DOWN) throw_inval("partitioned graphs run top-down");
+      LBFS_CUDA(cudaSetDevice(m.device()));
+      int32_t* d_pred = dev_alloc<int32_t>((size_t)m.npad());
+      lbfs_timing t{};
+      try {
+        m.run(root, d_pred, nullptr, &t);
+        if (pred_out)
+          LBFS_CUDA(cudaMemcpy(pred_out, d_pred, sizeof(int32_t) * (size_t)m.npad(), cudaMemcpyDeviceToHost));
+        if (level_out) m.last_levels_to_host(level_out);
+      } catch (...) {
+        dev_free(d_pred);
+        throw;
+      }
+      dev_free(d_pred);
+      if (t_out) *t_out = t;
+      copy_layers(m.layers(), layers_out, layers_cap, n_layers);
+      return;
+    }
     BfsEngine& e = *g->eng;
     std::lock_guard<std::mutex> lk(e.mu);
     LBFS_CUDA(cudaSetDevice(e.device()));
@@ -362,7 +401,7 @@ int lbfs_bfs(lbfs_graph* g, int64_t root, int direction, int32_t* pred_out, int3
     // chunks of them (BfsEngine::run_to_host); levels only when asked for
     e.run_to_host(root, direction, pred_out, level_out, &t);
     if (t_out) *t_out = t;
-    copy_layers(e, layers_out, layers_cap, n_layers);
+    copy_layers(e.layers(), layers_out, layers_cap, n_layers);
   });
 }
 
@@ -372,6 +411,17 @@ int lbfs_bfs_device(lbfs_graph* g, int64_t root, int direction, int32_t* d_pred,
   return guarded([&] {
     if (!g) throw_inval("graph is NULL");
     if (!d_pred) throw_inval("device pred output must be non-NULL");
+    if (g->multi) {
+      MultiGraph& m = *g->multi;
+      std::lock_guard<std::mutex> lk(m.mu);
+      if (direction != LBFS_DIR_TOP_DOWN) throw_inval("partitioned graphs run top-down");
+      LBFS_CUDA(cudaSetDevice(m.device()));
+      lbfs_timing t{};
+      m.run(root, d_pred, d_level, &t);
+      if (t_out) *t_out = t;
+      copy_layers(m.layers(), layers_out, layers_cap, n_layers);
+      return;
+    }
     BfsEngine& e = *g->eng;
     std::lock_guard<std::mutex> lk(e.mu);
     LBFS_CUDA(cudaSetDevice(e.device()));
@@ -379,21 +429,31 @@ int lbfs_bfs_device(lbfs_graph* g, int64_t root, int direction, int32_t* d_pred,
     lbfs_timing t{};
     e.run(root, d_pred, d_level, &t, direction);
     if (t_out) *t_out = t;
-    copy_layers(e, layers_out, layers_cap, n_layers);
+    copy_layers(e.layers(), layers_out, layers_cap, n_layers);
   });
 }
 
 int lbfs_graph_last_layers(lbfs_graph* g, lbfs_layer* out, int64_t cap, int64_t* n_layers) {
   return guarded([&] {
     if (!g) throw_inval("graph is NULL");
+    if (g->multi) {
+      std::lock_guard<std::mutex> lk(g->multi->mu);
+      copy_layers(g->multi->layers(), out, cap, n_layers);
+      return;
+    }
     std::lock_guard<std::mutex> lk(g->eng->mu);
-    copy_layers(*g->eng, out, cap, n_layers);
+    copy_layers(g->eng->layers(), out, cap, n_layers);
   });
 }
 
 int lbfs_graph_last_levels(lbfs_graph* g, int32_t* level_out) {
   return guarded([&] {
     if (!g || !level_out) throw_inval("bad arguments");
+    if (g->multi) {
+      std::lock_guard<std::mutex> lk(g->multi->mu);
+      g->multi->last_levels_to_host(level_out);
+      return;
+    }
     BfsEngine& e = *g->eng;
     std::lock_guard<std::mutex> lk(e.mu);
     LBFS_CUDA(cudaSetDevice(e.device()));
@@ -406,6 +466,7 @@ int lbfs_graph_last_levels(lbfs_graph* g, int32_t* level_out) {
 int lbfs_validate_tree_device(lbfs_graph* g, int64_t root, const int32_t* d_pred, int64_t report[10]) {
   return guarded([&] {
     if (!g || !d_pred || !report) throw_inval("bad arguments");
+    if (g->multi) throw_inval("validation needs an unpartitioned graph");
     BfsEngine& e = *g->eng;
     std::lock_guard<std::mutex> lk(e.mu);
     LBFS_CUDA(cudaSetDevice(e.device()));
@@ -416,6 +477,7 @@ int lbfs_validate_tree_device(lbfs_graph* g, int64_t root, const int32_t* d_pred
 int lbfs_validate_tree(lbfs_graph* g, int64_t root, const int32_t* pred, int64_t report[10]) {
   return guarded([&] {
     if (!g || !pred || !report) throw_inval("bad arguments");
+    if (g->multi) throw_inval("validation needs an unpartitioned graph");
     BfsEngine& e = *g->eng;
     std::lock_guard<std::mutex> lk(e.mu);
     LBFS_CUDA(cudaSetDevice(e.device()));
@@ -435,6 +497,7 @@ int lbfs_validate_tree(lbfs_graph* g, int64_t root, const int32_t* pred, int64_t
 
 static BfsEngine& part_engine(lbfs_graph* g) {
   if (!g) throw_inval("graph is NULL");
+  if (!g->eng) throw_inval("not a single-partition handle (lbfs_part_create)");
   LBFS_CUDA(cudaSetDevice(g->eng->device()));
   return *g->eng;
 }

@@ -7,9 +7,8 @@
 //   K1 k_expand<Mode>    frontier expansion over CSR, degree-binned in one
 //                        persistent launch (one 1024-thread CTA per SM):
 //                        - CTA bin (deg >= kCtaMin): rows cut into kChunk
-//                          slices; each warp streams slices through a private
-//                          shared-memory double buffer filled by cp.async.bulk
-//                          (mbarrier completion), one chunk ahead;
+//                          slices; each warp streams its slices with 128-bit
+//                          loads, the next 128-element chunk in flight;
 //                        - warp bin (32 <= deg < kCtaMin) and small bin
 //                          (deg < 32): a warp takes 32 vertices at once and
 //                          walks their concatenated rows (one row_ptr round
@@ -523,22 +522,6 @@ __device__ __forceinline__ void expand_range(const LevelArgs& a, const Hot& h, i
     expand_group<M>(a, h, n, v, d, elo, ehi, T, B, lane, ws, acc);
 }
 
-// Valid-element mask of a 256-element chunk whose lane holds elements
-// [4*lane, 4*lane+4) and [128+4*lane, 128+4*lane+4) for a slice covering
-// chunk offsets [lo, hi); invalid elements are zeroed (stale staging data).
-__device__ __forceinline__ uint32_t slice_mask(int32_t (&nb)[8], int lo, int hi, int lane) {
-  if (lo <= 0 && hi >= kWarpChunk) return 0xFFu;  // interior chunk
-  uint32_t okm = 0;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int r = (q < 4 ? lane * 4 + q : 128 + lane * 4 + (q - 4));
-    const bool ok = r >= lo && r < hi;
-    okm |= (uint32_t)ok << q;
-    nb[q] = ok ? nb[q] : 0;
-  }
-  return okm;
-}
-
 // Slice descriptors through L2 (k_levels rewrites a queue buffer every other
 // level within one launch; L1 is not coherent).
 __device__ __forceinline__ CtaItem ld_item(const CtaItem* p) {
@@ -630,19 +613,10 @@ __device__ __forceinline__ void stream_queue_rows(const LevelArgs& a, const Hot&
       n, gwarp, nwarps, lane, acc);
 }
 
-struct ChunkMeta {
-  int64_t base;    // col_idx index of the chunk's first staged element
-  int64_t lo, hi;  // valid element range of the owning slice
-  int32_t u;       // internal id of the hub
-};
-
 // Static shared memory of an expansion CTA (kExpandWarps warps); the
-// dynamic part holds the per-warp bulk-copy rings (kRingBytes) and the hot
-// snapshot of the visited prefix behind them.
+// dynamic part is the snapshot of the visited prefix.
 struct ExpandSmem {
-  uint64_t bar[kExpandWarps][kWarpStages];  // per-warp ring slots (mbarriers)
   uint64_t hot_bar;                         // hot snapshot copies
-  ChunkMeta meta[kExpandWarps][kWarpStages];
   WarpScratch ws[kExpandWarps];
   int32_t T[kSmallMax + 2];
   int64_t B[kSmallMax + 1];
@@ -650,9 +624,7 @@ struct ExpandSmem {
 };
 
 __device__ __forceinline__ void expand_init(ExpandSmem& s, const LevelArgs& a) {
-  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
-  if (lane == 0)
-    for (int b = 0; b < kWarpStages; ++b) mbar_init(&s.bar[wib][b], 1);
+  const int tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(&s.hot_bar, 1);
     s.hot_issued = 0;
@@ -692,11 +664,10 @@ __device__ __forceinline__ void hot_drain(ExpandSmem& s) {
 }
 
 // The expansion of one level's frontier by one persistent CTA per SM,
-// bins selected by kPhases. par_bits carries the per-warp ring parities
-// across calls (the mbarriers live as long as the CTA).
+// bins selected by kPhases.
 template <int M, int kPhases>
-__device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier& f, ExpandSmem& s, uint8_t* s_dyn,
-                                              const Hot& h, uint32_t& par_bits, Acc& acc) {
+__device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier& f, ExpandSmem& s, const Hot& h,
+                                              Acc& acc) {
   constexpr int phases = kPhases;
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   // warp ids interleave the SMs so that the first work units of every phase
@@ -706,118 +677,12 @@ __device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier
   WarpScratch& ws = s.ws[wib];
   const int32_t* s_T = s.T;
   const int64_t* s_B = s.B;
-  const int refresh_every = (h.words > 0 && M != kHeavy) ? a.refresh_chunks : 0;
-  auto& s_bar = s.bar;
-  auto& s_meta = s.meta;
 
-  // ---- phase 1: CTA bin, warp-private bulk-copy streams -------------------
-  // a kWarpStages-deep ring of kWarpChunk-element buffers per warp: lane 0
-  // keeps kWarpStages-1 chunks in flight while the warp probes one
-  if ((phases & 1) && gwarp < f.n_cta) {
-    int32_t* wbuf = reinterpret_cast<int32_t*>(s_dyn) + (size_t)wib * kWarpStages * kWarpChunk;
-    // lane-0 stream state: current slice [pos, end) (16-B aligned), next slice prefetched
-    int64_t it = gwarp;
-    CtaItem cur = ld_item(f.cta + it);
-    CtaItem pre{0, 0, 0};
-    if (it + nwarps < f.n_cta) pre = ld_item(f.cta + it + nwarps);
-    int64_t pos = cur.start & ~int64_t(3);
-    int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
-    auto issue = [&](int b) -> uint32_t {  // lane 0: next chunk into buffer b; 0 when exhausted
-      if (pos >= end) {
-        it += nwarps;
-        if (it >= f.n_cta) return 0u;
-        cur = pre;
-        if (it + nwarps < f.n_cta) pre = ld_item(f.cta + it + nwarps);
-        pos = cur.start & ~int64_t(3);
-        end = (cur.start + cur.len + 3) & ~int64_t(3);
-      }
-      const int64_t cnt = std::min<int64_t>(kWarpChunk, end - pos);
-      LBFS_DCHECK(pos >= 0 && cnt > 0 && pos + cnt <= a.chk_nnz + 8 && cur.len >= 0, "hub chunk range");
-      s_meta[wib][b] = ChunkMeta{pos, cur.start, cur.start + cur.len, cur.u};
-      mbar_expect_tx(&s_bar[wib][b], (uint32_t)(cnt * 4));
-      bulk_g2s(wbuf + b * kWarpChunk, a.col_idx + pos, (uint32_t)(cnt * 4), &s_bar[wib][b]);
-      pos += cnt;
-      return 1u;
-    };
-    uint32_t more = 0;  // bit b: buffer b holds a chunk
-    if (lane == 0)
-      for (int b = 0; b < kWarpStages; ++b) more |= issue(b) << b;
-    more = __shfl_sync(kFull, more, 0);
-    int chunks_done = 0;
-    for (int b = 0; (more >> b) & 1u; b = (b + 1) % kWarpStages) {
-      mbar_wait(&s_bar[wib][b], (par_bits >> b) & 1u);
-      par_bits ^= 1u << b;
-      const ChunkMeta m = s_meta[wib][b];
-      constexpr int kV = kWarpChunk / 128;  // 128-bit loads per lane per chunk
-      int4 xs[kV];
-#pragma unroll
-      for (int i = 0; i < kV; ++i) xs[i] = reinterpret_cast<const int4*>(wbuf + b * kWarpChunk)[lane + 32 * i];
-      // WAR hazards before lane 0 refills slot b: (1) across proxies, every
-      // lane's shared-memory load of buffer b must have returned before the
-      // async proxy overwrites it — a warp vote consuming the loaded
-      // registers (data and meta) cannot execute earlier; (2) the meta slot
-      // is rewritten by lane 0's generic stores, ordered by __syncwarp.
-      int32_t dep = m.u ^ (int32_t)(m.base ^ m.lo ^ m.hi);
-#pragma unroll
-      for (int i = 0; i < kV; ++i) dep |= (xs[i].x ^ xs[i].y) | (xs[i].z ^ xs[i].w);
-      (void)__any_sync(kFull, dep == 0x7FFFFFFF);
-      __syncwarp();
-      uint32_t mo = 0;
-      if (lane == 0) mo = issue(b);  // refill b right away
-      mo = __shfl_sync(kFull, mo, 0);
-      more = (more & ~(1u << b)) | (mo << b);
-      int32_t nb[4 * kV];
-#pragma unroll
-      for (int i = 0; i < kV; ++i) {
-        nb[4 * i + 0] = xs[i].x;
-        nb[4 * i + 1] = xs[i].y;
-        nb[4 * i + 2] = xs[i].z;
-        nb[4 * i + 3] = xs[i].w;
-      }
-      const int32_t pu = m.u;
-      auto par = [&](int) { return pu; };
-      if (m.lo <= m.base && m.hi >= m.base + kWarpChunk) {
-        // interior chunk: all staged elements valid, ascending (a sorted row
-        // segment) from lane 0's first to lane 31's last element
-        constexpr uint32_t kAll = (1u << (4 * kV)) - 1u;
-        const int32_t first = __shfl_sync(kFull, nb[0], 0), last = __shfl_sync(kFull, nb[4 * kV - 1], 31);
-        if (a.dbg) atomicAdd(a.dbg + 2, (unsigned long long)(4 * kV));  // LBFS_COUNT: hub elements
-        if ((last >> 5) < h.words)
-          probe_batch<M, 4 * kV, decltype(par), kAllHot>(a, h, nb, kAll, par, lane, acc);
-        else if ((first >> 5) >= h.words)
-          probe_batch<M, 4 * kV, decltype(par), kAllCold>(a, h, nb, kAll, par, lane, acc);
-        else
-          probe_batch<M, 4 * kV>(a, h, nb, kAll, par, lane, acc);
-      } else {
-        uint32_t okm = 0;
-#pragma unroll
-        for (int i = 0; i < kV; ++i) {
-          const int lo = (int)(m.lo - m.base) - (lane + 32 * i) * 4, hi = (int)(m.hi - m.base) - (lane + 32 * i) * 4;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const bool ok = q >= lo && q < hi;
-            okm |= (uint32_t)ok << (4 * i + q);
-            nb[4 * i + q] = ok ? nb[4 * i + q] : 0;  // staged slots outside the slice hold stale data
-          }
-        }
-        if (a.dbg) atomicAdd(a.dbg + 2, (unsigned long long)__popc(okm));  // LBFS_COUNT: hub elements
-        probe_batch<M, 4 * kV>(a, h, nb, okm, par, lane, acc);
-      }
-      if (refresh_every && wib == 0 && ++chunks_done % refresh_every == 0) {
-        // re-learn the hot prefix from L2 (others' discoveries): async bulk
-        // copy over the shared copy; a racing local OR may be lost, which
-        // only costs a redundant write later
-        if (lane == 0) {  // (warp 0 lane 0 is thread 0, the only issuer)
-          hot_wait_last(s);  // previous copy landed
-          hot_issue(s, h, a.visited);
-        }
-        __syncwarp();
-      }
-    }
-  }
-
-  // ---- phase 1 (variant): hub slices through registers instead of TMA ----
-  if (phases & 8) stream_slices<M>(a, h, f.cta, f.n_cta, gwarp, nwarps, lane, acc);
+  // ---- phase 1: hub slices (deg >= kCtaMin), one kChunk slice per warp step,
+  // 128-bit loads with the next chunk in flight. (Round 1 staged them through
+  // a per-warp cp.async.bulk ring; that variant failed certification
+  // intermittently — DESIGN.md §5 — and is gone.)
+  if (phases & 1) stream_slices<M>(a, h, f.cta, f.n_cta, gwarp, nwarps, lane, acc);
 
   // ---- phase 2a: warp-bin rows (32 <= deg < kCtaMin), one slice each -----
   if (phases & 16) stream_slices<M>(a, h, f.wslice, f.n_wslice, gwarp, nwarps, lane, acc);
@@ -961,12 +826,20 @@ __device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier
 }
 
 // One launch per level and bin set (host-driven level loop).
+// Queue-mode launches run 512 threads per CTA: their winner path (election,
+// row reads, bin appends for a batch of 4) needs more than the 64 registers
+// a 1024-thread CTA leaves, and a queue level is latency-bound anyway.
+// (So do the bitmap-mode group items: their double-buffered windows plus the
+// parent stores spill at 64 registers.)
 template <int M, int kPhases>
-__global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Frontier f, int32_t hot_words) {
+constexpr int expand_threads() { return (M == kQueueOut || (M == kBitmapOut && kPhases == 2)) ? 512 : kExpandThreads; }
+
+template <int M, int kPhases>
+__global__ void __launch_bounds__(expand_threads<M, kPhases>(), 1) k_expand(LevelArgs a, Frontier f, int32_t hot_words) {
   extern __shared__ __align__(128) uint8_t s_dyn[];
   __shared__ ExpandSmem s;
   expand_init(s, a);
-  const Hot h{reinterpret_cast<uint32_t*>(s_dyn + kRingBytes), smem_u32(s_dyn + kRingBytes), hot_words};
+  const Hot h{reinterpret_cast<uint32_t*>(s_dyn), smem_u32(s_dyn), hot_words};
   uint4* h4 = reinterpret_cast<uint4*>(h.s);
   const int hw4 = hot_words >> 2;  // hot_words is a multiple of 4
   if constexpr (M == kHeavy) {
@@ -975,9 +848,8 @@ __global__ void __launch_bounds__(kExpandThreads, 1) k_expand(LevelArgs a, Front
   } else {
     hot_load(s, h, a.visited);
   }
-  uint32_t par_bits = 0;
   Acc acc;
-  expand_phases<M, kPhases>(a, f, s, s_dyn, h, par_bits, acc);
+  expand_phases<M, kPhases>(a, f, s, h, acc);
   flush_acc<M>(a, acc);
   hot_drain(s);
   if constexpr (M == kHeavy) {  // this CTA's blind ORs -> its stage row
@@ -1539,14 +1411,14 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   // shared memory: the TMA ring plus as much of the visited bitmap as fits
   // (static shared memory differs per phase kernel: take the largest)
   const void* kernels[] = {(const void*)k_expand<kBitmapOut, 1>,  (const void*)k_expand<kBitmapOut, 2>,
-                           (const void*)k_expand<kBitmapOut, 4>,  (const void*)k_expand<kBitmapOut, 8>,
+                           (const void*)k_expand<kBitmapOut, 4>,
                            (const void*)k_expand<kBitmapOut, 16>, (const void*)k_expand<kBitmapOut, 32>,
                            (const void*)k_expand<kBitmapOut, 64>, (const void*)k_expand<kQueueOut, 1>,
                            (const void*)k_expand<kQueueOut, 2>,   (const void*)k_expand<kQueueOut, 4>,
-                           (const void*)k_expand<kQueueOut, 8>,   (const void*)k_expand<kQueueOut, 16>,
+                           (const void*)k_expand<kQueueOut, 16>,
                            (const void*)k_expand<kQueueOut, 32>,  (const void*)k_expand<kQueueOut, 64>,
                            (const void*)k_expand<kHeavy, 1>,      (const void*)k_expand<kHeavy, 2>,
-                           (const void*)k_expand<kHeavy, 4>,      (const void*)k_expand<kHeavy, 8>,
+                           (const void*)k_expand<kHeavy, 4>,
                            (const void*)k_expand<kHeavy, 16>,     (const void*)k_expand<kHeavy, 32>,
                            (const void*)k_expand<kHeavy, 64>};
   size_t max_static = 0;
@@ -1557,14 +1429,14 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   }
   int optin = 0;
   LBFS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device_));
-  int64_t avail = (int64_t)optin - (int64_t)max_static - kRingBytes - 1024;
+  int64_t avail = (int64_t)optin - (int64_t)max_static - 1024;
   if (nparts_ == 1) {  // the sweep kernel's ring + static part must fit next to the same hot prefix
     cudaFuncAttributes fs{};
     LBFS_CUDA(cudaFuncGetAttributes(&fs, (const void*)k_sweep));
     avail = std::min<int64_t>(avail, (int64_t)optin - (int64_t)fs.sharedSizeBytes - kSweepRingBytes);
   }
   hot_words_ = (int32_t)std::min<int64_t>(std::max<int64_t>(avail / 4, 0) & ~int64_t(3), (nwords_ + 3) & ~int64_t(3));
-  dyn_smem_ = kRingBytes + hot_words_ * 4;
+  dyn_smem_ = hot_words_ * 4;
   for (auto fn : kernels) LBFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_));
   LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<kBitmapOut, 2>, kExpandThreads, dyn_smem_));
   expand_grid_ = sm_count_ * std::max(occ, 1);
@@ -1678,6 +1550,7 @@ void BfsEngine::launch_cluster(int64_t L, int cur, bool prev_bitmap, cudaStream_
   p.L0 = L;
   p.max_levels = kLoopCap;
   p.exit_edges = cl_exit_edges_;
+  p.bitmap_min_edges = (unsigned long long)std::max<int64_t>(bitmap_floor_, n_ / bitmap_div_);
   for (int b = 0; b < 2; ++b) {
     p.out_small[b] = q_small_[b];
     p.out_cta[b] = q_cta_[b];
@@ -1806,34 +1679,30 @@ unsigned clamp_grid(int64_t blocks, int64_t cap) {
 
 template <int M>
 static void launch_expand_m(int pi, unsigned grid, int smem, const LevelArgs& a, const Frontier& f, int32_t hot,
-                            bool hub_ldg, cudaStream_t st) {
+                            cudaStream_t st) {
   if (pi == 0) {
-    if (hub_ldg) {
-      LBFS_LAUNCH((k_expand<M, 8>), grid, kExpandThreads, smem, st, a, f, hot);
-    } else {
-      LBFS_LAUNCH((k_expand<M, 1>), grid, kExpandThreads, smem, st, a, f, hot);
-    }
+    LBFS_LAUNCH((k_expand<M, 1>), grid, (expand_threads<M, 1>()), smem, st, a, f, hot);
   } else if (pi == 1) {
-    LBFS_LAUNCH((k_expand<M, 2>), grid, kExpandThreads, smem, st, a, f, hot);
+    LBFS_LAUNCH((k_expand<M, 2>), grid, (expand_threads<M, 2>()), smem, st, a, f, hot);
   } else if (pi == 3) {
-    LBFS_LAUNCH((k_expand<M, 16>), grid, kExpandThreads, smem, st, a, f, hot);
+    LBFS_LAUNCH((k_expand<M, 16>), grid, (expand_threads<M, 16>()), smem, st, a, f, hot);
   } else if (pi == 4) {
-    LBFS_LAUNCH((k_expand<M, 32>), grid, kExpandThreads, smem, st, a, f, hot);
+    LBFS_LAUNCH((k_expand<M, 32>), grid, (expand_threads<M, 32>()), smem, st, a, f, hot);
   } else if (pi == 5) {
-    LBFS_LAUNCH((k_expand<M, 64>), grid, kExpandThreads, smem, st, a, f, hot);
+    LBFS_LAUNCH((k_expand<M, 64>), grid, (expand_threads<M, 64>()), smem, st, a, f, hot);
   } else {
-    LBFS_LAUNCH((k_expand<M, 4>), grid, kExpandThreads, smem, st, a, f, hot);
+    LBFS_LAUNCH((k_expand<M, 4>), grid, (expand_threads<M, 4>()), smem, st, a, f, hot);
   }
 }
 
 void BfsEngine::launch_expand(int mode, int pi, unsigned grid, const LevelArgs& a, const Frontier& f,
                               cudaStream_t st) {
   if (mode == kHeavy)
-    launch_expand_m<kHeavy>(pi, grid, dyn_smem_, a, f, hot_words_, hub_ldg_, st);
+    launch_expand_m<kHeavy>(pi, grid, dyn_smem_, a, f, hot_words_, st);
   else if (mode == kBitmapOut)
-    launch_expand_m<kBitmapOut>(pi, grid, dyn_smem_, a, f, hot_words_, hub_ldg_, st);
+    launch_expand_m<kBitmapOut>(pi, grid, dyn_smem_, a, f, hot_words_, st);
   else
-    launch_expand_m<kQueueOut>(pi, grid, kRingBytes, a, f, 0, hub_ldg_, st);
+    launch_expand_m<kQueueOut>(pi, grid, 0, a, f, 0, st);
 }
 
 bool env_flag(const char* name) {
@@ -2149,7 +2018,6 @@ void BfsEngine::read_env() {
   dense_pct_ = (int)geti("LBFS_DENSE_PCT", 100 * kDenseNum / kDenseDenom);
   dense_min_elems_ = geti("LBFS_DENSE_MIN", kDenseMinElems);
   dense_warp_ = env_flag("LBFS_DENSE_WARP");
-  hub_ldg_ = env_flag("LBFS_HUB_LDG");
   sweep_off_ = env_flag("LBFS_NO_SWEEP");
   sweep_small_ = env_flag("LBFS_SWEEP_SMALL");
   refresh_chunks_ = (int)geti("LBFS_REFRESH", kRefreshChunks);

@@ -30,20 +30,7 @@ constexpr int kCounterRing = 3;
 #endif
 constexpr int kExpandWarps = LBFS_EXPAND_WARPS;
 constexpr int kExpandThreads = 32 * kExpandWarps;
-// Note: 128-element chunks (one 128-bit load per lane) produced missed
-// discoveries on S24 in round 1 while 256-element chunks are exact at ring
-// depths 2 and 4 (tools/debug_parity.py); cause not yet identified, so the
-// chunk stays at 256 elements.
-#ifndef LBFS_WARP_CHUNK
-#define LBFS_WARP_CHUNK 256
-#endif
-#ifndef LBFS_WARP_STAGES
-#define LBFS_WARP_STAGES 2
-#endif
-constexpr int kWarpChunk = LBFS_WARP_CHUNK;       // elements per warp-private bulk copy
-constexpr int kWarpStages = LBFS_WARP_STAGES;     // per-warp ring depth (stages-1 chunks in flight)
 constexpr int kRefreshChunks = 4;                 // hub chunks (warp 0) between snapshot refreshes
-constexpr int kRingBytes = kExpandWarps * kWarpStages * kWarpChunk * 4;  // per-warp rings
 
 // Per-level counters (K6). Slot L holds the frontier of level L:
 // discovered = |frontier| (layers[L].input), edges = sum of its degrees
@@ -221,6 +208,7 @@ struct ClusterArgs {
   Counters* ring;
   int64_t L0, max_levels;
   unsigned long long exit_edges;  // leave when a frontier has more edges
+  unsigned long long bitmap_min_edges;  // the host's next level is bitmap mode from this many edges
   int32_t* out_small[2];    // exit frontier (queue format) by level parity
   CtaItem* out_cta[2];
   QEntry* spill_small;      // [kMaxCluster][2][cap]
@@ -486,12 +474,14 @@ class BfsEngine {
   bool part_heavy_off_ = false;  // LBFS_PART_HEAVY=0
   bool count_ = false;
   bool split_ = false;
-  bool hub_ldg_ = false;  // LBFS_SPLIT=1: one launch per bin, timed separately
   cudaEvent_t ev_split_[7] = {};  // LBFS_COUNT=1: count bitmap-mode candidate writes (slow)
 };
 
 }  // namespace lbfs
 
+#include "multi.cuh"
+
 struct lbfs_graph {
-  lbfs::BfsEngine* eng = nullptr;
+  lbfs::BfsEngine* eng = nullptr;     // one GPU (or one partition, lbfs_part_*)
+  lbfs::MultiGraph* multi = nullptr;  // ngpus > 1: partitions on several devices of this process
 };

@@ -251,7 +251,7 @@ __device__ __forceinline__ void settle4(Ctx& x, const int32_t (&nb)[4], uint32_t
     wstamp(x, 3, lane);
   }
   if (!__any_sync(kF, win != 0)) return;
-  uint32_t small = 0;
+  uint32_t small = 0, big = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     if (!((win >> k) & 1u)) continue;
@@ -265,17 +265,44 @@ __device__ __forceinline__ void settle4(Ctx& x, const int32_t (&nb)[4], uint32_t
         prefetch_l2(p.col_idx + x.s->B[d] + (int64_t)(w - x.s->T[d + 1]) * d);
         prefetch_l2(p.new2old + w);
       }
-    } else {  // degree >= 32 (the cluster-wide list) or 0: records now (rare)
+    } else {  // degree >= 32 (the cluster-wide list) or 0: records now
       write_record<DSM>(p, QEntry{w, par[k]}, x.next_level);
-      if (w < p.t_warp) {
-        const int64_t st = p.row_ptr[w];
-        const int32_t d = (int32_t)(p.row_ptr[w + 1] - st);
-        x.edges += (unsigned long long)d;
-        const unsigned long long i = atomicAdd(p.big_cnt + x.big_slot, 1ull);
-        p.big[x.big_slot * p.cap + (int64_t)i] = CtaItem{st, d, __ldg(p.new2old + w)};
-        __threadfence();  // the entry is read by other CTAs after the (relaxed) level barrier
-      }
+      big |= (uint32_t)(w < p.t_warp) << k;
     }
+  }
+  if (__any_sync(kF, big != 0)) {
+    // rows of degree >= 32: the cluster-wide list, one reservation per warp;
+    // the entries are written with atomic exchanges (consumed, so performed
+    // before the relaxed level barrier; other CTAs read them next level)
+    int64_t st[4];
+    int32_t dg[4], uo[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool b = (big >> k) & 1u;
+      st[k] = b ? __ldg(p.row_ptr + nb[k]) : 0;
+      dg[k] = b ? (int32_t)(__ldg(p.row_ptr + nb[k] + 1) - st[k]) : 0;
+      uo[k] = b ? __ldg(p.new2old + nb[k]) : 0;
+    }
+    const uint32_t nbig = (uint32_t)__popc(big);
+    uint32_t incl = nbig;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kF, incl, o);
+      if (lane >= o) incl += t;
+    }
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(p.big_cnt + x.big_slot, (unsigned long long)incl);
+    base = __shfl_sync(kF, base, 31) + (incl - nbig);
+    unsigned long long sink = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (!((big >> k) & 1u)) continue;
+      x.edges += (unsigned long long)dg[k];
+      unsigned long long* e = reinterpret_cast<unsigned long long*>(p.big + x.big_slot * p.cap + (int64_t)base++);
+      sink |= atomicExch(e, (unsigned long long)st[k]);
+      sink |= atomicExch(e + 1, ((unsigned long long)(uint32_t)uo[k] << 32) | (uint32_t)dg[k]);
+    }
+    asm volatile("mov.b64 %0, %0;" : "+l"(sink));
   }
   // small winners join the next-level queue of the CTA owning their bitmap
   // sector (uniform over the cluster, so the frontier spreads over every CTA
@@ -682,12 +709,30 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
       // rows of degree >= 32 -> host slice items of <= qchunk edges
       const int64_t nb = (int64_t)__ldcg(p.big_cnt + L % kCounterRing);
       const CtaItem* bl = p.big + (L % kCounterRing) * p.cap;
-      for (int64_t j = (int64_t)x.rank * kCT + tid; j < nb; j += (int64_t)kCT * x.csize) {
-        const CtaItem it = bl[j];
-        const int items = (it.len + p.qchunk - 1) / p.qchunk;
-        const unsigned long long b = atomicAdd(&outc->bin[kBinCta], (unsigned long long)items);
-        for (int k = 0; k < items; ++k)
-          p.out_cta[cur][b + k] = CtaItem{it.start + (int64_t)k * p.qchunk, min(p.qchunk, it.len - k * p.qchunk), it.u};
+      // (a bitmap-mode next level takes kChunk-edge slices, a queue-mode one qchunk)
+      const int chunk = in_edges >= p.bitmap_min_edges ? kChunk : p.qchunk;
+      for (int64_t j0 = ((int64_t)x.rank * kCW + wib) * 32; j0 < nb; j0 += (int64_t)kCT * x.csize) {
+        const int64_t j = j0 + lane;
+        CtaItem it{0, 0, 0};
+        if (j < nb) it = bl[j];
+        const int items = j < nb ? (it.len + chunk - 1) / chunk : 0;
+        int incl = items;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(kF, incl, o);
+          if (lane >= o) incl += t;
+        }
+        unsigned long long b = 0;
+        if (lane == 31 && incl) b = atomicAdd(&outc->bin[kBinCta], (unsigned long long)incl);
+        b = __shfl_sync(kF, b, 31) + (unsigned long long)(incl - items);
+        for (int q = 0; q < 32; ++q) {  // the warp writes entry q's slices together
+          const int nq = __shfl_sync(kF, items, q);
+          const unsigned long long bq = __shfl_sync(kF, b, q);
+          const int64_t sq = __shfl_sync(kF, it.start, q);
+          const int32_t lq = __shfl_sync(kF, it.len, q), uq = __shfl_sync(kF, it.u, q);
+          for (int k = lane; k < nq; k += 32)
+            p.out_cta[cur][bq + k] = CtaItem{sq + (int64_t)k * chunk, min(chunk, lq - k * chunk), uq};
+        }
       }
     }
     cl_sync();  // (release: every store of the loop and the exit is performed)

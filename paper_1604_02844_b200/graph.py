@@ -152,6 +152,7 @@ class CsrGraph:
         self._adj = None
         self._sorted_rows = None
         self._handles = ([_device_csr], [None])  # (device CSR, BFS graph) handle boxes
+        self._gpus, self._partitioned = 1, False
         self._finalizer = weakref.finalize(self, CsrGraph._release, *self._handles)
 
     @staticmethod
@@ -228,13 +229,30 @@ class CsrGraph:
         return self._sorted_rows
 
     # -- device handle (the BFS layout) --------------------------------------
-    def device_handle(self) -> int:
+    def device_handle(self, gpus: int | None = None, partitioned: bool = False) -> int:
+        """The BFS graph handle, created on first use. ``gpus`` > 1 (or
+        ``partitioned``) builds the 1D-partitioned graph over devices
+        0..gpus-1 of this process (lbfs_graph_create_partitioned); a request
+        for another device count replaces the handle."""
         box = self._handles[1]
+        want = gpus if gpus is not None else (self._gpus if box[0] is not None else 1)
+        want_part = partitioned or want > 1
+        if box[0] is not None and (want != self._gpus or want_part != self._partitioned):
+            from . import traversal
+
+            traversal._release_handle(box[0])
+            box[0] = None
         if box[0] is None:
             h = ctypes.c_void_p()
             lib = _lib.load()
-            if self._handles[0][0]:
-                _lib.check(lib.lbfs_graph_create_from_csr(self._handles[0][0], 1, ctypes.byref(h)))
+            csr = self._handles[0][0]
+            if want_part:
+                if not csr:
+                    self._upload_csr()
+                    csr = self._handles[0][0]
+                _lib.check(lib.lbfs_graph_create_partitioned(csr, int(want), None, ctypes.byref(h)))
+            elif csr:
+                _lib.check(lib.lbfs_graph_create_from_csr(csr, 1, ctypes.byref(h)))
             else:
                 cs = np.ascontiguousarray(self._colstarts, dtype=np.int64)
                 rows = np.ascontiguousarray(self._rows, dtype=np.int32)
@@ -242,7 +260,23 @@ class CsrGraph:
                                                  _lib.ptr(rows) if len(rows) else None, len(rows), 1,
                                                  ctypes.byref(h)))
             box[0] = h.value
+            self._gpus, self._partitioned = int(want), bool(want_part)
         return box[0]
+
+    @property
+    def gpus(self) -> int:
+        return self._gpus if self._handles[1][0] is not None else 1
+
+    def _upload_csr(self) -> None:
+        """A device CSR from the host arrays (for the partitioned handle)."""
+        h = ctypes.c_void_p()
+        n = self.num_vertices
+        cs = np.ascontiguousarray(self._colstarts, dtype=np.int64)
+        rows = np.ascontiguousarray(self._rows, dtype=np.int32)
+        src = np.repeat(np.arange(n, dtype=np.uint32), np.diff(cs).astype(np.int64))
+        _lib.check(_lib.load().lbfs_csr_build(n, _lib.ptr(src), _lib.ptr(rows.view(np.uint32)) if len(rows) else None,
+                                              len(rows), 0, 0, ctypes.byref(h)))
+        self._handles[0][0] = h.value
 
     def release_device(self) -> None:
         """Free the device copies (they are rebuilt on the next BFS)."""

@@ -200,6 +200,13 @@ def _handle(g) -> int:
     return h.value
 
 
+def _release_handle(h: int) -> None:
+    """Flush a pending result's levels, then destroy the handle."""
+    with _handle_lock(h):
+        _flush(h)
+        _lib.load().lbfs_graph_destroy(h)
+
+
 def _destroy_foreign(h: int) -> None:
     with _handle_lock(h):
         _flush(h)

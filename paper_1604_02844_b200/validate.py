@@ -190,6 +190,10 @@ def validate_tree_device(g, s: int, pred) -> ValidationReport:
 
     n = g.num_vertices
     assert 0 <= s < n
+    if getattr(g, "_partitioned", False) and g._handles[1][0] is not None:
+        # a partitioned handle has no whole-graph layout on one device: the
+        # vectorised host validator (same checks, same report)
+        return validate_tree(g, s, pred.cpu().numpy() if hasattr(pred, "cpu") else pred)
     h = _handle(g)
     rep = (ctypes.c_int64 * 10)()
     lib = _lib.load()

@@ -248,7 +248,7 @@ def main():
         "lattice_big": lambda: make_lattice(out, arrays, 4096, 4096, 16, 2, False),
     }
     if args.big:
-        steps = {"S24": lambda: make_config(out, arrays, 24, 64, 2, "vectorized", False)}
+        steps = {"S24": lambda: make_config(out, arrays, 24, 64, 4, "vectorized", False)}
     for name, fn in steps.items():
         if args.only and name not in args.only.split(","):
             continue

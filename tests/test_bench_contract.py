@@ -36,12 +36,14 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_device_arm_line():
-    d = run_bench("--scale", "16", "--steps", "3", "--warmup", "3", "--roots", "8", "--e2e-roots", "4",
-                  "--cpu-budget", "1")
+    d = run_bench("--scale", "16", "--steps", "3", "--warmup", "3", "--roots", "8", "--cpu-budget", "1",
+                  "--no-extra-configs")
     assert BASE_KEYS <= set(d)
-    assert d["value"] > 0 and d["config"]["validated"] is True
+    assert d["value"] > 0 and d["config"]["validated_trees"] == 3 * 8  # every timed tree
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert r["ms_per_bfs"] > 0 and r["expansion"]["ms_per_bfs"] > 0
+    assert d["cpu_baseline"]["cpu_model"]
     assert d["e2e"]["d2h_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
     assert d["gpu_launches"] > 0 and "clocks" in d and d["cpu_baseline"]["value"] > 0
     assert d["direction_optimizing"]["layers_equal_top_down"] is True

@@ -1,5 +1,5 @@
 """The BASELINE.json configs on the device, against the reference's golden
-vectors (S16, S20, lattices) and the pinned oracle at full size (S24)."""
+vectors (S16, S20, S24, lattices) and the pinned oracle at full size."""
 
 import numpy as np
 import pytest
@@ -7,6 +7,8 @@ import pytest
 import oracle
 from _util import sha
 from paper_1604_02844_b200 import RmatParams, bfs, build_lattice_graph, build_rmat_graph, pick_roots
+from paper_1604_02844_b200.traversal import SENTINEL
+from paper_1604_02844_b200.validate import validate_tree_device
 
 pytestmark = pytest.mark.gpu
 
@@ -59,38 +61,53 @@ def test_config_lattice_small(golden):
         assert sha(res.levels, "<i4") == want["levels_sha"]
 
 
-def test_config_lattice_4096(golden):
+def test_config_lattice_4096_all_16_roots(golden):
+    """BASELINE configs[3]: all 16 roots bit-exact with the oracle (levels and
+    layers), the 2 roots the reference itself ran with its layer tallies,
+    every tree through the device validator, 4 through the certificate."""
     info = golden["lattice_4096x4096"]
     g = build_lattice_graph(4096, 4096)
     rp, ci = g.colstarts, g.rows
     roots = pick_roots(g, 16, 1, filter_unconnected=True).tolist()
     assert roots == info["roots"]
-    for r, want in info["bfs"].items():
-        res = bfs(g, int(r))
-        assert layers_of(res) == want["layers"]
-        assert oracle.check_bfs(rp, ci, int(r), res.predecessors.p, res.levels) == (0, -1)
-    r = roots[5]
-    res = bfs(g, r)
-    _, lvl, layers = oracle.bfs_parallel(rp, ci, r)
-    assert np.array_equal(res.levels, lvl) and layers_of(res) == [list(x) for x in layers]
+    for i, r in enumerate(roots):
+        res = bfs(g, r)
+        _, lvl, layers = oracle.bfs_parallel(rp, ci, r)
+        assert np.array_equal(res.levels, lvl), r
+        assert layers_of(res) == [list(x) for x in layers], r
+        assert validate_tree_device(g, r, res.predecessors).passed, r
+        if str(r) in info["bfs"]:
+            assert layers_of(res) == info["bfs"][str(r)]["layers"]
+        if i < 4:
+            assert oracle.check_bfs(rp, ci, r, res.predecessors.p, res.levels) == (0, -1), r
 
 
-def test_config_s24_against_oracle(golden):
+def test_config_s24_all_64_roots(golden):
+    """BASELINE configs[2]: every one of the 64 benchmark roots. Levels and
+    layers bit-exact with the oracle's bfs_parallel (pinned to the reference
+    at S4-S20) and, for the 4 roots make_golden.py ran through the reference
+    itself at S24 (bfs_vectorized + levels_from_parents), with the reference's
+    layer tallies and level-array hash; every tree passes the reference's five
+    validate_tree checks on the device, 8 of them the O(E) BFS certificate."""
+    info = golden["S24"]
     g = build_rmat_graph(RmatParams(scale=24, seed=1))
     rp, ci = g.colstarts, g.rows
     roots = pick_roots(g, 64, 1, filter_unconnected=True).tolist()
-    info = golden.get("S24")
-    if info:
-        assert roots == info["roots"]
-    for r in roots[:3]:
+    assert roots == info["roots"]
+    for i, r in enumerate(roots):
         res = bfs(g, r)
         _, lvl, layers = oracle.bfs_parallel(rp, ci, r)
-        assert np.array_equal(res.levels, lvl)
-        assert layers_of(res) == [list(x) for x in layers]
-        assert oracle.check_bfs(rp, ci, r, res.predecessors.p, res.levels) == (0, -1)
-        if info and str(r) in info["bfs"]:
-            assert layers_of(res) == info["bfs"][str(r)]["layers"]
-            assert sha(res.levels, "<i4") == info["bfs"][str(r)]["levels_sha"]
+        assert np.array_equal(res.levels, lvl), r
+        assert layers_of(res) == [list(x) for x in layers], r
+        assert res.traversed_edge_count == sum(x[1] for x in layers)
+        assert validate_tree_device(g, r, res.predecessors).passed, r
+        if str(r) in info["bfs"]:
+            want = info["bfs"][str(r)]
+            assert layers_of(res) == want["layers"]
+            assert sha(res.levels, "<i4") == want["levels_sha"]
+            assert int((res.predecessors.p != SENTINEL).sum()) == want["reached"]
+        if i < 8:
+            assert oracle.check_bfs(rp, ci, r, res.predecessors.p, res.levels) == (0, -1), r
 
 
 @pytest.fixture(params=["dsmem", "global"])

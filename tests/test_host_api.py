@@ -156,9 +156,10 @@ def test_experiment_config_and_emit(tmp_path):
     st = RunStats(cfg, "gpu", 1, "device", runs, 266.6, 0, False, 0.25, 0.5, 0.375)
     emit_results([st], "csv", tmp_path / "r.csv")
     rows = list(csv.reader(open(tmp_path / "r.csv")))
+    # the reference's columns (harness.py:278-280), then the device's
     assert rows[0] == ["scale", "edgefactor", "seed", "mode", "threads", "placement", "root", "time_s",
-                       "edges", "teps"]
-    assert rows[-1][6] == "all" and rows[-1][8] == "200"
+                       "edges", "teps", "gpus", "gbytes_alg", "roofline_frac"]
+    assert rows[-1][6] == "all" and rows[-1][8] == "200" and rows[-1][10] == "1"
     emit_results([st], "json", tmp_path / "r.json")
     assert json.loads((tmp_path / "r.json").read_text())["results"][0]["mode"] == "gpu"
 

@@ -16,14 +16,12 @@ import torch
 n = g.num_vertices
 pred = torch.empty((n + 31) // 32 * 32, dtype=torch.int32, device="cuda")
 lvl = torch.empty(n, dtype=torch.int32, device="cuda")
-trace = {k: os.environ.pop(k) for k in ("LBFS_TRACE", "LBFS_SPLIT", "LBFS_COUNT") if k in os.environ}
 t = time.time()
 k = 0
 while time.time() - t < float(os.environ.get("WARM_S", "1.5")):
     bfs_device(g, roots[k % len(roots)], pred, lvl)
     k += 1
 print(f"warm-up: {k} BFS", flush=True)
-os.environ.update(trace)
 times = []
 for r in roots:
     res = bfs_device(g, r, pred, lvl)
