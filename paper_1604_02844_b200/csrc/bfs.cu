@@ -73,9 +73,6 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
   do {                          \
   } while (0)
 #endif
-#ifndef LBFS_QUEUE_ROWS_STREAMED
-#define LBFS_QUEUE_ROWS_STREAMED 0  // warp-bin queue rows through stream_slices (experiment)
-#endif
 
 // ---------------------------------------------------------------- memory ops
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
@@ -533,12 +530,18 @@ __device__ __forceinline__ CtaItem ld_item(const CtaItem* p) {
   return c;
 }
 
-// A warp walks row slices (grid-stride over items) in 128-element chunks of
-// one 128-bit load per lane; the loads of chunk i+1 are issued before chunk
-// i is probed.
+// A warp walks row slices (grid-stride over items) in groups of D
+// 128-element windows, one 128-bit load per lane per window; the next
+// group's D loads are issued before the current group is probed, so a warp
+// keeps 2 x D x 512 B in flight (D = 4 for heavy levels, whose per-element
+// work is light; 2 where the settle path needs the registers).
+template <int M>
+constexpr int slice_depth() { return M == kHeavy || M == kQueueOut ? 4 : 2; }
+
 template <int M, typename Fetch>
 __device__ __forceinline__ void stream_slices_f(const LevelArgs& a, const Hot& h, Fetch fetch, int64_t n,
                                                 int64_t gwarp, int64_t nwarps, int lane, Acc& acc) {
+  constexpr int D = slice_depth<M>();
   if (gwarp >= n) return;
   int64_t it = gwarp;
   CtaItem cur = fetch(it);
@@ -547,16 +550,20 @@ __device__ __forceinline__ void stream_slices_f(const LevelArgs& a, const Hot& h
   CtaItem nxt = it + nwarps < n ? fetch(it + nwarps) : CtaItem{0, 0, 0};
   int64_t pos = cur.start & ~int64_t(3);
   int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
-  auto load = [&](int64_t p0, int64_t e0) {
-    const int64_t i1 = p0 + lane * 4;
-    LBFS_DCHECK(!(i1 < e0) || (i1 >= 0 && i1 + 4 <= a.chk_nnz + 8), "slice load");
-    return i1 < e0 ? ld_stream4(a.col_idx + i1) : make_int4(0, 0, 0, 0);
+  auto load_group = [&](int64_t p0, int64_t e0, int4 (&x)[D]) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int64_t i1 = p0 + d * 128 + lane * 4;
+      LBFS_DCHECK(!(i1 < e0) || (i1 >= 0 && i1 + 4 <= a.chk_nnz + 8), "slice load");
+      x[d] = i1 < e0 ? ld_stream4(a.col_idx + i1) : make_int4(0, 0, 0, 0);
+    }
   };
-  int4 x = load(pos, end);
+  int4 xa[D];
+  load_group(pos, end, xa);
   while (true) {
-    const int64_t cbase = pos;
+    const int64_t gbase = pos;
     const CtaItem ci = cur;
-    pos += 128;
+    pos += D * 128;
     bool more = true;
     if (pos >= end) {
       it += nwarps;
@@ -569,24 +576,36 @@ __device__ __forceinline__ void stream_slices_f(const LevelArgs& a, const Hot& h
         more = false;
       }
     }
-    const int4 nx = more ? load(pos, end) : make_int4(0, 0, 0, 0);
-    int32_t nb[4] = {x.x, x.y, x.z, x.w};
-    const int lo = (int)(ci.start - cbase) - lane * 4, hi = (int)(ci.start + ci.len - cbase) - lane * 4;
-    uint32_t okm = 0xFu;
-    if (lo > 0 || hi < 4) {  // first/last chunk of a slice
-      okm = 0;
+    int4 xb[D];
+    if (more) {
+      load_group(pos, end, xb);
+    } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool ok = q >= lo && q < hi;
-        okm |= (uint32_t)ok << q;
-        nb[q] = ok ? nb[q] : 0;
-      }
+      for (int d = 0; d < D; ++d) xb[d] = make_int4(0, 0, 0, 0);
     }
     const int32_t pu = ci.u;
-    if (a.dbg) atomicAdd(a.dbg + 2, (unsigned long long)__popc(okm));  // LBFS_COUNT: slice elements
-    probe_batch<M, 4>(a, h, nb, okm, [&](int) { return pu; }, lane, acc);
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int64_t cbase = gbase + d * 128;
+      if (cbase >= ci.start + ci.len) break;  // (warp-uniform) past the slice
+      int32_t nb[4] = {xa[d].x, xa[d].y, xa[d].z, xa[d].w};
+      const int lo = (int)(ci.start - cbase) - lane * 4, hi = (int)(ci.start + ci.len - cbase) - lane * 4;
+      uint32_t okm = 0xFu;
+      if (lo > 0 || hi < 4) {  // first/last window of a slice
+        okm = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool ok = q >= lo && q < hi;
+          okm |= (uint32_t)ok << q;
+          nb[q] = ok ? nb[q] : 0;
+        }
+      }
+      if (a.dbg) atomicAdd(a.dbg + 2, (unsigned long long)__popc(okm));  // LBFS_COUNT: slice elements
+      probe_batch<M, 4>(a, h, nb, okm, [&](int) { return pu; }, lane, acc);
+    }
     if (!more) break;
-    x = nx;
+#pragma unroll
+    for (int d = 0; d < D; ++d) xa[d] = xb[d];
   }
 }
 
@@ -802,26 +821,20 @@ __device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier
   // ---- phase 3: raw warp/small queues (after a queue-mode level): a warp
   // takes one warp-bin vertex or 32 small-bin vertices ---------------------
   if (phases & 4) {
-#if LBFS_QUEUE_ROWS_STREAMED
-    stream_queue_rows<M>(a, h, f.warp, f.n_warp, gwarp, nwarps, lane, acc);
-    const int64_t ng = (f.n_small + 31) / 32;
+    // heavy levels: warp-bin rows streamed like slices (the next row's
+    // descriptor and D windows in flight), then the small rows by 32
+    const bool rows_streamed = false;  // (streamed rows: 334 vs 370 GTEPS on S24; kept off)
+    if (rows_streamed) stream_queue_rows<M>(a, h, f.warp, f.n_warp, gwarp, nwarps, lane, acc);
+    const int64_t n_warp = rows_streamed ? 0 : f.n_warp;
+    const int64_t ng = n_warp + (f.n_small + 31) / 32;
     for (int64_t g = gwarp; g < ng; g += nwarps) {
-      const int64_t base = g * 32;
-      const int n = (int)std::min<int64_t>(32, f.n_small - base);
-      const int32_t v = lane < n ? __ldcg(f.small + base + lane) : 0;
-      expand_range<M>(a, h, n, v, 0, 1 << 30, s_T, s_B, lane, ws, acc);
-    }
-#else
-    const int64_t ng = f.n_warp + (f.n_small + 31) / 32;
-    for (int64_t g = gwarp; g < ng; g += nwarps) {
-      const bool wb = g < f.n_warp;
-      const int64_t base = wb ? g : (g - f.n_warp) * 32;
+      const bool wb = g < n_warp;
+      const int64_t base = wb ? g : (g - n_warp) * 32;
       const int n = wb ? 1 : (int)std::min<int64_t>(32, f.n_small - base);
       const int32_t v = lane < n ? __ldcg((wb ? f.warp : f.small) + base + lane) : 0;
       LBFS_DCHECK(!(lane < n) || (v >= 0 && (int64_t)v < a.chk_n), "queue entry");
       expand_range<M>(a, h, n, v, 0, 1 << 30, s_T, s_B, lane, ws, acc);
     }
-#endif
   }
 }
 
@@ -832,7 +845,7 @@ __device__ __forceinline__ void expand_phases(const LevelArgs& a, const Frontier
 // (So do the bitmap-mode group items: their double-buffered windows plus the
 // parent stores spill at 64 registers.)
 template <int M, int kPhases>
-constexpr int expand_threads() { return (M == kQueueOut || (M == kBitmapOut && kPhases == 2)) ? 512 : kExpandThreads; }
+constexpr int expand_threads() { return (M == kQueueOut || M == kBitmapOut) ? 512 : kExpandThreads; }
 
 template <int M, int kPhases>
 __global__ void __launch_bounds__(expand_threads<M, kPhases>(), 1) k_expand(LevelArgs a, Frontier f, int32_t hot_words) {
@@ -1888,7 +1901,9 @@ __global__ void __launch_bounds__(256) k_resolve(const int32_t* __restrict__ lev
                                                  int64_t n, int32_t lvl) {
   const int64_t n4 = (n + 3) / 4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    const int4 l4 = __ldg(reinterpret_cast<const int4*>(level_int) + i);  // (level_int is padded to 4)
+    // (plain L2 loads: later levels keep writing level_int while this runs on
+    // the side stream; the entries compared here were written before it)
+    const int4 l4 = __ldcg(reinterpret_cast<const int4*>(level_int) + i);  // (level_int is padded to 4)
     const int32_t lv4[4] = {l4.x, l4.y, l4.z, l4.w};
     bool need[4];
     int32_t u[4];
@@ -1899,7 +1914,7 @@ __global__ void __launch_bounds__(256) k_resolve(const int32_t* __restrict__ lev
     }
     int32_t lu[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) lu[q] = need[q] ? __ldg(level_int + u[q]) : 0;
+    for (int q = 0; q < 4; ++q) lu[q] = need[q] ? __ldcg(level_int + u[q]) : 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (!need[q]) continue;
@@ -1911,7 +1926,7 @@ __global__ void __launch_bounds__(256) k_resolve(const int32_t* __restrict__ lev
         const int64_t e = __ldg(row_ptr + v + 1);
         for (int64_t k = __ldg(row_ptr + v) + 1; k < e; ++k) {
           const int32_t x = __ldg(col_idx + k);
-          if (__ldg(level_int + x) == lvl - 1) {
+          if (__ldcg(level_int + x) == lvl - 1) {
             par = __ldg(new2old + x);
             break;
           }
@@ -2014,6 +2029,7 @@ void BfsEngine::read_env() {
   bitmap_floor_ = std::max<long long>(1, geti("LBFS_BITMAP_MIN", (long long)1 << 16));
   sweep_min_pct_ = (int)geti("LBFS_SWEEP_MIN", kSweepMinPct);
   heavy_div_ = (int)geti("LBFS_HEAVY_DIV", kHeavyDiv);  // heavy (blind-OR) from nnz / this edges (0: off)
+  heavy_vis_pct_ = (int)geti("LBFS_HEAVY_VIS", 0);     // ... while visited edge mass <= this % of the frontier's (0: off)
   dense_off_ = env_flag("LBFS_NO_DENSE");
   dense_pct_ = (int)geti("LBFS_DENSE_PCT", 100 * kDenseNum / kDenseDenom);
   dense_min_elems_ = geti("LBFS_DENSE_MIN", kDenseMinElems);
@@ -2124,8 +2140,14 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       bottom_up = prev_bu ? c.discovered * (unsigned long long)bu_beta_ >= (unsigned long long)n_
                           : c.edges * (unsigned long long)bu_alpha_ > m_u;
     }
+    // heavy (blind-OR) semantics pay off while most targets are unvisited:
+    // the edge mass of the vertices visited before this frontier (each was
+    // one frontier once) stays below heavy_vis_pct_ % of the frontier's own
+    unsigned long long seen_before = 0;
+    for (const auto& l : layers_) seen_before += (unsigned long long)l.edges;
     const bool heavy = !bottom_up && bitmap && stage_ && heavy_div_ > 0 &&
-                       c.edges * (unsigned long long)heavy_div_ >= (unsigned long long)nnz_;
+                       c.edges * (unsigned long long)heavy_div_ >= (unsigned long long)nnz_ &&
+                       (heavy_vis_pct_ <= 0 || seen_before * 100ull <= c.edges * (unsigned long long)heavy_vis_pct_);
     LBFS_CUDA(cudaEventRecord(ev_[2], st));
     const unsigned grid = bottom_up ? bottom_up_level(c, prev_bitmap, cur, st)
                                     : expand_level(a, c, heavy ? kHeavy : bitmap ? kBitmapOut : kQueueOut, prev_bitmap,

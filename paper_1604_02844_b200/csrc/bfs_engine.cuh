@@ -462,6 +462,7 @@ class BfsEngine {
   bool side_pending_ = false;
   bool sweep_small_ = false;     // LBFS_SWEEP_SMALL=1: sweep the small region as well (slower today)
   int heavy_div_ = kHeavyDiv;    // heavy when a bitmap level's edges >= nnz / heavy_div_ (0: off)
+  int heavy_vis_pct_ = 0;        // ... and the visited edge mass <= this % of the frontier's (0: no limit)
   int dyn_smem_ = 0;
   bool trace_ = false;  // LBFS_TRACE=1: per-level table on stderr
   int sweep_min_pct_ = kSweepMinPct;
