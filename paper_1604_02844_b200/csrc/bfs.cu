@@ -1455,7 +1455,8 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   expand_grid_ = sm_count_ * std::max(occ, 1);
   if (nparts_ > 1 && hot_words_ >= 4) {  // partitions: heavy levels without the sweep
     sweep_hot_words_ = hot_words_;
-    stage_ = dev_alloc<uint32_t>((size_t)expand_grid_ * hot_words_);
+    stage_words_ = hot_words_;
+    stage_ = dev_alloc<uint32_t>((size_t)expand_grid_ * stage_words_);
   }
   if (nparts_ == 1 && hot_words_ >= 4) {
     // the sweep has no per-warp rings: its hot prefix takes what its own ring leaves
@@ -1464,8 +1465,14 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
     const int64_t sw_avail = (int64_t)optin - (int64_t)fs.sharedSizeBytes - kSweepRingBytes;
     sweep_hot_words_ = (int32_t)std::max<int64_t>(
         hot_words_, std::min<int64_t>((sw_avail / 4) & ~int64_t(3), (nwords_ + 3) & ~int64_t(3)));
-    if (getenv("LBFS_SWEEP_HOT_SAME")) sweep_hot_words_ = hot_words_;  // (experiment)
-    stage_ = dev_alloc<uint32_t>((size_t)expand_grid_ * sweep_hot_words_);
+    // the window stream keeps nothing but the hot prefix in shared memory
+    stream_hot_words_ = (int32_t)std::min<int64_t>((((int64_t)optin - 1024) / 4) & ~int64_t(3),
+                                                   (nwords_ + 3) & ~int64_t(3));
+    stage_words_ = std::max(sweep_hot_words_, stream_hot_words_);
+    stage_ = dev_alloc<uint32_t>((size_t)expand_grid_ * stage_words_);
+    LBFS_CUDA(cudaFuncSetAttribute((const void*)k_stream_heavy<kStreamDepth>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, stream_hot_words_ * 4));
+    if (n_side_win_ > 0) wmask_ = dev_alloc<uint4>((size_t)n_side_win_);
     sweep_fits_ = (int64_t)fs.sharedSizeBytes + kSweepRingBytes + (int64_t)sweep_hot_words_ * 4 <= optin;
     if (sweep_fits_)
       LBFS_CUDA(cudaFuncSetAttribute((const void*)k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1632,6 +1639,7 @@ BfsEngine::~BfsEngine() {
   dev_free(side_);
   dev_free(first_nbr_);
   dev_free(svmask_);
+  dev_free(wmask_);
   dev_free(sdesc_);
   dev_free(pred_int_);
   dev_free(level_int_);
@@ -1771,7 +1779,8 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
   const bool bitmap = mode != kQueueOut;
   a.stage = stage_;
   a.stage_first = 1;
-  a.stage_words = sweep_hot_words_;
+  a.stage_words = stage_words_;
+  merge_words_ = hot_words_;
   a.next_level = (int32_t)(L + 1);
   a.next_cnt = &cnt_[(L + 1) % kCounterRing];
   a.next_small = q_small_[cur ^ 1];
@@ -1819,13 +1828,50 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
                                   (f.n_warp + (f.n_small + 31) / 32 + kExpandWarps - 1) / kExpandWarps,
                                   (int64_t)1});
   const unsigned grid = bitmap ? (unsigned)expand_grid_ : clamp_grid(need, expand_grid_);
+  // heavy level: the whole CSR as one window stream (stream.cu): the frontier
+  // bitmap (from the queues after a queue-mode level), the windows' valid
+  // masks, then k_stream_heavy; no per-bin launches
+  if (mode == kHeavy && stream_on_ && nparts_ == 1 && wmask_) {
+    if (!prev_bitmap) {
+      LBFS_CUDA(cudaMemsetAsync(front_, 0, sizeof(uint32_t) * (size_t)nwords_, st));
+      const int64_t ns = (int64_t)c.bin[kBinSmall], nw = (int64_t)c.bin[kBinWarp], nc = (int64_t)c.bin[kBinCta];
+      LBFS_LAUNCH(k_front_from_queues, clamp_grid((ns + nw + nc + 255) / 256, (int64_t)sm_count_ * 8), 256, 0, st,
+                  front_, q_small_[cur], ns, q_warp_[cur], nw, q_cta_[cur], nc, old2new_);
+    }
+    const int64_t nsw = svmask_ ? n_win_all_ - w_small0_ : 0;
+    if (nsw > 0)
+      LBFS_LAUNCH(k_sweep_plan_small, (unsigned)((nsw + 63) / 64), 256, 0, st, classes_, sdesc_, front_, e_nz_,
+                  w_small0_, nsw, svmask_);
+    LBFS_LAUNCH(k_window_masks, clamp_grid((n_side_win_ + 255) / 256, (int64_t)sm_count_ * 8), 256, 0, st, side_,
+                n_side_win_, e_big_, front_, nsw > 0 ? svmask_ : nullptr, w_small0_, wmask_);
+    StreamArgs sa{col_idx_, wmask_, svmask_, n_win_all_, n_side_win_, w_small0_, visited_, stage_, stage_words_,
+                  stream_hot_words_};
+    LBFS_LAUNCH(k_stream_heavy<kStreamDepth>, (unsigned)sm_count_, kStreamThreads, stream_hot_words_ * 4, st, sa);
+    merge_words_ = stream_hot_words_;
+    sweep_used_ = true;
+    split_any_ = true;
+    return (unsigned)sm_count_;
+  }
   // heavy level after a bitmap level: the big-row region is swept whole (sweep.cu)
   // (only when the frontier's big rows hold enough of the region's edges:
   // below that the sweep streams mostly rows outside the frontier)
-  const bool sweep = mode == kHeavy && nparts_ == 1 && prev_bitmap && side_ && sweep_fits_ && !sweep_off_ &&
-                     c.big_edges * 100ull >= (unsigned long long)e_big_ * (unsigned long long)sweep_min_pct_;
+  // after a queue-mode level (opt-in experiment, LBFS_SWEEP_AFTER_QUEUE): the
+  // frontier bitmap is rebuilt from the queues and the hub + warp-bin rows
+  // (the big-row region) are swept; the small queue keeps its own launch
+  const bool from_queues = mode == kHeavy && !prev_bitmap && sweep_after_queue_;
+  const bool sweep = mode == kHeavy && nparts_ == 1 && (prev_bitmap || from_queues) && side_ && sweep_fits_ &&
+                     !sweep_off_ &&
+                     (from_queues ||
+                      c.big_edges * 100ull >= (unsigned long long)e_big_ * (unsigned long long)sweep_min_pct_);
+  if (sweep && from_queues) {
+    LBFS_CUDA(cudaMemsetAsync(front_, 0, sizeof(uint32_t) * (size_t)nwords_, st));
+    const int64_t nw = (int64_t)c.bin[kBinWarp], nc = (int64_t)c.bin[kBinCta];
+    LBFS_LAUNCH(k_front_from_queues, clamp_grid((nw + nc + 255) / 256, (int64_t)sm_count_ * 8), 256, 0, st, front_,
+                q_small_[cur], 0, q_warp_[cur], nw, q_cta_[cur], nc, old2new_);
+    f.n_warp = 0;  // (the warp-bin rows are in the swept region)
+  }
   sweep_used_ = sweep;
-  merge_wide_ = sweep;
+  if (sweep) merge_words_ = sweep_hot_words_;
   if (sweep) {
     if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[0], st));
     // (window infos are computed by the sweep's producers from the side entries and front_)
@@ -1840,7 +1886,7 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
     SweepArgs sa{col_idx_, side_, n_side_win_, e_big_, sweep_small ? n_win_all_ : n_side_win_,
                  sweep_small ? e_nz_ : e_big_, sweep_small ? w_small0_ : n_win_all_ + 1, svmask_, front_,
                  visited_, pred_int_, new2old_loc_,
-                 stage_, 1, sweep_hot_words_, getenv("LBFS_SWEEP_PF") ? atoi(getenv("LBFS_SWEEP_PF")) : kSweepPrefetch,
+                 stage_, 1, stage_words_, sweep_hot_words_, getenv("LBFS_SWEEP_PF") ? atoi(getenv("LBFS_SWEEP_PF")) : kSweepPrefetch,
                  getenv("LBFS_SWEEP_DBG") ? atoi(getenv("LBFS_SWEEP_DBG")) : 0};
     LBFS_LAUNCH(k_sweep, (unsigned)expand_grid_, kSweepThreads, kSweepRingBytes + sweep_hot_words_ * 4, st, sa);
     a.stage_first = 0;
@@ -1894,16 +1940,18 @@ void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t 
 // the first neighbour one level up; rows are sorted by internal id, i.e. by
 // descending degree, and the first entry is almost always it (else scan on).
 // Any such neighbour is a valid parent (traversal.py:145-147).
-__global__ void __launch_bounds__(256) k_resolve(const int32_t* __restrict__ level_int,
+__global__ void __launch_bounds__(256) k_resolve(const int32_t* level_int,
                                                  const int32_t* __restrict__ first_nbr,
                                                  const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                                                  const int32_t* __restrict__ new2old, int32_t* __restrict__ pred_int,
                                                  int64_t n, int32_t lvl) {
   const int64_t n4 = (n + 3) / 4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    // (plain L2 loads: later levels keep writing level_int while this runs on
-    // the side stream; the entries compared here were written before it)
-    const int4 l4 = __ldcg(reinterpret_cast<const int4*>(level_int) + i);  // (level_int is padded to 4)
+    // (plain loads, not the read-only path: later levels keep writing
+    // level_int while this runs on the side stream; the entries compared here
+    // were written before it, and a concurrent write only ever stores a level
+    // above lvl, so a stale view cannot make a wrong match)
+    const int4 l4 = reinterpret_cast<const int4*>(level_int)[i];  // (level_int is padded to 4)
     const int32_t lv4[4] = {l4.x, l4.y, l4.z, l4.w};
     bool need[4];
     int32_t u[4];
@@ -1914,7 +1962,7 @@ __global__ void __launch_bounds__(256) k_resolve(const int32_t* __restrict__ lev
     }
     int32_t lu[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) lu[q] = need[q] ? __ldcg(level_int + u[q]) : 0;
+    for (int q = 0; q < 4; ++q) lu[q] = need[q] ? level_int[u[q]] : 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (!need[q]) continue;
@@ -1926,7 +1974,7 @@ __global__ void __launch_bounds__(256) k_resolve(const int32_t* __restrict__ lev
         const int64_t e = __ldg(row_ptr + v + 1);
         for (int64_t k = __ldg(row_ptr + v) + 1; k < e; ++k) {
           const int32_t x = __ldg(col_idx + k);
-          if (__ldcg(level_int + x) == lvl - 1) {
+          if (level_int[x] == lvl - 1) {
             par = __ldg(new2old + x);
             break;
           }
@@ -1939,10 +1987,10 @@ __global__ void __launch_bounds__(256) k_resolve(const int32_t* __restrict__ lev
 
 void BfsEngine::merge_hot(cudaStream_t st) {
   // (the sweep stores whole rows first in its level; expand kernels alone write only their prefix)
-  const int hw4 = (merge_wide_ ? sweep_hot_words_ : hot_words_) / 4;
+  const int hw4 = merge_words_ / 4;
   const dim3 grid((unsigned)((hw4 + 255) / 256), (unsigned)((expand_grid_ + kMergeRows - 1) / kMergeRows));
   LBFS_LAUNCH(k_merge_hot, grid, 256, 0, st, reinterpret_cast<const uint4*>(stage_), expand_grid_, hw4,
-              sweep_hot_words_ / 4, visited_);
+              stage_words_ / 4, visited_);
 }
 
 // Output pass: parents (pad32(n), SENTINEL padding) and, when asked for,
@@ -2035,6 +2083,8 @@ void BfsEngine::read_env() {
   dense_min_elems_ = geti("LBFS_DENSE_MIN", kDenseMinElems);
   dense_warp_ = env_flag("LBFS_DENSE_WARP");
   sweep_off_ = env_flag("LBFS_NO_SWEEP");
+  stream_on_ = geti("LBFS_STREAM", 0) != 0;  // (experiment: the full-CSR window stream; slower today)
+  sweep_after_queue_ = env_flag("LBFS_SWEEP_AFTER_QUEUE");
   sweep_small_ = env_flag("LBFS_SWEEP_SMALL");
   refresh_chunks_ = (int)geti("LBFS_REFRESH", kRefreshChunks);
   qchunk_ = (int)std::min<long long>(kChunk, std::max<long long>(kQChunkMin, geti("LBFS_QCHUNK", kQChunkDefault))) & ~3;

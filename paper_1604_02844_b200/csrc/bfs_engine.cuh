@@ -264,10 +264,32 @@ struct SweepArgs {
   const int32_t* new2old;
   uint32_t* stage;          // per-CTA rows of the hot prefix (see LevelArgs::stage)
   int32_t stage_first;
+  int32_t stage_words;      // row stride of stage
   int32_t hot_words;
   int32_t prefetch;         // L2 prefetch distance in chunks of a CTA (0: off)
   int32_t dbg_flags;        // LBFS_SWEEP_DBG (experiments; wrong results): 1 no hot ORs, 2 no cold probes
 };
+// Heavy levels as one window stream over [0, e_nz) (stream.cu).
+constexpr int kStreamThreads = 1024;
+#ifndef LBFS_STREAM_DEPTH
+#define LBFS_STREAM_DEPTH 2
+#endif
+constexpr int kStreamDepth = LBFS_STREAM_DEPTH;  // windows per group (two groups in flight per warp)
+struct StreamArgs {
+  const int32_t* col_idx;
+  const uint4* wmask;     // valid masks of the big-row windows [0, nwin_big)
+  const uint4* svmask;    // ... of the small-row windows [w_small0, nwin)
+  int64_t nwin, nwin_big, w_small0;
+  uint32_t* visited;
+  uint32_t* stage;        // per-CTA rows of the hot prefix (LevelArgs::stage)
+  int32_t stage_words;
+  int32_t hot_words;
+};
+__global__ void k_window_masks(const uint2* side, int64_t nwin, int64_t e_big, const uint32_t* front,
+                               const uint4* svmask, int64_t w_small0, uint4* wmask);
+template <int D>
+__global__ void k_stream_heavy(const __grid_constant__ StreamArgs s);
+
 struct BottomUpArgs {
   const int64_t* row_ptr;
   const int32_t* col_idx;
@@ -445,8 +467,13 @@ class BfsEngine {
   long long cl_prof_level_ = -1;
   unsigned long long* cl_prof_buf_ = nullptr;
   int32_t hot_words_ = 0;  // visited words mirrored in shared memory
-  int32_t sweep_hot_words_ = 0;  // the sweep's (longer) hot prefix; also the stage row stride
-  bool merge_wide_ = false;      // this level's stage rows hold the sweep's prefix
+  int32_t sweep_hot_words_ = 0;  // the sweep's (longer) hot prefix
+  int32_t stream_hot_words_ = 0; // k_stream_heavy's hot prefix (longest: no ring next to it)
+  int32_t stage_words_ = 0;      // stage row stride (>= every kernel's hot prefix)
+  int32_t merge_words_ = 0;      // hot words written to the stage rows by this level's kernels
+  uint4* wmask_ = nullptr;       // k_stream_heavy: valid masks of the big-row windows
+  bool stream_on_ = false;       // LBFS_STREAM=1: heavy levels as one full-CSR window stream (experiment)
+  bool sweep_after_queue_ = false;  // LBFS_SWEEP_AFTER_QUEUE=1: sweep heavy levels that follow a queue level
   uint32_t* stage_ = nullptr;    // heavy levels: expand_grid_ rows of hot_words_ words
   uint2* side_ = nullptr;        // sweep side entries (nparts 1)
   int32_t* first_nbr_ = nullptr; // first neighbour of each row (heavy-level parent resolution)

@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
   }
 
   __syncthreads();
-  uint4* row = reinterpret_cast<uint4*>(s.stage) + (size_t)blockIdx.x * hw4;
+  uint4* row = reinterpret_cast<uint4*>(s.stage) + (size_t)blockIdx.x * (s.stage_words >> 2);
   for (int i = tid; i < hw4; i += blockDim.x) {
     uint4 x = h4[i];
     if (!s.stage_first) {

@@ -11,7 +11,7 @@ OBJ=$OUT/obj_$NAME
 mkdir -p $OBJ
 NCCL_INC=$(python3 -c "import nvidia.nccl, os; print(os.path.join(list(nvidia.nccl.__path__)[0], \"include\"))")
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$ROOT/include -I$NCCL_INC --expt-relaxed-constexpr $*"
-for f in api bfs bottomup cluster construct layout multi partition sweep validate; do
+for f in api bfs bottomup cluster construct layout multi partition stream sweep validate; do
   $NV -c $SRC/$f.cu -o $OBJ/$f.o -Xptxas -v 2> $OBJ/$f.ptxas.log &
 done
 wait
