@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU-baseline sampling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra-configs", action="store_true", help="skip the S20 / lattice keys")
+    ap.add_argument("--part-driver", choices=("native", "python"), default="native",
+                    help="partitioned level loop: the library's (one call per BFS, library-owned NCCL "
+                         "communicator) or distributed.bfs_partitioned (per-step calls, torch.distributed)")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the partitioned (multi-GPU) driver even at N=1 (one NCCL rank)")
     return ap.parse_args()
@@ -294,15 +297,21 @@ def run_partitioned(args, rank, world, local):
     n, nnz = g.num_vertices, g.num_edges
     roots = pick_roots(g, args.roots, 1, filter_unconnected=True).tolist()
     part = PartitionedGraph(g, rank, world, device=local)
-    host_csr = (g.colstarts, g.rows) if rank == 0 else None  # for the tree check
-    del g  # only this rank's rows stay on the GPU
+    if rank != 0:
+        del g  # only this rank's rows stay on its GPU (rank 0 keeps the graph for the tree checks)
     build_s = time.perf_counter() - t0
     ex = TorchExchange()
     bufs = [part.new_buffers()]
     outs = [part.new_outputs()]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    native = args.part_driver == "native"
+    if native:
+        part.attach_nccl()
 
     def one(r, gather=False):
+        if native:  # the library's level loop; its own CUDA-event time on its stream
+            res = part.bfs_native(r, outs[0][0], outs[0][1], gather=gather)
+            return res, res.timing["bfs_ms"]
         ev0.record()
         res = bfs_partitioned([part], r, ex, bufs=bufs, outputs=outs, gather=gather)
         ev1.record()
@@ -339,12 +348,13 @@ def run_partitioned(args, rank, world, local):
     pred_h = torch.empty(outs[0][0].numel(), dtype=torch.int32, pin_memory=True)
     lvl_h = torch.empty(outs[0][1].numel(), dtype=torch.int32, pin_memory=True)
     for r in roots[:2]:  # untimed warm-up
-        bfs_partitioned([part], r, ex, bufs=bufs, outputs=outs, gather=True)
-    e2e_vals = []
+        one(r, gather=True)
+    from paper_1604_02844_b200.validate import validate_tree_device
+    e2e_vals, checked = [], 0
     for r in roots[:16]:
         dist.barrier()
         a = time.perf_counter()
-        res = bfs_partitioned([part], r, ex, bufs=bufs, outputs=outs, gather=True)
+        res, _ = one(r, gather=True)
         if rank == 0:
             pred_h.copy_(outs[0][0])
             lvl_h.copy_(outs[0][1])
@@ -352,14 +362,13 @@ def run_partitioned(args, rank, world, local):
         dt = torch.tensor([time.perf_counter() - a], dtype=torch.float64, device="cuda")
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e_vals.append(res.traversed_edge_count / float(dt.item()) / 1e9)
+        if rank == 0:  # every gathered tree, on the unpartitioned graph (outside the timed interval)
+            rep = validate_tree_device(g, r, outs[0][0])
+            checked += 1
+            if not rep.passed:
+                raise SystemExit(f"[bench] partitioned tree failed validation for root {r}: {rep.details}")
     e2e = hm(e2e_vals)
-    ok = None
-    if rank == 0 and e2e_vals:
-        from paper_1604_02844_b200 import CsrGraph, PredecessorArray
-        from paper_1604_02844_b200.validate import validate_tree
-
-        gh = CsrGraph(n, host_csr[1], host_csr[0])
-        ok = validate_tree(gh, roots[len(e2e_vals) - 1], PredecessorArray(n, _storage=pred_h.numpy())).passed
+    ok = checked if rank == 0 else None
     hbm_gbs, peak_kind = peaks()
     E = float(np.mean(edges))
     alg = b_alg(E, float(np.mean(reached)), n)
@@ -377,7 +386,7 @@ def run_partitioned(args, rank, world, local):
                    "edgefactor": 16, "roots": args.roots, "n": n, "nnz": nnz,
                    "parallelism": f"1d-partition-{world}gpu-nccl",
                    "l2": "inputs larger than L2; no flush", "graph_build_s": round(build_s, 2),
-                   "validated": ok},
+                   "validated_trees": ok, "driver": args.part_driver},
         "roofline": {"bound": "hbm", "achieved": alg / world / t_meas / 1e9, "peak": hbm_gbs, "unit": "GB/s",
                      "frac": t_roof / t_meas, "peak_kind": peak_kind, "traffic": None,
                      "kernel": "whole BFS per GPU (SURVEY §8e t_roof(P) formula)",
@@ -385,7 +394,8 @@ def run_partitioned(args, rank, world, local):
                      "nvlink_bytes_per_gpu": nvl_bytes, "levels": X},
         "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 8,
                 "d2h_bytes_per_step": (outs[0][0].numel() + n) * 4, "step": "one BFS (harmonic mean over roots)",
-                "api": "distributed.bfs_partitioned(gather=True) + rank-0 D2H", "roots_timed": len(e2e_vals)},
+                "api": ("PartitionedGraph.bfs_native" if native else "distributed.bfs_partitioned")
+                       + "(gather=True) + rank-0 D2H", "roots_timed": len(e2e_vals)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "wall_s_timed": wall,
@@ -393,6 +403,7 @@ def run_partitioned(args, rank, world, local):
     if rank == 0:
         print(json.dumps(line), flush=True)
     part.close()
+    dist.barrier()
     dist.destroy_process_group()
 
 

@@ -218,6 +218,23 @@ int lbfs_part_finish(lbfs_graph* g, int32_t* d_pred, int32_t* d_level, void* str
 /* Adjacency entries read by parent resolution since lbfs_part_start. */
 int lbfs_part_resolve_count(lbfs_graph* g, int64_t* out);
 
+/* The same level loop run by the library (one host thread, no per-step
+ * calls from the caller) over a library-owned NCCL communicator, for one
+ * partition per process (torchrun-style jobs):
+ *   rank 0: lbfs_nccl_unique_id(id); the caller broadcasts the 128 bytes
+ *   every rank: lbfs_part_attach_nccl(part, id, nparts, rank)   (collective)
+ *   every rank: lbfs_part_bfs(part, root, ...)                  (collective)
+ * lbfs_part_bfs writes pred (pad32(n)) / level (n, may be NULL) on the
+ * partition's device: with gather != 0 the full arrays on every rank (min /
+ * max all-reduce), else only the owned entries (SENTINEL / -1 elsewhere).
+ * Synchronous; layers and timing as lbfs_bfs_device (t->bfs_ms is this
+ * rank's CUDA-event time). After attaching, lbfs_bfs / lbfs_bfs_device on the
+ * handle run it with gather = 1. */
+int lbfs_nccl_unique_id(uint8_t id[128]);
+int lbfs_part_attach_nccl(lbfs_graph* part, const uint8_t id[128], int nranks, int rank);
+int lbfs_part_bfs(lbfs_graph* part, int64_t root, int32_t* d_pred, int32_t* d_level, int gather,
+                  lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers, lbfs_timing* t_out);
+
 #ifdef __cplusplus
 }
 #endif

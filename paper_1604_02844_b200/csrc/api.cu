@@ -334,9 +334,8 @@ int lbfs_graph_create_partitioned(const lbfs_csr* csr, int ngpus, const int* dev
 
 void lbfs_graph_destroy(lbfs_graph* g) {
   if (!g) return;
-  if (g->multi) {
-    delete g->multi;
-  } else {
+  delete g->multi;  // (borrows g->eng when attached to a partition)
+  if (g->eng) {
     cudaSetDevice(g->eng->device());
     delete g->eng;
   }
@@ -624,6 +623,40 @@ int lbfs_part_finish(lbfs_graph* g, int32_t* d_pred, int32_t* d_level, void* str
     BfsEngine& e = part_engine(g);
     std::lock_guard<std::mutex> lk(e.mu);
     e.part_finish(d_pred, d_level, as_stream(g, stream));
+  });
+}
+
+int lbfs_nccl_unique_id(uint8_t id[128]) {
+  return guarded([&] {
+    if (!id) throw_inval("id is NULL");
+    MultiGraph::unique_id(id);
+  });
+}
+
+int lbfs_part_attach_nccl(lbfs_graph* g, const uint8_t id[128], int nranks, int rank) {
+  return guarded([&] {
+    BfsEngine& e = part_engine(g);
+    if (!id) throw_inval("id is NULL");
+    if (g->multi) throw_inval("a communicator is already attached");
+    if (nranks != e.nparts() || rank != e.part_rank()) throw_inval("nranks / rank differ from the partition's");
+    std::lock_guard<std::mutex> lk(e.mu);
+    g->multi = new MultiGraph(&e, id);
+  });
+}
+
+int lbfs_part_bfs(lbfs_graph* g, int64_t root, int32_t* d_pred, int32_t* d_level, int gather,
+                  lbfs_layer* layers_out, int64_t layers_cap, int64_t* n_layers, lbfs_timing* t_out) {
+  return guarded([&] {
+    if (!g) throw_inval("graph is NULL");
+    if (!g->multi || !g->eng) throw_inval("no communicator attached (lbfs_part_attach_nccl)");
+    if (!d_pred) throw_inval("device pred output must be non-NULL");
+    MultiGraph& m = *g->multi;
+    std::lock_guard<std::mutex> lk(m.mu);
+    LBFS_CUDA(cudaSetDevice(m.device()));
+    lbfs_timing t{};
+    m.run(root, d_pred, d_level, &t, gather != 0);
+    if (t_out) *t_out = t;
+    copy_layers(m.layers(), layers_out, layers_cap, n_layers);
   });
 }
 

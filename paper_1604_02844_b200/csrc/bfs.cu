@@ -1382,6 +1382,7 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   LBFS_CUDA(cudaStreamCreateWithFlags(&res_st_, cudaStreamNonBlocking));
   LBFS_CUDA(cudaEventCreateWithFlags(&ev_resolve_, cudaEventDisableTiming));
   LBFS_CUDA(cudaEventCreateWithFlags(&ev_side_done_, cudaEventDisableTiming));
+  for (auto& e : ev_snap_) LBFS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   build_layout(csr);
   visited_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
   prev_ = dev_alloc<uint32_t>((size_t)nwords_ + 4);
@@ -1443,7 +1444,7 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   int optin = 0;
   LBFS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device_));
   int64_t avail = (int64_t)optin - (int64_t)max_static - 1024;
-  if (nparts_ == 1) {  // the sweep kernel's ring + static part must fit next to the same hot prefix
+  {  // the sweep kernel's ring + static part must fit next to the same hot prefix
     cudaFuncAttributes fs{};
     LBFS_CUDA(cudaFuncGetAttributes(&fs, (const void*)k_sweep));
     avail = std::min<int64_t>(avail, (int64_t)optin - (int64_t)fs.sharedSizeBytes - kSweepRingBytes);
@@ -1453,12 +1454,7 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   for (auto fn : kernels) LBFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_));
   LBFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_expand<kBitmapOut, 2>, kExpandThreads, dyn_smem_));
   expand_grid_ = sm_count_ * std::max(occ, 1);
-  if (nparts_ > 1 && hot_words_ >= 4) {  // partitions: heavy levels without the sweep
-    sweep_hot_words_ = hot_words_;
-    stage_words_ = hot_words_;
-    stage_ = dev_alloc<uint32_t>((size_t)expand_grid_ * stage_words_);
-  }
-  if (nparts_ == 1 && hot_words_ >= 4) {
+  if (hot_words_ >= 4) {
     // the sweep has no per-warp rings: its hot prefix takes what its own ring leaves
     cudaFuncAttributes fs{};
     LBFS_CUDA(cudaFuncGetAttributes(&fs, (const void*)k_sweep));
@@ -1686,6 +1682,8 @@ BfsEngine::~BfsEngine() {
   cudaStreamDestroy(res_st_);
   cudaEventDestroy(ev_resolve_);
   cudaEventDestroy(ev_side_done_);
+  for (auto& e : ev_snap_) cudaEventDestroy(e);
+  for (auto& s : snap_) dev_free(s);
   cudaStreamDestroy(stream_);
 }
 
@@ -1858,8 +1856,8 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
   // after a queue-mode level (opt-in experiment, LBFS_SWEEP_AFTER_QUEUE): the
   // frontier bitmap is rebuilt from the queues and the hub + warp-bin rows
   // (the big-row region) are swept; the small queue keeps its own launch
-  const bool from_queues = mode == kHeavy && !prev_bitmap && sweep_after_queue_;
-  const bool sweep = mode == kHeavy && nparts_ == 1 && (prev_bitmap || from_queues) && side_ && sweep_fits_ &&
+  const bool from_queues = mode == kHeavy && !prev_bitmap && sweep_after_queue_ && nparts_ == 1;
+  const bool sweep = mode == kHeavy && (prev_bitmap || from_queues) && side_ && sweep_fits_ &&
                      !sweep_off_ &&
                      (from_queues ||
                       c.big_edges * 100ull >= (unsigned long long)e_big_ * (unsigned long long)sweep_min_pct_);

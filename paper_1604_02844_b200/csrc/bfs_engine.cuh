@@ -499,6 +499,10 @@ class BfsEngine {
   int refresh_chunks_ = kRefreshChunks;
   int qchunk_ = kQChunkDefault;
   bool part_heavy_ = false;      // this partition level runs with heavy (blind-OR) semantics
+  uint32_t* snap_[2] = {nullptr, nullptr};  // F_L snapshots for k_part_resolve (heavy levels)
+  cudaEvent_t ev_snap_[2] = {nullptr, nullptr};
+  bool snap_used_[2] = {false, false};
+  int snap_next_ = 0;
   bool part_heavy_off_ = false;  // LBFS_PART_HEAVY=0
   bool count_ = false;
   bool split_ = false;

@@ -216,13 +216,13 @@ void BfsEngine::build_layout(const Csr& csr) {
   e_nz_ = h_rp[(size_t)t_nz_];
   n_win_all_ = (e_nz_ + kSweepWindow - 1) / kSweepWindow;
   w_small0_ = e_big_ / kSweepWindow;
-  if (nparts_ == 1 && n_win_all_ > w_small0_) {
+  if (n_win_all_ > w_small0_) {
     const int64_t nsw = n_win_all_ - w_small0_;
     svmask_ = dev_alloc<uint4>((size_t)nsw);
     sdesc_ = dev_alloc<uint2>((size_t)nsw);
   }
   n_side_win_ = t_warp_ > 0 ? (e_big_ + kSweepWindow - 1) / kSweepWindow : 0;
-  if (nparts_ == 1 && n_side_win_ > 0) {
+  if (n_side_win_ > 0) {
     side_ = dev_alloc<uint2>((size_t)n_side_win_);
     LBFS_LAUNCH(k_side_table, clamp_grid((n_side_win_ + 255) / 256, 148 * 16), 256, 0, st, row_ptr_, t_warp_,
                 n_side_win_, side_);

@@ -33,6 +33,8 @@ namespace {
 
 struct NcclApi {
   ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
@@ -63,6 +65,8 @@ const NcclApi& nccl() {
     auto sym = [&](const char* name) { return dlsym(h, name); };
     api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(sym("ncclCommInitAll"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
     api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
     api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
@@ -70,7 +74,8 @@ const NcclApi& nccl() {
     api.AlltoAll = reinterpret_cast<decltype(api.AlltoAll)>(sym("ncclAlltoAll"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
     api.GetVersion = reinterpret_cast<decltype(api.GetVersion)>(sym("ncclGetVersion"));
-    if (!api.CommInitAll || !api.GroupStart || !api.AllReduce || !api.AllGather || !api.AlltoAll) {
+    if (!api.CommInitAll || !api.CommInitRank || !api.GetUniqueId || !api.GroupStart || !api.AllReduce ||
+        !api.AllGather || !api.AlltoAll) {
       why = "libnccl.so.2 lacks ncclAlltoAll (needs NCCL >= 2.24)";
       api = NcclApi{};
     }
@@ -142,20 +147,7 @@ MultiGraph::MultiGraph(const Csr& csr, int ngpus, const int* devices) {
         throw;
       }
       if (copy.row_ptr) free_csr(copy);
-      BfsEngine& e = *parts_[p];
-      const int64_t nwl = e.nwords() / P_;
-      Bufs& b = b_[p];
-      b.nwl = nwl;
-      b.send = dev_alloc<uint32_t>((size_t)(P_ * nwl));
-      b.recv = dev_alloc<uint32_t>((size_t)(P_ * nwl));
-      b.fsend = dev_alloc<uint32_t>((size_t)(nwl + 4));
-      b.fgath = dev_alloc<uint32_t>((size_t)(P_ * (nwl + 4)));
-      b.red = dev_alloc<unsigned long long>(2);
-      b.pred = dev_alloc<int32_t>((size_t)npad_);
-      b.level = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_, 1));
-      LBFS_CUDA(cudaStreamCreateWithFlags(&st_[p], cudaStreamNonBlocking));
-      LBFS_CUDA(cudaEventCreate(&ev_[2 * p]));
-      LBFS_CUDA(cudaEventCreate(&ev_[2 * p + 1]));
+      alloc_bufs(p);
     }
   } catch (...) {
     release();
@@ -164,8 +156,57 @@ MultiGraph::MultiGraph(const Csr& csr, int ngpus, const int* devices) {
   LBFS_CUDA(cudaSetDevice(dev_[0]));
 }
 
+// (current device = dev_[p])
+void MultiGraph::alloc_bufs(int p) {
+  const int64_t nwl = parts_[p]->nwords() / P_;
+  Bufs& b = b_[p];
+  b.nwl = nwl;
+  b.send = dev_alloc<uint32_t>((size_t)(P_ * nwl));
+  b.recv = dev_alloc<uint32_t>((size_t)(P_ * nwl));
+  b.fsend = dev_alloc<uint32_t>((size_t)(nwl + 4));
+  b.fgath = dev_alloc<uint32_t>((size_t)(P_ * (nwl + 4)));
+  b.red = dev_alloc<unsigned long long>(2);
+  b.pred = dev_alloc<int32_t>((size_t)npad_);
+  b.level = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_, 1));
+  LBFS_CUDA(cudaStreamCreateWithFlags(&st_[p], cudaStreamNonBlocking));
+  LBFS_CUDA(cudaEventCreate(&ev_[2 * p]));
+  LBFS_CUDA(cudaEventCreate(&ev_[2 * p + 1]));
+}
+
+void MultiGraph::unique_id(void* out128) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+  memcpy(out128, &id, sizeof(id));
+}
+
+MultiGraph::MultiGraph(BfsEngine* part, const void* nccl_id) {
+  own_parts_ = false;
+  P_ = part->nparts();
+  n_ = part->n();
+  nnz_ = part->nnz();
+  npad_ = pad32(n_);
+  dev_.push_back(part->device());
+  const NcclApi& api = nccl();
+  ncclUniqueId id;
+  memcpy(&id, nccl_id, sizeof(id));
+  comm_.resize(1, nullptr);
+  LBFS_CUDA(cudaSetDevice(dev_[0]));
+  nccl_check(api.CommInitRank(&comm_[0], P_, id, part->part_rank()), "ncclCommInitRank");
+  parts_.push_back(part);
+  b_.resize(1);
+  st_.resize(1, nullptr);
+  ev_.resize(2, nullptr);
+  try {
+    alloc_bufs(0);
+  } catch (...) {
+    release();
+    throw;
+  }
+}
+
 void MultiGraph::last_levels_to_host(int32_t* h_level) {
-  if (b_.empty()) throw_inval("no BFS has run on this graph");
+  if (b_.empty() || !gathered_) throw_inval("no gathered BFS has run on this graph");
   LBFS_CUDA(cudaSetDevice(dev_[0]));
   LBFS_CUDA(cudaMemcpyAsync(h_level, b_[0].level, sizeof(int32_t) * (size_t)n_, cudaMemcpyDeviceToHost, st_[0]));
   LBFS_CUDA(cudaStreamSynchronize(st_[0]));
@@ -175,7 +216,7 @@ void MultiGraph::release() {
   for (int p = 0; p < (int)parts_.size(); ++p) {
     if (p < (int)dev_.size()) cudaSetDevice(dev_[p]);
     if (st_.size() > (size_t)p && st_[p]) cudaStreamSynchronize(st_[p]);
-    delete parts_[p];
+    if (own_parts_) delete parts_[p];
     parts_[p] = nullptr;
     Bufs& b = b_[p];
     dev_free(b.send);
@@ -199,13 +240,16 @@ void MultiGraph::release() {
 
 MultiGraph::~MultiGraph() { release(); }
 
-void MultiGraph::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t) {
+void MultiGraph::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing* t, bool gather) {
   if (root < 0 || root >= n_) throw_inval("root out of range");
+  if (!gather && parts_.size() != 1) throw_inval("gather = 0 needs one partition per process");
+  gathered_ = false;
+  const int nloc = (int)parts_.size();
   const NcclApi& api = nccl();
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t launches0 = g_launches.load();
   auto each = [&](auto&& fn) {
-    for (int p = 0; p < P_; ++p) {
+    for (int p = 0; p < nloc; ++p) {
       LBFS_CUDA(cudaSetDevice(dev_[p]));
       fn(p, *parts_[p], b_[p], st_[p]);
     }
@@ -254,16 +298,20 @@ void MultiGraph::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timin
     });
     layers_.push_back(ly);
   }
-  each([&](int, BfsEngine& e, Bufs& b, cudaStream_t st) { e.part_finish(b.pred, b.level, st); });
-  {
+  if (!gather) {  // this rank's owned entries, straight into the outputs
+    each([&](int, BfsEngine& e, Bufs&, cudaStream_t st) { e.part_finish(d_pred, d_level, st); });
+  } else {
+    // (levels always: lbfs_graph_last_levels reads them later)
+    each([&](int, BfsEngine& e, Bufs& b, cudaStream_t st) { e.part_finish(b.pred, b.level, st); });
     Group g;
     each([&](int p, BfsEngine&, Bufs& b, cudaStream_t st) {
       nccl_check(api.AllReduce(b.pred, b.pred, (size_t)npad_, ncclInt32, ncclMin, comm_[p], st), "ncclAllReduce");
       nccl_check(api.AllReduce(b.level, b.level, (size_t)n_, ncclInt32, ncclMax, comm_[p], st), "ncclAllReduce");
     });
   }
+  gathered_ = gather;
   each([&](int p, BfsEngine&, Bufs& b, cudaStream_t st) {
-    if (p == 0) {
+    if (p == 0 && gather) {
       LBFS_CUDA(cudaMemcpyAsync(d_pred, b.pred, sizeof(int32_t) * (size_t)npad_, cudaMemcpyDeviceToDevice, st));
       if (d_level)
         LBFS_CUDA(cudaMemcpyAsync(d_level, b.level, sizeof(int32_t) * (size_t)n_, cudaMemcpyDeviceToDevice, st));

@@ -44,11 +44,11 @@ __global__ void k_part_pack(const uint32_t* __restrict__ visited, const uint32_t
 
 // Warp per owned word (lane = bit): remote discoveries of this level and
 // their parents. recv[p*nwl + j] is peer p's marks for owned word j.
-// With prev (a heavy level: blind ORs wrote no parent), every new owned
-// vertex, local or remote discovery, gets its parent here.
+// Without fglob (a heavy level: blind ORs wrote no parent) only visited is
+// completed here; every new owned vertex, local or remote discovery, gets its
+// parent from k_part_resolve on the side stream.
 __global__ void k_part_merge(const uint32_t* __restrict__ recv, int64_t nwl, int part_log, int rank,
-                             uint32_t* __restrict__ visited, const uint32_t* __restrict__ prev,
-                             const uint32_t* __restrict__ fglob,
+                             uint32_t* __restrict__ visited, const uint32_t* __restrict__ fglob,
                              const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                              const int32_t* __restrict__ new2old, int32_t* __restrict__ pred_int,
                              unsigned long long* __restrict__ scanned) {
@@ -60,9 +60,9 @@ __global__ void k_part_merge(const uint32_t* __restrict__ recv, int64_t nwl, int
     for (int p = 0; p < (1 << part_log); ++p)
       if (p != rank) inc |= __ldg(recv + (int64_t)p * nwl + j);
     const int64_t gw = (j << part_log) | rank;
-    if (!inc && !prev) continue;  // warp-uniform
+    if (!inc) continue;  // warp-uniform
     const uint32_t vis = visited[gw];
-    const uint32_t nb = prev ? (vis | inc) & ~prev[gw] : inc & ~vis;
+    const uint32_t nb = fglob ? inc & ~vis : 0u;
     __syncwarp();
     if (lane == 0 && (inc & ~vis)) visited[gw] = vis | inc;
     if ((nb >> lane) & 1u) {
@@ -83,6 +83,34 @@ __global__ void k_part_merge(const uint32_t* __restrict__ recv, int64_t nwl, int
 #pragma unroll
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
   if (lane == 0 && cnt && scanned) atomicAdd(scanned, cnt);
+}
+
+// Parents of the owned vertices at level lvl after a heavy level (side
+// stream, off the critical path): the first neighbour in F_{lvl-1} (a
+// snapshot of the replicated frontier bitmap taken before the next level
+// overwrote it). Thread per owned vertex; vertices of later levels are only
+// ever written from -1 to a level > lvl, so the concurrent compactions of the
+// next levels never make a vertex look like one of this level.
+__global__ void k_part_resolve(const int32_t* level_int, int64_t n_loc, int32_t lvl,
+                               const uint32_t* __restrict__ fprev, const int64_t* __restrict__ row_ptr,
+                               const int32_t* __restrict__ col_idx, const int32_t* __restrict__ new2old,
+                               int32_t* __restrict__ pred_int, unsigned long long* __restrict__ scanned) {
+  unsigned long long cnt = 0;
+  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n_loc; l += (int64_t)gridDim.x * blockDim.x) {
+    if (level_int[l] != lvl) continue;
+    const int64_t e0 = row_ptr[l], e1 = row_ptr[l + 1];
+    int32_t par = kSentinel;
+    for (int64_t e = e0; e < e1; ++e) {
+      const int32_t u = __ldg(col_idx + e);
+      ++cnt;
+      if ((__ldg(fprev + (u >> 5)) >> (u & 31)) & 1u) {
+        par = __ldg(new2old + u);
+        break;
+      }
+    }
+    pred_int[l] = par;
+  }
+  if (cnt && scanned) atomicAdd(scanned, cnt);
 }
 
 // local counts of the next frontier -> the 4 words after the frontier words
@@ -121,27 +149,24 @@ __global__ void k_part_sync(const uint32_t* __restrict__ fgath, uint32_t* __rest
   }
 }
 
-__global__ void k_fill2(int32_t* __restrict__ a, int64_t na, int32_t va, int32_t* __restrict__ b, int64_t nb,
-                        int32_t vb) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < std::max(na, nb);
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < na) a[i] = va;
-    if (i < nb) b[i] = vb;
-  }
-}
-
-// owned records -> outputs in original ids (scatter); other entries keep
-// the fill (SENTINEL / -1), so the ranks' outputs combine by min / max
-__global__ void k_part_finalize(const int32_t* __restrict__ new2old_loc, const int32_t* __restrict__ level_int,
-                                const int32_t* __restrict__ pred_int, int64_t n_loc, int64_t n, int part_log,
+// Outputs in original ids, one sequential pass over them (gathered through
+// old2new): owned reached vertices get their record, every other entry the
+// fill (SENTINEL / -1), so the ranks' outputs combine by min / max.
+__global__ void k_part_finalize(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
+                                const int32_t* __restrict__ pred_int, int64_t n, int64_t npad, int part_log,
                                 int rank, int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out) {
-  for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < n_loc; l += (int64_t)gridDim.x * blockDim.x) {
-    if (part_global(l, part_log, rank) >= n) continue;
-    const int32_t lv = level_int[l];
-    if (lv < 0) continue;
-    const int32_t o = new2old_loc[l];
-    if (level_out) level_out[o] = lv;
-    if (pred_out) pred_out[o] = pred_int[l];
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < npad; v += (int64_t)gridDim.x * blockDim.x) {
+    int32_t lv = -1, p = kSentinel;
+    if (v < n) {
+      const int32_t i = __ldg(old2new + v);
+      if (part_owned(i, part_log, rank)) {
+        const int32_t l = part_local(i, part_log);
+        lv = level_int[l];
+        if (lv >= 0 && pred_out) p = pred_int[l];
+      }
+      if (level_out) level_out[v] = lv;
+    }
+    if (pred_out) pred_out[v] = p;
   }
 }
 
@@ -151,6 +176,10 @@ void BfsEngine::part_start(int64_t root, cudaStream_t st, unsigned long long* re
   if (root < 0 || root >= n_) throw_inval("root out of range");
   read_env();
   part_st_ = st;
+  if (side_pending_) {  // an abandoned BFS left side work: it reads level_int, which k_init resets
+    LBFS_CUDA(cudaStreamSynchronize(res_st_));
+    side_pending_ = false;
+  }
   if (!h_red_) LBFS_CUDA(cudaMallocHost(&h_red_, 2 * sizeof(unsigned long long)));
   LBFS_LAUNCH(k_init, grid_for(std::max(nwords_, n_loc_) / 4, sm_count_), 256, 0, st, (uint4*)visited_,
               (uint4*)prev_, (nwords_ + 3) / 4, (int4*)level_int_, (n_loc_ + 3) / 4);
@@ -197,11 +226,30 @@ void BfsEngine::part_pack(uint32_t* send, cudaStream_t st) {
 void BfsEngine::part_merge(const uint32_t* recv, uint32_t* fsend, cudaStream_t st) {
   part_st_ = st;
   const int64_t L = part_L_;
-  if (nparts_ > 1 || part_heavy_)
+  if (nparts_ > 1)
     LBFS_LAUNCH(k_part_merge, grid_for(nwl_ * 32, sm_count_), 256, 0, st, recv, nwl_, part_log_, part_rank_,
-                visited_, part_heavy_ ? prev_ : nullptr, nparts_ > 1 ? fglob_ : front_ /* F_L */, row_ptr_,
-                col_idx_, new2old_, pred_int_, resolve_cnt_);
-  compact_level(part_cur_, L, fsend, st);
+                visited_, part_heavy_ ? nullptr : fglob_ /* F_L */, row_ptr_, col_idx_, new2old_, pred_int_,
+                resolve_cnt_);
+  uint32_t* snap = nullptr;
+  if (part_heavy_) {  // F_L, for the parents of this level's vertices (resolved after the compaction)
+    const int k = snap_next_;
+    snap_next_ ^= 1;
+    if (!snap_[k]) snap_[k] = dev_alloc<uint32_t>((size_t)nwords_ + 4);
+    if (snap_used_[k]) LBFS_CUDA(cudaStreamWaitEvent(st, ev_snap_[k], 0));  // its last reader is done
+    snap = snap_[k];
+    LBFS_CUDA(cudaMemcpyAsync(snap, nparts_ > 1 ? fglob_ : front_, sizeof(uint32_t) * (size_t)nwords_,
+                              cudaMemcpyDeviceToDevice, st));
+    compact_level(part_cur_, L, fsend, st);
+    LBFS_CUDA(cudaEventRecord(ev_resolve_, st));
+    LBFS_CUDA(cudaStreamWaitEvent(res_st_, ev_resolve_, 0));
+    LBFS_LAUNCH(k_part_resolve, grid_for(n_loc_, sm_count_), 256, 0, res_st_, level_int_, n_loc_, (int32_t)(L + 1),
+                snap, row_ptr_, col_idx_, new2old_, pred_int_, resolve_cnt_);
+    LBFS_CUDA(cudaEventRecord(ev_snap_[k], res_st_));
+    snap_used_[k] = true;
+    side_pending_ = true;
+  } else {
+    compact_level(part_cur_, L, fsend, st);
+  }
   LBFS_LAUNCH(k_part_counts, 1, 1, 0, st, &cnt_[(L + 1) % kCounterRing], fsend + nwl_);
 }
 
@@ -252,10 +300,14 @@ void BfsEngine::part_level_done(const unsigned long long* red_global, lbfs_layer
 
 void BfsEngine::part_finish(int32_t* d_pred, int32_t* d_level, cudaStream_t st) {
   part_st_ = st;
-  LBFS_LAUNCH(k_fill2, grid_for(npad_, sm_count_), 256, 0, st, d_pred, d_pred ? npad_ : 0, kSentinel, d_level,
-              d_level ? n_ : 0, -1);
-  LBFS_LAUNCH(k_part_finalize, grid_for(n_loc_, sm_count_), 256, 0, st, new2old_loc_, level_int_, pred_int_, n_loc_,
-              n_, part_log_, part_rank_, d_level, d_pred);
+  if (side_pending_) {  // heavy-level parents resolved on the side stream
+    LBFS_CUDA(cudaEventRecord(ev_side_done_, res_st_));
+    LBFS_CUDA(cudaStreamWaitEvent(st, ev_side_done_, 0));
+    side_pending_ = false;
+  }
+  if (!d_pred && !d_level) return;
+  LBFS_LAUNCH(k_part_finalize, grid_for(npad_, sm_count_), 256, 0, st, old2new_, level_int_, pred_int_, n_, npad_,
+              part_log_, part_rank_, d_level, d_pred);
 }
 
 unsigned long long BfsEngine::resolve_scanned() const {

@@ -25,6 +25,12 @@ all-reduce at the start for the root's degree). Collectives go through an
 The driver is generic over the partition objects: ``PartitionedGraph`` (the
 device) or any object with the same step methods (the CPU restatement in
 oracle/part_emu.py, used by the gloo tests).
+
+The same loop also runs inside the library (``PartitionedGraph.attach_nccl``
++ ``bfs_native``; csrc/multi.cu): the library owns an NCCL communicator
+(ncclCommInitRank, the unique id broadcast over torch.distributed) and drives
+every step and collective from one C++ call per BFS, without the per-step
+Python and torch.distributed overhead. ``bench.py --gpus N`` times that path.
 """
 
 from __future__ import annotations
@@ -137,6 +143,41 @@ class PartitionedGraph:
                                                  level.data_ptr() if level is not None else None,
                                                  _stream_ptr(pred if pred is not None else level)))
 
+    # -- the library's own level loop (one call per BFS) ----------------------
+    def attach_nccl(self, group=None) -> None:
+        """Collective over the torch.distributed group (one partition per
+        rank): rank 0 draws an NCCL unique id, every rank joins the library's
+        communicator with it."""
+        import torch
+        import torch.distributed as dist
+        lib = _lib.load()
+        uid = (ctypes.c_uint8 * 128)()
+        if self.rank == 0:
+            _lib.check(lib.lbfs_nccl_unique_id(uid))
+        t = torch.tensor(list(bytes(uid)), dtype=torch.uint8,
+                         device=self.device if dist.get_backend(group) == "nccl" else "cpu")
+        dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (ctypes.c_uint8 * 128)(*t.cpu().tolist())
+        _lib.check(lib.lbfs_part_attach_nccl(self._h, uid, self.nparts, self.rank))
+        self.attached = True
+
+    def bfs_native(self, root: int, pred, level=None, gather: bool = True) -> "PartitionedResult":
+        """One BFS through the library's level loop (collective). pred /
+        level: device tensors (pad32(n) / n int32) written on return; with
+        ``gather`` the full arrays, else this rank's owned entries."""
+        lib = _lib.load()
+        cap = 4096
+        layers = (_lib.Layer * cap)()
+        nl, t = ctypes.c_int64(), _lib.Timing()
+        _lib.check(lib.lbfs_part_bfs(self._h, int(root), pred.data_ptr(),
+                                     level.data_ptr() if level is not None else None, int(bool(gather)),
+                                     layers, cap, ctypes.byref(nl), ctypes.byref(t)))
+        if nl.value > cap:  # (e.g. a lattice: thousands of levels)
+            layers = (_lib.Layer * nl.value)()
+            _lib.check(lib.lbfs_graph_last_layers(self._h, layers, nl.value, ctypes.byref(nl)))
+        ls = [LayerStats(int(x.input), int(x.edges), int(x.discovered)) for x in layers[:nl.value]]
+        return PartitionedResult(ls, sum(l.edges for l in ls), pred, level, gather, t.as_dict())
+
     def resolve_count(self) -> int:
         v = ctypes.c_int64()
         _lib.check(_lib.load().lbfs_part_resolve_count(self._h, ctypes.byref(v)))
@@ -214,6 +255,7 @@ class PartitionedResult:
     pred: object = None    # full outputs (after gather) or this rank's (owned entries only)
     level: object = None
     gathered: bool = False
+    timing: dict | None = None  # bfs_native: the library's timing (bfs_ms = this rank's device time)
 
 
 def bfs_partitioned(parts: list, root: int, exchange, bufs: list | None = None, outputs: list | None = None,
