@@ -503,6 +503,7 @@ class BfsEngine {
   cudaEvent_t ev_snap_[2] = {nullptr, nullptr};
   bool snap_used_[2] = {false, false};
   int snap_next_ = 0;
+  const uint32_t* part_fgath_ = nullptr;  // the gathered slices of the level (part_sync -> part_level_done)
   bool part_heavy_off_ = false;  // LBFS_PART_HEAVY=0
   bool count_ = false;
   bool split_ = false;

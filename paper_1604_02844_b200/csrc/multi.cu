@@ -245,6 +245,9 @@ void MultiGraph::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timin
   if (!gather && parts_.size() != 1) throw_inval("gather = 0 needs one partition per process");
   gathered_ = false;
   const int nloc = (int)parts_.size();
+  // one rank: every collective is the identity (nothing to send, the gather
+  // is this rank's own slice), so none is issued
+  const bool solo = P_ == 1;
   const NcclApi& api = nccl();
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t launches0 = g_launches.load();
@@ -258,7 +261,7 @@ void MultiGraph::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timin
     LBFS_CUDA(cudaEventRecord(ev_[2 * p], st));
     e.part_start(root, st, b.red);
   });
-  {
+  if (!solo) {
     Group g;
     each([&](int p, BfsEngine&, Bufs& b, cudaStream_t st) {
       nccl_check(api.AllReduce(b.red, b.red, 2, ncclUint64, ncclSum, comm_[p], st), "ncclAllReduce");
@@ -270,22 +273,22 @@ void MultiGraph::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timin
   while (!done) {
     each([&](int, BfsEngine& e, Bufs& b, cudaStream_t st) {
       e.part_expand(st);
-      e.part_pack(b.send, st);
+      if (!solo) e.part_pack(b.send, st);
     });
-    {
+    if (!solo) {
       Group g;
       each([&](int p, BfsEngine&, Bufs& b, cudaStream_t st) {
         nccl_check(api.AlltoAll(b.send, b.recv, (size_t)b.nwl, ncclUint32, comm_[p], st), "ncclAlltoAll");
       });
     }
     each([&](int, BfsEngine& e, Bufs& b, cudaStream_t st) { e.part_merge(b.recv, b.fsend, st); });
-    {
+    if (!solo) {
       Group g;
       each([&](int p, BfsEngine&, Bufs& b, cudaStream_t st) {
         nccl_check(api.AllGather(b.fsend, b.fgath, (size_t)(b.nwl + 4), ncclUint32, comm_[p], st), "ncclAllGather");
       });
     }
-    each([&](int, BfsEngine& e, Bufs& b, cudaStream_t st) { e.part_sync(b.fgath, st); });
+    each([&](int, BfsEngine& e, Bufs& b, cudaStream_t st) { e.part_sync(solo ? b.fsend : b.fgath, st); });
     lbfs_layer ly{};
     each([&](int p, BfsEngine& e, Bufs&, cudaStream_t) {
       lbfs_layer l{};
@@ -303,11 +306,13 @@ void MultiGraph::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timin
   } else {
     // (levels always: lbfs_graph_last_levels reads them later)
     each([&](int, BfsEngine& e, Bufs& b, cudaStream_t st) { e.part_finish(b.pred, b.level, st); });
-    Group g;
-    each([&](int p, BfsEngine&, Bufs& b, cudaStream_t st) {
-      nccl_check(api.AllReduce(b.pred, b.pred, (size_t)npad_, ncclInt32, ncclMin, comm_[p], st), "ncclAllReduce");
-      nccl_check(api.AllReduce(b.level, b.level, (size_t)n_, ncclInt32, ncclMax, comm_[p], st), "ncclAllReduce");
-    });
+    if (!solo) {
+      Group g;
+      each([&](int p, BfsEngine&, Bufs& b, cudaStream_t st) {
+        nccl_check(api.AllReduce(b.pred, b.pred, (size_t)npad_, ncclInt32, ncclMin, comm_[p], st), "ncclAllReduce");
+        nccl_check(api.AllReduce(b.level, b.level, (size_t)n_, ncclInt32, ncclMax, comm_[p], st), "ncclAllReduce");
+      });
+    }
   }
   gathered_ = gather;
   each([&](int p, BfsEngine&, Bufs& b, cudaStream_t st) {

@@ -121,17 +121,36 @@ __global__ void k_part_counts(const Counters* __restrict__ c, uint32_t* __restri
   tail[2] = (uint32_t)c->edges;
   tail[3] = (uint32_t)(c->edges >> 32);
 }
-// sum of the P gathered count tails -> red
-__global__ void k_part_sum(const uint32_t* __restrict__ fgath, int nparts, int64_t stride, int64_t nwl,
-                           unsigned long long* __restrict__ red) {
-  unsigned long long d = 0, e = 0;
-  for (int p = 0; p < nparts; ++p) {
-    const uint32_t* t = fgath + p * stride + nwl;
-    d += (unsigned long long)t[0] | ((unsigned long long)t[1] << 32);
-    e += (unsigned long long)t[2] | ((unsigned long long)t[3] << 32);
+// the level's local counters and the global counts -> mapped host memory,
+// then the sequence word (the host spins on it: a blocking stream sync costs
+// tens of microseconds of wake-up per level). The global counts are red
+// (the start's all-reduced root counts) or, after a level, the sum of the P
+// count tails of the gathered slices fgath.
+__global__ void k_part_publish(const Counters* __restrict__ cnt, const unsigned long long* __restrict__ red,
+                               const uint32_t* __restrict__ fgath, int nparts, int64_t stride, int64_t nwl,
+                               Counters* mail, unsigned long long* red_mail, unsigned long long* seq,
+                               unsigned long long value) {
+  const int t = threadIdx.x;
+  constexpr int kWords = (int)(sizeof(Counters) / 8);
+  if (cnt && t < kWords)
+    reinterpret_cast<volatile unsigned long long*>(mail)[t] = reinterpret_cast<const unsigned long long*>(cnt)[t];
+  if (t < 2) {
+    unsigned long long s = 0;
+    if (red) {
+      s = red[t];
+    } else {
+      for (int p = 0; p < nparts; ++p) {
+        const uint32_t* tail = fgath + p * stride + nwl + 2 * t;
+        s += (unsigned long long)tail[0] | ((unsigned long long)tail[1] << 32);
+      }
+    }
+    reinterpret_cast<volatile unsigned long long*>(red_mail)[t] = s;
   }
-  red[0] = d;
-  red[1] = e;
+  __syncwarp();
+  if (t == 0) {
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(seq) = value;
+  }
 }
 
 // fgath[h*stride + j] = rank h's owned word j of F_{L+1} (stride = nwl + 4)
@@ -149,24 +168,45 @@ __global__ void k_part_sync(const uint32_t* __restrict__ fgath, uint32_t* __rest
   }
 }
 
-// Outputs in original ids, one sequential pass over them (gathered through
-// old2new): owned reached vertices get their record, every other entry the
-// fill (SENTINEL / -1), so the ranks' outputs combine by min / max.
-__global__ void k_part_finalize(const int32_t* __restrict__ old2new, const int32_t* __restrict__ level_int,
-                                const int32_t* __restrict__ pred_int, int64_t n, int64_t npad, int part_log,
-                                int rank, int32_t* __restrict__ level_out, int32_t* __restrict__ pred_out) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < npad; v += (int64_t)gridDim.x * blockDim.x) {
-    int32_t lv = -1, p = kSentinel;
-    if (v < n) {
-      const int32_t i = __ldg(old2new + v);
-      if (part_owned(i, part_log, rank)) {
-        const int32_t l = part_local(i, part_log);
-        lv = level_int[l];
-        if (lv >= 0 && pred_out) p = pred_int[l];
-      }
-      if (level_out) level_out[v] = lv;
+// Outputs in original ids, one sequential pass over them (4 per thread,
+// gathered through old2new): owned reached vertices (their bit in the
+// replicated visited bitmap) get their record, every other entry the fill
+// (SENTINEL / -1), so the ranks' outputs combine by min / max. kVec: 16-byte
+// aligned outputs.
+template <bool kVec>
+__global__ void __launch_bounds__(256) k_part_finalize(const int32_t* __restrict__ old2new,
+                                                       const uint32_t* __restrict__ visited,
+                                                       const int32_t* __restrict__ level_int,
+                                                       const int32_t* __restrict__ pred_int, int64_t n, int64_t npad,
+                                                       int part_log, int rank, int32_t* __restrict__ level_out,
+                                                       int32_t* __restrict__ pred_out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i * 4 < npad; i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 v4 = __ldg(reinterpret_cast<const int4*>(old2new) + i);  // (old2new is padded)
+    const int32_t v[4] = {v4.x, v4.y, v4.z, v4.w};
+    int32_t p[4], lv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool ok = i * 4 + q < n && part_owned(v[q], part_log, rank) &&
+                      ((__ldg(visited + (v[q] >> 5)) >> (v[q] & 31)) & 1u);
+      const int32_t l = part_local(v[q], part_log);
+      p[q] = ok && pred_out ? pred_int[l] : kSentinel;
+      lv[q] = ok && level_out ? level_int[l] : -1;
     }
-    if (pred_out) pred_out[v] = p;
+    if (pred_out) {  // npad is a multiple of 32
+      if (kVec) reinterpret_cast<int4*>(pred_out)[i] = make_int4(p[0], p[1], p[2], p[3]);
+      else
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pred_out[i * 4 + q] = p[q];
+    }
+    if (level_out) {
+      if (kVec && i * 4 + 3 < n) {
+        reinterpret_cast<int4*>(level_out)[i] = make_int4(lv[0], lv[1], lv[2], lv[3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (i * 4 + q < n) level_out[i * 4 + q] = lv[q];
+      }
+    }
   }
 }
 
@@ -180,7 +220,11 @@ void BfsEngine::part_start(int64_t root, cudaStream_t st, unsigned long long* re
     LBFS_CUDA(cudaStreamSynchronize(res_st_));
     side_pending_ = false;
   }
-  if (!h_red_) LBFS_CUDA(cudaMallocHost(&h_red_, 2 * sizeof(unsigned long long)));
+  if (!h_red_) {
+    void* m = nullptr;
+    LBFS_CUDA(cudaHostAlloc(&m, 2 * sizeof(unsigned long long), cudaHostAllocMapped));
+    h_red_ = reinterpret_cast<unsigned long long*>(m);
+  }
   LBFS_LAUNCH(k_init, grid_for(std::max(nwords_, n_loc_) / 4, sm_count_), 256, 0, st, (uint4*)visited_,
               (uint4*)prev_, (nwords_ + 3) / 4, (int4*)level_int_, (n_loc_ + 3) / 4);
   if (fglob_) LBFS_CUDA(cudaMemsetAsync(fglob_, 0, sizeof(uint32_t) * (size_t)nwords_, st));
@@ -255,26 +299,27 @@ void BfsEngine::part_merge(const uint32_t* recv, uint32_t* fsend, cudaStream_t s
 
 void BfsEngine::part_sync(const uint32_t* fgath, cudaStream_t st) {
   part_st_ = st;
-  if (!red_dev_) red_dev_ = dev_alloc<unsigned long long>(2);
   // (one partition: visited and prev are already complete after k_compact)
   if (nparts_ > 1)
     LBFS_LAUNCH(k_part_sync, grid_for(nwords_, sm_count_), 256, 0, st, fgath, fglob_, visited_, prev_, nwords_,
                 nwl_ + 4, part_log_);
-  LBFS_LAUNCH(k_part_sum, 1, 1, 0, st, fgath, nparts_, nwl_ + 4, nwl_, red_dev_);
+  part_fgath_ = fgath;  // (part_level_done sums its count tails)
 }
 
 void BfsEngine::part_level_done(const unsigned long long* red_global, lbfs_layer* layer, int* done) {
   cudaStream_t st = part_st_;
   const int64_t L = part_L_;
   const int slot = (int)((L + 1) % kCounterRing);
-  if (L >= 0) LBFS_CUDA(cudaMemcpyAsync(&h_cnt_[slot], &cnt_[slot], sizeof(Counters), cudaMemcpyDeviceToHost, st));
-  if (!red_global) {  // a level: the counts part_sync summed from the gathered slices
-    if (L < 0) throw_inval("part_level_done: the start needs the summed root counts");
-    red_global = red_dev_;
-  }
-  LBFS_CUDA(cudaMemcpyAsync(h_red_, red_global, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  LBFS_CUDA(cudaStreamSynchronize(st));
-  const unsigned long long disc = h_red_[0], edges = h_red_[1];
+  if (!red_global && (L < 0 || !part_fgath_)) throw_inval("part_level_done: the start needs the summed root counts");
+  const unsigned long long want = ++seq_;
+  // (a level: the global counts are the sum of the gathered slices' tails)
+  LBFS_LAUNCH(k_part_publish, 1, 32, 0, st, L >= 0 ? &cnt_[slot] : nullptr, red_global, part_fgath_, nparts_,
+              nwl_ + 4, nwl_, h_mail_, h_red_, h_seq_, want);
+  part_fgath_ = nullptr;
+  wait_mail(want, st);
+  if (L >= 0) h_cnt_[slot] = *const_cast<const Counters*>(h_mail_);
+  const unsigned long long disc = reinterpret_cast<volatile unsigned long long*>(h_red_)[0],
+                           edges = reinterpret_cast<volatile unsigned long long*>(h_red_)[1];
   if (L < 0) {  // start: the summed root counts (1, deg(root)) become frontier 0
     part_in_ = disc;
     part_edges_ = edges;
@@ -306,8 +351,13 @@ void BfsEngine::part_finish(int32_t* d_pred, int32_t* d_level, cudaStream_t st) 
     side_pending_ = false;
   }
   if (!d_pred && !d_level) return;
-  LBFS_LAUNCH(k_part_finalize, grid_for(npad_, sm_count_), 256, 0, st, old2new_, level_int_, pred_int_, n_, npad_,
-              part_log_, part_rank_, d_level, d_pred);
+  const bool vec = ((uintptr_t)d_pred % 16) == 0 && ((uintptr_t)d_level % 16) == 0;
+  if (vec)
+    LBFS_LAUNCH(k_part_finalize<true>, grid_for(npad_ / 4, sm_count_), 256, 0, st, old2new_, visited_, level_int_,
+                pred_int_, n_, npad_, part_log_, part_rank_, d_level, d_pred);
+  else
+    LBFS_LAUNCH(k_part_finalize<false>, grid_for(npad_ / 4, sm_count_), 256, 0, st, old2new_, visited_, level_int_,
+                pred_int_, n_, npad_, part_log_, part_rank_, d_level, d_pred);
 }
 
 unsigned long long BfsEngine::resolve_scanned() const {
