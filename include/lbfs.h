@@ -215,6 +215,13 @@ int lbfs_part_level_done(lbfs_graph* g, const uint64_t* red_global, lbfs_layer* 
 /* Owned vertices' pred (pad32(n)) / level (n) in original ids; every other
  * entry is LBFS_SENTINEL / -1, so the ranks' outputs combine by min / max. */
 int lbfs_part_finish(lbfs_graph* g, int32_t* d_pred, int32_t* d_level, void* stream);
+/* The coming level's slice sizes, valid after lbfs_part_level_done: words
+ * per peer of the all-to-all (W for bitmaps, or a sparse id list) and per
+ * rank of the all-gather (W + 4, or a list). Identical on every rank (they
+ * follow from the level's global frontier edges E_L): levels with
+ * 2 (E_L + 8) <= W exchange [count, ids...] lists (SURVEY §8e sparse
+ * exchange). Buffers stay sized for the dense case. */
+int lbfs_part_plan(lbfs_graph* g, int64_t* a2a_words, int64_t* gather_words);
 /* Adjacency entries read by parent resolution since lbfs_part_start. */
 int lbfs_part_resolve_count(lbfs_graph* g, int64_t* out);
 

@@ -92,6 +92,7 @@ SIGNATURES = {
     "lbfs_part_level_done": (ctypes.c_int, [_p, _p, ctypes.POINTER(Layer), ctypes.POINTER(ctypes.c_int)]),
     "lbfs_part_finish": (ctypes.c_int, [_p, _p, _p, _p]),
     "lbfs_part_resolve_count": (ctypes.c_int, [_p, ctypes.POINTER(_i64)]),
+    "lbfs_part_plan": (ctypes.c_int, [_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "lbfs_nccl_unique_id": (ctypes.c_int, [_p]),
     "lbfs_part_attach_nccl": (ctypes.c_int, [_p, _p, ctypes.c_int, ctypes.c_int]),
     "lbfs_part_bfs": (ctypes.c_int, [_p, _i64, _p, _p, ctypes.c_int, ctypes.POINTER(Layer), _i64,

@@ -660,6 +660,14 @@ int lbfs_part_bfs(lbfs_graph* g, int64_t root, int32_t* d_pred, int32_t* d_level
   });
 }
 
+int lbfs_part_plan(lbfs_graph* g, int64_t* a2a_words, int64_t* gather_words) {
+  return guarded([&] {
+    BfsEngine& e = part_engine(g);
+    std::lock_guard<std::mutex> lk(e.mu);
+    e.part_plan(a2a_words, gather_words);
+  });
+}
+
 int lbfs_part_resolve_count(lbfs_graph* g, int64_t* out) {
   return guarded([&] {
     BfsEngine& e = part_engine(g);

@@ -1676,6 +1676,7 @@ BfsEngine::~BfsEngine() {
   dev_free(fglob_);
   if (h_red_) cudaFreeHost(h_red_);
   dev_free(red_dev_);
+  dev_free(part_err_);
   dev_free(resolve_cnt_);
   dev_free(old2new_);
   cudaStreamSynchronize(res_st_);
@@ -2069,6 +2070,7 @@ void BfsEngine::read_env() {
   split_ = env_flag("LBFS_SPLIT");   // one launch per bin, timed separately
   count_ = env_flag("LBFS_COUNT");   // candidate-write counters (slow)
   part_heavy_off_ = geti("LBFS_PART_HEAVY", 1) == 0;
+  part_sparse_mode_ = (int)geti("LBFS_PART_SPARSE", 1);
   bu_alpha_ = (int)std::max<long long>(1, geti("LBFS_BU_ALPHA", 14));
   bu_beta_ = (int)std::max<long long>(1, geti("LBFS_BU_BETA", 24));
   bitmap_div_ = (int)std::max<long long>(1, geti("LBFS_BITMAP_DIV", kBitmapDiv));  // bitmap mode from n / this edges

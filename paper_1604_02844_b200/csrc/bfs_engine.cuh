@@ -347,6 +347,8 @@ class BfsEngine {
   void part_sync(const uint32_t* fgath, cudaStream_t st);
   void part_level_done(const unsigned long long* red_global, lbfs_layer* layer, int* done);
   void part_finish(int32_t* d_pred, int32_t* d_level, cudaStream_t st);
+  // words per peer of the coming level's all-to-all / per rank of its all-gather
+  void part_plan(int64_t* a2a_words, int64_t* gather_words) const;
   int nparts() const { return nparts_; }
   int part_rank() const { return part_rank_; }
   int64_t nwords() const { return nwords_; }
@@ -504,6 +506,14 @@ class BfsEngine {
   bool snap_used_[2] = {false, false};
   int snap_next_ = 0;
   const uint32_t* part_fgath_ = nullptr;  // the gathered slices of the level (part_sync -> part_level_done)
+  // sparse exchange of the current level (partition.cu): S words per peer in
+  // the all-to-all, G per rank in the all-gather
+  bool part_sparse_ = false;
+  int part_sparse_mode_ = 1;  // LBFS_PART_SPARSE: 0 never, 1 when 2 (E_L + 8) <= W, 2 whenever E_L + 8 <= W
+  int64_t part_S_ = 0, part_G_ = 0;
+  uint32_t* part_send_ = nullptr;  // the level's send slices (own marks -> prev after a sparse level)
+  unsigned long long* part_err_ = nullptr;
+  void part_choose_format();
   bool part_heavy_off_ = false;  // LBFS_PART_HEAVY=0
   bool count_ = false;
   bool split_ = false;

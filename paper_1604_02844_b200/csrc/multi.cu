@@ -271,6 +271,10 @@ void MultiGraph::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timin
   each([&](int, BfsEngine& e, Bufs& b, cudaStream_t) { e.part_level_done(b.red, nullptr, &done); });
   layers_.clear();
   while (!done) {
+    // this level's slice sizes (dense bitmaps or sparse id lists; the same
+    // on every rank: they follow from the level's global frontier edges)
+    int64_t a2a_words = 0, gather_words = 0;
+    parts_[0]->part_plan(&a2a_words, &gather_words);
     each([&](int, BfsEngine& e, Bufs& b, cudaStream_t st) {
       e.part_expand(st);
       if (!solo) e.part_pack(b.send, st);
@@ -278,14 +282,14 @@ void MultiGraph::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timin
     if (!solo) {
       Group g;
       each([&](int p, BfsEngine&, Bufs& b, cudaStream_t st) {
-        nccl_check(api.AlltoAll(b.send, b.recv, (size_t)b.nwl, ncclUint32, comm_[p], st), "ncclAlltoAll");
+        nccl_check(api.AlltoAll(b.send, b.recv, (size_t)a2a_words, ncclUint32, comm_[p], st), "ncclAlltoAll");
       });
     }
     each([&](int, BfsEngine& e, Bufs& b, cudaStream_t st) { e.part_merge(b.recv, b.fsend, st); });
     if (!solo) {
       Group g;
       each([&](int p, BfsEngine&, Bufs& b, cudaStream_t st) {
-        nccl_check(api.AllGather(b.fsend, b.fgath, (size_t)(b.nwl + 4), ncclUint32, comm_[p], st), "ncclAllGather");
+        nccl_check(api.AllGather(b.fsend, b.fgath, (size_t)gather_words, ncclUint32, comm_[p], st), "ncclAllGather");
       });
     }
     each([&](int, BfsEngine& e, Bufs& b, cudaStream_t st) { e.part_sync(solo ? b.fsend : b.fgath, st); });

@@ -22,6 +22,17 @@
 //            the gathered counts summed on the device
 //   done     host reads the summed counts: the layer (input, edges,
 //            discovered) and termination, identical on every rank
+// Sparse levels: when the level's global frontier edges E_L are
+// small against the dense slices (2 (E_L + 8) <= W words), both exchanges
+// carry id lists instead of bitmaps — a rank marks at most E_L vertices and
+// discovers at most E_L, so slices of E_L + 1 (+ 4) words cannot overflow and
+// every rank sizes them alike from E_L:
+//   pack     [count, ids...] per peer (S words each)     -> all_to_all
+//   merge    test-and-set of the received ids + parents, compaction, then the
+//            owned new ids as [4 count words, count, ids...] (G words)
+//                                                        -> all_gather
+//   sync     F_{L+1} rebuilt from the lists; the rank's own sent marks
+//            enter prev (visited & ~prev stays this level's marks only)
 // The level structure is the reference's level-synchronous loop
 // (traversal.py:90, 152, 366); the exchange replaces nothing in the
 // reference (it is single-node CPU) and follows SURVEY §8e.
@@ -39,6 +50,100 @@ __global__ void k_part_pack(const uint32_t* __restrict__ visited, const uint32_t
     const int64_t h = i / nwl, j = i - h * nwl;
     const int64_t gw = (j << part_log) | h;
     send[i] = (h == rank) ? 0u : (visited[gw] & ~prev[gw]);
+  }
+}
+
+// ---- sparse levels: id lists instead of bitmaps ----------------------------
+// send[h*S] = number of ids for peer h, send[h*S + 1 + i] = the ids (global
+// internal); the counts are zeroed by the caller. err counts overflows (none
+// by construction: a rank marks at most E_L vertices).
+__global__ void k_part_pack_sparse(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ prev,
+                                   int64_t nwords, int part_log, int rank, uint32_t* __restrict__ send, int64_t S,
+                                   unsigned long long* err) {
+  const int64_t mask = (1 << part_log) - 1;
+  for (int64_t gw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gw < nwords; gw += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = gw & mask;
+    if (h == rank) continue;
+    uint32_t m = visited[gw] & ~prev[gw];
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t pos = atomicAdd(send + h * S, 1u);
+      if (pos + 1 < (uint64_t)S) send[h * S + 1 + pos] = (uint32_t)(gw * 32 + b);
+      else atomicAdd(err, 1ull);
+    }
+  }
+}
+
+// Received ids (owned by this rank): test-and-set; a new one gets its parent
+// (first neighbour in F_L = fglob). Thread per list slot.
+__global__ void k_part_merge_sparse(const uint32_t* __restrict__ recv, int64_t S, int nparts, int part_log, int rank,
+                                    uint32_t* __restrict__ visited, const uint32_t* __restrict__ fglob,
+                                    const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                                    const int32_t* __restrict__ new2old, int32_t* __restrict__ pred_int,
+                                    unsigned long long* __restrict__ scanned) {
+  unsigned long long cnt = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nparts * S; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / S, k = i - p * S;
+    if (p == rank || k == 0 || k > (int64_t)recv[p * S]) continue;
+    const int32_t v = (int32_t)recv[i];
+    const uint32_t bit = 1u << (v & 31);
+    if (atomicOr(visited + (v >> 5), bit) & bit) continue;
+    const int64_t l = part_local(v, part_log);
+    const int64_t e0 = row_ptr[l], e1 = row_ptr[l + 1];
+    int32_t par = kSentinel;
+    for (int64_t e = e0; e < e1; ++e) {
+      const int32_t u = __ldg(col_idx + e);
+      ++cnt;
+      if ((__ldg(fglob + (u >> 5)) >> (u & 31)) & 1u) {
+        par = __ldg(new2old + u);
+        break;
+      }
+    }
+    pred_int[l] = par;
+  }
+  if (cnt && scanned) atomicAdd(scanned, cnt);
+}
+
+// The owned new vertices (front: owned words of F_{L+1}, local numbering) as
+// the list out[5 ...], out[4] = count (zeroed by the caller).
+__global__ void k_part_listify(const uint32_t* __restrict__ front, int64_t nwl, int part_log, int rank,
+                               uint32_t* __restrict__ out, int64_t cap, unsigned long long* err) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nwl; j += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t m = front[j];
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t pos = atomicAdd(out + 4, 1u);
+      if (pos < (uint64_t)cap) out[5 + pos] = (uint32_t)part_global(j * 32 + b, part_log, rank);
+      else atomicAdd(err, 1ull);
+    }
+  }
+}
+
+// F_{L+1} from the gathered lists (fglob cleared by the caller): fglob,
+// visited and prev get every listed id; then (second kernel) this rank's own
+// sent marks enter prev.
+__global__ void k_part_sync_sparse(const uint32_t* __restrict__ fgath, int64_t G, int nparts,
+                                   uint32_t* __restrict__ fglob, uint32_t* __restrict__ visited,
+                                   uint32_t* __restrict__ prev) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nparts * G; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / G, k = i - p * G;
+    if (k < 5 || k - 5 >= (int64_t)fgath[p * G + 4]) continue;
+    const uint32_t v = fgath[i];
+    const uint32_t bit = 1u << (v & 31);
+    atomicOr(fglob + (v >> 5), bit);
+    atomicOr(visited + (v >> 5), bit);
+    atomicOr(prev + (v >> 5), bit);
+  }
+}
+__global__ void k_part_marks_to_prev(const uint32_t* __restrict__ send, int64_t S, int nparts, int rank,
+                                     uint32_t* __restrict__ prev) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nparts * S; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / S, k = i - p * S;
+    if (p == rank || k == 0 || k > (int64_t)send[p * S]) continue;
+    const uint32_t v = send[i];
+    atomicOr(prev + (v >> 5), 1u << (v & 31));
   }
 }
 
@@ -127,9 +232,9 @@ __global__ void k_part_counts(const Counters* __restrict__ c, uint32_t* __restri
 // (the start's all-reduced root counts) or, after a level, the sum of the P
 // count tails of the gathered slices fgath.
 __global__ void k_part_publish(const Counters* __restrict__ cnt, const unsigned long long* __restrict__ red,
-                               const uint32_t* __restrict__ fgath, int nparts, int64_t stride, int64_t nwl,
-                               Counters* mail, unsigned long long* red_mail, unsigned long long* seq,
-                               unsigned long long value) {
+                               const uint32_t* __restrict__ fgath, int nparts, int64_t stride, int64_t tail_off,
+                               const unsigned long long* __restrict__ err, Counters* mail,
+                               unsigned long long* red_mail, unsigned long long* seq, unsigned long long value) {
   const int t = threadIdx.x;
   constexpr int kWords = (int)(sizeof(Counters) / 8);
   if (cnt && t < kWords)
@@ -140,12 +245,13 @@ __global__ void k_part_publish(const Counters* __restrict__ cnt, const unsigned 
       s = red[t];
     } else {
       for (int p = 0; p < nparts; ++p) {
-        const uint32_t* tail = fgath + p * stride + nwl + 2 * t;
+        const uint32_t* tail = fgath + p * stride + tail_off + 2 * t;
         s += (unsigned long long)tail[0] | ((unsigned long long)tail[1] << 32);
       }
     }
     reinterpret_cast<volatile unsigned long long*>(red_mail)[t] = s;
   }
+  if (t == 2) reinterpret_cast<volatile unsigned long long*>(red_mail)[2] = err ? *err : 0ull;
   __syncwarp();
   if (t == 0) {
     __threadfence_system();
@@ -214,7 +320,6 @@ static unsigned grid_for(int64_t work, int sm_count) { return clamp_grid((work +
 
 void BfsEngine::part_start(int64_t root, cudaStream_t st, unsigned long long* red) {
   if (root < 0 || root >= n_) throw_inval("root out of range");
-  read_env();
   part_st_ = st;
   if (side_pending_) {  // an abandoned BFS left side work: it reads level_int, which k_init resets
     LBFS_CUDA(cudaStreamSynchronize(res_st_));
@@ -222,9 +327,12 @@ void BfsEngine::part_start(int64_t root, cudaStream_t st, unsigned long long* re
   }
   if (!h_red_) {
     void* m = nullptr;
-    LBFS_CUDA(cudaHostAlloc(&m, 2 * sizeof(unsigned long long), cudaHostAllocMapped));
+    LBFS_CUDA(cudaHostAlloc(&m, 4 * sizeof(unsigned long long), cudaHostAllocMapped));
     h_red_ = reinterpret_cast<unsigned long long*>(m);
   }
+  if (!part_err_) part_err_ = dev_alloc<unsigned long long>(1);
+  LBFS_CUDA(cudaMemsetAsync(part_err_, 0, sizeof(unsigned long long), st));
+  part_sparse_ = false;
   LBFS_LAUNCH(k_init, grid_for(std::max(nwords_, n_loc_) / 4, sm_count_), 256, 0, st, (uint4*)visited_,
               (uint4*)prev_, (nwords_ + 3) / 4, (int4*)level_int_, (n_loc_ + 3) / 4);
   if (fglob_) LBFS_CUDA(cudaMemsetAsync(fglob_, 0, sizeof(uint32_t) * (size_t)nwords_, st));
@@ -254,7 +362,6 @@ void BfsEngine::part_expand(cudaStream_t st) {
   // (the level's global frontier edges >= nnz / heavy_div) use the blind-OR
   // semantics: no parent is written during the expansion, part_merge resolves
   // the parents of every new owned vertex
-  read_env();
   part_heavy_ = stage_ && heavy_div_ > 0 && part_edges_ * (unsigned long long)heavy_div_ >= (unsigned long long)nnz_ &&
                 !part_heavy_off_;
   expand_level(a, c, part_heavy_ ? kHeavy : kBitmapOut, part_prev_bitmap_, part_cur_, L, st);
@@ -263,13 +370,45 @@ void BfsEngine::part_expand(cudaStream_t st) {
 
 void BfsEngine::part_pack(uint32_t* send, cudaStream_t st) {
   part_st_ = st;
+  part_send_ = send;
+  if (part_sparse_) {
+    LBFS_CUDA(cudaMemsetAsync(send, 0, sizeof(uint32_t) * (size_t)(nparts_ * part_S_), st));
+    LBFS_LAUNCH(k_part_pack_sparse, grid_for(nwords_, sm_count_), 256, 0, st, visited_, prev_, nwords_, part_log_,
+                part_rank_, send, part_S_, part_err_);
+    return;
+  }
   LBFS_LAUNCH(k_part_pack, grid_for(nwords_, sm_count_), 256, 0, st, visited_, prev_, send, nwl_, part_log_,
               part_rank_);
+}
+
+void BfsEngine::part_plan(int64_t* a2a_words, int64_t* gather_words) const {
+  if (a2a_words) *a2a_words = part_sparse_ ? part_S_ : nwl_;
+  if (gather_words) *gather_words = part_sparse_ ? part_G_ : nwl_ + 4;
+}
+
+// the next level's exchange format, from its global frontier edges (the same
+// on every rank)
+void BfsEngine::part_choose_format() {
+  const int64_t E = (int64_t)part_edges_;
+  part_sparse_ = nparts_ > 1 && part_sparse_mode_ != 0 &&
+                 (part_sparse_mode_ == 2 ? E + 8 <= nwl_ : 2 * (E + 8) <= nwl_);
+  part_S_ = (E + 1 + 3) & ~int64_t(3);
+  part_G_ = (E + 5 + 3) & ~int64_t(3);
 }
 
 void BfsEngine::part_merge(const uint32_t* recv, uint32_t* fsend, cudaStream_t st) {
   part_st_ = st;
   const int64_t L = part_L_;
+  if (part_sparse_) {  // (never heavy: a sparse level is small)
+    LBFS_LAUNCH(k_part_merge_sparse, grid_for(nparts_ * part_S_, sm_count_), 256, 0, st, recv, part_S_, nparts_,
+                part_log_, part_rank_, visited_, fglob_, row_ptr_, col_idx_, new2old_, pred_int_, resolve_cnt_);
+    compact_level(part_cur_, L, nullptr, st);
+    LBFS_CUDA(cudaMemsetAsync(fsend + 4, 0, sizeof(uint32_t), st));
+    LBFS_LAUNCH(k_part_listify, grid_for(nwl_, sm_count_), 256, 0, st, front_, nwl_, part_log_, part_rank_, fsend,
+                part_G_ - 5, part_err_);
+    LBFS_LAUNCH(k_part_counts, 1, 1, 0, st, &cnt_[(L + 1) % kCounterRing], fsend);
+    return;
+  }
   if (nparts_ > 1)
     LBFS_LAUNCH(k_part_merge, grid_for(nwl_ * 32, sm_count_), 256, 0, st, recv, nwl_, part_log_, part_rank_,
                 visited_, part_heavy_ ? nullptr : fglob_ /* F_L */, row_ptr_, col_idx_, new2old_, pred_int_,
@@ -300,9 +439,16 @@ void BfsEngine::part_merge(const uint32_t* recv, uint32_t* fsend, cudaStream_t s
 void BfsEngine::part_sync(const uint32_t* fgath, cudaStream_t st) {
   part_st_ = st;
   // (one partition: visited and prev are already complete after k_compact)
-  if (nparts_ > 1)
+  if (part_sparse_) {
+    LBFS_CUDA(cudaMemsetAsync(fglob_, 0, sizeof(uint32_t) * (size_t)nwords_, st));
+    LBFS_LAUNCH(k_part_sync_sparse, grid_for(nparts_ * part_G_, sm_count_), 256, 0, st, fgath, part_G_, nparts_,
+                fglob_, visited_, prev_);
+    LBFS_LAUNCH(k_part_marks_to_prev, grid_for(nparts_ * part_S_, sm_count_), 256, 0, st, part_send_, part_S_,
+                nparts_, part_rank_, prev_);
+  } else if (nparts_ > 1) {
     LBFS_LAUNCH(k_part_sync, grid_for(nwords_, sm_count_), 256, 0, st, fgath, fglob_, visited_, prev_, nwords_,
                 nwl_ + 4, part_log_);
+  }
   part_fgath_ = fgath;  // (part_level_done sums its count tails)
 }
 
@@ -314,16 +460,20 @@ void BfsEngine::part_level_done(const unsigned long long* red_global, lbfs_layer
   const unsigned long long want = ++seq_;
   // (a level: the global counts are the sum of the gathered slices' tails)
   LBFS_LAUNCH(k_part_publish, 1, 32, 0, st, L >= 0 ? &cnt_[slot] : nullptr, red_global, part_fgath_, nparts_,
-              nwl_ + 4, nwl_, h_mail_, h_red_, h_seq_, want);
+              part_sparse_ ? part_G_ : nwl_ + 4, part_sparse_ ? int64_t(0) : nwl_, part_err_, h_mail_, h_red_, h_seq_,
+              want);
   part_fgath_ = nullptr;
   wait_mail(want, st);
   if (L >= 0) h_cnt_[slot] = *const_cast<const Counters*>(h_mail_);
+  if (reinterpret_cast<volatile unsigned long long*>(h_red_)[2])
+    throw Failure(LBFS_ECUDA, "internal: sparse exchange slice overflow");
   const unsigned long long disc = reinterpret_cast<volatile unsigned long long*>(h_red_)[0],
                            edges = reinterpret_cast<volatile unsigned long long*>(h_red_)[1];
   if (L < 0) {  // start: the summed root counts (1, deg(root)) become frontier 0
     part_in_ = disc;
     part_edges_ = edges;
     part_L_ = 0;
+    part_choose_format();
     if (layer) *layer = lbfs_layer{0, 0, 0};
     if (done) *done = disc == 0;
     return;
@@ -339,6 +489,7 @@ void BfsEngine::part_level_done(const unsigned long long* red_global, lbfs_layer
   part_in_ = disc;
   part_edges_ = edges;
   part_L_ = L + 1;
+  part_choose_format();
   part_cur_ ^= 1;
   part_prev_bitmap_ = true;
 }

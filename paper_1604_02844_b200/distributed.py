@@ -178,6 +178,13 @@ class PartitionedGraph:
         ls = [LayerStats(int(x.input), int(x.edges), int(x.discovered)) for x in layers[:nl.value]]
         return PartitionedResult(ls, sum(l.edges for l in ls), pred, level, gather, t.as_dict())
 
+    def plan(self) -> tuple[int, int]:
+        """(all-to-all words per peer, all-gather words per rank) of the
+        coming level: the dense bitmap slices or, for a small level, id lists."""
+        a, g = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.load().lbfs_part_plan(self._h, ctypes.byref(a), ctypes.byref(g)))
+        return a.value, g.value
+
     def resolve_count(self) -> int:
         v = ctypes.c_int64()
         _lib.check(_lib.load().lbfs_part_resolve_count(self._h, ctypes.byref(v)))
@@ -276,17 +283,25 @@ def bfs_partitioned(parts: list, root: int, exchange, bufs: list | None = None, 
     for p, b in zip(parts, bufs):
         p.level_done(b["red"])
     layers = []
+    P = parts[0].nparts
     while True:
+        # this level's slice sizes (identical on every rank; objects without
+        # plan() exchange the dense slices)
+        S, G = parts[0].plan() if hasattr(parts[0], "plan") else (None, None)
+        send = [b["send"][:P * S] if S else b["send"] for b in bufs]
+        recv = [b["recv"][:P * S] if S else b["recv"] for b in bufs]
+        fsend = [b["fsend"][:G] if G else b["fsend"] for b in bufs]
+        fgath = [b["fgath"][:P * G] if G else b["fgath"] for b in bufs]
         for p in parts:
             p.expand()
-        for p, b in zip(parts, bufs):
-            p.pack(b["send"])
-        exchange.all_to_all([b["send"] for b in bufs], [b["recv"] for b in bufs])
-        for p, b in zip(parts, bufs):
-            p.merge(b["recv"], b["fsend"])
-        exchange.all_gather([b["fsend"] for b in bufs], [b["fgath"] for b in bufs])
-        for p, b in zip(parts, bufs):
-            p.sync(b["fgath"])
+        for p, s in zip(parts, send):
+            p.pack(s)
+        exchange.all_to_all(send, recv)
+        for p, r, f in zip(parts, recv, fsend):
+            p.merge(r, f)
+        exchange.all_gather(fsend, fgath)
+        for p, f in zip(parts, fgath):
+            p.sync(f)
         outs = [p.level_done() for p in parts]
         layer, done = outs[0]
         assert all(o == outs[0] for o in outs), "partitions disagree on the layer"

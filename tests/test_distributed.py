@@ -152,6 +152,35 @@ def test_gpu_partitions_rmat(nparts):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["0", "2"])
+@pytest.mark.parametrize("nparts", [2, 8])
+def test_gpu_partitions_sparse_exchange(monkeypatch, nparts, mode):
+    """LBFS_PART_SPARSE=2: every level whose lists fit the slices exchanges
+    [count, ids] lists (all-to-all of marks, all-gather of the new owned
+    ids); =0: never. Same layers, levels and certified trees either way; the
+    lattice (small frontiers, many levels) and an R-MAT graph."""
+    from paper_1604_02844_b200 import RmatParams, build_rmat_graph, bfs, CsrGraph
+    monkeypatch.setenv("LBFS_PART_SPARSE", mode)  # (read when the partition handle is made)
+    n, lrp, lci = _lattice(64, 50)
+    cases = [(build_rmat_graph(RmatParams(scale=13, edgefactor=16, seed=4)), None), (CsrGraph(n, lci, lrp), 0)]
+    for g, r0 in cases:
+        rp, ci, n = g.colstarts, g.rows, g.num_vertices
+        parts = _device_parts(g, nparts)
+        sizes = []
+        roots = [r0] if r0 is not None else [int(r) for r in oracle.pick_roots(np.diff(rp), 3, 7)]
+        for root in roots:
+            res = bfs_partitioned(parts, root, LocalExchange())
+            for pred, level in zip(res.pred, res.level):
+                _check(n, rp, ci, root, res, pred.cpu().numpy(), level.cpu().numpy())
+            sizes.append(parts[0].plan())
+        W = parts[0].words_per_peer
+        if mode == "0":
+            assert all(s == (W, W + 4) for s in sizes)
+        else:  # after the last level (E = 0) the plan is a list
+            assert all(s[0] < W for s in sizes)
+
+
+@pytest.mark.gpu
 def test_gpu_partitions_match_emulation_per_rank():
     """Owned outputs before the gather: levels identical to the oracle's
     partition; every rank's pred entries lie on its own vertices."""
