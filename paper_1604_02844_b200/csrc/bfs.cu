@@ -170,8 +170,8 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, const int32_t (
       st[k] = a.row_ptr[v];
       deg[k] = (int32_t)(a.row_ptr[v + 1] - st[k]);
       ns += (v >= a.t_warp && v < a.t_nz);
-      nw += (v >= a.t_cta && v < a.t_warp);
-      hub |= v < a.t_cta;
+      nw += (v >= a.t_cta && v < a.t_hub);
+      hub |= v < a.t_hub;
     }
   }
   // exclusive offsets of this lane's small (low half) and warp (high half) appends
@@ -198,14 +198,14 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, const int32_t (
     a.level_int[v] = a.next_level;                 // internal order; k_finalize writes the outputs
     a.pred_int[v] = par(k);                        // parents travel as original ids
     if (v >= a.t_warp && v < a.t_nz) a.next_small[os++] = v;
-    if (v >= a.t_cta && v < a.t_warp) a.next_warp[ow++] = v;
+    if (v >= a.t_cta && v < a.t_hub) a.next_warp[ow++] = v;
     acc.disc += 1;
     acc.edges += (unsigned long long)deg[k];
   }
   if (!__any_sync(kFull, hub)) return;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    const bool w = ((win >> k) & 1u) && nb[k] < a.t_cta;
+    const bool w = ((win >> k) & 1u) && nb[k] < a.t_hub;
     if (!__any_sync(kFull, w)) continue;
     const int items = w ? (deg[k] + a.qchunk - 1) / a.qchunk : 0;
     const int32_t vo = w ? __ldg(a.new2old + nb[k]) : 0;
@@ -237,6 +237,80 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, const int32_t (
 // traversal.py:145-147). Lanes hitting the same bitmap word elect one
 // writer: one red.or to the bitmap and one OR into the shared copy per word
 // per warp step; each lane stores its parent (original id) to pred_int[v].
+
+// Heavy levels: blind OR of target v (when ok != 0): into the CTA's shared
+// copy when its word is below hot_words, else into visited in L2. Predicated,
+// no branch.
+__device__ __forceinline__ void heavy_or(const Hot& h, const uint32_t* visited, uint32_t v, uint32_t ok,
+                                         uint32_t hot_words) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred pk, ph, pc;\n\t"
+      ".reg .u32 wi, sa, bit;\n\t"
+      ".reg .u64 ga;\n\t"
+      "shr.u32 wi, %0, 5;\n\t"
+      "shf.l.wrap.b32 bit, 0, 1, %0;\n\t"
+      "setp.ne.u32 pk, %1, 0;\n\t"
+      "setp.lt.and.u32 ph, wi, %2, pk;\n\t"
+      "setp.ge.and.u32 pc, wi, %2, pk;\n\t"
+      "shl.b32 sa, wi, 2;\n\t"
+      "add.u32 sa, sa, %3;\n\t"
+      "mad.wide.u32 ga, wi, 4, %4;\n\t"
+      "@ph red.shared.or.b32 [sa], bit;\n\t"
+      "@pc red.relaxed.gpu.global.or.b32 [ga], bit;\n\t"
+      "}" ::"r"(v),
+      "r"(ok), "r"(hot_words), "r"(h.base), "l"(visited)
+      : "memory");
+}
+// ... every lane's target known valid (a full interior window)
+__device__ __forceinline__ void heavy_or_full(const Hot& h, const uint32_t* visited, uint32_t v) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred ph;\n\t"
+      ".reg .u32 wi, sa, bit;\n\t"
+      ".reg .u64 ga;\n\t"
+      "shr.u32 wi, %0, 5;\n\t"
+      "shf.l.wrap.b32 bit, 0, 1, %0;\n\t"
+      "setp.lt.u32 ph, wi, %1;\n\t"
+      "shl.b32 sa, wi, 2;\n\t"
+      "add.u32 sa, sa, %2;\n\t"
+      "mad.wide.u32 ga, wi, 4, %3;\n\t"
+      "@ph red.shared.or.b32 [sa], bit;\n\t"
+      "@!ph red.relaxed.gpu.global.or.b32 [ga], bit;\n\t"
+      "}" ::"r"(v),
+      "r"((uint32_t)h.words), "r"(h.base), "l"(visited)
+      : "memory");
+}
+// ... target known to lie in the hot prefix
+__device__ __forceinline__ void heavy_or_hot(const Hot& h, uint32_t v, uint32_t ok) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred pk;\n\t"
+      ".reg .u32 sa, bit;\n\t"
+      "shf.l.wrap.b32 bit, 0, 1, %0;\n\t"
+      "setp.ne.u32 pk, %1, 0;\n\t"
+      "shr.u32 sa, %0, 3;\n\t"
+      "and.b32 sa, sa, 0xfffffffc;\n\t"
+      "add.u32 sa, sa, %2;\n\t"
+      "@pk red.shared.or.b32 [sa], bit;\n\t"
+      "}" ::"r"(v),
+      "r"(ok), "r"(h.base)
+      : "memory");
+}
+__device__ __forceinline__ void heavy_or_hot_full(const Hot& h, uint32_t v) {
+  asm volatile(
+      "{\n\t"
+      ".reg .u32 sa, bit;\n\t"
+      "shf.l.wrap.b32 bit, 0, 1, %0;\n\t"
+      "shr.u32 sa, %0, 3;\n\t"
+      "and.b32 sa, sa, 0xfffffffc;\n\t"
+      "add.u32 sa, sa, %1;\n\t"
+      "red.shared.or.b32 [sa], bit;\n\t"
+      "}" ::"r"(v),
+      "r"(h.base)
+      : "memory");
+}
+
 // Visited word of v's bitmap word wi: from the shared copy when wi is in the
 // hot prefix, else from L2 — two predicated loads, no branch, no generic
 // addressing. (Not through L1: within one k_bfs launch an L1 line may date
@@ -305,21 +379,18 @@ __device__ __forceinline__ uint32_t probe_mask(const LevelArgs& a, const Hot& h,
   uint32_t cmask = 0;
   if constexpr (M == kHeavy) {
     // hot: one red.shared.or into the CTA copy, cold: one red.or into visited
-    // in L2; nothing waits on memory and no parent is recorded (k_compact
-    // resolves the parents of every new vertex of a heavy level)
+    // in L2; nothing waits on memory and no parent is recorded (k_resolve
+    // gives every new vertex of a heavy level its parent). Branch-free: the
+    // heavy kernels are issue-bound (ncu: 81% issue slots busy with a branchy
+    // hot/cold split, ~22 instructions per element), so each element is a
+    // word index, a bit, two predicates and two predicated reductions.
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      uint32_t bit;
-      asm("shf.l.wrap.b32 %0, 0, 1, %1;" : "=r"(bit) : "r"(nb[k]));
-      const bool ok = (okmask >> k) & 1u;
-      const bool hot = W == kAllHot || (W != kAllCold && (nb[k] >> 5) < h.words);
-      LBFS_DCHECK(!ok || (nb[k] >= 0 && (int64_t)nb[k] < a.chk_n), "heavy probe target id");
-      LBFS_DCHECK(!(ok && hot) || (nb[k] >> 5) < h.words, "heavy hot word");
-      if (ok && hot) {
-        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(h.base + 4u * (uint32_t)(nb[k] >> 5)), "r"(bit) : "memory");
-      } else if (ok) {
-        red_or(a.visited + (nb[k] >> 5), bit);
-      }
+      LBFS_DCHECK(!((okmask >> k) & 1u) || (nb[k] >= 0 && (int64_t)nb[k] < a.chk_n), "heavy probe target id");
+      if constexpr (W == kAllHot)
+        heavy_or_hot(h, (uint32_t)nb[k], okmask & (1u << k));
+      else
+        heavy_or(h, a.visited, (uint32_t)nb[k], okmask & (1u << k), W == kAllCold ? 0u : (uint32_t)h.words);
     }
     return 0u;
   }
@@ -539,57 +610,88 @@ template <int M>
 constexpr int slice_depth() { return M == kHeavy || M == kQueueOut ? 4 : 2; }
 
 template <int M, typename Fetch>
-__device__ __forceinline__ void stream_slices_f(const LevelArgs& a, const Hot& h, Fetch fetch, int64_t n,
-                                                int64_t gwarp, int64_t nwarps, int lane, Acc& acc) {
+__device__ __forceinline__ void stream_slices_f(const LevelArgs& a, const Hot& h, Fetch fetch, int64_t n64,
+                                                int64_t gwarp, int64_t nwarps64, int lane, Acc& acc) {
   constexpr int D = slice_depth<M>();
-  if (gwarp >= n) return;
-  int64_t it = gwarp;
+  if (gwarp >= n64) return;
+  // (item counts are bounded by the item buffers: nnz / 128 + hubs < 2^31)
+  const int32_t n = (int32_t)n64, nwarps = (int32_t)nwarps64;
+  int32_t it = (int32_t)gwarp;
   CtaItem cur = fetch(it);
   // the descriptor after cur is loaded one row ahead, so a row switch never
   // waits on it before issuing the row's first col_idx load
   CtaItem nxt = it + nwarps < n ? fetch(it + nwarps) : CtaItem{0, 0, 0};
-  int64_t pos = cur.start & ~int64_t(3);
-  int64_t end = (cur.start + cur.len + 3) & ~int64_t(3);
-  auto load_group = [&](int64_t p0, int64_t e0, int4 (&x)[D]) {
+  // A slice in window coordinates: lp points at this lane's first element of
+  // the slice's first 128-bit-aligned window; mis = start & 3 elements of that
+  // window precede the slice, which ends at offset mis + len; span = the
+  // aligned extent. (32-bit offsets from one 64-bit pointer: the loop's
+  // address and bounds arithmetic stays out of 64-bit registers.)
+  const int32_t* lp = a.col_idx + (cur.start & ~int64_t(3)) + lane * 4;
+  int32_t mis = (int32_t)(cur.start & 3);
+  int32_t span = (mis + cur.len + 3) & ~3;
+  int32_t w = 0;  // offset of the next group's first window
+  auto load_group = [&](const int32_t* q, int32_t w0, int32_t sp, int4 (&x)[D]) {
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const int64_t i1 = p0 + d * 128 + lane * 4;
-      LBFS_DCHECK(!(i1 < e0) || (i1 >= 0 && i1 + 4 <= a.chk_nnz + 8), "slice load");
-      x[d] = i1 < e0 ? ld_stream4(a.col_idx + i1) : make_int4(0, 0, 0, 0);
+      const int32_t o = w0 + d * 128;
+      LBFS_DCHECK(!(o + lane * 4 < sp) || (q + o >= a.col_idx && q + o + 4 <= a.col_idx + a.chk_nnz + 8), "slice load");
+      x[d] = o + lane * 4 < sp ? ld_stream4(q + o) : make_int4(0, 0, 0, 0);
     }
   };
   int4 xa[D];
-  load_group(pos, end, xa);
+  load_group(lp, 0, span, xa);
   while (true) {
-    const int64_t gbase = pos;
-    const CtaItem ci = cur;
-    pos += D * 128;
+    const int32_t g_w = w, g_lo = mis, g_hi = mis + cur.len;  // this group's slice bounds
+    const int32_t pu = cur.u;
+    w += D * 128;
     bool more = true;
-    if (pos >= end) {
+    if (w >= span) {
       it += nwarps;
       if (it < n) {
         cur = nxt;
         if (it + nwarps < n) nxt = fetch(it + nwarps);
-        pos = cur.start & ~int64_t(3);
-        end = (cur.start + cur.len + 3) & ~int64_t(3);
+        lp = a.col_idx + (cur.start & ~int64_t(3)) + lane * 4;
+        mis = (int32_t)(cur.start & 3);
+        span = (mis + cur.len + 3) & ~3;
+        w = 0;
       } else {
         more = false;
       }
     }
     int4 xb[D];
     if (more) {
-      load_group(pos, end, xb);
+      load_group(lp, w, span, xb);
     } else {
 #pragma unroll
       for (int d = 0; d < D; ++d) xb[d] = make_int4(0, 0, 0, 0);
     }
-    const int32_t pu = ci.u;
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const int64_t cbase = gbase + d * 128;
-      if (cbase >= ci.start + ci.len) break;  // (warp-uniform) past the slice
+      const int32_t cw = g_w + d * 128;  // the window's offset
+      if (cw >= g_hi) break;             // (warp-uniform) past the slice
+      if constexpr (M == kHeavy) {
+        // (warp-uniform) a window inside the slice: no valid masks; a slice is
+        // part of one sorted row, so lane 31's last element is the window's
+        // largest id and tells whether every target is in the hot prefix
+        if (cw >= g_lo && cw + 128 <= g_hi) {
+          if (a.dbg) atomicAdd(a.dbg + 2, 4ull);  // LBFS_COUNT: slice elements
+          const uint32_t last = __shfl_sync(kFull, (uint32_t)xa[d].w, 31);
+          if ((last >> 5) < (uint32_t)h.words) {
+            heavy_or_hot_full(h, (uint32_t)xa[d].x);
+            heavy_or_hot_full(h, (uint32_t)xa[d].y);
+            heavy_or_hot_full(h, (uint32_t)xa[d].z);
+            heavy_or_hot_full(h, (uint32_t)xa[d].w);
+          } else {
+            heavy_or_full(h, a.visited, (uint32_t)xa[d].x);
+            heavy_or_full(h, a.visited, (uint32_t)xa[d].y);
+            heavy_or_full(h, a.visited, (uint32_t)xa[d].z);
+            heavy_or_full(h, a.visited, (uint32_t)xa[d].w);
+          }
+          continue;
+        }
+      }
       int32_t nb[4] = {xa[d].x, xa[d].y, xa[d].z, xa[d].w};
-      const int lo = (int)(ci.start - cbase) - lane * 4, hi = (int)(ci.start + ci.len - cbase) - lane * 4;
+      const int lo = g_lo - cw - lane * 4, hi = g_hi - cw - lane * 4;
       uint32_t okm = 0xFu;
       if (lo > 0 || hi < 4) {  // first/last window of a slice
         okm = 0;
@@ -852,7 +954,11 @@ __global__ void __launch_bounds__(expand_threads<M, kPhases>(), 1) k_expand(Leve
   extern __shared__ __align__(128) uint8_t s_dyn[];
   __shared__ ExpandSmem s;
   expand_init(s, a);
-  const Hot h{reinterpret_cast<uint32_t*>(s_dyn), smem_u32(s_dyn), hot_words};
+  // (the shared-window base is made opaque: left alone, the compiler
+  // rematerialises it — S2UR + three uniform ops — next to every shared OR)
+  uint32_t hot_base = smem_u32(s_dyn);
+  asm volatile("" : "+r"(hot_base));
+  const Hot h{reinterpret_cast<uint32_t*>(s_dyn), hot_base, hot_words};
   uint4* h4 = reinterpret_cast<uint4*>(h.s);
   const int hw4 = hot_words >> 2;  // hot_words is a multiple of 4
   if constexpr (M == kHeavy) {
@@ -1398,7 +1504,7 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   }
   // Bins, double-buffered: a vertex enters a bin once per BFS, so n entries
   // bound the small/warp bins; CTA items <= nnz/kChunk + #(deg >= kCtaMin).
-  cap_cta_ = nnz_loc_ / kQChunkMin + t_cta_ + 2;
+  cap_cta_ = nnz_loc_ / kQChunkMin + t_warp_ + 2;  // (queue-mode winners also emit warp-bin rows as items)
   // group items: one per started kItemElems of each 32-entry group, per block
   cap_items_ = nnz_loc_ / kItemElems + n_loc_ / 32 + 2 * ((n_loc_ + kCompactVerts - 1) / kCompactVerts) + 16;
   for (int b = 0; b < 2; ++b) {
@@ -1745,6 +1851,7 @@ LevelArgs BfsEngine::level_args() const {
   a.t_cta = t_cta_;
   a.t_warp = t_warp_;
   a.t_nz = t_nz_;
+  a.t_hub = warp_items_ ? t_warp_ : t_cta_;
   a.part_log = part_log_;
   a.part_rank = part_rank_;
   a.chk_n = n_;
@@ -1820,11 +1927,13 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
     f.n_small = (int64_t)c.bin[kBinSmall];
     f.n_warp = (int64_t)c.bin[kBinWarp];
   }
-  const int64_t need = std::max({(f.n_cta + kExpandWarps - 1) / kExpandWarps, f.dense_warp ? (int64_t)1 << 30 : 0,
-                                  (f.n_dense + kExpandWarps - 1) / kExpandWarps,
-                                  (f.n_wslice + kExpandWarps - 1) / kExpandWarps,
-                                  (f.n_items + kExpandWarps - 1) / kExpandWarps,
-                                  (f.n_warp + (f.n_small + 31) / 32 + kExpandWarps - 1) / kExpandWarps,
+  // (a queue-mode CTA has 512 threads: one work unit per warp where the grid allows it)
+  const int64_t wpc = bitmap || qgrid_old_ ? kExpandWarps : 512 / 32;
+  const int64_t need = std::max({(f.n_cta + wpc - 1) / wpc, f.dense_warp ? (int64_t)1 << 30 : 0,
+                                  (f.n_dense + wpc - 1) / wpc,
+                                  (f.n_wslice + wpc - 1) / wpc,
+                                  (f.n_items + wpc - 1) / wpc,
+                                  (f.n_warp + (f.n_small + 31) / 32 + wpc - 1) / wpc,
                                   (int64_t)1});
   const unsigned grid = bitmap ? (unsigned)expand_grid_ : clamp_grid(need, expand_grid_);
   // heavy level: the whole CSR as one window stream (stream.cu): the frontier
@@ -2092,6 +2201,9 @@ void BfsEngine::read_env() {
   cl_exit_edges_ = (unsigned long long)std::max<long long>(64, geti("LBFS_CLUSTER_EDGES", kClusterExitEdges));
   cl_no_dsm_ = env_flag("LBFS_CLUSTER_GLOBAL");  // claim on the global bitmap even when the slices fit
   cl_off_ = env_flag("LBFS_NO_CLUSTER");
+  // (experiment, off: S24 373 vs 389 GTEPS) queue-mode winners emit warp-bin rows as slice items
+  warp_items_ = env_flag("LBFS_WARP_ITEMS");
+  qgrid_old_ = env_flag("LBFS_QGRID_OLD");  // (A/B) size queue-mode grids for 32 warps per CTA
   cl_prof_ = env_flag("LBFS_CLUSTER_PROF");
   cl_force_size_ = (int)geti("LBFS_CLUSTER_SIZE", 0);  // (experiment) 2, 4, 8 or 16
   cl_dbg_ = (int)geti("LBFS_CLUSTER_DBG", 0);

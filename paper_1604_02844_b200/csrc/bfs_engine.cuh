@@ -109,6 +109,10 @@ struct LevelArgs {
   int32_t refresh_chunks;   // hub chunks between hot-snapshot refreshes (warp 0)
   int32_t next_level;
   int32_t t_cta, t_warp, t_nz;  // internal-id bin boundaries (local rows)
+  // queue-mode winners with id < t_hub emit their rows as slice items
+  // (t_warp: hubs and warp-bin rows — the next level streams them with the
+  // descriptor in hand, no row_ptr round trip per row; t_cta: hubs only)
+  int32_t t_hub;
   // partitioned run (nparts = 1 << part_log > 1): this rank owns the ids of
   // bitmap words w with w % nparts == part_rank; pred_int/level_int, rows and
   // frontier entries use local row ids, bitmaps and neighbours global ids
@@ -455,6 +459,8 @@ class BfsEngine {
   int cl_size_ = 0;               // CTAs per cluster (0: unavailable)
   bool cl_dsm_ = false;           // visited bitmap in distributed shared memory
   bool cl_no_dsm_ = false, cl_off_ = false;
+  bool qgrid_old_ = false;
+  bool warp_items_ = false;
   int64_t cl_slice_words_ = 0;
   int32_t cl_qs_ = 0;
   int cl_smem_ = 0;
