@@ -170,7 +170,7 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, const int32_t (
       st[k] = a.row_ptr[v];
       deg[k] = (int32_t)(a.row_ptr[v + 1] - st[k]);
       ns += (v >= a.t_warp && v < a.t_nz);
-      nw += (v >= a.t_cta && v < a.t_hub);
+      nw += (v >= a.t_hub && v < a.t_warp);
       hub |= v < a.t_hub;
     }
   }
@@ -198,7 +198,7 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, const int32_t (
     a.level_int[v] = a.next_level;                 // internal order; k_finalize writes the outputs
     a.pred_int[v] = par(k);                        // parents travel as original ids
     if (v >= a.t_warp && v < a.t_nz) a.next_small[os++] = v;
-    if (v >= a.t_cta && v < a.t_hub) a.next_warp[ow++] = v;
+    if (v >= a.t_hub && v < a.t_warp) a.next_warp[ow++] = v;
     acc.disc += 1;
     acc.edges += (unsigned long long)deg[k];
   }
@@ -677,10 +677,14 @@ __device__ __forceinline__ void stream_slices_f(const LevelArgs& a, const Hot& h
           if (a.dbg) atomicAdd(a.dbg + 2, 4ull);  // LBFS_COUNT: slice elements
           const uint32_t last = __shfl_sync(kFull, (uint32_t)xa[d].w, 31);
           if ((last >> 5) < (uint32_t)h.words) {
+#ifdef LBFS_NO_RUN_MERGE
             heavy_or_hot_full(h, (uint32_t)xa[d].x);
             heavy_or_hot_full(h, (uint32_t)xa[d].y);
             heavy_or_hot_full(h, (uint32_t)xa[d].z);
             heavy_or_hot_full(h, (uint32_t)xa[d].w);
+#else
+            heavy_or_hot4(h.base, (uint32_t)xa[d].x, (uint32_t)xa[d].y, (uint32_t)xa[d].z, (uint32_t)xa[d].w);
+#endif
           } else {
             heavy_or_full(h, a.visited, (uint32_t)xa[d].x);
             heavy_or_full(h, a.visited, (uint32_t)xa[d].y);
@@ -1484,8 +1488,15 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   nwl_ = nwords_ / nparts_;
   n_loc_ = nparts_ == 1 ? n_ : nwl_ * 32;
   npad_ = pad32(n_);
-  LBFS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  LBFS_CUDA(cudaStreamCreateWithFlags(&res_st_, cudaStreamNonBlocking));
+  {
+    // (experiment, off: level kernels at the highest stream priority and the
+    // side work at the lowest measured 385 vs 389 GTEPS at equal priorities)
+    int prio_lo = 0, prio_hi = 0;
+    LBFS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    const bool prio = env_flag("LBFS_STREAM_PRIO");
+    LBFS_CUDA(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio ? prio_hi : 0));
+    LBFS_CUDA(cudaStreamCreateWithPriority(&res_st_, cudaStreamNonBlocking, prio ? prio_lo : 0));
+  }
   LBFS_CUDA(cudaEventCreateWithFlags(&ev_resolve_, cudaEventDisableTiming));
   LBFS_CUDA(cudaEventCreateWithFlags(&ev_side_done_, cudaEventDisableTiming));
   for (auto& e : ev_snap_) LBFS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -2038,8 +2049,13 @@ void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t 
     LBFS_CUDA(cudaEventRecord(ev_resolve_, st));
     LBFS_CUDA(cudaStreamWaitEvent(res_st_, ev_resolve_, 0));
     const int64_t n4 = (n_loc_ + 3) / 4;
-    LBFS_LAUNCH(k_resolve, clamp_grid((n4 + 255) / 256, (int64_t)sm_count_ * 16), 256, 0, res_st_, level_int_,
-                first_nbr_, row_ptr_, col_idx_, new2old_loc_, pred_int_, n_loc_, (int32_t)(L + 1));
+    // (short blocks, no grid-stride clamp: a block that lives for the whole
+    // kernel would keep the next level's one-CTA-per-SM kernels off its SM)
+    cudaStream_t rs = resolve_inline_ ? st : res_st_;
+    LBFS_LAUNCH(k_resolve, resolve_clamp_ ? clamp_grid((n4 + 255) / 256, (int64_t)sm_count_ * 16)
+                                          : (unsigned)((n4 + 255) / 256),
+                256, 0, rs, level_int_, first_nbr_, row_ptr_, col_idx_, new2old_loc_, pred_int_, n_loc_,
+                (int32_t)(L + 1));
     side_pending_ = true;
   }
 }
@@ -2201,9 +2217,13 @@ void BfsEngine::read_env() {
   cl_exit_edges_ = (unsigned long long)std::max<long long>(64, geti("LBFS_CLUSTER_EDGES", kClusterExitEdges));
   cl_no_dsm_ = env_flag("LBFS_CLUSTER_GLOBAL");  // claim on the global bitmap even when the slices fit
   cl_off_ = env_flag("LBFS_NO_CLUSTER");
-  // (experiment, off: S24 373 vs 389 GTEPS) queue-mode winners emit warp-bin rows as slice items
-  warp_items_ = env_flag("LBFS_WARP_ITEMS");
-  qgrid_old_ = env_flag("LBFS_QGRID_OLD");  // (A/B) size queue-mode grids for 32 warps per CTA
+  // queue-mode winners emit warp-bin rows as slice items (S24 379 -> 385 GTEPS);
+  // LBFS_NO_WARP_ITEMS=1: append them to the raw warp queue instead
+  warp_items_ = !env_flag("LBFS_NO_WARP_ITEMS");
+  qgrid_old_ = env_flag("LBFS_QGRID_OLD");
+  publish_after_heavy_ = !env_flag("LBFS_NO_PUBLISH_AFTER_HEAVY");  // (A/B) always hand the next frontier to the cluster
+  resolve_inline_ = env_flag("LBFS_RESOLVE_INLINE");  // (A/B) k_resolve on the level stream
+  resolve_clamp_ = env_flag("LBFS_RESOLVE_CLAMP");    // (A/B) k_resolve as a clamped grid-stride grid  // (A/B) size queue-mode grids for 32 warps per CTA
   cl_prof_ = env_flag("LBFS_CLUSTER_PROF");
   cl_force_size_ = (int)geti("LBFS_CLUSTER_SIZE", 0);  // (experiment) 2, 4, 8 or 16
   cl_dbg_ = (int)geti("LBFS_CLUSTER_DBG", 0);
@@ -2241,6 +2261,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   layers_.clear();
   double expand_ms = 0.0, cluster_ms = 0.0;
   bool prev_bitmap = false, prev_bu = false, timed_level = false;
+  bool expect_big = false;  // the level just launched was heavy: its output is published by k_publish
   const unsigned long long bitmap_min_edges = (unsigned long long)std::max<int64_t>(bitmap_floor_, n_ / bitmap_div_);
   int64_t L = 0;
   int cur = 0;  // queue parity == L & 1
@@ -2251,7 +2272,16 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     // counters of the frontier a full-GPU level just produced
     Counters c{};
     int64_t k = 0;
-    if (use_cluster) {
+    bool small_next = true;
+    if (use_cluster && expect_big) {
+      // after a heavy level the next frontier is almost never small: a one-warp
+      // publish kernel instead of a 16-CTA cluster launch that would only
+      // publish (the cluster follows when the frontier is small after all)
+      publish_and_wait((int)(L % kCounterRing), (int)((L + 1) % kCounterRing), st);
+      c = h_cnt_[L % kCounterRing];
+      small_next = c.discovered > 0 && c.edges <= cl_exit_edges_;
+    }
+    if (use_cluster && small_next) {
       const int ce = n_cl_ev_ < kClEvents ? n_cl_ev_++ : -1;
       if (ce >= 0) LBFS_CUDA(cudaEventRecord(ev_cl_[2 * ce], st));
       launch_cluster(L, cur, prev_bitmap, st, L == 0 ? (int32_t)root : -1);
@@ -2261,6 +2291,8 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       c = *const_cast<const Counters*>(h_mail_);
       k = (int64_t)c.pad[0] - L;
       if (k < 0 || k > kLoopCap) throw Failure(LBFS_ECUDA, "internal: cluster level loop state");
+    } else if (use_cluster) {
+      // (published above)
     } else if (L == 0) {
       c = *const_cast<const Counters*>(h_mail_);
     } else {
@@ -2344,6 +2376,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       fprintf(stderr, "[lbfs]      candidate writes hot=%llu cold=%llu streamed elements=%llu dwarp rows=%llu\n",
               dbg[0], dbg[1], dbg[2], dbg[3]);
     }
+    expect_big = heavy && publish_after_heavy_;
     pend = lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, 0};
     pending = true;
     cur ^= 1;

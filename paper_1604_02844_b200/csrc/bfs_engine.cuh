@@ -171,6 +171,44 @@ __host__ __device__ __forceinline__ int64_t part_global(int64_t l, int32_t part_
   return ((((l >> 5) << part_log) | part_rank) << 5) | (l & 31);
 }
 
+// Heavy levels, a lane's four consecutive elements of a sorted row, all in the
+// hot prefix: blind ORs into the CTA's shared copy (shared-window address
+// `base`), with runs in one bitmap word merged into a single reduction. The
+// shared-atomic pipe bounds the heavy kernels (ncu: ~3.7 wavefronts per
+// ATOMS from bank and same-word conflicts), and in hub rows ~45% of the
+// elements share a word with their predecessor.
+__device__ __forceinline__ void heavy_or_hot4(uint32_t base, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p1, p2, p3;\n\t"
+      ".reg .u32 ax, ay, az, aw, bx, by, bz, bw;\n\t"
+      "shf.l.wrap.b32 bx, 0, 1, %0;\n\t"
+      "shf.l.wrap.b32 by, 0, 1, %1;\n\t"
+      "shf.l.wrap.b32 bz, 0, 1, %2;\n\t"
+      "shf.l.wrap.b32 bw, 0, 1, %3;\n\t"
+      "shr.u32 ax, %0, 5;\n\t"
+      "shr.u32 ay, %1, 5;\n\t"
+      "shr.u32 az, %2, 5;\n\t"
+      "shr.u32 aw, %3, 5;\n\t"
+      "setp.ne.u32 p1, ax, ay;\n\t"
+      "setp.ne.u32 p2, ay, az;\n\t"
+      "setp.ne.u32 p3, az, aw;\n\t"
+      "@!p1 or.b32 by, by, bx;\n\t"
+      "@!p2 or.b32 bz, bz, by;\n\t"
+      "@!p3 or.b32 bw, bw, bz;\n\t"
+      "mad.lo.u32 ax, ax, 4, %4;\n\t"
+      "mad.lo.u32 ay, ay, 4, %4;\n\t"
+      "mad.lo.u32 az, az, 4, %4;\n\t"
+      "mad.lo.u32 aw, aw, 4, %4;\n\t"
+      "@p1 red.shared.or.b32 [ax], bx;\n\t"
+      "@p2 red.shared.or.b32 [ay], by;\n\t"
+      "@p3 red.shared.or.b32 [az], bz;\n\t"
+      "red.shared.or.b32 [aw], bw;\n\t"
+      "}" ::"r"(x),
+      "r"(y), "r"(z), "r"(w), "r"(base)
+      : "memory");
+}
+
 constexpr int64_t kLoopCap = 1 << 16;  // levels per cluster-kernel launch
 
 // Small-frontier levels on one thread-block cluster (cluster.cu).
@@ -252,7 +290,12 @@ constexpr int kBitmapDiv = LBFS_BITMAP_DIV;  // bitmap-mode output when a fronti
 constexpr int kHeavyDiv = 32;  // heavy (blind-OR) semantics when a bitmap level's edges >= nnz / this
 constexpr int kSweepMinPct = LBFS_SWEEP_MIN_PCT;  // sweep a heavy level when its big-row edges >= this % of e_big
 constexpr int kSweepPrefetch = 0;    // L2 prefetch distance (chunks of a CTA)
-constexpr int kSweepRingBytes = kSweepStages * 32 * kSweepWindow * 4;
+#ifndef LBFS_SWEEP_CHUNK_WINS
+#define LBFS_SWEEP_CHUNK_WINS 32
+#endif
+constexpr int kSweepChunkWins = LBFS_SWEEP_CHUNK_WINS;  // windows per chunk (<= 32: one producer lane each), a multiple of the consumer warps
+static_assert(kSweepChunkWins <= 32 && kSweepChunkWins % kSweepConsumers == 0, "sweep chunk shape");
+constexpr int kSweepRingBytes = kSweepStages * kSweepChunkWins * kSweepWindow * 4;
 struct SweepArgs {
   const int32_t* col_idx;
   const uint2* side;        // per window: {row of its first element, offsets of rows starting inside}
@@ -460,7 +503,9 @@ class BfsEngine {
   bool cl_dsm_ = false;           // visited bitmap in distributed shared memory
   bool cl_no_dsm_ = false, cl_off_ = false;
   bool qgrid_old_ = false;
-  bool warp_items_ = false;
+  bool publish_after_heavy_ = true;
+  bool resolve_inline_ = false, resolve_clamp_ = false;
+  bool warp_items_ = true;
   int64_t cl_slice_words_ = 0;
   int32_t cl_qs_ = 0;
   int cl_smem_ = 0;

@@ -197,7 +197,7 @@ namespace {
 // CTA layout: kSweepConsumers consumer warps + 1 producer warp. The CTA
 // walks chunks blockIdx.x, blockIdx.x + gridDim.x, ... of kChunkWins
 // windows; chunk i goes through ring stage i % kStages.
-constexpr int kChunkWins = 32;                       // windows per chunk (16 KB)
+constexpr int kChunkWins = kSweepChunkWins;          // windows per chunk (16 KB at 32)
 constexpr int kConsumers = kSweepConsumers;          // consumer warps
 constexpr int kWinPerWarp = kChunkWins / kConsumers;  // windows per consumer warp per chunk
 constexpr int kEl = 4 * kWinPerWarp;                 // elements per consumer lane per chunk
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
     // a free stage; the small-region mask is loaded one ahead
     auto win_of = [&](int64_t i) {
       const int64_t w0 = (blockIdx.x + i * gridDim.x) * kChunkWins;
-      return w0 + lane < s.nwin_all ? w0 + lane : (int64_t)-1;
+      return lane < kChunkWins && w0 + lane < s.nwin_all ? w0 + lane : (int64_t)-1;
     };
     auto is_big = [&](int64_t w) { return w >= 0 && w < s.nwin; };
     auto ld_side = [&](int64_t i) {
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
         for (int k = 0; k < 4; ++k) m.vmask[k] = vmask[k];
         m.info = info;
         m.pad[0] = m.pad[1] = m.pad[2] = 0u;
-        sm.meta[st][lane] = m;
+        if (lane < kChunkWins) sm.meta[st][lane] = m;
       }
       // one bulk copy per chunk, spanning its first to last window with frontier
       // rows (a bulk copy costs ~0.25 us of TMA issue per SM: few large ones)
@@ -464,6 +464,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
             const uint32_t a = (cw[q] & bit[q]) ? dummy : sa[q];
             if (!(kSweepDbg & 1)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(bit[q]) : "memory");
           }
+#elif !defined(LBFS_NO_RUN_MERGE)
+          // (adjacent elements in one bitmap word — common in hub rows — take one OR)
+          if (!(kSweepDbg & 1))
+            heavy_or_hot4(hoff, (uint32_t)e4[0], (uint32_t)e4[1], (uint32_t)e4[2], (uint32_t)e4[3]);
 #else
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
