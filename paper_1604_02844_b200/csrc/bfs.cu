@@ -1551,7 +1551,8 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
                            (const void*)k_expand<kHeavy, 1>,      (const void*)k_expand<kHeavy, 2>,
                            (const void*)k_expand<kHeavy, 4>,
                            (const void*)k_expand<kHeavy, 16>,     (const void*)k_expand<kHeavy, 32>,
-                           (const void*)k_expand<kHeavy, 64>};
+                           (const void*)k_expand<kHeavy, 64>,     (const void*)k_expand<kHeavy, 5>,
+                           (const void*)k_expand<kQueueOut, 5>};
   size_t max_static = 0;
   for (auto fn : kernels) {
     cudaFuncAttributes fa{};
@@ -1827,6 +1828,11 @@ static void launch_expand_m(int pi, unsigned grid, int smem, const LevelArgs& a,
     LBFS_LAUNCH((k_expand<M, 32>), grid, (expand_threads<M, 32>()), smem, st, a, f, hot);
   } else if (pi == 5) {
     LBFS_LAUNCH((k_expand<M, 64>), grid, (expand_threads<M, 64>()), smem, st, a, f, hot);
+  } else if (pi == 6) {  // slice items, then the raw queues, in one launch
+    if constexpr (M == kBitmapOut)
+      throw Failure(LBFS_ECUDA, "internal: no fused bitmap-mode launch");
+    else
+      LBFS_LAUNCH((k_expand<M, 5>), grid, (expand_threads<M, 5>()), smem, st, a, f, hot);
   } else {
     LBFS_LAUNCH((k_expand<M, 4>), grid, (expand_threads<M, 4>()), smem, st, a, f, hot);
   }
@@ -2021,8 +2027,16 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
   if (any) {
     // one launch per non-empty bin: each phase kernel gets its own register
     // allocation (the fused kernel was capped at 64 registers by 1024 threads)
-    const bool has[6] = {f.n_cta > 0, f.n_items > 0, f.n_warp + f.n_small > 0, f.n_wslice > 0, f.n_dense > 0,
-                         f.dense_warp};
+    bool has[6] = {f.n_cta > 0, f.n_items > 0, f.n_warp + f.n_small > 0, f.n_wslice > 0, f.n_dense > 0,
+                   f.dense_warp};
+    // after a queue-mode level the frontier is slice items + raw queues: one
+    // launch for both (a launch costs ~5-10 us here: a queue level is short,
+    // a heavy launch zeroes and stores its hot rows)
+    if (fuse_queues_ && !prev_bitmap && mode != kBitmapOut && has[0] && has[2] && !split_) {
+      launch_expand(mode, 6, grid, a, f, st);
+      a.stage_first = 0;
+      has[0] = has[2] = false;
+    }
     for (int pi = 0; pi < 6; ++pi) {
       if (split_ && !(sweep && pi == 0)) LBFS_CUDA(cudaEventRecord(ev_split_[pi], st));
       if (!has[pi]) continue;
@@ -2221,6 +2235,7 @@ void BfsEngine::read_env() {
   // LBFS_NO_WARP_ITEMS=1: append them to the raw warp queue instead
   warp_items_ = !env_flag("LBFS_NO_WARP_ITEMS");
   qgrid_old_ = env_flag("LBFS_QGRID_OLD");
+  fuse_queues_ = !env_flag("LBFS_NO_FUSE_QUEUES");  // (A/B) one launch per bin after a queue-mode level
   publish_after_heavy_ = !env_flag("LBFS_NO_PUBLISH_AFTER_HEAVY");  // (A/B) always hand the next frontier to the cluster
   resolve_inline_ = env_flag("LBFS_RESOLVE_INLINE");  // (A/B) k_resolve on the level stream
   resolve_clamp_ = env_flag("LBFS_RESOLVE_CLAMP");    // (A/B) k_resolve as a clamped grid-stride grid  // (A/B) size queue-mode grids for 32 warps per CTA

@@ -503,6 +503,7 @@ class BfsEngine {
   bool cl_dsm_ = false;           // visited bitmap in distributed shared memory
   bool cl_no_dsm_ = false, cl_off_ = false;
   bool qgrid_old_ = false;
+  bool fuse_queues_ = true;
   bool publish_after_heavy_ = true;
   bool resolve_inline_ = false, resolve_clamp_ = false;
   bool warp_items_ = true;
