@@ -2391,7 +2391,9 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       fprintf(stderr, "[lbfs]      candidate writes hot=%llu cold=%llu streamed elements=%llu dwarp rows=%llu\n",
               dbg[0], dbg[1], dbg[2], dbg[3]);
     }
-    expect_big = heavy && publish_after_heavy_;
+    // ... or a level of the growth phase (its frontier has 8x the edges of the one before)
+    const unsigned long long before_edges = layers_.empty() ? 0ull : (unsigned long long)layers_.back().edges;
+    expect_big = publish_after_heavy_ && (heavy || (!bottom_up && c.edges >= 8ull * before_edges));
     pend = lbfs_layer{(int64_t)c.discovered, (int64_t)c.edges, 0};
     pending = true;
     cur ^= 1;

@@ -209,6 +209,27 @@ __device__ __forceinline__ void heavy_or_hot4(uint32_t base, uint32_t x, uint32_
       : "memory");
 }
 
+// ... one target, valid in every lane, hot or cold: the word index decides
+// between the shared copy and visited in L2 (ptxas turns the two predicated
+// reductions into short forward branches; no other control flow).
+__device__ __forceinline__ void heavy_or_any(uint32_t base, uint32_t hot_words, const uint32_t* visited, uint32_t v) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred ph;\n\t"
+      ".reg .u32 wi, sa, bit;\n\t"
+      ".reg .u64 ga;\n\t"
+      "shr.u32 wi, %0, 5;\n\t"
+      "shf.l.wrap.b32 bit, 0, 1, %0;\n\t"
+      "setp.lt.u32 ph, wi, %1;\n\t"
+      "mad.lo.u32 sa, wi, 4, %2;\n\t"
+      "mad.wide.u32 ga, wi, 4, %3;\n\t"
+      "@ph red.shared.or.b32 [sa], bit;\n\t"
+      "@!ph red.relaxed.gpu.global.or.b32 [ga], bit;\n\t"
+      "}" ::"r"(v),
+      "r"(hot_words), "r"(base), "l"(visited)
+      : "memory");
+}
+
 constexpr int64_t kLoopCap = 1 << 16;  // levels per cluster-kernel launch
 
 // Small-frontier levels on one thread-block cluster (cluster.cu).

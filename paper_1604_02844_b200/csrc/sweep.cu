@@ -478,6 +478,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
                            : "memory");
           }
 #endif
+        } else if (!(kSweepDbg & 3) && __all_sync(kAll, vm[j] == 0xFu)) {
+          // whole window valid, hot and cold targets: no valid masks to test
+#pragma unroll
+          for (int q = 0; q < 4; ++q) heavy_or_any(hoff, (uint32_t)s.hot_words, s.visited, (uint32_t)e4[q]);
         } else {
 #if LBFS_SWEEP_HOTCHK
           uint32_t sa[4], cw[4];
