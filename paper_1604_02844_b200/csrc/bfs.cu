@@ -1670,6 +1670,7 @@ void BfsEngine::launch_cluster(int64_t L, int cur, bool prev_bitmap, cudaStream_
   p.slice_words = cl_slice_words_;
   p.qs = cl_qs_;
   p.qchunk = qchunk_;
+  p.exit_warps = exit_fair_ ? expand_grid_ * (512 / 32) : 0;
   p.cap = cl_cap_;
   p.in_small = q_small_[cur];
   p.in_items = q_cta_[cur];
@@ -2235,6 +2236,7 @@ void BfsEngine::read_env() {
   // LBFS_NO_WARP_ITEMS=1: append them to the raw warp queue instead
   warp_items_ = !env_flag("LBFS_NO_WARP_ITEMS");
   qgrid_old_ = env_flag("LBFS_QGRID_OLD");
+  exit_fair_ = !env_flag("LBFS_NO_EXIT_FAIR");  // (A/B) cluster exit items of qchunk edges whatever the frontier
   fuse_queues_ = !env_flag("LBFS_NO_FUSE_QUEUES");  // (A/B) one launch per bin after a queue-mode level
   publish_after_heavy_ = !env_flag("LBFS_NO_PUBLISH_AFTER_HEAVY");  // (A/B) always hand the next frontier to the cluster
   resolve_inline_ = env_flag("LBFS_RESOLVE_INLINE");  // (A/B) k_resolve on the level stream

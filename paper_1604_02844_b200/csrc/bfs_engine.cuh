@@ -259,7 +259,8 @@ struct ClusterArgs {
   int64_t nwords;
   int64_t slice_words;      // DSMEM mode: bitmap words per CTA (multiple of 8)
   int32_t qs;               // entries per shared-memory small queue
-  int32_t qchunk;           // edges per exit slice item
+  int32_t qchunk;           // edges per exit slice item (at most)
+  int32_t exit_warps;       // warps of the full-GPU queue-mode grid (0: fixed qchunk items)
   int64_t cap;              // spill / big-list capacity per buffer (>= exit_edges)
   // frontier of level L0 (counters in ring[L0 % 3]): the host's queue format,
   // or a bitmap level's list (in_small) + warp slices (in_items2) + hub slices
@@ -524,6 +525,7 @@ class BfsEngine {
   bool cl_dsm_ = false;           // visited bitmap in distributed shared memory
   bool cl_no_dsm_ = false, cl_off_ = false;
   bool qgrid_old_ = false;
+  bool exit_fair_ = true;
   bool fuse_queues_ = true;
   bool publish_after_heavy_ = true;
   bool resolve_inline_ = false, resolve_clamp_ = false;

@@ -5,7 +5,7 @@
 // ~5-8 K levels; R-MAT: the first and the last levels) is bounded by latency,
 // not bandwidth: load a row, claim its neighbours, append the winners,
 // synchronise. This kernel runs consecutive such levels inside ONE cluster of
-// C CTAs (C = 16 with non-portable cluster sizes, else 8), 1024 threads each:
+// C CTAs (C = 16 with non-portable cluster sizes, else 8), 512 threads each:
 //
 //   * visited bitmap in distributed shared memory (when it fits: n <= ~64 M
 //     vertices at C = 16): 32-byte sectors of the global bitmap are dealt to
@@ -710,7 +710,11 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
       const int64_t nb = (int64_t)__ldcg(p.big_cnt + L % kCounterRing);
       const CtaItem* bl = p.big + (L % kCounterRing) * p.cap;
       // (a bitmap-mode next level takes kChunk-edge slices, a queue-mode one qchunk)
-      const int chunk = in_edges >= p.bitmap_min_edges ? kChunk : p.qchunk;
+      // a queue-mode level is a latency chain per 128-element window: cut the
+      // items so that every warp of the full grid gets about one (>= 128 edges)
+      const int fair = (int)min((unsigned long long)p.qchunk,
+                                max(128ull, (in_edges / (unsigned long long)max(p.exit_warps, 1) + 127ull) & ~127ull));
+      const int chunk = in_edges >= p.bitmap_min_edges ? kChunk : (p.exit_warps > 0 ? fair : p.qchunk);
       for (int64_t j0 = ((int64_t)x.rank * kCW + wib) * 32; j0 < nb; j0 += (int64_t)kCT * x.csize) {
         const int64_t j = j0 + lane;
         CtaItem it{0, 0, 0};
