@@ -1634,6 +1634,11 @@ void BfsEngine::setup_cluster(int optin) {
       (void)cudaGetLastError();
       continue;
     }
+    if (dsm) {  // late segments of a shallow BFS run the global-claim kernel in the same launch shape
+      const void* fg = (const void*)k_cluster_levels<false>;
+      if (cs > 8) LBFS_CUDA(cudaFuncSetAttribute(fg, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      LBFS_CUDA(cudaFuncSetAttribute(fg, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
     cl_size_ = cs;
     cl_dsm_ = dsm;
     cl_slice_words_ = dsm ? slice : 0;
@@ -1716,7 +1721,12 @@ void BfsEngine::launch_cluster(int64_t L, int cur, bool prev_bitmap, cudaStream_
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (cl_dsm_)
+  // The bitmap lives in the cluster's shared memory for a BFS's first segment
+  // (nothing to load: visited = {root}) and for deep traversals (the lattice);
+  // a late segment of a shallow BFS (R-MAT: the last one or two levels) claims
+  // on the global bitmap instead of loading and writing back 16 slices of it
+  const bool dsm = cl_dsm_ && (root_orig >= 0 || L >= 32 || cl_dsm_always_);
+  if (dsm)
     LBFS_CUDA(cudaLaunchKernelEx(&cfg, k_cluster_levels<true>, p));
   else
     LBFS_CUDA(cudaLaunchKernelEx(&cfg, k_cluster_levels<false>, p));
@@ -2236,6 +2246,7 @@ void BfsEngine::read_env() {
   // LBFS_NO_WARP_ITEMS=1: append them to the raw warp queue instead
   warp_items_ = !env_flag("LBFS_NO_WARP_ITEMS");
   qgrid_old_ = env_flag("LBFS_QGRID_OLD");
+  cl_dsm_always_ = env_flag("LBFS_CLUSTER_DSM_ALWAYS");  // (A/B) every cluster segment with the bitmap in DSMEM
   exit_fair_ = !env_flag("LBFS_NO_EXIT_FAIR");  // (A/B) cluster exit items of qchunk edges whatever the frontier
   fuse_queues_ = !env_flag("LBFS_NO_FUSE_QUEUES");  // (A/B) one launch per bin after a queue-mode level
   publish_after_heavy_ = !env_flag("LBFS_NO_PUBLISH_AFTER_HEAVY");  // (A/B) always hand the next frontier to the cluster

@@ -525,6 +525,7 @@ class BfsEngine {
   bool cl_dsm_ = false;           // visited bitmap in distributed shared memory
   bool cl_no_dsm_ = false, cl_off_ = false;
   bool qgrid_old_ = false;
+  bool cl_dsm_always_ = false;
   bool exit_fair_ = true;
   bool fuse_queues_ = true;
   bool publish_after_heavy_ = true;
