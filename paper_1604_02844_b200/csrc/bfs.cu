@@ -1609,10 +1609,22 @@ void BfsEngine::setup_cluster(int optin) {
     const int64_t budget = (int64_t)optin - stat - 1024 - (int64_t)kMaxCluster * kClusterStage * (int64_t)sizeof(QEntry);
     const int64_t qbytes = 2 * (int64_t)sizeof(QEntry);  // per queue slot (two queues)
     bool dsm = !cl_no_dsm_ && slice * 4 + qbytes * 1024 <= budget;
-    int64_t qs = dsm ? std::min<int64_t>(8192, (budget - slice * 4) / qbytes) : std::min<int64_t>(8192, budget / qbytes);
+    // candidate mailboxes (DSMEM mode): mail_cap entries per sender, as many as
+    // fit next to the slice and queues of >= 2048 entries (else remote claims)
+    int64_t mail_cap = 0;
+    if (dsm && !cl_no_mail_)
+      for (int64_t c : {512, 256, 128})
+        if (slice * 4 + (int64_t)kMaxCluster * c * 8 + qbytes * 2048 <= budget) {
+          mail_cap = c;
+          break;
+        }
+    const int64_t mail_bytes = (int64_t)kMaxCluster * mail_cap * 8;
+    int64_t qs = dsm ? std::min<int64_t>(8192, (budget - slice * 4 - mail_bytes) / qbytes)
+                     : std::min<int64_t>(8192, budget / qbytes);
     qs &= ~int64_t(3);
     const void* fn = dsm ? (const void*)k_cluster_levels<true> : (const void*)k_cluster_levels<false>;
-    const int smem = (int)((dsm ? slice * 4 : 0) + qbytes * qs + (int64_t)kMaxCluster * kClusterStage * sizeof(QEntry));
+    const int smem = (int)((dsm ? slice * 4 : 0) + qbytes * qs + (int64_t)kMaxCluster * kClusterStage * sizeof(QEntry) +
+                           mail_bytes);
     if (cs > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
       (void)cudaGetLastError();
       continue;
@@ -1643,6 +1655,7 @@ void BfsEngine::setup_cluster(int optin) {
     cl_dsm_ = dsm;
     cl_slice_words_ = dsm ? slice : 0;
     cl_qs_ = (int32_t)qs;
+    cl_mail_cap_ = (int32_t)mail_cap;
     cl_smem_ = smem;
     break;
   }
@@ -1674,6 +1687,7 @@ void BfsEngine::launch_cluster(int64_t L, int cur, bool prev_bitmap, cudaStream_
   p.nwords = nwords_;
   p.slice_words = cl_slice_words_;
   p.qs = cl_qs_;
+  p.mail_cap = cl_mail_cap_;
   p.qchunk = qchunk_;
   p.exit_warps = exit_fair_ ? expand_grid_ * (512 / 32) : 0;
   p.cap = cl_cap_;
@@ -2240,6 +2254,7 @@ void BfsEngine::read_env() {
   qchunk_ = (int)std::min<long long>(kChunk, std::max<long long>(kQChunkMin, geti("LBFS_QCHUNK", kQChunkDefault))) & ~3;
   // small-frontier levels run on the cluster while a frontier has at most this many edges
   cl_exit_edges_ = (unsigned long long)std::max<long long>(64, geti("LBFS_CLUSTER_EDGES", kClusterExitEdges));
+  cl_no_mail_ = env_flag("LBFS_CLUSTER_NO_MAIL");  // (A/B) DSMEM mode with remote claims instead of candidate mailboxes
   cl_no_dsm_ = env_flag("LBFS_CLUSTER_GLOBAL");  // claim on the global bitmap even when the slices fit
   cl_off_ = env_flag("LBFS_NO_CLUSTER");
   // queue-mode winners emit warp-bin rows as slice items (S24 379 -> 385 GTEPS);

@@ -259,6 +259,7 @@ struct ClusterArgs {
   int64_t nwords;
   int64_t slice_words;      // DSMEM mode: bitmap words per CTA (multiple of 8)
   int32_t qs;               // entries per shared-memory small queue
+  int32_t mail_cap;         // DSMEM mode: candidates per sender in a CTA's mailbox area (0: remote claims)
   int32_t qchunk;           // edges per exit slice item (at most)
   int32_t exit_warps;       // warps of the full-GPU queue-mode grid (0: fixed qchunk items)
   int64_t cap;              // spill / big-list capacity per buffer (>= exit_edges)
@@ -533,6 +534,8 @@ class BfsEngine {
   bool warp_items_ = true;
   int64_t cl_slice_words_ = 0;
   int32_t cl_qs_ = 0;
+  int32_t cl_mail_cap_ = 0;
+  bool cl_no_mail_ = false;
   int cl_smem_ = 0;
   int64_t cl_cap_ = 0;
   unsigned long long cl_exit_edges_ = kClusterExitEdges;

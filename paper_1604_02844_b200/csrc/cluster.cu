@@ -79,6 +79,12 @@ __device__ __forceinline__ unsigned long long atom_exch_dsm64(uint32_t a, unsign
   asm volatile("atom.relaxed.cluster.shared::cluster.exch.b64 %0, [%1], %2;" : "=l"(old) : "r"(a), "l"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ void st_dsm64(uint32_t a, unsigned long long v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_dsm32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_dsm32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
@@ -137,6 +143,13 @@ struct ClusterSmem {
   unsigned long long red[2][kCW];
   int32_t qcnt[2];                // entries appended to this CTA's small queue (parity)
   int32_t scnt[kMaxCluster];      // entries staged for each CTA's next queue
+  // candidate mailboxes (DSMEM mode): a neighbour is not claimed remotely but
+  // sent to the CTA owning its bitmap sector, which claims it in its own
+  // shared memory and appends the winners to its own queue
+  uint32_t rmail[kMaxCluster];    // shared::cluster address of each CTA's mailbox area
+  uint32_t rincnt[kMaxCluster];   // ... of each CTA's in_cnt[0]
+  int32_t out_cnt[kMaxCluster];   // candidates sent to each CTA this level (may exceed the cap: the rest went the remote way)
+  int32_t in_cnt[kMaxCluster];    // candidates received from each CTA this level (written by the senders)
   int32_t off[kCW][33];           // per-warp group offsets (window path)
   int64_t start[kCW][32];
   int32_t par[kCW][32];
@@ -149,6 +162,8 @@ struct Ctx {
   QEntry* q0;        // this CTA's small queues in shared memory (parity 0 / 1)
   QEntry* q1;
   QEntry* stage;     // [kMaxCluster][kClusterStage] winners staged per target CTA
+  unsigned long long* mail;  // [kMaxCluster][mail_cap] candidates received, by sender
+  int32_t mail_cap;          // 0: claim remotely (no mailboxes)
   uint32_t vis_base; // shared address of this CTA's slice
   uint32_t rank, csize, clog;
   int32_t next_level;
@@ -224,7 +239,8 @@ __device__ __forceinline__ void write_record(const ClusterArgs& p, QEntry e, int
 // Claim a batch of 4 neighbours per lane (elements outside okm hold junk);
 // winners join the next frontier (warp-collective).
 template <bool DSM>
-__device__ __forceinline__ void settle4(Ctx& x, const int32_t (&nb)[4], uint32_t okm, const int32_t (&par)[4], int lane) {
+__device__ __forceinline__ void settle4_remote(Ctx& x, const int32_t (&nb)[4], uint32_t okm, const int32_t (&par)[4],
+                                               int lane) {
   const ClusterArgs& p = *x.p;
   if (p.prof && lane == 0) atomicMax(&x.s->tm[0], gtimer());  // (the loads of nb have returned)
   if (x.wt) {
@@ -337,6 +353,146 @@ __device__ __forceinline__ void settle4(Ctx& x, const int32_t (&nb)[4], uint32_t
   }
   asm volatile("mov.b64 %0, %0;" : "+l"(sink));  // (performed before the level barrier)
   wstamp(x, 4, lane);
+}
+
+// Claim a batch of 4 neighbours per lane (warp-collective). DSMEM mode with
+// mailboxes: a remote claim is an atomic round trip through the SM-to-SM
+// network, and their rate (not their latency) bounds a level — ~17 K claims
+// per lattice level on 16 SMs. So a candidate (neighbour, parent) is written
+// into the mailbox of the CTA owning the neighbour's bitmap sector instead (a
+// plain remote store into this sender's private region there: one local
+// shared-memory atomic for the slot, no remote atomic); after the cluster
+// barrier the owner claims its candidates locally (accept_mail). A full
+// region sends the rest the remote-claim way.
+template <bool DSM>
+__device__ __forceinline__ void settle4(Ctx& x, const int32_t (&nb)[4], uint32_t okm, const int32_t (&par)[4], int lane) {
+  if constexpr (DSM) {
+    if (x.mail_cap > 0) {
+      ClusterSmem& s = *x.s;
+      int32_t slot[4];
+      uint32_t tgt[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        tgt[k] = (((uint32_t)nb[k] >> 8) & (x.csize - 1));  // owner of the 32-byte bitmap sector (256 ids)
+        slot[k] = ((okm >> k) & 1u) ? atomicAdd(&s.out_cnt[tgt[k]], 1) : 0;
+      }
+      uint32_t ovf = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (!((okm >> k) & 1u)) continue;
+        if (slot[k] < x.mail_cap)
+          st_dsm64(s.rmail[tgt[k]] + 8u * (uint32_t)((int32_t)x.rank * x.mail_cap + slot[k]),
+                   ((unsigned long long)(uint32_t)par[k] << 32) | (uint32_t)nb[k]);
+        else
+          ovf |= 1u << k;
+      }
+      if (__any_sync(kF, ovf != 0)) settle4_remote<DSM>(x, nb, ovf, par, lane);
+      return;
+    }
+  }
+  settle4_remote<DSM>(x, nb, okm, par, lane);
+}
+
+// (after the barrier that follows the expansion) warp w claims the candidates
+// CTA w sent to this CTA, in this CTA's own slice of the bitmap; the winners
+// join this CTA's next queue (rows of degree >= 32: the cluster-wide list).
+__device__ __forceinline__ void accept_mail(Ctx& x, uint32_t* slice, int lane, int wib) {
+  const ClusterArgs& p = *x.p;
+  ClusterSmem& s = *x.s;
+  if (wib >= (int)x.csize) return;
+  const int32_t cnt = min(s.in_cnt[wib], x.mail_cap);
+  const unsigned long long* mb = x.mail + (size_t)wib * x.mail_cap;
+  QEntry* qn = x.nx ? x.q1 : x.q0;
+  // 4 candidates per lane per step: their claims, degree look-ups and row
+  // prefetches overlap (a step is a chain of shared-memory round trips)
+  for (int32_t i0 = 0; i0 < cnt; i0 += 128) {
+    int32_t w[4], par[4];
+    uint32_t win = 0, small = 0, big = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int32_t i = i0 + k * 32 + lane;
+      const unsigned long long e = i < cnt ? mb[i] : 0ull;
+      w[k] = (int32_t)(uint32_t)e;
+      par[k] = (int32_t)(uint32_t)(e >> 32);
+      if (i < cnt) {
+        const uint32_t gw = (uint32_t)w[k] >> 5, bit = 1u << (w[k] & 31);
+        const uint32_t lw = (((gw >> 3) >> x.clog) << 3) | (gw & 7u);
+        win |= (uint32_t)!(atomicOr(slice + lw, bit) & bit) << k;
+      }
+    }
+    if (!__any_sync(kF, win != 0)) continue;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (!((win >> k) & 1u)) continue;
+      x.disc += 1;
+      if (w[k] >= p.t_warp && w[k] < p.t_nz) {
+        const int d = small_degree(s.T, w[k]);
+        x.edges += (unsigned long long)d;
+        small |= 1u << k;
+        if (!(p.dbg & 1)) {
+          prefetch_l2(p.col_idx + s.B[d] + (int64_t)(w[k] - s.T[d + 1]) * d);
+          prefetch_l2(p.new2old + w[k]);
+        }
+      } else {  // degree >= 32 (the cluster-wide list) or 0: records now
+        write_record<true>(p, QEntry{w[k], par[k]}, x.next_level);
+        big |= (uint32_t)(w[k] < p.t_warp) << k;
+      }
+    }
+    // small winners: one reservation in this CTA's next queue per warp step
+    {
+      const uint32_t mine = (uint32_t)__popc(small);
+      uint32_t incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kF, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const uint32_t tot = __shfl_sync(kF, incl, 31);
+      if (tot) {
+        int32_t base = 0;
+        if (lane == 31) base = atomicAdd(&s.qcnt[x.nx], (int32_t)tot);
+        int32_t j = __shfl_sync(kF, base, 31) + (int32_t)(incl - mine);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (!((small >> k) & 1u)) continue;
+          if (j < p.qs) qn[j] = QEntry{w[k], par[k]};
+          else spill_of(x, x.rank, x.nx)[j - p.qs] = QEntry{w[k], par[k]};
+          ++j;
+        }
+      }
+    }
+    if (__any_sync(kF, big != 0)) {  // rows of degree >= 32: the cluster-wide list
+      int64_t st[4];
+      int32_t dg[4], uo[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool b = (big >> k) & 1u;
+        st[k] = b ? __ldg(p.row_ptr + w[k]) : 0;
+        dg[k] = b ? (int32_t)(__ldg(p.row_ptr + w[k] + 1) - st[k]) : 0;
+        uo[k] = b ? __ldg(p.new2old + w[k]) : 0;
+      }
+      const uint32_t nbig = (uint32_t)__popc(big);
+      uint32_t incl = nbig;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kF, incl, o);
+        if (lane >= o) incl += t;
+      }
+      unsigned long long base = 0;
+      if (lane == 31) base = atomicAdd(p.big_cnt + x.big_slot, (unsigned long long)incl);
+      base = __shfl_sync(kF, base, 31) + (incl - nbig);
+      unsigned long long sink = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (!((big >> k) & 1u)) continue;
+        x.edges += (unsigned long long)dg[k];
+        unsigned long long* e2 = reinterpret_cast<unsigned long long*>(p.big + x.big_slot * p.cap + (int64_t)base++);
+        sink |= atomicExch(e2, (unsigned long long)st[k]);
+        sink |= atomicExch(e2 + 1, ((unsigned long long)(uint32_t)uo[k] << 32) | (uint32_t)dg[k]);
+      }
+      asm volatile("mov.b64 %0, %0;" : "+l"(sink));
+    }
+  }
 }
 
 // After the expansion (CTA-synchronised): warp t pushes the entries staged
@@ -528,6 +684,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
   x.q0 = reinterpret_cast<QEntry*>(s_dyn + slice_words * 4);
   x.q1 = x.q0 + p.qs;
   x.stage = x.q1 + p.qs;
+  x.mail = reinterpret_cast<unsigned long long*>(x.stage + kMaxCluster * kClusterStage);
+  x.mail_cap = DSM ? p.mail_cap : 0;
   x.vis_base = (uint32_t)__cvta_generic_to_shared(slice);
   if (tid < kSmallMax + 2) s.T[tid] = p.classes->T[tid];
   if (tid < kSmallMax + 1) s.B[tid] = p.classes->base[tid];
@@ -536,7 +694,10 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
     s.rq[0][tid] = mapa((uint32_t)__cvta_generic_to_shared(x.q0), (uint32_t)tid);
     s.rq[1][tid] = mapa((uint32_t)__cvta_generic_to_shared(x.q1), (uint32_t)tid);
     s.rqcnt[tid] = mapa((uint32_t)__cvta_generic_to_shared(&s.qcnt[0]), (uint32_t)tid);
+    s.rmail[tid] = mapa((uint32_t)__cvta_generic_to_shared(x.mail), (uint32_t)tid);
+    s.rincnt[tid] = mapa((uint32_t)__cvta_generic_to_shared(&s.in_cnt[0]), (uint32_t)tid);
   }
+  if (tid < kMaxCluster) s.out_cnt[tid] = s.in_cnt[tid] = 0;
   if (tid < 2) s.qcnt[tid] = 0;
   if (tid < kMaxCluster) s.scnt[tid] = 0;
   if (tid < 4) s.tm[tid] = 0;
@@ -619,6 +780,20 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
       unsigned long long* pl = (prof && L - p.L0 < 64) ? prof + 8 + 4 * (L - p.L0) : nullptr;
       if (p.prof && lane == 0) atomicMax(&s.tm[2], gtimer());
       wstamp(x, 5, lane);
+      if (x.mail_cap > 0) {
+        // candidates delivered: every sender tells every owner how many it
+        // wrote, the cluster barrier (release / acquire: the remote stores are
+        // visible), then each CTA claims what it received
+        __syncthreads();
+        if (tid < (int)x.csize) {
+          st_dsm32(s.rincnt[tid] + 4u * x.rank, (uint32_t)min(s.out_cnt[tid], x.mail_cap));
+          s.out_cnt[tid] = 0;
+        }
+        cl_sync();
+        wstamp(x, 3, lane);
+        accept_mail(x, slice, lane, wib);
+        wstamp(x, 4, lane);
+      }
       // this CTA's counts, added into every CTA's totals of level L+1
       unsigned long long d = x.disc, e = x.edges;
 #pragma unroll
