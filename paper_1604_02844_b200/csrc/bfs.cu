@@ -1358,6 +1358,52 @@ __global__ void k_init(uint4* __restrict__ vis4, uint4* __restrict__ prev4, int6
     reinterpret_cast<unsigned long long*>(ring)[threadIdx.x] = 0ull;
 }
 
+// K4 for one unpartitioned BFS in one launch: k_init with the root seeded in
+// place (its visited / prev bit and level 0 are written by the threads that
+// clear those words), the rest of seed_root by thread 0 of block 0 after the
+// ring is cleared. Saves the one-thread k_seed launch.
+__global__ void k_init_seed(uint4* __restrict__ vis4, uint4* __restrict__ prev4, int64_t nwords4,
+                            int4* __restrict__ lvl4, int64_t n4, Counters* __restrict__ ring, LevelArgs a,
+                            const int32_t* __restrict__ old2new, int32_t root_orig) {
+  const int32_t r = __ldg(old2new + root_orig);
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t rw4 = (int64_t)(r >> 5) >> 2, rl4 = (int64_t)r >> 2;
+  for (int64_t i = t; i < nwords4; i += stride) {
+    const uint32_t bit = i == rw4 ? 1u << (r & 31) : 0u;
+    const int sel = (r >> 5) & 3;
+    vis4[i] = prev4[i] = make_uint4(sel == 0 ? bit : 0u, sel == 1 ? bit : 0u, sel == 2 ? bit : 0u, sel == 3 ? bit : 0u);
+  }
+  for (int64_t i = t; i < n4; i += stride) {
+    const int hit = i == rl4 ? (r & 3) : -1;
+    lvl4[i] = make_int4(hit == 0 ? 0 : -1, hit == 1 ? 0 : -1, hit == 2 ? 0 : -1, hit == 3 ? 0 : -1);
+  }
+  if (blockIdx.x != 0) return;
+  if (threadIdx.x < (int)(kCounterRing * sizeof(Counters) / 8))
+    reinterpret_cast<unsigned long long*>(ring)[threadIdx.x] = 0ull;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int64_t st = a.row_ptr[r];
+    const int32_t deg = (int32_t)(a.row_ptr[r + 1] - st);
+    a.pred_int[r] = root_orig;
+    Counters c{};
+    c.discovered = 1;
+    c.edges = (unsigned long long)deg;
+    if (r < a.t_cta) {
+      const int items = (deg + a.qchunk - 1) / a.qchunk;
+      for (int k = 0; k < items; ++k)
+        a.next_cta[k] = CtaItem{st + (int64_t)k * a.qchunk, min(a.qchunk, deg - k * a.qchunk), root_orig};
+      c.bin[kBinCta] = (unsigned long long)items;
+    } else if (r < a.t_warp) {
+      a.next_warp[0] = r;
+      c.bin[kBinWarp] = 1;
+    } else if (r < a.t_nz) {
+      a.next_small[0] = r;
+      c.bin[kBinSmall] = 1;
+    }
+    ring[0] = c;
+  }
+}
+
 // Outputs in original ids, once per BFS (PredecessorArray semantics,
 // traversal.py:42-50: unreached and padding = SENTINEL): output x takes the
 // record of internal id old2new[x]; reached = its visited bit (a 2 MiB
@@ -2285,16 +2331,15 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   const int64_t launches0 = g_launches.load();
   n_cl_ev_ = 0;
   LBFS_CUDA(cudaEventRecord(ev_[0], st));
-  {  // K4: bitmaps + internal levels + counter ring (outputs are written once, by k_finalize)
-    const unsigned grid = clamp_grid((n_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
-    LBFS_LAUNCH(k_init, grid, 256, 0, st, (uint4*)visited_, (uint4*)prev_, (nwords_ + 3) / 4, (int4*)level_int_,
-                (n_ + 3) / 4, cnt_);
-  }
   LevelArgs a = level_args();
   a.next_small = q_small_[0];
   a.next_warp = q_warp_[0];
   a.next_cta = q_cta_[0];
-  LBFS_LAUNCH(k_seed, 1, 1, 0, st, a, prev_, old2new_, (int32_t)root, &cnt_[0], nullptr, nullptr);
+  {  // K4: bitmaps + internal levels + counter ring + the root (outputs are written once, by k_finalize)
+    const unsigned grid = clamp_grid((n_ / 4 + 255) / 256, (int64_t)sm_count_ * 8);
+    LBFS_LAUNCH(k_init_seed, grid, 256, 0, st, (uint4*)visited_, (uint4*)prev_, (nwords_ + 3) / 4, (int4*)level_int_,
+                (n_ + 3) / 4, cnt_, a, old2new_, (int32_t)root);
+  }
   LBFS_CUDA(cudaEventRecord(ev_[1], st));
   const bool use_cluster = cl_size_ > 0 && !cl_off_ && !split_ && !count_;
   if (!use_cluster) {
