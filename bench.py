@@ -55,7 +55,8 @@ def parse():
     ap.add_argument("--cpu-roots", type=int, default=8, help="roots per step of the --impl reference arm")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU-baseline sampling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extra-configs", action="store_true", help="skip the S20 / lattice keys")
+    ap.add_argument("--no-extra-configs", action="store_true", help="skip the S20 / lattice / S27 keys")
+    ap.add_argument("--no-s27", action="store_true", help="skip the SCALE-27 key of the extra configs")
     ap.add_argument("--part-driver", choices=("native", "python"), default="native",
                     help="partitioned level loop: the library's (one call per BFS, library-owned NCCL "
                          "communicator) or distributed.bfs_partitioned (per-step calls, torch.distributed)")
@@ -566,10 +567,24 @@ def run_ours(args, rank, world, local):
         extra["rmat-s20-ef16-64roots"] = extra_config(lambda: build_rmat_graph(RmatParams(scale=20, seed=1)), 64,
                                                       warm_passes=2, passes=2)
         extra["lattice-4096x4096-16roots"] = extra_config(lambda: build_lattice_graph(4096, 4096), 16)
+        # configs[4] (SCALE 27, 4.2e9 CSR entries, ~40 GB with the layout's
+        # temporaries): on one GPU when the memory is there; a failure here is
+        # reported in its key and does not touch the headline
+        if not args.no_s27:
+            free_b, _ = torch.cuda.mem_get_info()
+            if free_b >= 100 * (1 << 30):
+                try:
+                    extra["rmat-s27-ef16-64roots"] = extra_config(
+                        lambda: build_rmat_graph(RmatParams(scale=27, seed=1)), 64, warm_passes=1, passes=1)
+                except Exception as e:  # noqa: BLE001
+                    extra["rmat-s27-ef16-64roots"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+                    torch.cuda.empty_cache()
+            else:
+                extra["rmat-s27-ef16-64roots"] = {"skipped": f"{free_b >> 30} GiB free on the device"}
     line = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "int32",
+        "scaling": "strong", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic: R-MAT (reference generator, bit-exact) + seeded permutation",
         "config": {"workload": f"rmat-s{args.scale}-ef16-{args.roots}roots", "scale": args.scale,
                    "edgefactor": 16, "roots": args.roots, "n": n, "nnz": nnz,

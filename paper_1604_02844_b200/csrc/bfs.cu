@@ -1664,6 +1664,8 @@ void BfsEngine::setup_cluster(int optin) {
           mail_cap = c;
           break;
         }
+    if (mail_cap > 0 && cl_mail_cap_env_ > 0)  // (tests) a tiny region exercises the overflow path
+      mail_cap = std::min<int64_t>(mail_cap, cl_mail_cap_env_);
     const int64_t mail_bytes = (int64_t)kMaxCluster * mail_cap * 8;
     int64_t qs = dsm ? std::min<int64_t>(8192, (budget - slice * 4 - mail_bytes) / qbytes)
                      : std::min<int64_t>(8192, budget / qbytes);
@@ -2300,6 +2302,7 @@ void BfsEngine::read_env() {
   qchunk_ = (int)std::min<long long>(kChunk, std::max<long long>(kQChunkMin, geti("LBFS_QCHUNK", kQChunkDefault))) & ~3;
   // small-frontier levels run on the cluster while a frontier has at most this many edges
   cl_exit_edges_ = (unsigned long long)std::max<long long>(64, geti("LBFS_CLUSTER_EDGES", kClusterExitEdges));
+  cl_mail_cap_env_ = (int)geti("LBFS_CLUSTER_MAIL_CAP", 0);
   cl_no_mail_ = env_flag("LBFS_CLUSTER_NO_MAIL");  // (A/B) DSMEM mode with remote claims instead of candidate mailboxes
   cl_no_dsm_ = env_flag("LBFS_CLUSTER_GLOBAL");  // claim on the global bitmap even when the slices fit
   cl_off_ = env_flag("LBFS_NO_CLUSTER");

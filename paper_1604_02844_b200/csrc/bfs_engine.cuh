@@ -536,6 +536,7 @@ class BfsEngine {
   int32_t cl_qs_ = 0;
   int32_t cl_mail_cap_ = 0;
   bool cl_no_mail_ = false;
+  int cl_mail_cap_env_ = 0;
   int cl_smem_ = 0;
   int64_t cl_cap_ = 0;
   unsigned long long cl_exit_edges_ = kClusterExitEdges;

@@ -9,17 +9,24 @@
 //
 //   * visited bitmap in distributed shared memory (when it fits: n <= ~64 M
 //     vertices at C = 16): 32-byte sectors of the global bitmap are dealt to
-//     the C CTAs round robin; a claim is one `atom.shared::cluster.or` on the
-//     owner's copy (the winner is the lane whose old word lacked the bit —
-//     the atomicOr election of traversal.py:143-148 without a global atomic).
-//     Larger graphs claim on the global bitmap in L2;
-//   * per-CTA frontier queues in shared memory (small-degree vertices; a
-//     winner appends to the queue of the CTA that found it, warp-aggregated),
-//     vertices of degree >= 32 in a cluster-wide list in global memory whose
-//     rows every warp of the cluster shares in 512-element chunks;
-//   * one hardware cluster barrier per level (barrier.cluster arrive.release /
-//     wait.acquire); the level's counts are summed by reading every CTA's
-//     slot through DSMEM, so all CTAs take the same continue / exit decision.
+//     the C CTAs round robin. A neighbour is not claimed remotely (remote
+//     atomics are rate-bound: ~17 K claims per lattice level on 16 SMs): the
+//     candidate (neighbour, parent) is stored into the mailbox of the CTA
+//     owning its sector — a private region per sender there, slot from a
+//     local counter — and after a cluster barrier the owner claims its
+//     candidates with local shared-memory atomics (the winner is the one
+//     whose old word lacked the bit: the atomicOr election of
+//     traversal.py:143-148) and appends the winners to its own queue. A full
+//     region falls back to `atom.shared::cluster.or` claims and remote
+//     pushes. Larger graphs, and late segments of shallow traversals, claim
+//     on the global bitmap in L2;
+//   * per-CTA frontier queues in shared memory (small-degree vertices live
+//     on the CTA that owns their bitmap sector), vertices of degree >= 32 in
+//     a cluster-wide list in global memory whose rows every warp of the
+//     cluster shares in 512-element chunks;
+//   * two hardware cluster barriers per level (candidates delivered; winners
+//     counted): the level's counts are added into every CTA's totals through
+//     DSMEM, so all CTAs take the same continue / exit decision.
 //
 // The loop leaves when the frontier is empty (BFS done) or its edge count
 // exceeds exit_edges (the full-GPU kernels take over): the frontier is then

@@ -203,3 +203,32 @@ def test_bfs_device_torch_outputs():
     ref = bfs(g, 17)
     assert np.array_equal(lvl.cpu().numpy(), ref.levels)
     assert res.layers == ref.layers
+
+
+@pytest.mark.parametrize("env", [
+    {"LBFS_CLUSTER_MAIL_CAP": "4"},      # candidate mailboxes overflow: the remote-claim path next to them
+    {"LBFS_CLUSTER_NO_MAIL": "1"},       # remote claims only
+    {"LBFS_CLUSTER_GLOBAL": "1"},        # claims on the global bitmap
+    {"LBFS_CLUSTER_DSM_ALWAYS": "1"},    # late segments with the bitmap in DSMEM too
+    {"LBFS_NO_WARP_ITEMS": "1", "LBFS_NO_FUSE_QUEUES": "1", "LBFS_NO_PUBLISH_AFTER_HEAVY": "1"},
+    {"LBFS_NO_EXIT_FAIR": "1", "LBFS_QGRID_OLD": "1", "LBFS_RESOLVE_CLAMP": "1"},
+])
+def test_level_loop_switches_keep_the_results(monkeypatch, env):
+    """The A/B switches of the level loop (read once per graph handle) select
+    other code paths, never other results: levels and layers against the
+    oracle on a lattice (thousands of cluster levels), R-MAT graphs whose
+    levels cross every mode, and a hub-heavy star-of-stars."""
+    from paper_1604_02844_b200 import build_lattice_graph, pick_roots
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = build_lattice_graph(192, 160)
+    for r in pick_roots(g, 2, 3, filter_unconnected=True).tolist():
+        check_against_oracle(g, int(r))
+    for scale in (12, 16, 18):
+        g = build_rmat_graph(RmatParams(scale=scale, edgefactor=16, seed=5))
+        for r in pick_roots(g, 3, 7, filter_unconnected=True).tolist():
+            check_against_oracle(g, int(r))
+    # two hubs of 3000 and 2000 leaves joined by a path, leaves sharing bitmap sectors
+    pairs = [(0, 10 + i) for i in range(3000)] + [(1, 4000 + i) for i in range(2000)] + [(0, 2), (2, 3), (3, 1)]
+    check_against_oracle(graph(pairs, 6100), 10)
