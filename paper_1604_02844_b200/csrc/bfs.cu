@@ -2085,7 +2085,13 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
                  sweep_small ? e_nz_ : e_big_, sweep_small ? w_small0_ : n_win_all_ + 1, svmask_, front_,
                  visited_, pred_int_, new2old_loc_,
                  stage_, 1, stage_words_, sweep_hot_words_, getenv("LBFS_SWEEP_PF") ? atoi(getenv("LBFS_SWEEP_PF")) : kSweepPrefetch,
-                 getenv("LBFS_SWEEP_DBG") ? atoi(getenv("LBFS_SWEEP_DBG")) : 0};
+                 getenv("LBFS_SWEEP_DBG") ? atoi(getenv("LBFS_SWEEP_DBG")) : 0, nullptr, 0, classes_};
+    // the dense small region rides along on the sweep's worker warps
+    if (f.n_dense > 0 && !sweep_small && sweep_workers_ && kSweepWorkers > 0) {
+      sa.dense = f.dense;
+      sa.n_dense = f.n_dense;
+      f.n_dense = 0;
+    }
     LBFS_LAUNCH(k_sweep, (unsigned)expand_grid_, kSweepThreads, kSweepRingBytes + sweep_hot_words_ * 4, st, sa);
     a.stage_first = 0;
     f.n_cta = 0;
@@ -2310,6 +2316,7 @@ void BfsEngine::read_env() {
   // LBFS_NO_WARP_ITEMS=1: append them to the raw warp queue instead
   warp_items_ = !env_flag("LBFS_NO_WARP_ITEMS");
   qgrid_old_ = env_flag("LBFS_QGRID_OLD");
+  sweep_workers_ = !env_flag("LBFS_NO_SWEEP_WORKERS");  // (A/B) the dense small region as its own launch
   cl_dsm_always_ = env_flag("LBFS_CLUSTER_DSM_ALWAYS");  // (A/B) every cluster segment with the bitmap in DSMEM
   exit_fair_ = !env_flag("LBFS_NO_EXIT_FAIR");  // (A/B) cluster exit items of qchunk edges whatever the frontier
   fuse_queues_ = !env_flag("LBFS_NO_FUSE_QUEUES");  // (A/B) one launch per bin after a queue-mode level

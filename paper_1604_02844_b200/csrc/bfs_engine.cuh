@@ -230,6 +230,28 @@ __device__ __forceinline__ void heavy_or_any(uint32_t base, uint32_t hot_words, 
       : "memory");
 }
 
+// ... one target, valid when ok != 0
+__device__ __forceinline__ void heavy_or_ok(uint32_t base, uint32_t hot_words, const uint32_t* visited, uint32_t v,
+                                            uint32_t ok) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred pk, ph, pc;\n\t"
+      ".reg .u32 wi, sa, bit;\n\t"
+      ".reg .u64 ga;\n\t"
+      "shr.u32 wi, %0, 5;\n\t"
+      "shf.l.wrap.b32 bit, 0, 1, %0;\n\t"
+      "setp.ne.u32 pk, %1, 0;\n\t"
+      "setp.lt.and.u32 ph, wi, %2, pk;\n\t"
+      "setp.ge.and.u32 pc, wi, %2, pk;\n\t"
+      "mad.lo.u32 sa, wi, 4, %3;\n\t"
+      "mad.wide.u32 ga, wi, 4, %4;\n\t"
+      "@ph red.shared.or.b32 [sa], bit;\n\t"
+      "@pc red.relaxed.gpu.global.or.b32 [ga], bit;\n\t"
+      "}" ::"r"(v),
+      "r"(ok), "r"(hot_words), "r"(base), "l"(visited)
+      : "memory");
+}
+
 constexpr int64_t kLoopCap = 1 << 16;  // levels per cluster-kernel launch
 
 // Small-frontier levels on one thread-block cluster (cluster.cu).
@@ -298,7 +320,14 @@ constexpr int kSweepWindow = 128;   // col_idx elements per window / side entry
 #endif
 constexpr int kSweepConsumers = LBFS_SWEEP_CONSUMERS;  // consumer warps; one CTA per SM
 constexpr int kSweepProducers = 4;   // producer warps (each a latency-bound side -> frontier -> copy chain)
-constexpr int kSweepThreads = 32 * (kSweepConsumers + kSweepProducers);
+#ifndef LBFS_SWEEP_WORKERS
+#define LBFS_SWEEP_WORKERS 0
+#endif
+// (experiment, off: with 4 worker warps S24 measured 385 vs 402 GTEPS — the
+// extra warps slow the ring's consumers by more than the saved launch)
+// worker warps: the dense small region's tasks, streamed next to the ring
+constexpr int kSweepWorkers = LBFS_SWEEP_WORKERS;
+constexpr int kSweepThreads = 32 * (kSweepConsumers + kSweepProducers + kSweepWorkers);
 #ifndef LBFS_SWEEP_STAGES
 #define LBFS_SWEEP_STAGES 4
 #endif
@@ -338,6 +367,11 @@ struct SweepArgs {
   int32_t hot_words;
   int32_t prefetch;         // L2 prefetch distance in chunks of a CTA (0: off)
   int32_t dbg_flags;        // LBFS_SWEEP_DBG (experiments; wrong results): 1 no hot ORs, 2 no cold probes
+  // dense small region (rows of degree 1..31, most of them in the frontier):
+  // its tasks go to the worker warps (n_dense 0: none)
+  const DenseTask* dense;
+  int64_t n_dense;
+  const ClassTable* classes;
 };
 // Heavy levels as one window stream over [0, e_nz) (stream.cu).
 constexpr int kStreamThreads = 1024;
@@ -526,6 +560,7 @@ class BfsEngine {
   bool cl_dsm_ = false;           // visited bitmap in distributed shared memory
   bool cl_no_dsm_ = false, cl_off_ = false;
   bool qgrid_old_ = false;
+  bool sweep_workers_ = true;
   bool cl_dsm_always_ = false;
   bool exit_fair_ = true;
   bool fuse_queues_ = true;

@@ -287,6 +287,12 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
   const int hw4 = s.hot_words >> 2;
   uint4* h4 = reinterpret_cast<uint4*>(s_hot);
   for (int i = tid; i < hw4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
+  __shared__ int32_t s_T[kSmallMax + 2];
+  __shared__ int64_t s_B[kSmallMax + 1];
+  if (s.n_dense > 0) {
+    if (tid < kSmallMax + 2) s_T[tid] = s.classes->T[tid];
+    if (tid < kSmallMax + 1) s_B[tid] = s.classes->base[tid];
+  }
   if (tid == 0) {
     for (int b = 0; b < kStages; ++b) {
       bar_init(&sm.full[b], 1);
@@ -298,7 +304,50 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
   const int64_t nchunks = (s.nwin_all + kChunkWins - 1) / kChunkWins;
   const int64_t my_chunks = nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
-  if (warp >= kConsumers) {
+  if (warp >= kConsumers + kSweepProducers) {
+    // ---------------- workers: the dense small region (rows of degree 1..31
+    // are one contiguous col_idx range cut at layout time into tasks inside
+    // one degree class d): a warp streams a task with 128-bit loads, the next
+    // window in flight, and keeps an element when its owner
+    // lo_d + (p - base_d) / d is in the frontier bitmap; the targets are OR'ed
+    // like the consumers' (same shared copy of the hot prefix)
+    const uint32_t hoff = saddr(s_hot);
+    const int64_t nw = (int64_t)kSweepWorkers * gridDim.x;
+    for (int64_t it = (int64_t)(warp - kConsumers - kSweepProducers) * gridDim.x + blockIdx.x; it < s.n_dense;
+         it += nw) {
+      const DenseTask dt = s.dense[it];
+      const int d = dt.d;
+      const int32_t lo = s_T[d + 1];
+      const int64_t base = s_B[d];
+      const uint32_t rcp = (uint32_t)(0xFFFFFFFFull / (uint32_t)d + 1ull);
+      const int64_t a0 = dt.p0 & ~int64_t(3), a1 = dt.p0 + dt.len;
+      auto load = [&](int64_t c0) {
+        const int64_t p = c0 + lane * 4;
+        return p < a1 ? ld_stream4(s.col_idx + p) : make_int4(0, 0, 0, 0);
+      };
+      int4 cur = load(a0);
+      for (int64_t c0 = a0; c0 < a1; c0 += kWin) {
+        const int4 nxt = c0 + kWin < a1 ? load(c0 + kWin) : make_int4(0, 0, 0, 0);
+        const int64_t p = c0 + lane * 4;
+        const int32_t e4[4] = {cur.x, cur.y, cur.z, cur.w};
+        int32_t own[4];
+        bool in_task[4];
+        uint32_t fw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t pq = p + q;
+          const uint32_t rel = (uint32_t)(pq - base);
+          own[q] = lo + (d == 1 ? (int32_t)rel : (int32_t)__umulhi(rel, rcp));
+          in_task[q] = pq >= dt.p0 && pq < a1;
+          fw[q] = in_task[q] ? __ldg(s.front + (own[q] >> 5)) : 0u;  // (read-only during the launch)
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          heavy_or_ok(hoff, (uint32_t)s.hot_words, s.visited, (uint32_t)e4[q], (fw[q] >> (own[q] & 31)) & 1u);
+        cur = nxt;
+      }
+    }
+  } else if (warp >= kConsumers) {
     // ---------------- producers: producer warp p takes the CTA's chunks
     // p, p + kProducers, ...; lane j owns window j of a chunk and derives its
     // window info from the side entry and the frontier bitmap.

@@ -212,6 +212,7 @@ def test_bfs_device_torch_outputs():
     {"LBFS_CLUSTER_DSM_ALWAYS": "1"},    # late segments with the bitmap in DSMEM too
     {"LBFS_NO_WARP_ITEMS": "1", "LBFS_NO_FUSE_QUEUES": "1", "LBFS_NO_PUBLISH_AFTER_HEAVY": "1"},
     {"LBFS_NO_EXIT_FAIR": "1", "LBFS_QGRID_OLD": "1", "LBFS_RESOLVE_CLAMP": "1"},
+    {"LBFS_DENSE_MIN": "0"},             # dense small-region streaming on small graphs too
 ])
 def test_level_loop_switches_keep_the_results(monkeypatch, env):
     """The A/B switches of the level loop (read once per graph handle) select
