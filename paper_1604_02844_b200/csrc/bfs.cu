@@ -1158,7 +1158,7 @@ __device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk,
       c.next_list[s_base[0] + r] = (int32_t)v;
       s_deg[r] = deg;
     }
-    if (v < c.t_cta) atomicAdd(&s_hitems[wl], (deg + kChunk - 1) / kChunk);
+    if (v < c.t_cta) atomicAdd(&s_hitems[wl], slice_items(st, deg, kChunk));
   };
   if (n_new * kCompactSparseDiv > kCompactVerts) {
 #pragma unroll 1
@@ -1276,11 +1276,10 @@ __device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk,
       const int64_t v = v0 + t + j * kCompactThreads;
       if (v >= c.t_cta || !((s_new[wl] >> b) & 1u)) continue;
       const int64_t st = __ldg(c.row_ptr + v), deg = __ldg(c.row_ptr + v + 1) - st;
-      const int items = (int)((deg + kChunk - 1) / kChunk);
+      const int items = slice_items(st, (int32_t)deg, kChunk);
       const int32_t vo = __ldg(c.new2old + v);
       unsigned long long p = s_base[1] + atomicAdd(&s_hitems[wl], items);
-      for (int64_t k = 0; k < items; ++k)
-        c.next_cta[p++] = CtaItem{st + k * kChunk, (int32_t)std::min<int64_t>(kChunk, deg - k * kChunk), vo};
+      for (int k = 0; k < items; ++k) c.next_cta[p++] = slice_item(st, (int32_t)deg, kChunk, k, vo);
     }
   }
   // groups of 32 consecutive list entries -> kItemElems-element items
@@ -1389,9 +1388,8 @@ __global__ void k_init_seed(uint4* __restrict__ vis4, uint4* __restrict__ prev4,
     c.discovered = 1;
     c.edges = (unsigned long long)deg;
     if (r < a.t_cta) {
-      const int items = (deg + a.qchunk - 1) / a.qchunk;
-      for (int k = 0; k < items; ++k)
-        a.next_cta[k] = CtaItem{st + (int64_t)k * a.qchunk, min(a.qchunk, deg - k * a.qchunk), root_orig};
+      const int items = slice_items(st, deg, a.qchunk);
+      for (int k = 0; k < items; ++k) a.next_cta[k] = slice_item(st, deg, a.qchunk, k, root_orig);
       c.bin[kBinCta] = (unsigned long long)items;
     } else if (r < a.t_warp) {
       a.next_warp[0] = r;
@@ -1455,9 +1453,8 @@ __device__ __forceinline__ void seed_root(const LevelArgs& a, uint32_t* prev, co
     c.discovered = 1;
     c.edges = (unsigned long long)deg;
     if (l < a.t_cta) {
-      const int items = (deg + a.qchunk - 1) / a.qchunk;
-      for (int k = 0; k < items; ++k)
-        a.next_cta[k] = CtaItem{st + (int64_t)k * a.qchunk, min(a.qchunk, deg - k * a.qchunk), root_orig};
+      const int items = slice_items(st, deg, a.qchunk);
+      for (int k = 0; k < items; ++k) a.next_cta[k] = slice_item(st, deg, a.qchunk, k, root_orig);
       c.bin[kBinCta] = (unsigned long long)items;
     } else if (l < a.t_warp) {
       a.next_warp[0] = l;
@@ -1561,7 +1558,8 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   }
   // Bins, double-buffered: a vertex enters a bin once per BFS, so n entries
   // bound the small/warp bins; CTA items <= nnz/kChunk + #(deg >= kCtaMin).
-  cap_cta_ = nnz_loc_ / kQChunkMin + t_warp_ + 2;  // (queue-mode winners also emit warp-bin rows as items)
+  // (queue-mode winners also emit warp-bin rows as items; aligned cuts add at most one item per row)
+  cap_cta_ = nnz_loc_ / kQChunkMin + 2 * (int64_t)t_warp_ + 2;
   // group items: one per started kItemElems of each 32-entry group, per block
   cap_items_ = nnz_loc_ / kItemElems + n_loc_ / 32 + 2 * ((n_loc_ + kCompactVerts - 1) / kCompactVerts) + 16;
   for (int b = 0; b < 2; ++b) {
@@ -2305,7 +2303,7 @@ void BfsEngine::read_env() {
   sweep_after_queue_ = env_flag("LBFS_SWEEP_AFTER_QUEUE");
   sweep_small_ = env_flag("LBFS_SWEEP_SMALL");
   refresh_chunks_ = (int)geti("LBFS_REFRESH", kRefreshChunks);
-  qchunk_ = (int)std::min<long long>(kChunk, std::max<long long>(kQChunkMin, geti("LBFS_QCHUNK", kQChunkDefault))) & ~3;
+  qchunk_ = (int)std::min<long long>(kChunk, std::max<long long>(kQChunkMin, geti("LBFS_QCHUNK", kQChunkDefault))) & ~127;
   // small-frontier levels run on the cluster while a frontier has at most this many edges
   cl_exit_edges_ = (unsigned long long)std::max<long long>(64, geti("LBFS_CLUSTER_EDGES", kClusterExitEdges));
   cl_mail_cap_env_ = (int)geti("LBFS_CLUSTER_MAIL_CAP", 0);

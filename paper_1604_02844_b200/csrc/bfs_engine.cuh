@@ -21,7 +21,7 @@ constexpr int kQChunkMin = 128;              // smallest queue-mode hub item (si
 #define LBFS_QCHUNK_DEFAULT 512
 #endif
 constexpr int kQChunkDefault = LBFS_QCHUNK_DEFAULT;  // default queue-mode hub item (LBFS_QCHUNK overrides)
-constexpr int kChunk = 3960;                  // edges per CTA-bin item (<= 992 staged int4 slots)
+constexpr int kChunk = 3968;                  // edges per CTA-bin item (31 windows of 128)
 constexpr int kBinSmall = 0, kBinWarp = 1, kBinCta = 2, kBinItems = 3, kBinWSlice = 4;
 constexpr int kItemElems = 512;               // elements per group item (load balance unit)
 constexpr int kCounterRing = 3;
@@ -62,6 +62,23 @@ struct alignas(16) CtaItem {  // one kChunk-edge slice of a hub's row
   int32_t len;     // <= kChunk
   int32_t u;       // original id of the hub (the parent written to pred)
 };
+
+// Slice items of a row [st, st + deg): a row longer than `chunk` (a multiple
+// of 128) is cut at multiples of `chunk` elements above the 128-element
+// boundary below st, so every item but the row's first and last starts and
+// ends on a window boundary of the slice streamer (its windows then carry no
+// valid masks and can take the all-hot path); a shorter row is one item.
+__host__ __device__ __forceinline__ int slice_items(int64_t st, int32_t deg, int chunk) {
+  if (deg <= chunk) return deg > 0 ? 1 : 0;
+  return (int)((st + deg - (st & ~int64_t(127)) + chunk - 1) / chunk);
+}
+__host__ __device__ __forceinline__ CtaItem slice_item(int64_t st, int32_t deg, int chunk, int j, int32_t u) {
+  if (deg <= chunk) return CtaItem{st, deg, u};
+  const int64_t a0 = st & ~int64_t(127);
+  const int64_t lo = a0 + (int64_t)j * chunk > st ? a0 + (int64_t)j * chunk : st;
+  const int64_t e = st + deg, hi = a0 + (int64_t)(j + 1) * chunk < e ? a0 + (int64_t)(j + 1) * chunk : e;
+  return CtaItem{lo, (int32_t)(hi - lo), u};
+}
 
 // A contiguous element range of the small region inside one degree class.
 struct alignas(16) DenseTask {

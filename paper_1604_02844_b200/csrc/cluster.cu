@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
         const int64_t j = j0 + lane;
         CtaItem it{0, 0, 0};
         if (j < nb) it = bl[j];
-        const int items = j < nb ? (it.len + chunk - 1) / chunk : 0;
+        const int items = j < nb ? slice_items(it.start, it.len, chunk) : 0;
         int incl = items;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -917,7 +917,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
           const int64_t sq = __shfl_sync(kF, it.start, q);
           const int32_t lq = __shfl_sync(kF, it.len, q), uq = __shfl_sync(kF, it.u, q);
           for (int k = lane; k < nq; k += 32)
-            p.out_cta[cur][bq + k] = CtaItem{sq + (int64_t)k * chunk, min(chunk, lq - k * chunk), uq};
+            p.out_cta[cur][bq + k] = slice_item(sq, lq, chunk, k, uq);
         }
       }
     }
