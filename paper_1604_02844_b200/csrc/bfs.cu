@@ -1764,8 +1764,8 @@ void BfsEngine::launch_cluster(int64_t L, int cur, bool prev_bitmap, cudaStream_
   p.seq_value = ++seq_;
   p.dbg = cl_dbg_;
   if (cl_prof_) {
-    if (!cl_prof_buf_) cl_prof_buf_ = dev_alloc<unsigned long long>(512 + 8 * 32);
-    LBFS_CUDA(cudaMemsetAsync(cl_prof_buf_, 0, sizeof(unsigned long long) * (512 + 8 * 32), st));
+    if (!cl_prof_buf_) cl_prof_buf_ = dev_alloc<unsigned long long>(512 + 16 * 32);
+    LBFS_CUDA(cudaMemsetAsync(cl_prof_buf_, 0, sizeof(unsigned long long) * (512 + 16 * 32), st));
     p.prof = cl_prof_buf_;
     p.prof_level = cl_prof_level_;
   }
@@ -1793,7 +1793,7 @@ void BfsEngine::launch_cluster(int64_t L, int cur, bool prev_bitmap, cudaStream_
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (g_sync_each) sync_check(st, "k_cluster_levels", __FILE__, __LINE__);
   if (cl_prof_) {
-    unsigned long long pr[512 + 8 * 32];
+    unsigned long long pr[512 + 16 * 32];
     LBFS_CUDA(cudaMemcpyAsync(pr, cl_prof_buf_, sizeof(pr), cudaMemcpyDeviceToHost, st));
     LBFS_CUDA(cudaStreamSynchronize(st));
     fprintf(stderr, "[lbfs] cluster L0=%lld: load %.2fus total %.2fus\n", (long long)L, (pr[1] - pr[0]) * 1e-3,
@@ -1807,10 +1807,13 @@ void BfsEngine::launch_cluster(int64_t L, int cur, bool prev_bitmap, cudaStream_
     }
     if (cl_prof_level_ >= 0 && pr[512]) {
       for (int w = 0; w < kClusterThreads / 32; ++w) {
-        const unsigned long long* q = pr + 512 + 8 * w;
+        const unsigned long long* q = pr + 512 + 16 * w;
         fprintf(stderr, "[lbfs]   level %lld warp %2d:", cl_prof_level_, w);
-        for (int k = 1; k < 8; ++k) fprintf(stderr, " %6.2f", q[k] ? (q[k] - pr[512]) * 1e-3 : -1.0);
-        fprintf(stderr, "  (us after warp 0's level start: group, loads, claims, winners, expanded, cta sync, cluster sync)\n");
+        for (int k = 1; k < 12; ++k) fprintf(stderr, " %6.2f", q[k] ? (q[k] - pr[512]) * 1e-3 : -1.0);
+        fprintf(stderr,
+                "  (us after warp 0's level start: group, loads back, claims | candidates delivered, winners | accepted, "
+                "expanded, cta sync, cluster sync, accept: claims back, degrees + prefetches, queue appended, "
+                "expand: degrees known; each stamp costs a globaltimer read)\n");
       }
     }
   }

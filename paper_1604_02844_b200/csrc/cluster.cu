@@ -376,6 +376,10 @@ __device__ __forceinline__ void settle4(Ctx& x, const int32_t (&nb)[4], uint32_t
   if constexpr (DSM) {
     if (x.mail_cap > 0) {
       ClusterSmem& s = *x.s;
+      if (x.wt) {  // (LBFS_CLUSTER_PROF_LEVEL) the loads of nb have returned
+        const uint32_t w = __reduce_or_sync(kF, (uint32_t)(nb[0] | nb[1] | nb[2] | nb[3]));
+        if (w != 0x7fffffffu) wstamp(x, 2, lane);
+      }
       int32_t slot[4];
       uint32_t tgt[4];
 #pragma unroll
@@ -427,6 +431,7 @@ __device__ __forceinline__ void accept_mail(Ctx& x, uint32_t* slice, int lane, i
         win |= (uint32_t)!(atomicOr(slice + lw, bit) & bit) << k;
       }
     }
+    wstamp(x, 8, lane);   // (claims returned)
     if (!__any_sync(kF, win != 0)) continue;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -445,6 +450,7 @@ __device__ __forceinline__ void accept_mail(Ctx& x, uint32_t* slice, int lane, i
         big |= (uint32_t)(w[k] < p.t_warp) << k;
       }
     }
+    wstamp(x, 9, lane);   // (degrees, prefetches issued)
     // small winners: one reservation in this CTA's next queue per warp step
     {
       const uint32_t mine = (uint32_t)__popc(small);
@@ -468,6 +474,7 @@ __device__ __forceinline__ void accept_mail(Ctx& x, uint32_t* slice, int lane, i
         }
       }
     }
+    wstamp(x, 10, lane);  // (queue appended)
     if (__any_sync(kF, big != 0)) {  // rows of degree >= 32: the cluster-wide list
       int64_t st[4];
       int32_t dg[4], uo[4];
@@ -544,6 +551,7 @@ __device__ __forceinline__ void expand_small_group(Ctx& x, int n, int32_t v, int
   }
   const int32_t uo = lane < n ? __ldg(p.new2old + v) : 0;
   const int dmax = __reduce_max_sync(kF, (unsigned)d);
+  wstamp(x, 11, lane);  // (degrees known, loads about to issue)
   if (dmax <= 8) {
     int32_t nb[8];
 #pragma unroll
@@ -756,7 +764,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
       x.big_slot = (L + 1) % kCounterRing;
       x.disc = 0;
       x.edges = 0;
-      x.wt = (p.prof && x.rank == 0 && L == p.prof_level) ? p.prof + 512 + 8 * wib : nullptr;
+      x.wt = (p.prof && x.rank == 0 && L == p.prof_level) ? p.prof + 512 + 16 * wib : nullptr;
       x.wdone = 0;
       wstamp(x, 0, lane);
       if (x.rank == 0 && tid == 0 && L > p.L0)  // read during level L-1, appended from level L+1
