@@ -2,37 +2,50 @@
 // (traversal.py:413-422 -> bfs_serial / bfs_parallel_naive / _bitmap_bfs,
 // traversal.py:80-389).
 //
-//   K4 k_init / k_seed   PredecessorArray fill + Bitmap clear + root seed
-//                        (traversal.py:42-46, 135-139, 343-347)
-//   K1 k_expand<Mode>    frontier expansion over CSR, degree-binned in one
-//                        persistent launch (one 1024-thread CTA per SM):
-//                        - CTA bin (deg >= kCtaMin): rows cut into kChunk
-//                          slices; each warp streams its slices with 128-bit
-//                          loads, the next 128-element chunk in flight;
-//                        - warp bin (32 <= deg < kCtaMin) and small bin
-//                          (deg < 32): a warp takes 32 vertices at once and
-//                          walks their concatenated rows (one row_ptr round
-//                          trip per 32 vertices); small-bin groups of one
-//                          degree class map elements to rows in closed form.
+//   K4 k_init_seed       PredecessorArray fill + Bitmap clear + root seed in
+//                        one launch (traversal.py:42-46, 135-139, 343-347;
+//                        the partitioned path keeps k_init + k_seed)
+//   K1 k_expand<Mode, bins>  frontier expansion over CSR by one persistent
+//                        CTA per SM, one launch per non-empty bin (slice
+//                        items + raw queues share one after a queue level):
+//                        - slice items (rows of deg >= kCtaMin cut on window
+//                          boundaries into <= kChunk / qchunk elements; after
+//                          a queue or cluster level also the rows with
+//                          32 <= deg < kCtaMin): a warp streams its slices in
+//                          groups of D 128-element windows, 128-bit loads,
+//                          the next group in flight;
+//                        - warp slices (32 <= deg < kCtaMin after a bitmap
+//                          level): one slice per row, same streamer;
+//                        - group items / raw small queue (deg < 32): a warp
+//                          takes up to 32 vertices and walks their
+//                          concatenated rows; groups of one degree class map
+//                          elements to rows in closed form (no row_ptr read);
+//                        - dense small region: the rows of degree 1..31 as
+//                          one stream filtered by the frontier bitmap.
 //                        Replaces _frontier_neighbors + the 16-lane Listing-1
-//                        gather (traversal.py:107-119, 297-332).
+//                        gather (traversal.py:107-119, 297-332). Heavy levels
+//                        also use k_sweep (sweep.cu), small levels
+//                        k_cluster_levels (cluster.cu).
 //   K2 probe + settle    visited test: words of the hot bitmap prefix from a
-//                        per-SM shared-memory copy, the rest through L1. In
-//                        bitmap mode a clear bit is settled without waiting:
-//                        red.or on the bitmap + the parent into pred_int (any
+//                        per-SM shared-memory copy, the rest from L2. Bitmap
+//                        mode settles a clear bit without waiting: red.or on
+//                        the bitmap + the parent into pred_int (any
 //                        equal-level parent is valid, traversal.py:145-147);
-//                        in queue mode atomicOr elects one winner. Replaces
-//                        the unsynchronised OR + negative marks + restoration
+//                        queue mode elects one winner with atomicOr; heavy
+//                        mode ORs blindly (no probe, no parent: k_resolve
+//                        finds the parents afterwards). Replaces the
+//                        unsynchronised OR + negative marks + restoration
 //                        pass (traversal.py:175-279).
-//   K3 next frontier     queue mode (small levels): warp-aggregated
-//                        ballot/popc appends by the winners; bitmap mode
-//                        (large levels): k_compact turns the new visited
-//                        bits into the next frontier bitmap + warp/CTA-bin
-//                        queues with block-aggregated appends, writes levels
-//                        and translates parents to original ids. Replaces the
-//                        np.unique merge / nonzero-word scans
+//   K3 next frontier     queue mode: warp-aggregated appends by the winners
+//                        (small queue + slice items); bitmap / heavy mode:
+//                        k_compact turns the new visited bits into the next
+//                        frontier bitmap, list, group items and slices with
+//                        block-aggregated appends and writes the levels.
+//                        Replaces the np.unique merge / nonzero-word scans
 //                        (traversal.py:157-158, 168-172, 366-384).
-//   K5 BfsEngine::run    level driver (the while loops traversal.py:90,152,366)
+//   K5 BfsEngine::run    level driver (the while loops traversal.py:90,152,366):
+//                        mapped-memory mailbox per level, k_publish or the
+//                        cluster kernel as the publisher
 //   K6 Counters          LayerStats(input, edges, discovered) per level
 //                        (traversal.py:66-70, 100, 159, 383)
 #include <algorithm>
@@ -49,12 +62,12 @@
 namespace lbfs {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-// kQueueDirect: queue mode without the visited pre-probe (k_levels: small
-// frontiers, where the probe's round trip costs more than extra atomics)
+// kQueueDirect: queue mode without the visited pre-probe
 // kHeavy: bitmap mode for the heavy levels (most of the graph's edges in one
-// level): targets in the hot prefix are OR'ed blindly into the CTA's zeroed
-// shared copy (no probe, no parent; k_merge_hot folds the copies into the
-// visited bitmap and k_compact resolves their parents), the rest as kBitmapOut.
+// level): every target is OR'ed blindly — hot-prefix targets into the CTA's
+// zeroed shared copy (k_merge_hot folds the copies into the visited bitmap),
+// the rest into visited in L2 — with no probe and no parent (k_resolve gives
+// the level's new vertices their parents on a side stream).
 // (enum Mode: bfs_engine.cuh)
 #ifndef LBFS_CHECKS
 #define LBFS_CHECKS 0  // debug builds: bounds checks that trap with a location
