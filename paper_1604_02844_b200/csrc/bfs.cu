@@ -216,26 +216,34 @@ __device__ __forceinline__ void settle_queue(const LevelArgs& a, const int32_t (
     acc.edges += (unsigned long long)deg[k];
   }
   if (!__any_sync(kFull, hub)) return;
+  // rows below t_hub become slice items (cut on window boundaries): one
+  // reservation per warp for the items of all K candidates (each reservation
+  // is an L2 atomic round trip on the level's critical chain)
+  int items[K];
+  int32_t vo[K];
+  int mine = 0;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const bool w = ((win >> k) & 1u) && nb[k] < a.t_hub;
-    if (!__any_sync(kFull, w)) continue;
-    const int items = w ? (deg[k] + a.qchunk - 1) / a.qchunk : 0;
-    const int32_t vo = w ? __ldg(a.new2old + nb[k]) : 0;
-    int inc = items;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(kFull, inc, o);
-      if (lane >= o) inc += t;
-    }
-    const int total = __shfl_sync(kFull, inc, 31);
-    unsigned long long base = 0;
-    if (lane == 31) base = atomicAdd(&a.next_cnt->bin[kBinCta], (unsigned long long)total);
-    base = __shfl_sync(kFull, base, 31);
-    const int off = inc - items;
-    for (int j = 0; j < items; ++j)
-      a.next_cta[base + off + j] = CtaItem{st[k] + (int64_t)j * a.qchunk, min(a.qchunk, deg[k] - j * a.qchunk), vo};
+    items[k] = !w ? 0 : a.align_items ? slice_items(st[k], deg[k], a.qchunk) : (deg[k] + a.qchunk - 1) / a.qchunk;
+    vo[k] = w ? __ldg(a.new2old + nb[k]) : 0;
+    mine += items[k];
   }
+  int inc = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += t;
+  }
+  const int total = __shfl_sync(kFull, inc, 31);
+  unsigned long long base = 0;
+  if (lane == 31) base = atomicAdd(&a.next_cnt->bin[kBinCta], (unsigned long long)total);
+  base = __shfl_sync(kFull, base, 31) + (unsigned long long)(inc - mine);
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    for (int j = 0; j < items[k]; ++j)
+      a.next_cta[base++] = a.align_items ? slice_item(st[k], deg[k], a.qchunk, j, vo[k])
+                                         : CtaItem{st[k] + (int64_t)j * a.qchunk, min(a.qchunk, deg[k] - j * a.qchunk), vo[k]};
 }
 
 // Probe a batch of K neighbours. Words of the hot prefix come from the
@@ -1956,6 +1964,7 @@ LevelArgs BfsEngine::level_args() const {
   a.t_warp = t_warp_;
   a.t_nz = t_nz_;
   a.t_hub = warp_items_ ? t_warp_ : t_cta_;
+  a.align_items = align_items_ ? 1 : 0;
   a.part_log = part_log_;
   a.part_rank = part_rank_;
   a.chk_n = n_;
@@ -2330,6 +2339,7 @@ void BfsEngine::read_env() {
   // LBFS_NO_WARP_ITEMS=1: append them to the raw warp queue instead
   warp_items_ = !env_flag("LBFS_NO_WARP_ITEMS");
   qgrid_old_ = env_flag("LBFS_QGRID_OLD");
+  align_items_ = env_flag("LBFS_ALIGN_ITEMS");  // (A/B) queue-mode winners cut their slice items on window boundaries
   sweep_workers_ = !env_flag("LBFS_NO_SWEEP_WORKERS");  // (A/B) the dense small region as its own launch
   cl_dsm_always_ = env_flag("LBFS_CLUSTER_DSM_ALWAYS");  // (A/B) every cluster segment with the bitmap in DSMEM
   exit_fair_ = !env_flag("LBFS_NO_EXIT_FAIR");  // (A/B) cluster exit items of qchunk edges whatever the frontier

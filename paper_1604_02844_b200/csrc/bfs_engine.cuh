@@ -130,6 +130,7 @@ struct LevelArgs {
   // (t_warp: hubs and warp-bin rows — the next level streams them with the
   // descriptor in hand, no row_ptr round trip per row; t_cta: hubs only)
   int32_t t_hub;
+  int32_t align_items;      // queue-mode winners cut slice items on 128-element window boundaries
   // partitioned run (nparts = 1 << part_log > 1): this rank owns the ids of
   // bitmap words w with w % nparts == part_rank; pred_int/level_int, rows and
   // frontier entries use local row ids, bitmaps and neighbours global ids
@@ -577,6 +578,7 @@ class BfsEngine {
   bool cl_dsm_ = false;           // visited bitmap in distributed shared memory
   bool cl_no_dsm_ = false, cl_off_ = false;
   bool qgrid_old_ = false;
+  bool align_items_ = false;
   bool sweep_workers_ = true;
   bool cl_dsm_always_ = false;
   bool exit_fair_ = true;
