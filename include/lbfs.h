@@ -47,7 +47,7 @@ typedef struct lbfs_layer {
 typedef struct lbfs_timing {
   double bfs_ms;           /* init kernel start -> end of last level         */
   double init_ms;          /* K4 init (pred/level fill, bitmap clear, seed)  */
-  double expand_ms;        /* full-GPU levels: expansion kernels (summed)    */
+  double expand_ms;        /* full-GPU levels: expansion + merge + compaction kernels (summed) */
   double cluster_ms;       /* small-frontier levels on the cluster (summed)  */
   double finalize_ms;      /* output pass (parents / levels in original ids) */
   double d2h_ms;           /* host-output variant: output copy to host       */

@@ -15,6 +15,10 @@ bool g_sync_each = [] {
   const char* v = getenv("LBFS_SYNC_EACH");
   return v && *v && *v != '0';
 }();
+bool g_pdl = [] {
+  const char* v = getenv("LBFS_NO_PDL");
+  return !(v && *v && *v != '0');
+}();
 void sync_check(cudaStream_t st, const char* kernel, const char* file, int line) {
   const cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {

@@ -978,6 +978,7 @@ template <int M, int kPhases>
 __global__ void __launch_bounds__(expand_threads<M, kPhases>(), 1) k_expand(LevelArgs a, Frontier f, int32_t hot_words) {
   extern __shared__ __align__(128) uint8_t s_dyn[];
   __shared__ ExpandSmem s;
+  griddep_launch();
   expand_init(s, a);
   // (the shared-window base is made opaque: left alone, the compiler
   // rematerialises it — S2UR + three uniform ops — next to every shared OR)
@@ -989,7 +990,9 @@ __global__ void __launch_bounds__(expand_threads<M, kPhases>(), 1) k_expand(Leve
   if constexpr (M == kHeavy) {
     for (int i = threadIdx.x; i < hw4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
+    griddep_wait();  // (the prologue above overlaps the previous kernel's tail)
   } else {
+    griddep_wait();
     hot_load(s, h, a.visited);
   }
   Acc acc;
@@ -1015,6 +1018,8 @@ __global__ void __launch_bounds__(expand_threads<M, kPhases>(), 1) k_expand(Leve
 constexpr int kMergeRows = 16;
 __global__ void __launch_bounds__(256) k_merge_hot(const uint4* __restrict__ stage, int rows, int hw4, int stride4,
                                                    uint32_t* __restrict__ visited) {
+  griddep_launch();
+  griddep_wait();
   const int i = blockIdx.x * 256 + threadIdx.x;
   if (i >= hw4) return;
   const int r0 = blockIdx.y * kMergeRows, r1 = min(rows, r0 + kMergeRows);
@@ -1355,6 +1360,8 @@ __device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk,
 }
 
 __global__ void __launch_bounds__(kCompactThreads, LBFS_COMPACT_MINB) k_compact(CompactArgs c) {
+  griddep_launch();
+  griddep_wait();
   __shared__ CompactSmem sm;
   compact_block(c, blockIdx.x, sm, threadIdx.x, 1);
 }
@@ -1385,6 +1392,7 @@ __global__ void k_init(uint4* __restrict__ vis4, uint4* __restrict__ prev4, int6
 __global__ void k_init_seed(uint4* __restrict__ vis4, uint4* __restrict__ prev4, int64_t nwords4,
                             int4* __restrict__ lvl4, int64_t n4, Counters* __restrict__ ring, LevelArgs a,
                             const int32_t* __restrict__ old2new, int32_t root_orig) {
+  griddep_launch();
   const int32_t r = __ldg(old2new + root_orig);
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t rw4 = (int64_t)(r >> 5) >> 2, rl4 = (int64_t)r >> 2;
@@ -1503,6 +1511,7 @@ __global__ void k_publish(Counters* ring, int slot, int zero_slot, Counters* mai
                           unsigned long long value) {
   const int t = threadIdx.x;
   constexpr int kWords = (int)(sizeof(Counters) / 8);
+  griddep_wait();
   if (t < kWords) {
     reinterpret_cast<volatile unsigned long long*>(mail)[t] = reinterpret_cast<unsigned long long*>(&ring[slot])[t];
     reinterpret_cast<unsigned long long*>(&ring[zero_slot])[t] = 0ull;
@@ -1516,7 +1525,7 @@ __global__ void k_publish(Counters* ring, int slot, int zero_slot, Counters* mai
 
 void BfsEngine::publish_and_wait(int slot, int zero_slot, cudaStream_t st) {
   const unsigned long long want = ++seq_;
-  LBFS_LAUNCH(k_publish, 1, 32, 0, st, cnt_, slot, zero_slot, h_mail_, h_seq_, want);
+  LBFS_LAUNCH_PDL(k_publish, 1, 32, 0, st, cnt_, slot, zero_slot, h_mail_, h_seq_, want);
   wait_mail(want, st);
   h_cnt_[slot] = *const_cast<const Counters*>(h_mail_);
 }
@@ -1795,13 +1804,15 @@ void BfsEngine::launch_cluster(int64_t L, int cur, bool prev_bitmap, cudaStream_
   cfg.blockDim = dim3(kClusterThreads);
   cfg.dynamicSmemBytes = cl_smem_;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = cl_size_;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (behind k_init_seed / k_compact)
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_pdl ? 2 : 1;
   // The bitmap lives in the cluster's shared memory for a BFS's first segment
   // (nothing to load: visited = {root}) and for deep traversals (the lattice);
   // a late segment of a shallow BFS (R-MAT: the last one or two levels) claims
@@ -1910,37 +1921,47 @@ unsigned clamp_grid(int64_t blocks, int64_t cap) {
   return (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
 }
 
+// pdl: the launch directly follows another kernel of the level on the stream
+// (programmatic dependent launch: its prologue overlaps that kernel's tail)
+#define LBFS_LAUNCH_EXPAND(M, P)                                                                        \
+  do {                                                                                                  \
+    if (pdl)                                                                                            \
+      LBFS_LAUNCH_PDL((k_expand<M, P>), grid, (expand_threads<M, P>()), smem, st, a, f, hot);           \
+    else                                                                                                \
+      LBFS_LAUNCH((k_expand<M, P>), grid, (expand_threads<M, P>()), smem, st, a, f, hot);               \
+  } while (0)
+
 template <int M>
 static void launch_expand_m(int pi, unsigned grid, int smem, const LevelArgs& a, const Frontier& f, int32_t hot,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool pdl) {
   if (pi == 0) {
-    LBFS_LAUNCH((k_expand<M, 1>), grid, (expand_threads<M, 1>()), smem, st, a, f, hot);
+    LBFS_LAUNCH_EXPAND(M, 1);
   } else if (pi == 1) {
-    LBFS_LAUNCH((k_expand<M, 2>), grid, (expand_threads<M, 2>()), smem, st, a, f, hot);
+    LBFS_LAUNCH_EXPAND(M, 2);
   } else if (pi == 3) {
-    LBFS_LAUNCH((k_expand<M, 16>), grid, (expand_threads<M, 16>()), smem, st, a, f, hot);
+    LBFS_LAUNCH_EXPAND(M, 16);
   } else if (pi == 4) {
-    LBFS_LAUNCH((k_expand<M, 32>), grid, (expand_threads<M, 32>()), smem, st, a, f, hot);
+    LBFS_LAUNCH_EXPAND(M, 32);
   } else if (pi == 5) {
-    LBFS_LAUNCH((k_expand<M, 64>), grid, (expand_threads<M, 64>()), smem, st, a, f, hot);
+    LBFS_LAUNCH_EXPAND(M, 64);
   } else if (pi == 6) {  // slice items, then the raw queues, in one launch
     if constexpr (M == kBitmapOut)
       throw Failure(LBFS_ECUDA, "internal: no fused bitmap-mode launch");
     else
-      LBFS_LAUNCH((k_expand<M, 5>), grid, (expand_threads<M, 5>()), smem, st, a, f, hot);
+      LBFS_LAUNCH_EXPAND(M, 5);
   } else {
-    LBFS_LAUNCH((k_expand<M, 4>), grid, (expand_threads<M, 4>()), smem, st, a, f, hot);
+    LBFS_LAUNCH_EXPAND(M, 4);
   }
 }
 
 void BfsEngine::launch_expand(int mode, int pi, unsigned grid, const LevelArgs& a, const Frontier& f,
-                              cudaStream_t st) {
+                              cudaStream_t st, bool pdl) {
   if (mode == kHeavy)
-    launch_expand_m<kHeavy>(pi, grid, dyn_smem_, a, f, hot_words_, st);
+    launch_expand_m<kHeavy>(pi, grid, dyn_smem_, a, f, hot_words_, st, pdl);
   else if (mode == kBitmapOut)
-    launch_expand_m<kBitmapOut>(pi, grid, dyn_smem_, a, f, hot_words_, st);
+    launch_expand_m<kBitmapOut>(pi, grid, dyn_smem_, a, f, hot_words_, st, pdl);
   else
-    launch_expand_m<kQueueOut>(pi, grid, 0, a, f, 0, st);
+    launch_expand_m<kQueueOut>(pi, grid, 0, a, f, 0, st, pdl);
 }
 
 bool env_flag(const char* name) {
@@ -2134,16 +2155,19 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
     // after a queue-mode level the frontier is slice items + raw queues: one
     // launch for both (a launch costs ~5-10 us here: a queue level is short,
     // a heavy launch zeroes and stores its hot rows)
+    bool follows = sweep && !split_;  // a kernel of this level is already on the stream
     if (fuse_queues_ && !prev_bitmap && mode != kBitmapOut && has[0] && has[2] && !split_) {
-      launch_expand(mode, 6, grid, a, f, st);
+      launch_expand(mode, 6, grid, a, f, st, follows);
       a.stage_first = 0;
       has[0] = has[2] = false;
+      follows = true;
     }
     for (int pi = 0; pi < 6; ++pi) {
       if (split_ && !(sweep && pi == 0)) LBFS_CUDA(cudaEventRecord(ev_split_[pi], st));
       if (!has[pi]) continue;
-      launch_expand(mode, pi, grid, a, f, st);
+      launch_expand(mode, pi, grid, a, f, st, follows);
       a.stage_first = 0;
+      follows = !split_;
     }
     if (split_) LBFS_CUDA(cudaEventRecord(ev_split_[6], st));
   }
@@ -2151,14 +2175,17 @@ unsigned BfsEngine::expand_level(LevelArgs& a, const Counters& c, int mode, bool
   return grid;
 }
 
-void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st, bool heavy) {
+void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st, bool heavy, bool pdl) {
   CompactArgs ca{row_ptr_, new2old_loc_, visited_, prev_, nwl_, level_int_, (int32_t)(L + 1),
                  t_cta_, t_warp_, t_nz_, &cnt_[(L + 1) % kCounterRing], q_small_[cur ^ 1], q_cta_[cur ^ 1],
                  q_items_[cur ^ 1], q_wslice_[cur ^ 1], front_, part_log_, part_rank_, fsend,
                  col_idx_, first_nbr_, pred_int_,
                  0,  // heavy: blind ORs leave no parent; k_resolve gives them one off the critical path
                  (int32_t)L};
-  LBFS_LAUNCH(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
+  if (pdl)
+    LBFS_LAUNCH_PDL(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
+  else
+    LBFS_LAUNCH(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
   if (heavy) {
     // the parents of level L+1's vertices are read by k_finalize only: resolve
     // them on the side stream while the next levels run (joined before k_finalize)
@@ -2229,8 +2256,13 @@ void BfsEngine::merge_hot(cudaStream_t st) {
   // (the sweep stores whole rows first in its level; expand kernels alone write only their prefix)
   const int hw4 = merge_words_ / 4;
   const dim3 grid((unsigned)((hw4 + 255) / 256), (unsigned)((expand_grid_ + kMergeRows - 1) / kMergeRows));
-  LBFS_LAUNCH(k_merge_hot, grid, 256, 0, st, reinterpret_cast<const uint4*>(stage_), expand_grid_, hw4,
-              stage_words_ / 4, visited_);
+  // (directly behind the level's last expansion kernel)
+  if (split_)
+    LBFS_LAUNCH(k_merge_hot, grid, 256, 0, st, reinterpret_cast<const uint4*>(stage_), expand_grid_, hw4,
+                stage_words_ / 4, visited_);
+  else
+    LBFS_LAUNCH_PDL(k_merge_hot, grid, 256, 0, st, reinterpret_cast<const uint4*>(stage_), expand_grid_, hw4,
+                    stage_words_ / 4, visited_);
 }
 
 // Output pass: parents (pad32(n), SENTINEL padding) and, when asked for,
@@ -2469,9 +2501,14 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
                                     : expand_level(a, c, heavy ? kHeavy : bitmap ? kBitmapOut : kQueueOut, prev_bitmap,
                                                    cur, L, st);
     if (heavy) merge_hot(st);
-    LBFS_CUDA(cudaEventRecord(ev_[3], st));
+    // the level's kernels (expansion, merge, compaction) follow one another
+    // directly on the stream (programmatic dependent launches); the timing
+    // event closes the level behind the compaction (trace modes: before it)
+    const bool ev_mid = trace_ || split_ || bottom_up;
+    if (ev_mid) LBFS_CUDA(cudaEventRecord(ev_[3], st));
     timed_level = true;
-    if (bitmap) compact_level(cur, L, nullptr, st, heavy);
+    if (bitmap) compact_level(cur, L, nullptr, st, heavy, !ev_mid);
+    if (!ev_mid) LBFS_CUDA(cudaEventRecord(ev_[3], st));
     if (trace_ || split_) {
       LBFS_CUDA(cudaEventRecord(ev_[5], st));
       LBFS_CUDA(cudaEventSynchronize(ev_[5]));

@@ -189,6 +189,11 @@ __host__ __device__ __forceinline__ int64_t part_global(int64_t l, int32_t part_
   return ((((l >> 5) << part_log) | part_rank) << 5) | (l & 31);
 }
 
+// Programmatic dependent launch (see LBFS_LAUNCH_PDL): both are no-ops in a
+// kernel launched the plain way.
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Heavy levels, a lane's four consecutive elements of a sorted row, all in the
 // hot prefix: blind ORs into the CTA's shared copy (shared-window address
 // `base`), with runs in one bitmap word merged into a single reduction. The
@@ -493,14 +498,15 @@ class BfsEngine {
 
  private:
   void build_layout(const Csr& csr);
-  void launch_expand(int mode, int pi, unsigned grid, const LevelArgs& a, const Frontier& f, cudaStream_t st);
+  void launch_expand(int mode, int pi, unsigned grid, const LevelArgs& a, const Frontier& f, cudaStream_t st,
+                     bool pdl = false);
   LevelArgs level_args() const;
   // frontier of level L (queue slot cur, counters c) -> launches; returns the grid
   // mode: 0 bitmap, 1 queue, 3 heavy bitmap (blind hot ORs, see LevelArgs::stage)
   unsigned bottom_up_level(const Counters& c, bool prev_bitmap, int cur, cudaStream_t st);
   unsigned expand_level(LevelArgs& a, const Counters& c, int mode, bool prev_bitmap, int cur, int64_t L,
                         cudaStream_t st);
-  void compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st, bool heavy = false);
+  void compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st, bool heavy = false, bool pdl = false);
   void merge_hot(cudaStream_t st);
   void read_env();
   void finalize(int32_t* d_pred, int32_t* d_level, cudaStream_t st);

@@ -686,6 +686,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
   extern __shared__ __align__(16) uint8_t s_dyn[];
   __shared__ ClusterSmem s;
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+  griddep_wait();  // (a programmatic dependent launch behind k_init_seed / k_compact)
   Ctx x;
   x.wt = nullptr;
   x.wdone = 0;

@@ -43,6 +43,33 @@ void sync_check(cudaStream_t st, const char* kernel, const char* file, int line)
     if (::lbfs::g_sync_each) ::lbfs::sync_check((stream), #kernel, __FILE__, __LINE__); \
   } while (0)
 
+// Programmatic dependent launch: the kernel may start (its CTAs take the SMs the
+// previous kernel of the stream frees, and run their prologue) before that
+// kernel has completed; it calls griddep_wait() before touching anything the
+// previous kernel wrote. Only for a kernel that directly follows another
+// kernel on the stream (LBFS_NO_PDL=1: plain launches).
+extern bool g_pdl;
+#define LBFS_LAUNCH_PDL(KERNEL, GRID, BLOCK, SMEM, STREAM, ...)                          \
+  do {                                                                                  \
+    if (::lbfs::g_pdl) {                                                                \
+      cudaLaunchConfig_t cfg_{};                                                        \
+      cfg_.gridDim = dim3(GRID);                                                        \
+      cfg_.blockDim = dim3(BLOCK);                                                      \
+      cfg_.dynamicSmemBytes = (size_t)(SMEM);                                           \
+      cfg_.stream = (STREAM);                                                           \
+      cudaLaunchAttribute at_[1];                                                       \
+      at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                   \
+      at_[0].val.programmaticStreamSerializationAllowed = 1;                            \
+      cfg_.attrs = at_;                                                                 \
+      cfg_.numAttrs = 1;                                                                \
+      LBFS_CUDA(cudaLaunchKernelEx(&cfg_, KERNEL, __VA_ARGS__));                        \
+      ::lbfs::g_launches.fetch_add(1, std::memory_order_relaxed);                       \
+      if (::lbfs::g_sync_each) ::lbfs::sync_check((STREAM), #KERNEL, __FILE__, __LINE__); \
+    } else {                                                                            \
+      LBFS_LAUNCH(KERNEL, GRID, BLOCK, SMEM, STREAM, __VA_ARGS__);                      \
+    }                                                                                   \
+  } while (0)
+
 void set_error(const std::string& m);
 
 template <typename T>

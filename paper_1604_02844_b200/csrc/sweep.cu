@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int hw4 = s.hot_words >> 2;
   uint4* h4 = reinterpret_cast<uint4*>(s_hot);
+  griddep_launch();
   for (int i = tid; i < hw4; i += blockDim.x) h4[i] = make_uint4(0, 0, 0, 0);
   __shared__ int32_t s_T[kSmallMax + 2];
   __shared__ int64_t s_B[kSmallMax + 1];
@@ -301,6 +302,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) k_sweep(const __grid_constan
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  griddep_wait();  // (a programmatic dependent launch: the prologue above ran under the previous kernel's tail)
   const int64_t nchunks = (s.nwin_all + kChunkWins - 1) / kChunkWins;
   const int64_t my_chunks = nchunks > blockIdx.x ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
