@@ -501,8 +501,9 @@ def run_ours(args, rank, world, local):
     value_local = hm(teps)
     ms_step_local = sum(r.timing["bfs_ms"] for r in runs) / args.steps
     # roofline: the whole BFS against B_alg; expansion = the
-    # level kernels alone (full-GPU levels: expansion, merge and compaction —
-    # the 40 B/vertex term is written there — plus the cluster's small levels)
+    # level loop (init, every level's kernels incl. compaction — the 40 B/vertex
+    # term is written there —, launch latency and host round trips): the BFS
+    # without its output pass
     alg = sum(b_alg(r.traversed_edge_count, r.timing["reached"], n) for r in runs)
     bfs_ms = sum(r.timing["bfs_ms"] for r in runs)
     exp_bytes = sum(8 * r.traversed_edge_count + 40 * r.timing["reached"] for r in runs)
@@ -601,8 +602,9 @@ def run_ours(args, rank, world, local):
                      "dram": dram,
                      "expansion": {"alg_bytes_per_bfs": exp_bytes / len(runs), "ms_per_bfs": exp_ms / len(runs),
                                    "frac_of_peak": exp_bytes / (exp_ms * 1e-3) / 1e9 / hbm_gbs,
-                                   "kernels": "full-GPU level launches (expansion bins, merge, compaction) + "
-                                              "the cluster's small levels"}},
+                                   "kernels": "the level loop: init, every level's kernels (expansion bins, merge, "
+                                              "compaction, cluster segments), launch latency and host round trips; "
+                                              "the output pass excluded"}},
         "e2e": {"value": e2e, "unit": "GTEPS", "h2d_bytes_per_step": 8,
                 "d2h_bytes_per_step": d2h_bytes, "step": "one bfs(g, root) call (harmonic mean over roots)",
                 "api": "paper_1604_02844_b200.bfs(g, root), parents to host (levels on first access)",

@@ -43,9 +43,16 @@ typedef struct lbfs_layer {
   int64_t discovered; /* vertices first reached in this layer        */
 } lbfs_layer;
 
-/* Device-side timing of one BFS (CUDA events on the BFS stream). */
+/* Device-side timing of one BFS. bfs_ms and finalize_ms come from CUDA events
+ * on the BFS stream. No event is recorded between the kernels of a BFS (an
+ * event there serialises the stream and ends a chain of programmatic
+ * dependent launches): cluster_ms is the device time the cluster kernel
+ * measured inside its launches, expand_ms the rest of the level loop (init,
+ * full-GPU level kernels, launch latency and host round trips), init_ms 0.
+ * LBFS_FULL_EVENTS=1 brackets init, every full-GPU level and every cluster
+ * launch with events instead (slower; the meanings in the comments below). */
 typedef struct lbfs_timing {
-  double bfs_ms;           /* init kernel start -> end of last level         */
+  double bfs_ms;           /* init kernel start -> end of the output pass    */
   double init_ms;          /* K4 init (pred/level fill, bitmap clear, seed)  */
   double expand_ms;        /* full-GPU levels: expansion + merge + compaction kernels (summed) */
   double cluster_ms;       /* small-frontier levels on the cluster (summed)  */

@@ -1526,6 +1526,7 @@ __global__ void k_publish(Counters* ring, int slot, int zero_slot, Counters* mai
 void BfsEngine::publish_and_wait(int slot, int zero_slot, cudaStream_t st) {
   const unsigned long long want = ++seq_;
   LBFS_LAUNCH_PDL(k_publish, 1, 32, 0, st, cnt_, slot, zero_slot, h_mail_, h_seq_, want);
+  flush_resolve(st);
   wait_mail(want, st);
   h_cnt_[slot] = *const_cast<const Counters*>(h_mail_);
 }
@@ -2186,9 +2187,27 @@ void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t 
     LBFS_LAUNCH_PDL(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
   else
     LBFS_LAUNCH(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
-  if (heavy) {
-    // the parents of level L+1's vertices are read by k_finalize only: resolve
-    // them on the side stream while the next levels run (joined before k_finalize)
+  if (heavy && lean_events_ && nparts_ == 1) {
+    resolve_deferred_ = L + 1;  // (launched behind the level's publish / cluster kernel: launch_resolve)
+    return;
+  }
+  if (heavy) launch_resolve(L + 1, st);
+}
+
+// (lean events) the side work of the level just launched, behind its publish /
+// cluster kernel on the stream and before the host waits for the mailbox
+void BfsEngine::flush_resolve(cudaStream_t st) {
+  if (resolve_deferred_ < 0) return;
+  launch_resolve(resolve_deferred_, st);
+  resolve_deferred_ = -1;
+}
+
+// The parents of a heavy level's new vertices (level lvl) are read by
+// k_finalize only: resolve them on the side stream while the next levels run
+// (joined before k_finalize).
+void BfsEngine::launch_resolve(int64_t lvl, cudaStream_t st) {
+  const int64_t L = lvl - 1;
+  {
     LBFS_CUDA(cudaEventRecord(ev_resolve_, st));
     LBFS_CUDA(cudaStreamWaitEvent(res_st_, ev_resolve_, 0));
     const int64_t n4 = (n_loc_ + 3) / 4;
@@ -2371,6 +2390,12 @@ void BfsEngine::read_env() {
   // LBFS_NO_WARP_ITEMS=1: append them to the raw warp queue instead
   warp_items_ = !env_flag("LBFS_NO_WARP_ITEMS");
   qgrid_old_ = env_flag("LBFS_QGRID_OLD");
+  // No timing events between the kernels of a BFS: an event record between two
+  // kernels costs a few microseconds of stream serialisation each and ends a
+  // chain of programmatic dependent launches (S24 401 -> 414, S20 106 -> 117
+  // GTEPS). The cluster segments report their own device time through the
+  // mailbox; LBFS_FULL_EVENTS=1 (and the trace modes) bracket every level.
+  lean_events_ = !env_flag("LBFS_FULL_EVENTS") && !trace_ && !split_;
   align_items_ = env_flag("LBFS_ALIGN_ITEMS");  // (A/B) queue-mode winners cut their slice items on window boundaries
   sweep_workers_ = !env_flag("LBFS_NO_SWEEP_WORKERS");  // (A/B) the dense small region as its own launch
   cl_dsm_always_ = env_flag("LBFS_CLUSTER_DSM_ALWAYS");  // (A/B) every cluster segment with the bitmap in DSMEM
@@ -2396,6 +2421,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   }
   const int64_t launches0 = g_launches.load();
   n_cl_ev_ = 0;
+  resolve_deferred_ = -1;
   LBFS_CUDA(cudaEventRecord(ev_[0], st));
   LevelArgs a = level_args();
   a.next_small = q_small_[0];
@@ -2406,7 +2432,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     LBFS_LAUNCH(k_init_seed, grid, 256, 0, st, (uint4*)visited_, (uint4*)prev_, (nwords_ + 3) / 4, (int4*)level_int_,
                 (n_ + 3) / 4, cnt_, a, old2new_, (int32_t)root);
   }
-  LBFS_CUDA(cudaEventRecord(ev_[1], st));
+  if (!lean_events_) LBFS_CUDA(cudaEventRecord(ev_[1], st));
   const bool use_cluster = cl_size_ > 0 && !cl_off_ && !split_ && !count_;
   if (!use_cluster) {
     LBFS_CUDA(cudaMemcpyAsync(h_mail_, &cnt_[0], sizeof(Counters), cudaMemcpyDeviceToHost, st));
@@ -2436,13 +2462,15 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       small_next = c.discovered > 0 && c.edges <= cl_exit_edges_;
     }
     if (use_cluster && small_next) {
-      const int ce = n_cl_ev_ < kClEvents ? n_cl_ev_++ : -1;
+      const int ce = !lean_events_ && n_cl_ev_ < kClEvents ? n_cl_ev_++ : -1;
       if (ce >= 0) LBFS_CUDA(cudaEventRecord(ev_cl_[2 * ce], st));
       launch_cluster(L, cur, prev_bitmap, st, L == 0 ? (int32_t)root : -1);
       if (ce >= 0) LBFS_CUDA(cudaEventRecord(ev_cl_[2 * ce + 1], st));
+      flush_resolve(st);
       wait_mail(seq_, st);
       std::atomic_thread_fence(std::memory_order_acquire);
       c = *const_cast<const Counters*>(h_mail_);
+      if (lean_events_) cluster_ms += 1e-6 * (double)const_cast<volatile unsigned long long*>(h_seq_)[1];
       k = (int64_t)c.pad[0] - L;
       if (k < 0 || k > kLoopCap) throw Failure(LBFS_ECUDA, "internal: cluster level loop state");
     } else if (use_cluster) {
@@ -2453,7 +2481,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       publish_and_wait((int)(L % kCounterRing), (int)((L + 1) % kCounterRing), st);
       c = h_cnt_[L % kCounterRing];
     }
-    if (timed_level) {  // the last full-GPU level's expansion (its events completed before the mailbox)
+    if (timed_level && !lean_events_) {  // the last full-GPU level's expansion (its events completed before the mailbox)
       float ms = 0.f;
       LBFS_CUDA(cudaEventElapsedTime(&ms, ev_[2], ev_[3]));
       expand_ms += ms;
@@ -2496,7 +2524,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     const bool heavy = !bottom_up && bitmap && stage_ && heavy_div_ > 0 &&
                        c.edges * (unsigned long long)heavy_div_ >= (unsigned long long)nnz_ &&
                        (heavy_vis_pct_ <= 0 || seen_before * 100ull <= c.edges * (unsigned long long)heavy_vis_pct_);
-    LBFS_CUDA(cudaEventRecord(ev_[2], st));
+    if (!lean_events_) LBFS_CUDA(cudaEventRecord(ev_[2], st));
     const unsigned grid = bottom_up ? bottom_up_level(c, prev_bitmap, cur, st)
                                     : expand_level(a, c, heavy ? kHeavy : bitmap ? kBitmapOut : kQueueOut, prev_bitmap,
                                                    cur, L, st);
@@ -2504,11 +2532,11 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
     // the level's kernels (expansion, merge, compaction) follow one another
     // directly on the stream (programmatic dependent launches); the timing
     // event closes the level behind the compaction (trace modes: before it)
-    const bool ev_mid = trace_ || split_ || bottom_up;
+    const bool ev_mid = (trace_ || split_ || bottom_up) && !lean_events_;
     if (ev_mid) LBFS_CUDA(cudaEventRecord(ev_[3], st));
     timed_level = true;
     if (bitmap) compact_level(cur, L, nullptr, st, heavy, !ev_mid);
-    if (!ev_mid) LBFS_CUDA(cudaEventRecord(ev_[3], st));
+    if (!ev_mid && !lean_events_) LBFS_CUDA(cudaEventRecord(ev_[3], st));
     if (trace_ || split_) {
       LBFS_CUDA(cudaEventRecord(ev_[5], st));
       LBFS_CUDA(cudaEventSynchronize(ev_[5]));
@@ -2568,8 +2596,13 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
   if (t) {
     float total = 0.f, init = 0.f, fin = 0.f;
     LBFS_CUDA(cudaEventElapsedTime(&total, ev_[0], ev_[4]));
-    LBFS_CUDA(cudaEventElapsedTime(&init, ev_[0], ev_[1]));
+    if (!lean_events_) LBFS_CUDA(cudaEventElapsedTime(&init, ev_[0], ev_[1]));
     LBFS_CUDA(cudaEventElapsedTime(&fin, ev_[6], ev_[4]));
+    if (lean_events_) {  // everything before the output pass that is not a cluster segment
+      float loop = 0.f;
+      LBFS_CUDA(cudaEventElapsedTime(&loop, ev_[0], ev_[6]));
+      expand_ms = std::max(0.0, (double)loop - cluster_ms);
+    }
     t->bfs_ms = total;
     t->init_ms = init;
     t->expand_ms = expand_ms;

@@ -508,6 +508,8 @@ class BfsEngine {
                         cudaStream_t st);
   void compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t st, bool heavy = false, bool pdl = false);
   void merge_hot(cudaStream_t st);
+  void launch_resolve(int64_t lvl, cudaStream_t st);
+  void flush_resolve(cudaStream_t st);
   void read_env();
   void finalize(int32_t* d_pred, int32_t* d_level, cudaStream_t st);
   void levels_out(int32_t* d_level, cudaStream_t st);
@@ -584,6 +586,8 @@ class BfsEngine {
   bool cl_dsm_ = false;           // visited bitmap in distributed shared memory
   bool cl_no_dsm_ = false, cl_off_ = false;
   bool qgrid_old_ = false;
+  bool lean_events_ = false;
+  int64_t resolve_deferred_ = -1;
   bool align_items_ = false;
   bool sweep_workers_ = true;
   bool cl_dsm_always_ = false;

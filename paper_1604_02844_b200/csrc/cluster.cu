@@ -687,6 +687,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
   __shared__ ClusterSmem s;
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   griddep_wait();  // (a programmatic dependent launch behind k_init_seed / k_compact)
+  const unsigned long long t_start = gtimer();  // (the segment's device time goes to the mailbox: no events around it)
   Ctx x;
   x.wt = nullptr;
   x.wdone = 0;
@@ -941,6 +942,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&m);
 #pragma unroll
     for (int i = 0; i < (int)(sizeof(Counters) / 8); ++i) dst[i] = src[i];
+    reinterpret_cast<volatile unsigned long long*>(p.seq)[1] = gtimer() - t_start;  // ns inside this launch
     __threadfence_system();
     *reinterpret_cast<volatile unsigned long long*>(p.seq) = p.seq_value;
   }
