@@ -1781,6 +1781,7 @@ void BfsEngine::launch_cluster(int64_t L, int cur, bool prev_bitmap, cudaStream_
   p.L0 = L;
   p.max_levels = kLoopCap;
   p.exit_edges = cl_exit_edges_;
+  p.exit_hub_edges = cl_exit_hub_edges_;
   p.bitmap_min_edges = (unsigned long long)std::max<int64_t>(bitmap_floor_, n_ / bitmap_div_);
   for (int b = 0; b < 2; ++b) {
     p.out_small[b] = q_small_[b];
@@ -2382,6 +2383,7 @@ void BfsEngine::read_env() {
   qchunk_ = (int)std::min<long long>(kChunk, std::max<long long>(kQChunkMin, geti("LBFS_QCHUNK", kQChunkDefault))) & ~127;
   // small-frontier levels run on the cluster while a frontier has at most this many edges
   cl_exit_edges_ = (unsigned long long)std::max<long long>(64, geti("LBFS_CLUSTER_EDGES", kClusterExitEdges));
+  cl_exit_hub_edges_ = (unsigned long long)std::max<long long>(64, geti("LBFS_CLUSTER_HUB_EDGES", kClusterExitHubEdges));
   cl_mail_cap_env_ = (int)geti("LBFS_CLUSTER_MAIL_CAP", 0);
   cl_no_mail_ = env_flag("LBFS_CLUSTER_NO_MAIL");  // (A/B) DSMEM mode with remote claims instead of candidate mailboxes
   cl_no_dsm_ = env_flag("LBFS_CLUSTER_GLOBAL");  // claim on the global bitmap even when the slices fit
@@ -2459,7 +2461,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       // publish (the cluster follows when the frontier is small after all)
       publish_and_wait((int)(L % kCounterRing), (int)((L + 1) % kCounterRing), st);
       c = h_cnt_[L % kCounterRing];
-      small_next = c.discovered > 0 && c.edges <= cl_exit_edges_;
+      small_next = c.discovered > 0 && cluster_takes(c.discovered, c.edges, cl_exit_edges_, cl_exit_hub_edges_);
     }
     if (use_cluster && small_next) {
       const int ce = !lean_events_ && n_cl_ev_ < kClEvents ? n_cl_ev_++ : -1;
@@ -2502,7 +2504,7 @@ void BfsEngine::run(int64_t root, int32_t* d_pred, int32_t* d_level, lbfs_timing
       prev_bitmap = prev_bu = false;
     }
     if (c.discovered == 0) break;
-    if (k > 0 && c.edges <= cl_exit_edges_) continue;  // the cluster stopped at its level cap
+    if (k > 0 && cluster_takes(c.discovered, c.edges, cl_exit_edges_, cl_exit_hub_edges_)) continue;  // the cluster stopped at its level cap
     // (2) one level on the whole GPU
     const bool bitmap = c.edges >= bitmap_min_edges;
     // direction-optimising (opt-in): bottom-up while the frontier's edges

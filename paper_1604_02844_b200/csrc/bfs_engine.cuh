@@ -280,6 +280,16 @@ constexpr int64_t kLoopCap = 1 << 16;  // levels per cluster-kernel launch
 // Small-frontier levels on one thread-block cluster (cluster.cu).
 constexpr int kClusterThreads = 512;
 constexpr unsigned long long kClusterExitEdges = 1ull << 16;  // default LBFS_CLUSTER_EDGES
+constexpr unsigned long long kClusterExitHubEdges = 1ull << 14;  // default LBFS_CLUSTER_HUB_EDGES
+// A frontier stays on the cluster while it is thin: at most exit_edges edges
+// (a lattice level: thousands of vertices of degree <= 4), and at most
+// exit_hub_edges when its rows are long (average degree > 32: an R-MAT level
+// of hubs, which 16 SMs stream slowly and the full grid takes in one step).
+__host__ __device__ __forceinline__ bool cluster_takes(unsigned long long verts, unsigned long long edges,
+                                                       unsigned long long exit_edges,
+                                                       unsigned long long exit_hub_edges) {
+  return edges <= exit_edges && !(edges > exit_hub_edges && edges > 32ull * verts);
+}
 constexpr int kMaxCluster = 16;
 constexpr int kClusterStage = 128;  // winners staged per target CTA before the push
 // A frontier entry of the cluster's small queues: the vertex (internal id)
@@ -318,6 +328,7 @@ struct ClusterArgs {
   Counters* ring;
   int64_t L0, max_levels;
   unsigned long long exit_edges;  // leave when a frontier has more edges
+  unsigned long long exit_hub_edges;  // ... or more than this many with an average degree above 32 (hub rows)
   unsigned long long bitmap_min_edges;  // the host's next level is bitmap mode from this many edges
   int32_t* out_small[2];    // exit frontier (queue format) by level parity
   CtaItem* out_cta[2];
@@ -604,6 +615,7 @@ class BfsEngine {
   int cl_smem_ = 0;
   int64_t cl_cap_ = 0;
   unsigned long long cl_exit_edges_ = kClusterExitEdges;
+  unsigned long long cl_exit_hub_edges_ = kClusterExitHubEdges;
   QEntry* cl_spill_ = nullptr;
   CtaItem* cl_big_ = nullptr;
   unsigned long long* cl_big_cnt_ = nullptr;

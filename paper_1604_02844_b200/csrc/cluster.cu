@@ -728,7 +728,8 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
     p.big_cnt[(p.L0 + 1) % kCounterRing] = 0ull;  // appended during level L0
     p.big_cnt[(p.L0 + 2) % kCounterRing] = 0ull;
   }
-  const bool run = c0.discovered > 0 && c0.edges <= p.exit_edges && p.max_levels > 0;
+  const bool run = c0.discovered > 0 && cluster_takes(c0.discovered, c0.edges, p.exit_edges, p.exit_hub_edges) &&
+                   p.max_levels > 0;
   if (DSM && run) {  // this CTA's sectors of the visited bitmap
     const int64_t nsec = (p.nwords + 7) / 8, my = slice_words / 8;
     if (p.root_orig >= 0) {  // first level of a BFS: visited = {root}
@@ -864,7 +865,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1) k_cluster_levels(const __g
         done = true;
         break;
       }
-      if (te > p.exit_edges || L - p.L0 >= p.max_levels) break;
+      if (!cluster_takes(td, te, p.exit_edges, p.exit_hub_edges) || L - p.L0 >= p.max_levels) break;
     }
   }
   // ---- exit: the frontier of level L in the host's queue format (slot L % 3)
