@@ -1528,6 +1528,7 @@ void BfsEngine::publish_and_wait(int slot, int zero_slot, cudaStream_t st) {
   LBFS_LAUNCH_PDL(k_publish, 1, 32, 0, st, cnt_, slot, zero_slot, h_mail_, h_seq_, want);
   flush_resolve(st);
   wait_mail(want, st);
+  std::atomic_thread_fence(std::memory_order_acquire);  // (the counters are read after the sequence word)
   h_cnt_[slot] = *const_cast<const Counters*>(h_mail_);
 }
 

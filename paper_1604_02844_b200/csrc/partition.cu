@@ -464,6 +464,7 @@ void BfsEngine::part_level_done(const unsigned long long* red_global, lbfs_layer
               want);
   part_fgath_ = nullptr;
   wait_mail(want, st);
+  std::atomic_thread_fence(std::memory_order_acquire);  // (the mailbox is read after the sequence word)
   if (L >= 0) h_cnt_[slot] = *const_cast<const Counters*>(h_mail_);
   if (reinterpret_cast<volatile unsigned long long*>(h_red_)[2])
     throw Failure(LBFS_ECUDA, "internal: sparse exchange slice overflow");
