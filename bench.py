@@ -580,7 +580,10 @@ def run_ours(args, rank, world, local):
                         lambda: build_rmat_graph(RmatParams(scale=27, seed=1)), 64, warm_passes=1, passes=1)
                 except Exception as e:  # noqa: BLE001
                     extra["rmat-s27-ef16-64roots"] = {"error": f"{type(e).__name__}: {e}"[:300]}
-                    torch.cuda.empty_cache()
+                    try:
+                        torch.cuda.empty_cache()
+                    except Exception:  # noqa: BLE001  (the headline line below is printed regardless)
+                        pass
             else:
                 extra["rmat-s27-ef16-64roots"] = {"skipped": f"{free_b >> 30} GiB free on the device"}
     line = {
