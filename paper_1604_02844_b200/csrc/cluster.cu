@@ -41,7 +41,10 @@ namespace {
 constexpr unsigned kF = 0xFFFFFFFFu;
 constexpr int kCT = kClusterThreads;
 constexpr int kCW = kCT / 32;
-constexpr int kBigChunk = 512;  // elements per warp task of a degree >= 32 row
+#ifndef LBFS_BIG_CHUNK
+#define LBFS_BIG_CHUNK 512
+#endif
+constexpr int kBigChunk = LBFS_BIG_CHUNK;  // elements per warp task of a degree >= 32 row
 
 __device__ __forceinline__ uint32_t cl_rank() {
   uint32_t r;
