@@ -52,7 +52,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--roots", type=int, default=64)
-    ap.add_argument("--cpu-roots", type=int, default=8, help="roots per step of the --impl reference arm")
+    ap.add_argument("--cpu-roots", type=int, default=0,
+                    help="roots per step of the --impl reference arm (0: enough for the timed steps to cover "
+                         "every root of the set once, at most 16)")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of CPU-baseline sampling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra-configs", action="store_true", help="skip the S20 / lattice / S27 keys")
@@ -228,7 +230,9 @@ def run_reference(args, rank, world):
     build_s = time.perf_counter() - t0
     roots = oracle.pick_roots(np.diff(rp), args.roots, 1, True).tolist()
     threads = oracle.max_threads()
-    per_step = max(1, args.cpu_roots)
+    # (default: the timed steps together cover the whole root set — the same
+    # roots the device arm times — in at most 16 BFS of ~0.2 s per step)
+    per_step = args.cpu_roots if args.cpu_roots > 0 else min(16, -(-args.roots // max(1, args.steps)))
     vals, step_times = [], []
     cursor = 0
     for step in range(args.warmup + args.steps):
