@@ -1049,9 +1049,11 @@ __global__ void __launch_bounds__(256) k_merge_hot(const uint4* __restrict__ sta
 #define LBFS_COMPACT_MINB 1
 #endif
 constexpr int kCompactThreads = 256;
-constexpr int kCompactVerts = 4096;
-constexpr int kCompactWords = kCompactVerts / 32;
-constexpr int kCompactSteps = kCompactVerts / kCompactThreads;
+// ids per compaction block: 4096, or 2048 for small graphs (n < 4 M: the
+// compaction of a small graph is a handful of blocks per SM, each a chain of
+// scans and barriers — smaller blocks shorten the chain: S20 +3%; S24 -3%)
+constexpr int kCompactVertsBig = 4096, kCompactVertsSmall = 2048;
+constexpr int64_t kCompactSmallGraph = (int64_t)1 << 22;
 constexpr int kCompactSparseDiv = 8;  // pass 2 walks only the new ids when fewer than 1/8 of the block's ids are new
 
 // A compaction group is 256 threads synchronised on named barrier `bar`
@@ -1091,24 +1093,27 @@ __device__ __forceinline__ int scan128(int t, int bar, int val, int* s_w, int* t
   return before + incl - val;
 }
 
+template <int V>
 struct CompactSmem {
   unsigned long long base[4];
   unsigned long long red[3][kCompactThreads / 32];
-  uint32_t new_[kCompactWords];
-  uint32_t lmask[kCompactWords];
-  int32_t lpre[kCompactWords];
-  int32_t npre[kCompactWords];  // exclusive prefix of new vertices per word
-  uint32_t wmask[kCompactWords];
-  int32_t wpre[kCompactWords];
-  int32_t gsum[kCompactWords];
-  int32_t hitems[kCompactWords];  // hub slices per word, then their word offsets
+  uint32_t new_[V / 32];
+  uint32_t lmask[V / 32];
+  int32_t lpre[V / 32];
+  int32_t npre[V / 32];  // exclusive prefix of new vertices per word
+  uint32_t wmask[V / 32];
+  int32_t wpre[V / 32];
+  int32_t gsum[V / 32];
+  int32_t hitems[V / 32];  // hub slices per word, then their word offsets
   int32_t w[4];
-  int32_t deg[kCompactVerts];
+  int32_t deg[V];
 };
 
 // One compaction block (kCompactVerts ids) by a 256-thread group: thread t
 // of the group, named barrier `bar`, shared scratch sm.
-__device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk, CompactSmem& sm, int t, int bar) {
+template <int V>
+__device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk, CompactSmem<V>& sm, int t, int bar) {
+  constexpr int kCompactVerts = V, kCompactWords = V / 32, kCompactSteps = V / kCompactThreads;
   uint32_t* s_new = sm.new_;
   uint32_t* s_lmask = sm.lmask;
   int32_t* s_lpre = sm.lpre;
@@ -1359,11 +1364,12 @@ __device__ __forceinline__ void compact_block(const CompactArgs& c, int64_t blk,
   }
 }
 
+template <int V>
 __global__ void __launch_bounds__(kCompactThreads, LBFS_COMPACT_MINB) k_compact(CompactArgs c) {
   griddep_launch();
   griddep_wait();
-  __shared__ CompactSmem sm;
-  compact_block(c, blockIdx.x, sm, threadIdx.x, 1);
+  __shared__ CompactSmem<V> sm;
+  compact_block<V>(c, blockIdx.x, sm, threadIdx.x, 1);
 }
 
 
@@ -1593,7 +1599,7 @@ BfsEngine::BfsEngine(const Csr& csr, int rank, int nparts) {
   // (queue-mode winners also emit warp-bin rows as items; aligned cuts add at most one item per row)
   cap_cta_ = nnz_loc_ / kQChunkMin + 2 * (int64_t)t_warp_ + 2;
   // group items: one per started kItemElems of each 32-entry group, per block
-  cap_items_ = nnz_loc_ / kItemElems + n_loc_ / 32 + 2 * ((n_loc_ + kCompactVerts - 1) / kCompactVerts) + 16;
+  cap_items_ = nnz_loc_ / kItemElems + n_loc_ / 32 + 2 * ((n_loc_ + kCompactVertsSmall - 1) / kCompactVertsSmall) + 16;
   for (int b = 0; b < 2; ++b) {
     q_small_[b] = dev_alloc<int32_t>((size_t)std::max<int64_t>(n_loc_, 1));
     q_warp_[b] = dev_alloc<int32_t>((size_t)std::max<int64_t>(t_warp_, 1));
@@ -2185,10 +2191,20 @@ void BfsEngine::compact_level(int cur, int64_t L, uint32_t* fsend, cudaStream_t 
                  col_idx_, first_nbr_, pred_int_,
                  0,  // heavy: blind ORs leave no parent; k_resolve gives them one off the critical path
                  (int32_t)L};
-  if (pdl)
-    LBFS_LAUNCH_PDL(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
-  else
-    LBFS_LAUNCH(k_compact, (unsigned)((n_loc_ + kCompactVerts - 1) / kCompactVerts), kCompactThreads, 0, st, ca);
+  const bool small_graph = n_loc_ < kCompactSmallGraph && !compact_big_;
+  const int cv = small_graph ? kCompactVertsSmall : kCompactVertsBig;
+  const unsigned cgrid = (unsigned)((n_loc_ + cv - 1) / cv);
+  if (small_graph) {
+    if (pdl)
+      LBFS_LAUNCH_PDL(k_compact<kCompactVertsSmall>, cgrid, kCompactThreads, 0, st, ca);
+    else
+      LBFS_LAUNCH(k_compact<kCompactVertsSmall>, cgrid, kCompactThreads, 0, st, ca);
+  } else {
+    if (pdl)
+      LBFS_LAUNCH_PDL(k_compact<kCompactVertsBig>, cgrid, kCompactThreads, 0, st, ca);
+    else
+      LBFS_LAUNCH(k_compact<kCompactVertsBig>, cgrid, kCompactThreads, 0, st, ca);
+  }
   if (heavy && lean_events_ && nparts_ == 1) {
     resolve_deferred_ = L + 1;  // (launched behind the level's publish / cluster kernel: launch_resolve)
     return;
@@ -2393,6 +2409,7 @@ void BfsEngine::read_env() {
   // LBFS_NO_WARP_ITEMS=1: append them to the raw warp queue instead
   warp_items_ = !env_flag("LBFS_NO_WARP_ITEMS");
   qgrid_old_ = env_flag("LBFS_QGRID_OLD");
+  compact_big_ = env_flag("LBFS_COMPACT_BIG");  // (A/B) 4096-id compaction blocks on small graphs too
   // No timing events between the kernels of a BFS: an event record between two
   // kernels costs a few microseconds of stream serialisation each and ends a
   // chain of programmatic dependent launches (S24 401 -> 414, S20 106 -> 117

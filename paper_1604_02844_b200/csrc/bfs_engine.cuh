@@ -597,6 +597,7 @@ class BfsEngine {
   bool cl_dsm_ = false;           // visited bitmap in distributed shared memory
   bool cl_no_dsm_ = false, cl_off_ = false;
   bool qgrid_old_ = false;
+  bool compact_big_ = false;
   bool lean_events_ = false;
   int64_t resolve_deferred_ = -1;
   bool align_items_ = false;
